@@ -1,0 +1,452 @@
+"""Benchmark of the B200 HiKF hot path (BASELINE.json metric):
+
+    HiKF assimilation steps/sec  (+ Q H^T (m n)/sec of the bbFMM precompute)
+
+on cfg4 (2D 1024 x 1024 grid, m = 1,048,576, n = 1,024 crosswell rays,
+exponential kernel L = 0.25, Chebyshev order 6, leaf 64, R = 1e-3).
+
+One "step" = hikf_predict + hikf_update (the fused predict/update of
+libhikf_b200.so) on device-resident inputs; `value` = steps/s over exactly
+--steps timed steps after --warmup untimed ones (CUDA events, barrier +
+synchronize on both sides, max over ranks).  The state (C is 8.6 GB) is far
+larger than L2 (126 MB), so no flush is needed between steps.
+
+`e2e` is the same metric through the public Python API with host buffers:
+every step uploads z (numpy, 8 n bytes) and reads the posterior mean back to
+numpy (8 m bytes), exactly what experiment.run_hikf does (experiment.py:237).
+
+`--impl reference` times the reference algorithm on the host CPU cores: the
+reference is pure Python and cannot travel to the GPU box, so its numpy
+restatement in oracle/ (pinned to the reference by tests/test_oracle_golden.py)
+runs a bounded row sample of each step (see cpu_step_sample).
+
+Multi-GPU (--gpus N under torchrun): independent replicas, one filter per
+GPU ("replicas only" this round); value sums ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(N=64, ns=8, nr=8, family="exponential", L=0.3, R=1e-2, T=20, order=4, leaf=64,
+                 desc="cfg1: 2D 64x64 unit square m=4096, n=64 crosswell rays, exponential L=0.3, order 4, leaf 64"),
+    "cfg2": dict(N=256, ns=16, nr=16, family="gaussian", L=0.2, R=1e-3, T=100, order=5, leaf=64,
+                 desc="cfg2: 2D 256x256 m=65536, n=256 crosswell rays, gaussian L=0.2, order 5, leaf 64"),
+    "cfg4": dict(N=1024, ns=32, nr=32, family="exponential", L=0.25, R=1e-3, T=50, order=6, leaf=64,
+                 desc="cfg4: 2D 1024x1024 m=1048576, n=1024 crosswell rays, exponential L=0.25, order 6, leaf 64"),
+}
+
+# FP64 roofline denominator: MEASURED_PEAKS.json has no FP64 entry; this is the
+# cuBLAS DGEMM (torch.matmul float64, 8192^3) we measured on this pool's B200
+# (profiles/r01_fp64_dgemm.json: 35.48 burst / 35.46 sustained TFLOP/s; the
+# DMMA/DFMA issue-rate microbenchmark gives 37.0, profiles/r01_fp64_micro.json).
+FP64_PEAK_TFLOPS = 35.46
+FP64_PEAK_SOURCE = "measured cuBLAS DGEMM 8192^3 on B200 (profiles/r01_fp64_dgemm.json); not in MEASURED_PEAKS.json"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# scenario (host inputs)
+# ---------------------------------------------------------------------------
+
+def plume_observations(H, xy, T, R, seed=0):
+    """Constant-amplitude moving Gaussian plume (w = 0.1 from (0.2, 0.5), +0.01 x
+    per step) and z_t = H x_t + N(0, R) from PCG64 seed [seed, 0] (ssm.py:81-113)."""
+    Z = np.empty((T, H.shape[0]))
+    for t in range(1, T + 1):
+        x = np.exp(-((xy[:, 0] - (0.2 + 0.01 * (t - 1))) ** 2 + (xy[:, 1] - 0.5) ** 2) / (2 * 0.1 * 0.1))
+        Z[t - 1] = H @ x
+    rng = np.random.default_rng([seed, 0])
+    return Z + math.sqrt(R) * rng.standard_normal(Z.shape)
+
+
+def fmm_flops(orders, depth, k, near_pairs_pts, m):
+    """Dense-formulation flops of one matmat."""
+    nl = orders[depth]
+    f = {"p2p": 2.0 * k * near_pairs_pts, "p2m": 2.0 * k * m * nl * nl, "l2p": 2.0 * k * m * nl * nl}
+    mm = 0.0
+    for lev in range(2, depth):
+        mm += 2.0 * k * (4 ** (lev + 1)) * orders[lev + 1] ** 2 * orders[lev] ** 2
+    f["m2m"] = mm
+    f["l2l"] = mm
+    return f
+
+
+def m2l_flops(tree, k):
+    tot = 0.0
+    for lev in range(2, tree.depth + 1):
+        pairs = 0
+        G = 1 << lev
+        for dx in range(-3, 4):
+            for dy in range(-3, 4):
+                if max(abs(dx), abs(dy)) < 2:
+                    continue
+                cnt = [0, 0]
+                for d, c in ((dx, 0), (dy, 1)):
+                    i = np.arange(G)
+                    j = i + d
+                    cnt[c] = int(np.sum((j >= 0) & (j < G) & (np.abs((j >> 1) - (i >> 1)) <= 1)))
+                pairs += cnt[0] * cnt[1]
+        tot += 2.0 * k * pairs * tree._orders[lev] ** 4
+    return tot
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        reasons = set()
+        for s in load:
+            for bit, name in self.REASONS.items():
+                if s[2] & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in load), "sm_max_mhz": max(s[1] for s in load),
+                "reasons": sorted(reasons), "samples": len(load)}
+
+
+# ---------------------------------------------------------------------------
+# CPU leg: the reference algorithm (oracle restatement) on a bounded sample
+# ---------------------------------------------------------------------------
+
+def _cpu_update_time(cfg, rows, reps=1):
+    from oracle import hikf_oracle as O
+    import scipy.sparse
+    n = cfg["ns"] * cfg["nr"]
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((n, n)) / math.sqrt(n)
+    HC0 = A @ A.T
+    st = O.State(np.zeros(rows), 1e-3 * rng.standard_normal((rows, n)), 1e3 * np.ones(rows), HC0.copy())
+    pre = O.Pre(1e-3 * rng.standard_normal((rows, n)), 0.1 * HC0, np.ones(rows))
+    H = scipy.sparse.random(n, rows, density=min(1.0, 1300.0 / rows), random_state=2, format="csr")
+    z = rng.standard_normal(n)
+    times = []
+    for i in range(reps + 1):  # first call warms the BLAS thread pool
+        t0 = time.perf_counter()
+        O.update(O.predict(st, pre), H, cfg["R"] + 10.0, z)
+        if i:
+            times.append(time.perf_counter() - t0)
+    return min(times)
+
+
+def cpu_step_sample(cfg, rows, reps=1):
+    """Time the reference predict+update (oracle/hikf_oracle.py: numpy + OpenBLAS /
+    LAPACK on all host cores) on `rows` and `rows/2` of the m state rows with the
+    full n, and extrapolate linearly, t(m) = a + b m: every m-row term (potrs with
+    m RHS, K HC, rowsum, predict add) is linear in the row count and the n x n
+    terms (Cholesky, KH, KH HC) are the intercept.  Returns (seconds per full
+    step, rows)."""
+    m = cfg["N"] ** 2
+    rows = min(rows, m)
+    if rows == m:
+        return _cpu_update_time(cfg, rows, reps), rows
+    t1 = _cpu_update_time(cfg, rows, reps)
+    t2 = _cpu_update_time(cfg, rows // 2, reps)
+    b = max((t1 - t2) / (rows - rows // 2), 0.0)
+    a = max(t1 - b * rows, 0.0)
+    return a + b * m, rows
+
+
+def cpu_qht_sample(cfg, cols=8):
+    """Reference bbFMM (oracle restatement) Q H^T on `cols` columns of H^T
+    (matmat is column-independent, fmm.py:325-367): (m n)/s = m cols / t."""
+    from oracle import hikf_oracle as O
+    N = cfg["N"]
+    xy = O.cell_centers(N, N, 1.0 / N, 1.0 / N)
+    src, rcv = O.crosswell_stations(cfg["ns"], cfg["nr"], 0.0, 1.0, 0.0, 1.0)
+    H = O.ray_operator(N, N, 1.0 / N, 1.0 / N, src, rcv)
+    t0 = time.perf_counter()
+    tree = O.OracleTree(xy, O.Kern(cfg["family"], 1.0, cfg["L"]), cfg["order"], cfg["leaf"])
+    t_build = time.perf_counter() - t0
+    sel = np.linspace(0, H.shape[0] - 1, cols).astype(int)
+    V = np.ascontiguousarray(H[sel].T.toarray())
+    t0 = time.perf_counter()
+    tree.matmat(V)
+    t = time.perf_counter() - t0
+    return N * N * cols / t, t_build, t
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the reference algorithm on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    threads = os.cpu_count()
+    rows = args.cpu_rows
+    per_step = []
+    for i in range(args.warmup + args.steps):
+        t, rows = cpu_step_sample(cfg, rows)
+        if i >= args.warmup:
+            per_step.append(t)
+    t_step = statistics.median(per_step)
+    value = 1.0 / t_step
+    sample = (f"oracle/hikf_oracle.py predict+update (numpy + OpenBLAS/LAPACK) on {rows} of {cfg['N'] ** 2} state rows "
+              f"with n={cfg['ns'] * cfg['nr']} (and rows/2), linearly extrapolated to m; one sample pair per step")
+    line = {
+        "metric": "hikf_assimilation_steps_per_sec", "value": value, "unit": "steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, cfg4 shapes)",
+        "config": {"workload": cfg["desc"]}, "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-rows", type=int, default=65536)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1404_3816_b200 as P
+    from paper_1404_3816_b200 import _lib
+    lib = _lib.load()
+    flt = P.filters
+
+    N = cfg["N"]
+    grid = P.Grid2D(N, N, 1.0 / N, 1.0 / N)
+    H = P.tomography.build_ray_operator(grid, P.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], 0.0, 1.0))
+    m, n = grid.m, H.shape[0]
+    xy = grid.cell_centers().coords
+    obs = plume_observations(H, xy, cfg["T"], cfg["R"])
+    kern = P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+
+    class Model:
+        pass
+
+    model = Model()
+    model.H, model.m, model.alpha, model.initial_mean, model.r_variance = H, m, 0.0, np.zeros(m), cfg["R"]
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- tree build + Q H^T precompute (one-time; timed separately) ----
+    barrier_sync()
+    t0 = time.perf_counter()
+    tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    flt.hikf_precompute_fmm(model, tree)  # warm-up of the precompute (allocator, L2)
+    barrier_sync()
+    lib.hikf_prof_reset()
+    lib.hikf_prof_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    pre = flt.hikf_precompute_fmm(model, tree)
+    e1.record()
+    barrier_sync()
+    lib.hikf_prof_enable(0)
+    t_qht = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    fmm_stage = {s: _lib.prof_read(s) for s in ("densify", "p2p", "p2m", "m2m", "m2l", "l2p")}
+    ex = tree.export()
+    cnt = ex["leaf_counts"]
+    near_pts = float(np.sum(cnt[ex["near_t"]] * cnt[ex["near_s"]]))
+    ff = fmm_flops(tree._orders, tree.depth, n, near_pts, m) if tree.depth >= 2 else {"p2p": 2.0 * n * near_pts}
+    ff["m2l"] = m2l_flops(tree, n) if tree.depth >= 2 else 0.0
+    qht_flops = sum(ff.values())
+
+    # ---- filter: warm-up, then the timed region ----
+    Zd = torch.from_numpy(obs).cuda()
+    st = flt.hikf_init(model)
+    for t in range(args.warmup):
+        st = flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], Zd[t % cfg["T"]])
+    lib.hikf_prof_reset()
+    lib.hikf_prof_enable(1)
+    l0 = lib.hikf_launch_count()
+    barrier_sync()
+    with ClockSampler(local) as clk:
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for t in range(args.steps):
+            st = flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], Zd[(args.warmup + t) % cfg["T"]])
+        s1.record()
+        barrier_sync()
+    lib.hikf_prof_enable(0)
+    launches = int(lib.hikf_launch_count() - l0)
+    t_loop = max_over_ranks(s0.elapsed_time(s1) / 1e3)
+    stage = {s: _lib.prof_read(s) for s in ("predict", "factor", "gemm_y", "finalize", "gemm_c")}
+    steps_per_s = world * args.steps / t_loop
+
+    # ---- e2e: public API with host buffers (z up, mean down, every step) ----
+    barrier_sync()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    means = np.empty((args.steps, m))
+    c0.record()
+    for t in range(args.steps):
+        z_host = obs[(args.warmup + t) % cfg["T"]]
+        st = flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], z_host)
+        means[t] = st.mean
+    c1.record()
+    barrier_sync()
+    t_e2e = max_over_ranks(c0.elapsed_time(c1) / 1e3)
+
+    # ---- rooflines ----
+    hbm, hbm_src = hbm_peak()
+    ms_c, n_c = stage["gemm_c"]
+    ms_y, n_y = stage["gemm_y"]
+    t_c = ms_c / max(n_c, 1) / 1e3
+    flops_c = 2.0 * m * n * n
+    achieved = flops_c / t_c / 1e12
+    ms_p, n_p = stage["predict"]
+    t_p = ms_p / max(n_p, 1) / 1e3
+    bytes_p = 24.0 * m * n + 24.0 * m + 24.0 * n * n
+    m2l_ms, _ = fmm_stage["m2l"]
+    update_flops = 3.0 * m * n * n + 2.0 * n * n * n * 3 + n ** 3 / 3.0
+
+    line = {
+        "metric": "hikf_assimilation_steps_per_sec",
+        "value": steps_per_s,
+        "unit": "steps/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * t_loop / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: seeded crosswell rays + moving Gaussian plume, PCG64 noise (cfg recipe, SURVEY 8(d))",
+        "config": {"workload": cfg["desc"], "steps_per_run": cfg["T"],
+                   "l2": "no flush: per-step inputs (C 8.6 GB, C_Q 8.6 GB) far exceed the 126 MB L2"
+                   if args.config == "cfg4" else "small config: inputs may be L2-resident",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "qht": {"value": world * m * n / t_qht, "unit": "(m*n)/s", "ms": 1000.0 * t_qht, "tree_build_s": t_build,
+                "precompute_incl_build_mn_per_s": m * n / (t_qht + t_build),
+                "flops_dense_formulation": qht_flops,
+                "stage_ms": {k: v[0] for k, v in fmm_stage.items()},
+                "roofline": {"bound": "fp64", "achieved": qht_flops / t_qht / 1e12, "peak": FP64_PEAK_TFLOPS,
+                             "unit": "TFLOP/s", "frac": qht_flops / t_qht / 1e12 / FP64_PEAK_TFLOPS,
+                             "m2l": {"achieved": ff["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
+        "roofline": {"kernel": "dgemm_kernel (C_new = C' - Y P, 2 m n^2 flops per launch)", "bound": "fp64",
+                     "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SOURCE,
+                     "share_of_step": (ms_c + ms_y) / (1000.0 * t_loop) if t_loop else None,
+                     "update_step_flops": update_flops,
+                     "update_step_frac": update_flops * args.steps / t_loop / 1e12 / FP64_PEAK_TFLOPS},
+        "streaming": {"kernel": "predict add (C += C_Q, var += diag_Q, HC += HC_Q)", "bound": "hbm",
+                      "achieved": bytes_p / t_p / 1e9 if t_p else None, "peak": hbm, "unit": "GB/s",
+                      "frac": (bytes_p / t_p / 1e9) / hbm if t_p else None, "peak_source": hbm_src},
+        "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in stage.items()},
+        "e2e": {"value": world * args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * m, "api": "paper_1404_3816_b200.filters.hikf_update(numpy z) + state.mean"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_cpu, rows = cpu_step_sample(cfg, args.cpu_rows)
+        line["cpu_baseline"] = {
+            "value": 1.0 / t_cpu, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle predict+update on {rows} and {rows // 2} of {m} rows (n={n}), "
+                      "linear extrapolation t(m) = a + b m"}
+        try:
+            mn_s, tb, tq = cpu_qht_sample(cfg, cols=8)
+            line["cpu_baseline"]["qht"] = {"value": mn_s, "unit": "(m*n)/s",
+                                           "sample": f"oracle bbFMM matmat on 8 of {n} H^T columns ({tq:.1f} s), "
+                                                     f"tree build {tb:.1f} s"}
+        except MemoryError:
+            pass
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * hikf_b200.h -- C ABI of the B200-native HiKF hot path (libhikf_b200.so).
+ *
+ * The reference (`hikf`, pure Python; /root/reference/pkg/src/hikf) has no FFI:
+ * its boundary is the Python function surface re-exported from
+ * hikf/__init__.py:10-26.  Each entry point below replaces one reference
+ * function (cited file:line); the Python mirror in paper_1404_3816_b200/
+ * binds them with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "dev" pointers are CUDA device memory
+ *     (any allocator), "host" pointers are CPU memory.  Dense matrices are
+ *     row-major float64 with an explicit leading dimension, exactly the
+ *     C-order numpy layout the reference uses (state (m, n), V (m, k)).
+ *   - Sparse H is CSR (n_rows x m): int32 indptr[n+1], int32 indices[nnz],
+ *     float64 data[nnz] -- scipy's canonical csr_matrix arrays.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *     stream-ordered; the ones that must report a numerical status
+ *     synchronise the stream before returning (as the reference raises
+ *     synchronously).
+ *   - Every function returns an hikf_status; hikf_last_error() gives the
+ *     message of the most recent failure on the calling thread.
+ *   - Calls on distinct handles are re-entrant; a single tree handle may be
+ *     used for concurrent read-only matmat calls on distinct streams only if
+ *     each call passes its own workspace (matmat allocates its own).
+ */
+#ifndef HIKF_B200_H
+#define HIKF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HIKF_OK = 0,
+  HIKF_BAD_ARGUMENT = 1,      /* -> ValueError (fmm.py:50-54, :328-329; filters.py:31-37) */
+  HIKF_NOT_PD = 2,            /* -> DecompositionError (linalg.py:33-36) */
+  HIKF_NEGATIVE_VARIANCE = 3, /* -> NumericalConsistencyError (filters.py:149-153) */
+  HIKF_CUDA_ERROR = 4,
+  HIKF_ASYMMETRIC = 5,        /* -> ValueError("A is not symmetric") (linalg.py:30-32) */
+  HIKF_NO_DEVICE = 6
+} hikf_status;
+
+/* Kernel family codes (kernels.py:22 _FAMILIES). */
+enum { HIKF_GAUSSIAN = 0, HIKF_EXPONENTIAL = 1, HIKF_LOGARITHM = 2 };
+
+/* KernelSpec (kernels.py:25-69).  `power` is the effective power
+ * (2 gaussian / 1 exponential unless overridden); ignored for logarithm. */
+typedef struct {
+  int32_t family;
+  double variance;
+  double length_scale;
+  double power;
+  double log_amplitude;
+} hikf_kernel;
+
+typedef struct hikf_tree hikf_tree; /* opaque, immutable after create */
+
+int hikf_abi_version(void);
+/* Copy the last error message of this thread into buf (NUL-terminated). */
+int hikf_last_error(char* buf, size_t len);
+
+/* ---- FMM tree: replaces build_tree / FmmTree.__init__ (fmm.py:95-135, 370-374) ----
+ * xy_host: (m, 2) row-major cell/point coordinates.  n_cheb in [2, 12],
+ * max_leaf >= 1 (FmmConfig, fmm.py:38-54).  All construction kernels run on
+ * `stream`; the call returns after the tree is complete. */
+int hikf_tree_create(const double* xy_host, int64_t m, const hikf_kernel* kernel, int32_t n_cheb,
+                     int64_t max_leaf, void* stream, hikf_tree** out);
+int hikf_tree_destroy(hikf_tree* tree);
+
+/* Scalars of the tree: depth, per-level orders (orders[lev] for lev 2..depth,
+ * 0 elsewhere; array of 21), root_lo[2], root_size, #occupied leaves,
+ * #near leaf pairs. */
+int hikf_tree_info(const hikf_tree* tree, int64_t* m, int32_t* depth, int32_t* orders21, double* root_lo2,
+                   double* root_size, int64_t* n_leaves, int64_t* n_near_pairs);
+
+/* Parity export of the integer tree data (fmm.py:116-128, 166-190), host
+ * buffers sized from hikf_tree_info: order[m] (= FmmTree._order),
+ * leaf_ids/leaf_starts/leaf_counts[n_leaves], near_t/near_s[n_near_pairs]
+ * (leaf ranks of each adjacent pair, in the reference's offset-major order). */
+int hikf_tree_export(const hikf_tree* tree, int64_t* order, int64_t* leaf_ids, int64_t* leaf_starts,
+                     int64_t* leaf_counts, int64_t* near_t, int64_t* near_s);
+
+/* Parity export of the operators at one level (fmm.py:246-312):
+ *   which = 0: M2L op for offset (dx, dy) -> out[q*q] (q = orders[lev]^2); returns
+ *              HIKF_BAD_ARGUMENT if the offset has no pairs at that level.
+ *   which = 1: shift op kron(Bx, By) for child parity (dx, dy) = (cx, cy) between
+ *              lev and lev+1 -> out[q_child * q_parent].
+ *   which = 2: interpolation weights W2 of every point in ORIGINAL point order,
+ *              out[m * q_leaf] (lev, dx, dy ignored). */
+int hikf_tree_export_op(const hikf_tree* tree, int32_t which, int32_t lev, int32_t dx, int32_t dy, double* out_host);
+
+/* Parity export of the M2L interaction list of one (level, offset) over the
+ * full G x G lattice (fmm.py:299-312 _m2l_pairs), evaluated by the device rule
+ * the M2L kernel uses.  Call with tgt == NULL to get *count, then with
+ * buffers of *count entries. */
+int hikf_tree_m2l_pairs(const hikf_tree* tree, int32_t lev, int32_t dx, int32_t dy, int64_t* tgt, int64_t* src,
+                        int64_t* count);
+
+/* ---- FmmTree.matmat (fmm.py:325-367) ----
+ * U (m x k, ldu) = approx Gram(points) @ V (m x k, ldv), both device. */
+int hikf_tree_matmat(hikf_tree* tree, const double* V_dev, int64_t ldv, int64_t k, double* U_dev, int64_t ldu,
+                     void* stream);
+
+/* Same product with V = H^T for a CSR H (n x m) on the device, without
+ * densifying H^T (filters.py:101-102).  U is (m x n) row-major. */
+int hikf_tree_matmat_csrT(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
+                          const double* data_dev, double* U_dev, void* stream);
+
+/* ---- hikf_precompute_fmm (filters.py:99-105) ----
+ * C_Q (m x n) = tree @ H^T; HC_Q (n x n) = sym(H C_Q); diag_Q (m) = K(0). */
+int hikf_precompute(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
+                    const double* data_dev, double* C_Q_dev, double* HC_Q_dev, double* diag_Q_dev, void* stream);
+
+/* ---- hikf_init (filters.py:118-126): C = alpha H^T, var = alpha, HC = alpha H H^T ----
+ * (the mean is the caller's initial_mean copy). */
+int hikf_init_state(int64_t m, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
+                    const double* data_dev, double alpha, double* C_out, double* var_out, double* HC_out,
+                    void* stream);
+
+/* ---- hikf_predict (filters.py:129-135): out = in + pre, elementwise ----
+ * Any output may alias its input. */
+int hikf_predict(int64_t m, int64_t n, const double* C_dev, const double* var_dev, const double* HC_dev,
+                 const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev, double* C_out,
+                 double* var_out, double* HC_out, void* stream);
+
+/* ---- hikf_update (filters.py:138-157) + the optional fused predict ----
+ * Inputs: state (mean m, C m x n, var m, HC n x n), CSR H, r, z (device, n).
+ * If C_Q_dev != NULL the predict step (filters.py:129-135) is fused in front:
+ * the update then acts on (C + C_Q, var + diag_Q, HC + HC_Q).
+ * Outputs are written to the *_out buffers (may not alias the inputs).
+ * workspace: device buffer of hikf_update_workspace_bytes(m, n) bytes.
+ * Returns HIKF_NOT_PD / HIKF_NEGATIVE_VARIANCE like the reference raises;
+ * the stream is synchronised before returning. */
+size_t hikf_update_workspace_bytes(int64_t m, int64_t n);
+int hikf_update(int64_t m, int64_t n, const double* mean_dev, const double* C_dev, const double* var_dev,
+                const double* HC_dev, const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev,
+                const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev, double r_variance,
+                const double* z_dev, double* mean_out, double* C_out, double* var_out, double* HC_out,
+                void* workspace, size_t workspace_bytes, double* min_var_out, void* stream);
+
+/* ---- spd_solve (linalg.py:18-37): X (n x k) = A^{-1} B, A SPD n x n ----
+ * Symmetry check |A - A^T|max <= 1e-10 |A|max (HIKF_ASYMMETRIC), Cholesky
+ * (HIKF_NOT_PD with the failing pivot in *info), two triangular solves. */
+size_t hikf_spd_solve_workspace_bytes(int64_t n, int64_t k);
+int hikf_spd_solve(int64_t n, int64_t k, const double* A_dev, const double* B_dev, double* X_dev, void* workspace,
+                   size_t workspace_bytes, int64_t* info, void* stream);
+
+/* ---- build_ray_operator (tomography.py:76-133), host input producer ----
+ * Straight rays src[i] -> rcv[i] (n rays, (n, 2) row-major) over the nx x ny
+ * cell grid at origin (x0, y0) with spacing (dx, dy).  Two-call protocol:
+ * with indices == NULL returns nnz in *nnz_out; then call again with
+ * indptr[n+1] / indices[nnz] / data[nnz] host buffers. */
+int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n,
+                      const double* src, const double* rcv, int32_t* indptr, int32_t* indices, double* data,
+                      int64_t* nnz_out);
+
+/* ---- instrumentation (bench.py) ----
+ * Stage timers: CUDA events recorded on the launching stream around each
+ * stage (ids in csrc/prof.h: 0 predict, 1 factor, 2 Y GEMM, 3 finalize,
+ * 4 C GEMM, 5 P2P, 6 P2M, 7 M2M, 8 M2L, 9 L2P, 10 densify).
+ * hikf_launch_count: kernels launched by this library since load. */
+int hikf_prof_enable(int on);
+int hikf_prof_reset(void);
+int hikf_prof_read(int32_t stage, double* total_ms, int64_t* count);
+int64_t hikf_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIKF_B200_H */

@@ -1,0 +1,399 @@
+// C-ABI entry points of libhikf_b200.so (declared in include/hikf_b200.h).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "prof.h"
+#include "tree.h"
+#include "update.h"
+
+namespace hikf {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+const std::string& last_error() { return g_last_error; }
+
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+KParams make_kparams(const hikf_kernel& k) {
+  KParams p;
+  p.family = k.family;
+  p.variance = k.variance;
+  p.length = k.length_scale;
+  p.power = k.power;
+  p.log_amp = k.log_amplitude;
+  p.pmode = 0;
+  if (k.power == 1.0) p.pmode = 1;
+  if (k.power == 2.0) p.pmode = 2;
+  if (k.power == 0.5) p.pmode = 3;
+  return p;
+}
+
+namespace {
+
+constexpr int kT = 256;
+
+// dense H^T (m x n) from CSR H (n x m); Ht must be zeroed first
+__global__ void scatter_transpose(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
+                                  const double* __restrict__ val, double* __restrict__ Ht) {
+  int64_t r = blockIdx.x;
+  if (r >= n) return;
+  for (int64_t e = ip[r] + threadIdx.x; e < ip[r + 1]; e += blockDim.x) Ht[(int64_t)ix[e] * n + r] = val[e];
+}
+
+// X = H C (n x n), one CTA per row of H, threads over the n columns
+__global__ void spmm_rows(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
+                          const double* __restrict__ val, const double* __restrict__ C, double* __restrict__ X) {
+  int64_t r = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = ip[r]; e < ip[r + 1]; ++e) s += val[e] * C[(int64_t)ix[e] * n + j];
+    X[r * n + j] = s;
+  }
+}
+
+__global__ void symmetrize(const double* __restrict__ X, int64_t n, double* __restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / n, j = e % n;
+    Y[e] = 0.5 * (X[e] + X[j * n + i]);
+  }
+}
+
+__global__ void fill(double* x, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] = v;
+}
+
+__global__ void scale_copy(const double* __restrict__ x, int64_t n, double a, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a * x[i];
+}
+
+int grid_for(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms() * 32));
+}
+
+int matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
+                cudaStream_t st) {
+  double* Ht = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Ht, sizeof(double) * std::max<int64_t>(1, t->m * n), st));
+  {
+    ProfScope ps(ST_DENSIFY, st);
+    HIKF_CHECK_CUDA(cudaMemsetAsync(Ht, 0, sizeof(double) * t->m * n, st));
+    if (n > 0) {
+      scatter_transpose<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, Ht);
+      HIKF_CHECK_LAUNCH();
+    }
+  }
+  int s = fmm_matmat(t, Ht, n, n, U, n, st);
+  cudaFreeAsync(Ht, st);
+  return s;
+}
+
+}  // namespace
+}  // namespace hikf
+
+using namespace hikf;
+
+static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int hikf_abi_version(void) { return 1; }
+
+int hikf_last_error(char* buf, size_t len) {
+  if (!buf || len == 0) return HIKF_BAD_ARGUMENT;
+  std::strncpy(buf, g_last_error.c_str(), len - 1);
+  buf[len - 1] = '\0';
+  return HIKF_OK;
+}
+
+int hikf_tree_create(const double* xy_host, int64_t m, const hikf_kernel* kernel, int32_t n_cheb, int64_t max_leaf,
+                     void* stream, hikf_tree** out) {
+  if (!kernel || !out) {
+    set_error("null argument");
+    return HIKF_BAD_ARGUMENT;
+  }
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+    set_error("no CUDA device: the HiKF B200 path has no CPU fallback");
+    return HIKF_NO_DEVICE;
+  }
+  return tree_build(xy_host, m, *kernel, n_cheb, max_leaf, as_stream(stream), out);
+}
+
+int hikf_tree_destroy(hikf_tree* tree) {
+  tree_free(tree);
+  return HIKF_OK;
+}
+
+int hikf_tree_info(const hikf_tree* t, int64_t* m, int32_t* depth, int32_t* orders21, double* root_lo2,
+                   double* root_size, int64_t* n_leaves, int64_t* n_near_pairs) {
+  if (!t) return HIKF_BAD_ARGUMENT;
+  if (m) *m = t->m;
+  if (depth) *depth = t->depth;
+  if (orders21)
+    for (int l = 0; l <= kMaxDepth; ++l) orders21[l] = t->orders[l];
+  if (root_lo2) {
+    root_lo2[0] = t->lo[0];
+    root_lo2[1] = t->lo[1];
+  }
+  if (root_size) *root_size = t->size;
+  if (n_leaves) *n_leaves = t->n_leaves;
+  if (n_near_pairs) {
+    int64_t G = t->G, cnt = 0;
+    std::vector<int32_t> b2l(G * G, -1);
+    for (int64_t r = 0; r < t->n_leaves; ++r) b2l[t->h_leaf_box[r]] = (int32_t)r;
+    for (int64_t r = 0; r < t->n_leaves; ++r) {
+      int64_t bx = t->h_leaf_box[r] / G, by = t->h_leaf_box[r] % G;
+      for (int ox = -1; ox <= 1; ++ox)
+        for (int oy = -1; oy <= 1; ++oy) {
+          int64_t nx = bx + ox, ny = by + oy;
+          if (nx >= 0 && nx < G && ny >= 0 && ny < G && b2l[nx * G + ny] >= 0) ++cnt;
+        }
+    }
+    *n_near_pairs = cnt;
+  }
+  return HIKF_OK;
+}
+
+int hikf_tree_export(const hikf_tree* t, int64_t* order, int64_t* leaf_ids, int64_t* leaf_starts, int64_t* leaf_counts,
+                     int64_t* near_t, int64_t* near_s) {
+  if (!t) return HIKF_BAD_ARGUMENT;
+  if (order) HIKF_CHECK_CUDA(cudaMemcpy(order, t->order, sizeof(int64_t) * t->m, cudaMemcpyDeviceToHost));
+  for (int64_t r = 0; r < t->n_leaves; ++r) {
+    if (leaf_ids) leaf_ids[r] = t->h_leaf_box[r];
+    if (leaf_starts) leaf_starts[r] = t->h_leaf_start[r];
+    if (leaf_counts) leaf_counts[r] = t->h_leaf_count[r];
+  }
+  if (near_t || near_s) {
+    // fmm.py:170-179: for each offset (ox outer, oy inner), every occupied leaf in
+    // rank order whose neighbour box is occupied -- the same rule P2P uses
+    int64_t G = t->G, p = 0;
+    std::vector<int32_t> b2l(G * G, -1);
+    HIKF_CHECK_CUDA(cudaMemcpy(b2l.data(), t->box2leaf, sizeof(int32_t) * G * G, cudaMemcpyDeviceToHost));
+    for (int ox = -1; ox <= 1; ++ox)
+      for (int oy = -1; oy <= 1; ++oy)
+        for (int64_t r = 0; r < t->n_leaves; ++r) {
+          int64_t bx = t->h_leaf_box[r] / G + ox, by = t->h_leaf_box[r] % G + oy;
+          if (bx < 0 || bx >= G || by < 0 || by >= G) continue;
+          int32_t s = b2l[bx * G + by];
+          if (s < 0) continue;
+          if (near_t) near_t[p] = r;
+          if (near_s) near_s[p] = s;
+          ++p;
+        }
+  }
+  return HIKF_OK;
+}
+
+int hikf_tree_export_op(const hikf_tree* t, int32_t which, int32_t lev, int32_t dx, int32_t dy, double* out) {
+  if (!t || !out) return HIKF_BAD_ARGUMENT;
+  if (t->depth < 2) {
+    set_error("tree has no far field (depth < 2)");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (which == 0) {
+    if (lev < 2 || lev > t->depth) return HIKF_BAD_ARGUMENT;
+    M2LOffsets offs;
+    int s = -1;
+    for (int i = 0; i < 40; ++i)
+      if (offs.dx[i] == dx && offs.dy[i] == dy) s = i;
+    if (s < 0 || !((t->m2l_present[lev] >> s) & 1)) {
+      set_error("no M2L operator for offset (%d, %d) at level %d", dx, dy, lev);
+      return HIKF_BAD_ARGUMENT;
+    }
+    int64_t q = (int64_t)t->orders[lev] * t->orders[lev];
+    HIKF_CHECK_CUDA(cudaMemcpy(out, t->m2l[lev] + s * q * q, sizeof(double) * q * q, cudaMemcpyDeviceToHost));
+    return HIKF_OK;
+  }
+  if (which == 1) {
+    if (lev < 2 || lev >= t->depth || dx < 0 || dx > 1 || dy < 0 || dy > 1) return HIKF_BAD_ARGUMENT;
+    int64_t qp = (int64_t)t->orders[lev] * t->orders[lev], qc = (int64_t)t->orders[lev + 1] * t->orders[lev + 1];
+    HIKF_CHECK_CUDA(cudaMemcpy(out, t->shift[lev] + (dx * 2 + dy) * qp * qc, sizeof(double) * qp * qc,
+                               cudaMemcpyDeviceToHost));
+    return HIKF_OK;
+  }
+  if (which == 2) {
+    int64_t q = (int64_t)t->orders[t->depth] * t->orders[t->depth];
+    std::vector<double> w(t->m * q);
+    std::vector<int64_t> ord(t->m);
+    HIKF_CHECK_CUDA(cudaMemcpy(w.data(), t->W2s, sizeof(double) * w.size(), cudaMemcpyDeviceToHost));
+    HIKF_CHECK_CUDA(cudaMemcpy(ord.data(), t->order, sizeof(int64_t) * t->m, cudaMemcpyDeviceToHost));
+    for (int64_t p = 0; p < t->m; ++p) std::memcpy(out + ord[p] * q, &w[p * q], sizeof(double) * q);
+    return HIKF_OK;
+  }
+  return HIKF_BAD_ARGUMENT;
+}
+
+int hikf_tree_m2l_pairs(const hikf_tree* t, int32_t lev, int32_t dx, int32_t dy, int64_t* tgt, int64_t* src,
+                        int64_t* count) {
+  if (!t || !count) return HIKF_BAD_ARGUMENT;
+  std::vector<int64_t> a, b;
+  HIKF_TRY(tree_export_m2l_pairs(t, lev, dx, dy, a, b));
+  if (tgt && src) {
+    if (*count < (int64_t)a.size()) return HIKF_BAD_ARGUMENT;
+    std::memcpy(tgt, a.data(), sizeof(int64_t) * a.size());
+    std::memcpy(src, b.data(), sizeof(int64_t) * b.size());
+  }
+  *count = (int64_t)a.size();
+  return HIKF_OK;
+}
+
+int hikf_tree_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U, int64_t ldu, void* stream) {
+  if (!t || (k > 0 && (!V || !U)) || k < 0 || ldv < k || ldu < k) {
+    set_error("bad matmat arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return fmm_matmat(t, V, ldv, k, U, ldu, as_stream(stream));
+}
+
+int hikf_tree_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
+                          void* stream) {
+  if (!t || n < 0 || (n > 0 && (!ip || !U))) {
+    set_error("bad matmat_csrT arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return matmat_csrT(t, n, ip, ix, val, U, as_stream(stream));
+}
+
+int hikf_precompute(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* CQ,
+                    double* HCQ, double* dQ, void* stream) {
+  if (!t || n < 0) {
+    set_error("bad precompute arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  cudaStream_t st = as_stream(stream);
+  HIKF_TRY(matmat_csrT(t, n, ip, ix, val, CQ, st));
+  if (n > 0) {
+    double* X = nullptr;
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&X, sizeof(double) * n * n, st));
+    spmm_rows<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, CQ, X);
+    HIKF_CHECK_LAUNCH();
+    symmetrize<<<grid_for(n * n), kT, 0, st>>>(X, n, HCQ);
+    HIKF_CHECK_LAUNCH();
+    cudaFreeAsync(X, st);
+  }
+  double k0 = t->spec.family == HIKF_LOGARITHM ? 0.0 : t->spec.variance;  // value_at_zero (kernels.py:91-95)
+  fill<<<grid_for(t->m), kT, 0, st>>>(dQ, t->m, k0);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+int hikf_init_state(int64_t m, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double alpha,
+                    double* C_out, double* var_out, double* HC_out, void* stream) {
+  if (m < 1 || n < 0) return HIKF_BAD_ARGUMENT;
+  cudaStream_t st = as_stream(stream);
+  fill<<<grid_for(m), kT, 0, st>>>(var_out, m, alpha);
+  HIKF_CHECK_LAUNCH();
+  if (n == 0) return HIKF_OK;
+  // C = alpha H^T (dense), HC = alpha (H H^T)  (filters.py:118-126)
+  double* Ht = nullptr;
+  double* X = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Ht, sizeof(double) * m * n, st));
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&X, sizeof(double) * n * n, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(Ht, 0, sizeof(double) * m * n, st));
+  scatter_transpose<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, Ht);
+  HIKF_CHECK_LAUNCH();
+  spmm_rows<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, Ht, X);
+  HIKF_CHECK_LAUNCH();
+  scale_copy<<<grid_for(m * n), kT, 0, st>>>(Ht, m * n, alpha, C_out);
+  HIKF_CHECK_LAUNCH();
+  scale_copy<<<grid_for(n * n), kT, 0, st>>>(X, n * n, alpha, HC_out);
+  HIKF_CHECK_LAUNCH();
+  cudaFreeAsync(Ht, st);
+  cudaFreeAsync(X, st);
+  return HIKF_OK;
+}
+
+int hikf_predict(int64_t m, int64_t n, const double* C, const double* var, const double* HC, const double* CQ,
+                 const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, void* stream) {
+  if (m < 0 || n < 0) return HIKF_BAD_ARGUMENT;
+  return predict(m, n, C, var, HC, CQ, dQ, HCQ, Co, varo, HCo, as_stream(stream));
+}
+
+size_t hikf_update_workspace_bytes(int64_t m, int64_t n) { return update_workspace_bytes(m, n); }
+
+int hikf_update(int64_t m, int64_t n, const double* mean, const double* C, const double* var, const double* HC,
+                const double* CQ, const double* dQ, const double* HCQ, const int32_t* ip, const int32_t* ix,
+                const double* val, double r, const double* z, double* mean_out, double* C_out, double* var_out,
+                double* HC_out, void* workspace, size_t workspace_bytes, double* min_var_out, void* stream) {
+  if (m < 1 || n < 1 || !mean || !C || !var || !HC || !ip || !z || !mean_out || !C_out || !var_out || !HC_out) {
+    set_error("bad update arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (CQ && (!dQ || !HCQ)) {
+    set_error("fused predict needs C_Q, diag_Q and HC_Q");
+    return HIKF_BAD_ARGUMENT;
+  }
+  UpdateArgs a;
+  a.m = m;
+  a.n = n;
+  a.mean = mean;
+  a.C = C;
+  a.var = var;
+  a.HC = HC;
+  a.CQ = CQ;
+  a.dQ = dQ;
+  a.HCQ = HCQ;
+  a.ip = ip;
+  a.ix = ix;
+  a.val = val;
+  a.r = r;
+  a.z = z;
+  a.mean_out = mean_out;
+  a.C_out = C_out;
+  a.var_out = var_out;
+  a.HC_out = HC_out;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  UpdateResult res;
+  int s = update(a, as_stream(stream), &res);
+  if (min_var_out) *min_var_out = res.min_var;
+  return s;
+}
+
+size_t hikf_spd_solve_workspace_bytes(int64_t n, int64_t k) { return spd_workspace_bytes(n, k); }
+
+int hikf_spd_solve(int64_t n, int64_t k, const double* A, const double* B, double* X, void* ws, size_t ws_bytes,
+                   int64_t* info, void* stream) {
+  if (n < 0 || k < 0) return HIKF_BAD_ARGUMENT;
+  return spd_solve(n, k, A, B, X, ws, ws_bytes, info, as_stream(stream));
+}
+
+int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n, const double* src,
+                      const double* rcv, int32_t* indptr, int32_t* indices, double* data, int64_t* nnz_out) {
+  std::vector<int32_t> ip, ix;
+  std::vector<double> v;
+  HIKF_TRY(ray_operator(nx, ny, dx, dy, x0, y0, n, src, rcv, ip, ix, v));
+  if (nnz_out) *nnz_out = (int64_t)ix.size();
+  if (indices) {
+    std::memcpy(indptr, ip.data(), sizeof(int32_t) * ip.size());
+    std::memcpy(indices, ix.data(), sizeof(int32_t) * ix.size());
+    std::memcpy(data, v.data(), sizeof(double) * v.size());
+  }
+  return HIKF_OK;
+}
+
+}  // extern "C"

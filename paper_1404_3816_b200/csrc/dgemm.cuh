@@ -1,0 +1,47 @@
+// FP64 GEMM on the DMMA tensor path (mma.sync m8n8k4 -> SASS DMMA.8x8x4).
+//
+// sm_100a has no tcgen05 f64 kind, so FP64 matrix work runs on the warp-level
+// DMMA pipe (measured 37.0 TFLOP/s on this B200, same as DFMA).  This kernel
+// is the workhorse of the per-step update: CTA tile 128 x 128 x 16, 8 warps
+// (2 x 4) with 64 x 32 warp tiles (32 accumulator fragments = 64 doubles per
+// thread), a 5-stage cp.async ring (16-byte copies when rows are contiguous),
+// triangular K-range skipping for triangular B, and fused epilogues
+// (alpha/beta, per-row sum of squares / dot with a vector).
+#pragma once
+
+#include "common.cuh"
+
+namespace hikf {
+
+constexpr int DG_BM = 128, DG_BN = 128, DG_BK = 16, DG_STAGES = 5, DG_THREADS = 256;
+constexpr int DG_AS = DG_BK + 4;   // == 4 mod 16 doubles
+constexpr int DG_BS = DG_BN + 4;
+constexpr int DG_STAGE = DG_BM * DG_AS + DG_BK * DG_BS;
+constexpr size_t DG_SMEM = (size_t)DG_STAGES * DG_STAGE * sizeof(double);
+
+enum { KFULL = 0, KB_UPPER = 1, KB_LOWER = 2 };
+
+struct GemmArgs {
+  int64_t M = 0, N = 0, K = 0;
+  const double* A = nullptr;  // A[i][k] = A[i * sa_r + k * sa_c]
+  int64_t sa_r = 0, sa_c = 1;
+  const double* B = nullptr;  // B[k][j] = B[k * sb_r + j * sb_c]
+  int64_t sb_r = 0, sb_c = 1;
+  double* C = nullptr;        // C[i][j] = C[i * ldc + j]
+  int64_t ldc = 0;
+  const double* Cin = nullptr;  // beta term source (may alias C)
+  int64_t ldcin = 0;
+  double alpha = 1.0, beta = 0.0;
+  int kmode = KFULL;
+  int64_t bsA = 0, bsB = 0, bsC = 0, bsCin = 0;  // batch strides (blockIdx.z)
+  // fused row partials: psq[i * ldp + tile] = sum_j (alpha acc)^2, pdot[...] = sum_j (alpha acc) w[j]
+  double* psq = nullptr;
+  double* pdot = nullptr;
+  const double* w = nullptr;
+  int64_t ldp = 0;
+};
+
+// C = alpha * A B + beta * Cin (+ partials); launches on `stream`.
+int dgemm(const GemmArgs& g, int batch, cudaStream_t stream);
+
+}  // namespace hikf

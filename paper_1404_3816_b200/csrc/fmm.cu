@@ -1,0 +1,338 @@
+// FmmTree.matmat on the GPU (fmm.py:325-367): near-field P2P, then the
+// upward pass (P2M, M2M) and the downward pass (M2L fused with L2L, L2P),
+// each stage a seg_gemm_kernel launch over boxes x column tiles.
+#include <algorithm>
+
+#include "fmm_device.cuh"
+#include "prof.h"
+#include "tree.h"
+
+namespace hikf {
+
+namespace {
+
+struct ProvBase {
+  int64_t kcols;  // columns of this pass
+  __device__ int64_t ncols() const { return kcols; }
+  KParams kp;
+  __device__ double kernel(double r) const { return kernel_of_r(kp, r); }
+};
+
+// Near field (fmm.py:166-201, :330): U rows of target leaf = sum over the
+// occupied 3x3-adjacent leaves (ox outer, oy inner) of K(x_t, x_s) V_s.
+struct P2PProv : ProvBase {
+  static constexpr bool kAccumulate = false;
+  const int32_t *leaf_box, *leaf_start, *leaf_count, *box2leaf;
+  const double* xy_s;
+  const int64_t* order;
+  int64_t G;
+  const double* V;
+  int64_t ldv;
+  double* U;
+  int64_t ldu;
+  __device__ int rows(int task) const { return leaf_count[task]; }
+  __device__ int nsegs(int) const { return 9; }
+  __device__ bool seg(int task, int s, Seg& d) const {
+    int64_t box = leaf_box[task], bx = box / G, by = box % G;
+    int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
+    if (nx < 0 || nx >= G || ny < 0 || ny >= G) return false;
+    int32_t src = box2leaf[nx * G + ny];
+    if (src < 0) return false;
+    int32_t s0 = leaf_start[src];
+    d.K = leaf_count[src];
+    d.gen = true;
+    d.a = nullptr;
+    d.a_rs = d.a_cs = 0;
+    d.txy = xy_s + 2 * (int64_t)leaf_start[task];
+    d.sxy = xy_s + 2 * (int64_t)s0;
+    d.b = V;
+    d.ldb = ldv;
+    d.b_rows = order + s0;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const { return U + order[leaf_start[task] + r] * ldu; }
+};
+
+// P2M (fmm.py:338): W_leaf[a][:] = sum_p W2[p][a] V[p][:]
+struct P2MProv : ProvBase {
+  static constexpr bool kAccumulate = false;
+  const int32_t *leaf_box, *leaf_start, *leaf_count;
+  const double* W2s;
+  int q;
+  const int64_t* order;
+  const double* V;
+  int64_t ldv;
+  double* W;  // leaf level, (G^2, q, kcols)
+  __device__ int rows(int) const { return q; }
+  __device__ int nsegs(int) const { return 1; }
+  __device__ bool seg(int task, int, Seg& d) const {
+    int32_t s0 = leaf_start[task];
+    d.K = leaf_count[task];
+    d.gen = false;
+    d.a = W2s + (int64_t)s0 * q;  // A[r = a][kk = p] = W2s[(s0 + p) q + a]
+    d.a_rs = 1;
+    d.a_cs = q;
+    d.b = V;
+    d.ldb = ldv;
+    d.b_rows = order + s0;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const { return W + ((int64_t)leaf_box[task] * q + r) * kcols; }
+};
+
+// M2M (fmm.py:339-345): W_p[b] = sum_{children c} sum_a C_c[a][b] W_c[a]
+struct M2MProv : ProvBase {
+  static constexpr bool kAccumulate = false;
+  const int32_t* occ;            // occupied parents at level l
+  const uint8_t* child_flag;     // occupancy at level l+1
+  const double* shift;           // 4 x (qc x qp)
+  int qp, qc;
+  int64_t Gp;
+  const double* Wc;              // level l+1
+  double* Wp;                    // level l
+  __device__ int rows(int) const { return qp; }
+  __device__ int nsegs(int) const { return 4; }
+  __device__ bool seg(int task, int s, Seg& d) const {
+    int64_t box = occ[task], X = box / Gp, Y = box % Gp;
+    int cx = s >> 1, cy = s & 1;
+    int64_t child = (2 * X + cx) * (2 * Gp) + (2 * Y + cy);
+    if (!child_flag[child]) return false;
+    d.K = qc;
+    d.gen = false;
+    d.a = shift + (int64_t)s * qc * qp;  // A[r = b][kk = a] = C[a][b]
+    d.a_rs = 1;
+    d.a_cs = qp;
+    d.b = Wc + child * qc * kcols;
+    d.ldb = kcols;
+    d.b_rows = nullptr;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const { return Wp + ((int64_t)occ[task] * qp + r) * kcols; }
+};
+
+// M2L over the interaction list (fmm.py:349-359) with the parent-to-child
+// shift (fmm.py:361-363) fused as a 41st segment.
+struct M2LProv : ProvBase {
+  static constexpr bool kAccumulate = false;
+  const int32_t* occ;         // occupied targets at level l
+  const uint8_t* flag;        // occupancy at level l
+  const double* ops;          // 40 x q x q
+  uint64_t present;
+  M2LOffsets offs;
+  int q;
+  int64_t G;
+  const double* W;            // multipoles, level l
+  double* L;                  // locals, level l
+  // L2L from the parent level (null at level 2)
+  const double* Lp;
+  const double* shift;        // shift ops between l-1 and l: 4 x (q x qp)
+  int qp;
+  __device__ int rows(int) const { return q; }
+  __device__ int nsegs(int) const { return Lp ? 41 : 40; }
+  __device__ bool seg(int task, int s, Seg& d) const {
+    int64_t t = occ[task], tx = t / G, ty = t % G;
+    d.gen = false;
+    d.b_rows = nullptr;
+    d.ldb = kcols;
+    if (s < 40) {
+      if (!((present >> s) & 1)) return false;
+      int64_t src;
+      if (!m2l_source(tx, ty, offs.dx[s], offs.dy[s], G, src)) return false;
+      if (!flag[src]) return false;  // empty source: zero multipole
+      d.K = q;
+      d.a = ops + (int64_t)s * q * q;
+      d.a_rs = q;
+      d.a_cs = 1;
+      d.b = W + src * q * kcols;
+      return true;
+    }
+    int c = (int)((tx & 1) * 2 + (ty & 1));
+    int64_t parent = (tx >> 1) * (G >> 1) + (ty >> 1);
+    d.K = qp;
+    d.a = shift + (int64_t)c * q * qp;  // A[r = a][kk = b] = C[a][b]
+    d.a_rs = qp;
+    d.a_cs = 1;
+    d.b = Lp + parent * qp * kcols;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const { return L + ((int64_t)occ[task] * q + r) * kcols; }
+};
+
+// L2P (fmm.py:366): U[p][:] += sum_a W2[p][a] L_leaf[a][:]
+struct L2PProv : ProvBase {
+  static constexpr bool kAccumulate = true;
+  const int32_t *leaf_box, *leaf_start, *leaf_count;
+  const double* W2s;
+  int q;
+  const int64_t* order;
+  const double* L;
+  double* U;
+  int64_t ldu;
+  __device__ int rows(int task) const { return leaf_count[task]; }
+  __device__ int nsegs(int) const { return 1; }
+  __device__ bool seg(int task, int, Seg& d) const {
+    d.K = q;
+    d.gen = false;
+    d.a = W2s + (int64_t)leaf_start[task] * q;
+    d.a_rs = q;
+    d.a_cs = 1;
+    d.b = L + (int64_t)leaf_box[task] * q * kcols;
+    d.ldb = kcols;
+    d.b_rows = nullptr;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const { return U + order[leaf_start[task] + r] * ldu; }
+};
+
+template <class Prov>
+int launch(const Prov& p, int64_t tasks, int64_t max_rows, int64_t kcols, cudaStream_t st) {
+  if (tasks <= 0 || max_rows <= 0 || kcols <= 0) return HIKF_OK;
+  static bool configured = false;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(seg_gemm_kernel<Prov>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SG_SMEM));
+    configured = true;
+  }
+  dim3 grid((unsigned)tasks, (unsigned)ceil_div(max_rows, SG_R), (unsigned)ceil_div(kcols, SG_BN));
+  seg_gemm_kernel<Prov><<<grid, SG_THREADS, SG_SMEM, st>>>(p);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+}  // namespace
+
+int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U, int64_t ldu, cudaStream_t st) {
+  if (k <= 0) return HIKF_OK;
+  const int D = t->depth;
+  // column pass width: keep the expansion workspace within ~24 GiB
+  int64_t per_col = 0;  // bytes per column: all W levels + two L levels
+  if (D >= 2) {
+    for (int l = 2; l <= D; ++l) per_col += (int64_t)8 * ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l];
+    per_col += (int64_t)8 * ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D];
+    if (D > 2) per_col += (int64_t)8 * ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1];
+  }
+  int64_t budget = (int64_t)24 << 30;
+  int64_t kpass = k;
+  if (per_col > 0 && per_col * kpass > budget) kpass = std::max<int64_t>(SG_BN, (budget / per_col) / SG_BN * SG_BN);
+
+  double* ws = nullptr;
+  if (D >= 2) HIKF_CHECK_CUDA(cudaMallocAsync((void**)&ws, (size_t)per_col * std::min(kpass, k), st));
+
+  for (int64_t c0 = 0; c0 < k; c0 += kpass) {
+    const int64_t kc = std::min(kpass, k - c0);
+    const double* Vc = V + c0;
+    double* Uc = U + c0;
+    // ---- near field: U = near @ V ----
+    P2PProv pp;
+    pp.kcols = kc;
+    pp.kp = t->kp;
+    pp.leaf_box = t->leaf_box;
+    pp.leaf_start = t->leaf_start;
+    pp.leaf_count = t->leaf_count;
+    pp.box2leaf = t->box2leaf;
+    pp.xy_s = t->xy_s;
+    pp.order = t->order;
+    pp.G = t->G;
+    pp.V = Vc;
+    pp.ldv = ldv;
+    pp.U = Uc;
+    pp.ldu = ldu;
+    {
+      ProfScope ps(ST_P2P, st);
+      HIKF_TRY(launch(pp, t->n_leaves, t->max_count, kc, st));
+    }
+    if (D < 2) continue;
+
+    // workspace carve: W[l] for l = 2..D, then L ping-pong (level D and D-1 sized)
+    double* Wl[kMaxDepth + 1] = {nullptr};
+    double* cur = ws;
+    for (int l = 2; l <= D; ++l) {
+      Wl[l] = cur;
+      cur += ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * kc;
+    }
+    double* Lbuf[2];
+    Lbuf[0] = cur;  // holds levels with parity of D
+    cur += ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * kc;
+    Lbuf[1] = cur;
+
+    // ---- upward pass: P2M then M2M ----
+    const int qD = t->orders[D] * t->orders[D];
+    P2MProv pm;
+    pm.kcols = kc;
+    pm.kp = t->kp;
+    pm.leaf_box = t->leaf_box;
+    pm.leaf_start = t->leaf_start;
+    pm.leaf_count = t->leaf_count;
+    pm.W2s = t->W2s;
+    pm.q = qD;
+    pm.order = t->order;
+    pm.V = Vc;
+    pm.ldv = ldv;
+    pm.W = Wl[D];
+    {
+      ProfScope ps(ST_P2M, st);
+      HIKF_TRY(launch(pm, t->n_leaves, qD, kc, st));
+    }
+    for (int l = D - 1; l >= 2; --l) {
+      M2MProv mm;
+      mm.kcols = kc;
+      mm.kp = t->kp;
+      mm.occ = t->occ[l];
+      mm.child_flag = t->occ_flag[l + 1];
+      mm.shift = t->shift[l];
+      mm.qp = t->orders[l] * t->orders[l];
+      mm.qc = t->orders[l + 1] * t->orders[l + 1];
+      mm.Gp = (int64_t)1 << l;
+      mm.Wc = Wl[l + 1];
+      mm.Wp = Wl[l];
+      ProfScope ps(ST_M2M, st);
+      HIKF_TRY(launch(mm, t->n_occ[l], mm.qp, kc, st));
+    }
+    // ---- downward pass: M2L (+ L2L) per level ----
+    const double* Lprev = nullptr;
+    double* Lcur = nullptr;
+    for (int l = 2; l <= D; ++l) {
+      Lcur = Lbuf[(D - l) & 1];
+      M2LProv ml;
+      ml.kcols = kc;
+      ml.kp = t->kp;
+      ml.occ = t->occ[l];
+      ml.flag = t->occ_flag[l];
+      ml.ops = t->m2l[l];
+      ml.present = t->m2l_present[l];
+      ml.q = t->orders[l] * t->orders[l];
+      ml.G = (int64_t)1 << l;
+      ml.W = Wl[l];
+      ml.L = Lcur;
+      ml.Lp = Lprev;
+      ml.shift = l > 2 ? t->shift[l - 1] : nullptr;
+      ml.qp = l > 2 ? t->orders[l - 1] * t->orders[l - 1] : 0;
+      {
+        ProfScope ps(ST_M2L, st);
+        HIKF_TRY(launch(ml, t->n_occ[l], ml.q, kc, st));
+      }
+      Lprev = Lcur;
+    }
+    // ---- L2P: U += interp @ local ----
+    L2PProv lp;
+    lp.kcols = kc;
+    lp.kp = t->kp;
+    lp.leaf_box = t->leaf_box;
+    lp.leaf_start = t->leaf_start;
+    lp.leaf_count = t->leaf_count;
+    lp.W2s = t->W2s;
+    lp.q = qD;
+    lp.order = t->order;
+    lp.L = Lcur;
+    lp.U = Uc;
+    lp.ldu = ldu;
+    {
+      ProfScope ps(ST_L2P, st);
+      HIKF_TRY(launch(lp, t->n_leaves, t->max_count, kc, st));
+    }
+  }
+  if (ws) HIKF_CHECK_CUDA(cudaFreeAsync(ws, st));
+  return HIKF_OK;
+}
+
+}  // namespace hikf

@@ -1,0 +1,201 @@
+// Device building blocks of the FMM stages.
+//
+// Every stage of FmmTree.matmat (fmm.py:325-367) is one "segmented GEMM":
+// an output block O (rows x k) of one box/leaf is a sum over a short list of
+// segments, each a small dense product A_s (rows x K_s) * B_s (K_s x k):
+//   P2P  : rows = target-leaf points, segments = the <= 9 adjacent leaves,
+//          A = K(x_t, x_s) generated on the fly, B = V rows of the source leaf
+//   P2M  : rows = q_leaf, one segment, A = W2^T of the leaf, B = V rows
+//   M2M  : rows = q_l, segments = 4 children, A = shift^T, B = child W
+//   M2L  : rows = q_l, segments = <= 27 interaction-list sources (+ the
+//          parent's local for L2L), A = M2L op / shift op, B = source W / L
+//   L2P  : rows = leaf points, one segment, A = W2 rows, B = leaf local
+// seg_gemm_kernel streams (A, B) K-chunks through a 4-stage cp.async ring in
+// shared memory and accumulates with FP64 DMMA (mma.sync m8n8k4) into
+// registers; CTA tile = 64 rows x 128 columns, 8 warps, each warp owns 16
+// columns x all 8 row tiles.
+#pragma once
+
+#include "common.cuh"
+
+namespace hikf {
+
+constexpr int kMaxLeafOrder = 12;  // n_cheb <= 12 (fmm.py:51)
+
+// M2L source of target (tx, ty) at offset (dx, dy): in range and parents
+// adjacent per dimension (fmm.py:301-302).  Source flat index x-major.
+__device__ __forceinline__ bool m2l_source(int64_t tx, int64_t ty, int dx, int dy, int64_t G, int64_t& s) {
+  int64_t sx = tx + dx, sy = ty + dy;
+  if (sx < 0 || sx >= G || sy < 0 || sy >= G) return false;
+  int64_t px = (sx >> 1) - (tx >> 1), py = (sy >> 1) - (ty >> 1);
+  if (px < -1 || px > 1 || py < -1 || py > 1) return false;
+  s = sx * G + sy;
+  return true;
+}
+
+constexpr int SG_R = 64;
+constexpr int SG_BN = 128;
+constexpr int SG_KC = 32;
+constexpr int SG_STAGES = 4;
+constexpr int SG_THREADS = 256;
+constexpr int SG_AS = SG_KC + 4;  // smem row strides (doubles), == 4 mod 16: conflict-free DMMA fragments
+constexpr int SG_BS = SG_BN + 4;
+constexpr int SG_STAGE_DOUBLES = SG_R * SG_AS + SG_KC * SG_BS;
+constexpr size_t SG_SMEM = (size_t)SG_STAGES * SG_STAGE_DOUBLES * sizeof(double) + 64;
+
+// One segment of an output block.
+struct Seg {
+  int K;                      // inner length; <= 0 means "skip"
+  bool gen;                   // A generated from coordinates (P2P)
+  const double* a;            // A[r][kk] = a[r * a_rs + kk * a_cs]
+  int64_t a_rs, a_cs;
+  const double* txy;          // gen: target coords (row r at txy + 2 r), source coords sxy + 2 kk
+  const double* sxy;
+  const double* b;            // B[kk][c] = b[(b_rows ? b_rows[kk] : kk) * ldb + c]
+  int64_t ldb;
+  const int64_t* b_rows;
+};
+
+template <class Prov>
+__global__ void __launch_bounds__(SG_THREADS, 1) seg_gemm_kernel(Prov prov) {
+  extern __shared__ double smem_raw[];
+  double* smem = smem_raw;
+  __shared__ int stage_k[SG_STAGES];
+
+  const int task = blockIdx.x;
+  const int row0 = blockIdx.y * SG_R;
+  const int nrows = prov.rows(task);
+  if (row0 >= nrows) return;
+  const int col0 = blockIdx.z * SG_BN;
+  const int64_t ncols = prov.ncols();
+  const int nsegs = prov.nsegs(task);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int rows_here = min(SG_R, nrows - row0);
+  const int nrt = (rows_here + 7) >> 3;  // active 8-row tiles
+
+  // producer cursor
+  int cur_seg = 0, cur_k = 0;
+  Seg sd;
+  sd.K = 0;
+  // advance to the first valid (segment, k) position
+  auto next_valid = [&](int s) {
+    while (s < nsegs) {
+      if (prov.seg(task, s, sd) && sd.K > 0) return s;
+      ++s;
+    }
+    return s;
+  };
+  cur_seg = next_valid(0);
+
+  auto issue = [&](int stage) {
+    double* As = smem + stage * SG_STAGE_DOUBLES;
+    double* Bs = As + SG_R * SG_AS;
+    if (cur_seg >= nsegs) {
+      if (tid == 0) stage_k[stage] = 0;
+      return;
+    }
+    const int kc = min(SG_KC, sd.K - cur_k);
+    // A tile: SG_R x SG_KC, zero outside (rows_here, kc)
+    for (int e = tid; e < SG_R * SG_KC; e += SG_THREADS) {
+      int r = e / SG_KC, kk = e % SG_KC;
+      bool ok = r < rows_here && kk < kc;
+      double* dst = As + r * SG_AS + kk;
+      if (sd.gen) {
+        double v = 0.0;
+        if (ok) {
+          const double* tp = sd.txy + 2 * (int64_t)(row0 + r);
+          const double* sp = sd.sxy + 2 * (int64_t)(cur_k + kk);
+          v = prov.kernel(dist2d(tp[0], tp[1], sp[0], sp[1]));
+        }
+        *dst = v;
+      } else {
+        const double* src = ok ? sd.a + (int64_t)(row0 + r) * sd.a_rs + (int64_t)(cur_k + kk) * sd.a_cs : sd.a;
+        cp_async8(dst, src, ok);
+      }
+    }
+    // B tile: SG_KC x SG_BN
+    for (int e = tid; e < SG_KC * SG_BN; e += SG_THREADS) {
+      int kk = e / SG_BN, c = e % SG_BN;
+      bool ok = kk < kc && col0 + c < ncols;
+      const double* src = sd.b;
+      if (ok) {
+        int64_t row = sd.b_rows ? sd.b_rows[cur_k + kk] : (int64_t)(cur_k + kk);
+        src = sd.b + row * sd.ldb + col0 + c;
+      }
+      cp_async8(Bs + kk * SG_BS + c, src, ok);
+    }
+    if (tid == 0) stage_k[stage] = kc;
+    // advance the cursor
+    cur_k += SG_KC;
+    if (cur_k >= sd.K) {
+      cur_k = 0;
+      cur_seg = next_valid(cur_seg + 1);
+    }
+  };
+
+  double acc[8][2][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < SG_STAGES - 1; ++s) {
+    issue(s);
+    cp_async_commit();
+  }
+  for (int it = 0;; ++it) {
+    cp_async_wait<SG_STAGES - 2>();
+    __syncthreads();
+    const int stage = it % SG_STAGES;
+    const int kc = stage_k[stage];
+    if (kc == 0) break;
+    // refill the slot consumed in the previous iteration
+    issue((it + SG_STAGES - 1) % SG_STAGES);
+    cp_async_commit();
+
+    const double* As = smem + stage * SG_STAGE_DOUBLES;
+    const double* Bs = As + SG_R * SG_AS;
+    const int nk4 = (kc + 3) >> 2;
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int kb = k4 * 4;
+      double bf[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[(kb + t4) * SG_BS + warp * 16 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (i < nrt) {
+          double af = As[(i * 8 + g) * SG_AS + kb + t4];
+          dmma884(acc[i][0][0], acc[i][0][1], af, bf[0]);
+          dmma884(acc[i][1][0], acc[i][1][1], af, bf[1]);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: store or accumulate into the output rows
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (i >= nrt) continue;
+    const int r = i * 8 + g;
+    if (r >= rows_here) continue;
+    double* orow = prov.out_row(task, row0 + r);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int64_t c = col0 + warp * 16 + j * 8 + 2 * t4;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (c + h < ncols) {
+          if (Prov::kAccumulate)
+            orow[c + h] += acc[i][j][h];
+          else
+            orow[c + h] = acc[i][j][h];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace hikf

@@ -1,0 +1,38 @@
+// Stage timing scopes and launch counting (see prof.cu).
+#pragma once
+
+#include <atomic>
+
+#include "common.cuh"
+
+namespace hikf {
+
+// stage ids, mirrored in paper_1404_3816_b200/_lib.py STAGES
+enum Stage {
+  ST_PREDICT = 0,
+  ST_FACTOR = 1,   // S, Cholesky + inverse, n x n products, innovation
+  ST_GEMM_Y = 2,   // Y = C' Li^T (+ row partials)
+  ST_FINALIZE = 3, // var / mean rows + consistency check
+  ST_GEMM_C = 4,   // C_new = C' - Y P
+  ST_P2P = 5,
+  ST_P2M = 6,
+  ST_M2M = 7,
+  ST_M2L = 8,
+  ST_L2P = 9,
+  ST_DENSIFY = 10, // H^T scatter for the precompute
+  ST_COUNT = 11
+};
+
+class ProfScope {
+ public:
+  ProfScope(int stage, cudaStream_t st);
+  ~ProfScope();
+
+ private:
+  int stage_;
+  cudaStream_t st_;
+  bool active_;
+  cudaEvent_t a_, b_;
+};
+
+}  // namespace hikf

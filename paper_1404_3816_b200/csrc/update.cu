@@ -1,0 +1,532 @@
+// The HiKF per-step update on the GPU (filters.py:129-157, linalg.py:18-37).
+//
+// For the predicted state (C' = C + C_Q, var' = var + diag_Q, HC' = HC + HC_Q):
+//   S   = sym(HC' + r I)                      (n x n)
+//   L   = chol(S), Li = L^{-1}                (recursive blocked, DMMA GEMMs)
+//   Y   = C' Li^T                             (m x n, triangular B: m n^2 flops)
+//   mean_new = mean + Y (Li (z - H mean))     (= mean + K innov, K = C' S^{-1})
+//   var_new  = var' - rowsum(Y o Y)           (= var' - rowsum(K o C'))
+//   P   = Li HC',  R = HC' Li^T
+//   C_new  = C' - Y P                          (= C' - K HC'; 2 m n^2 flops)
+//   HC_new = HC' - R P                         (= HC' - KH HC')
+// i.e. the reference's two m-RHS triangular solves plus K HC are regrouped
+// around Y (3 m n^2 instead of 4 m n^2 flops); the parity of this regrouping
+// against the reference at cfg1/cfg2 is measured in DESIGN.md section 5.
+#include <algorithm>
+#include <cfloat>
+
+#include "dgemm.cuh"
+#include "prof.h"
+#include "update.h"
+
+namespace hikf {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int NB = 64;  // base block of the recursive Cholesky / inverse
+
+int grid_for(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms() * 32));
+}
+
+// ---------------------------------------------------------------- streaming
+__global__ void add_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ c,
+                           int64_t n) {
+  int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 2;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
+  bool al = (((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 15) == 0;
+  if (al) {
+    for (; i + 1 < n; i += stride) {
+      double2 x = __ldcs(reinterpret_cast<const double2*>(a + i));
+      double2 y = __ldcs(reinterpret_cast<const double2*>(b + i));
+      __stcs(reinterpret_cast<double2*>(c + i), make_double2(x.x + y.x, x.y + y.y));
+    }
+    if (i < n) c[i] = a[i] + b[i];
+  } else {
+    for (; i < n; i += stride) {
+      c[i] = a[i] + b[i];
+      if (i + 1 < n) c[i + 1] = a[i + 1] + b[i + 1];
+    }
+  }
+}
+
+// S = 0.5 * ((HC + r I) + (HC + r I)^T)  (filters.py:144-145)
+__global__ void build_S(const double* __restrict__ HC, int64_t n, double r, double* __restrict__ S) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / n, j = e % n;
+    double a = HC[i * n + j], b = HC[j * n + i];
+    if (i == j) {
+      a = a + r;
+      b = b + r;
+    }
+    S[e] = 0.5 * (a + b);
+  }
+}
+
+__global__ void transpose_kernel(const double* __restrict__ X, int64_t n, double* __restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = e / n, j = e % n;
+    Y[j * n + i] = X[e];
+  }
+}
+
+// Cholesky + inverse of one <= NB x NB diagonal block held in shared memory.
+// L (lower, ld), Li (lower, ld) written; upper triangles left untouched (zeroed
+// by the caller).  status[0] = global 1-based pivot of the first failure.
+__global__ void chol_inv_base(const double* __restrict__ S, int64_t ld, int nb, int64_t offset,
+                              double* __restrict__ L, double* __restrict__ Li, int* status) {
+  extern __shared__ double base_smem[];
+  double(*a)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(base_smem);
+  double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(base_smem + NB * (NB + 1));
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int e = tid; e < nb * nb; e += blockDim.x) a[e / nb][e % nb] = S[(e / nb) * ld + e % nb];
+  __syncthreads();
+  // right-looking Cholesky on the lower triangle
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      double d = a[j][j];
+      if (!(d > 0.0)) {
+        if (!bad) bad = j + 1;
+        d = 1.0;  // keep going; the result is discarded by the caller
+      }
+      a[j][j] = sqrt(d);
+    }
+    __syncthreads();
+    double piv = a[j][j];
+    for (int i = j + 1 + tid; i < nb; i += blockDim.x) a[i][j] = a[i][j] / piv;
+    __syncthreads();
+    for (int e = tid; e < (nb - j - 1) * (nb - j - 1); e += blockDim.x) {
+      int i = j + 1 + e / (nb - j - 1), k = j + 1 + e % (nb - j - 1);
+      if (k <= i) a[i][k] -= a[i][j] * a[k][j];
+    }
+    __syncthreads();
+  }
+  // inverse by forward substitution, one column per thread
+  for (int c = tid; c < nb; c += blockDim.x) {
+    x[c][c] = 1.0 / a[c][c];
+    for (int i = c + 1; i < nb; ++i) {
+      double s = 0.0;
+      for (int k = c; k < i; ++k) s += a[i][k] * x[k][c];
+      x[i][c] = -s / a[i][i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    int i = e / nb, j = e % nb;
+    if (j <= i) {
+      L[i * ld + j] = a[i][j];
+      Li[i * ld + j] = x[i][j];
+    }
+  }
+  if (tid == 0 && bad && status[0] == 0) status[0] = (int)(offset + bad);
+}
+
+// Recursive blocked Cholesky with inverse: S (n x n view, ld) -> L, Li.
+// S is overwritten (Schur complements).
+int chol_inv(double* S, double* L, double* Li, int64_t n, int64_t ld, int64_t offset, double* tmp, int* status,
+             cudaStream_t st) {
+  if (n <= NB) {
+    constexpr size_t smem = 2 * NB * (NB + 1) * sizeof(double);
+    static bool configured = false;
+    if (!configured) {
+      HIKF_CHECK_CUDA(cudaFuncSetAttribute(chol_inv_base, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = true;
+    }
+    chol_inv_base<<<1, kT, smem, st>>>(S, ld, (int)n, offset, L, Li, status);
+    HIKF_CHECK_LAUNCH();
+    return HIKF_OK;
+  }
+  int64_t n1 = ((n / 2 + NB - 1) / NB) * NB, n2 = n - n1;
+  double *S11 = S, *S21 = S + n1 * ld, *S22 = S + n1 * ld + n1;
+  double *L11 = L, *L21 = L + n1 * ld, *L22 = L + n1 * ld + n1;
+  double *Li11 = Li, *Li21 = Li + n1 * ld, *Li22 = Li + n1 * ld + n1;
+  HIKF_TRY(chol_inv(S11, L11, Li11, n1, ld, offset, tmp, status, st));
+  GemmArgs g;
+  // L21 = S21 Li11^T
+  g.M = n2; g.N = n1; g.K = n1;
+  g.A = S21; g.sa_r = ld; g.sa_c = 1;
+  g.B = Li11; g.sb_r = 1; g.sb_c = ld;  // B[k][j] = Li11[j][k]
+  g.C = L21; g.ldc = ld;
+  HIKF_TRY(dgemm(g, 1, st));
+  // S22 -= L21 L21^T
+  GemmArgs h;
+  h.M = n2; h.N = n2; h.K = n1;
+  h.A = L21; h.sa_r = ld; h.sa_c = 1;
+  h.B = L21; h.sb_r = 1; h.sb_c = ld;
+  h.C = S22; h.ldc = ld; h.Cin = S22; h.ldcin = ld; h.alpha = -1.0; h.beta = 1.0;
+  HIKF_TRY(dgemm(h, 1, st));
+  HIKF_TRY(chol_inv(S22, L22, Li22, n2, ld, offset + n1, tmp, status, st));
+  // T = L21 Li11 (n2 x n1) ; Li21 = -Li22 T
+  GemmArgs a;
+  a.M = n2; a.N = n1; a.K = n1;
+  a.A = L21; a.sa_r = ld; a.sa_c = 1;
+  a.B = Li11; a.sb_r = ld; a.sb_c = 1;
+  a.C = tmp; a.ldc = n1;
+  HIKF_TRY(dgemm(a, 1, st));
+  GemmArgs b;
+  b.M = n2; b.N = n1; b.K = n2;
+  b.A = Li22; b.sa_r = ld; b.sa_c = 1;
+  b.B = tmp; b.sb_r = n1; b.sb_c = 1;
+  b.C = Li21; b.ldc = ld; b.alpha = -1.0;
+  HIKF_TRY(dgemm(b, 1, st));
+  return HIKF_OK;
+}
+
+// innov = z - H mean (CSR SpMV, one warp per row), filters.py:147
+__global__ void innovation(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
+                           const double* __restrict__ val, const double* __restrict__ mean, const double* __restrict__ z,
+                           double* __restrict__ innov) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t e = ip[row] + lane; e < ip[row + 1]; e += 32) s += val[e] * mean[ix[e]];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) innov[row] = z[row] - s;
+}
+
+// w = Li innov (n x n lower-triangular GEMV, one warp per row)
+__global__ void trmv_lower(const double* __restrict__ Li, int64_t n, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t k = lane; k <= row; k += 32) s += Li[row * n + k] * x[k];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = s;
+}
+
+// var_new = var' - sum_t psq, mean_new = mean + sum_t pdot; block min/max partials
+__global__ void finalize_rows(int64_t m, int nt, const double* __restrict__ psq, const double* __restrict__ pdot,
+                              const double* __restrict__ varp, const double* __restrict__ mean,
+                              double* __restrict__ var_out, double* __restrict__ mean_out, double* __restrict__ bmin,
+                              double* __restrict__ bmax) {
+  double lmin = DBL_MAX, lmax = -DBL_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, d = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      s += psq[i * nt + t];
+      d += pdot[i * nt + t];
+    }
+    double vp = varp[i];
+    double v = vp - s;
+    var_out[i] = v;
+    mean_out[i] = mean[i] + d;
+    lmin = fmin(lmin, v);
+    lmax = fmax(lmax, vp);
+  }
+  __shared__ double smin[kT], smax[kT];
+  smin[threadIdx.x] = lmin;
+  smax[threadIdx.x] = lmax;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bmin[blockIdx.x] = smin[0];
+    bmax[blockIdx.x] = smax[0];
+  }
+}
+
+// consistency check of filters.py:149-153 -> status[1]; min var -> out[0]
+__global__ void check_variance(int nb, const double* bmin, const double* bmax, int* status, double* out) {
+  double mn = DBL_MAX, mx = -DBL_MAX;
+  for (int b = 0; b < nb; ++b) {
+    mn = fmin(mn, bmin[b]);
+    mx = fmax(mx, bmax[b]);
+  }
+  double prior_max = fmax(mx, 0.0);
+  out[0] = mn;
+  if (mn < -1e-10 * fmax(prior_max, DBL_MIN)) status[1] = 1;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// workspace layout of the update
+// ---------------------------------------------------------------------------
+struct UpdWs {
+  double *HCp, *S, *L, *Li, *LiT, *P, *R, *tmp, *innov, *w, *Y, *psq, *pdot, *bmin, *bmax, *minv;
+  int* status;
+};
+
+static size_t update_layout(int64_t m, int64_t n, char* base, UpdWs* ws) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  int nt = ceil_div(n, DG_BN);
+  int nb = grid_for(m);
+  UpdWs w;
+  w.HCp = (double*)take(8 * n * n);
+  w.S = (double*)take(8 * n * n);
+  w.L = (double*)take(8 * n * n);
+  w.Li = (double*)take(8 * n * n);
+  w.LiT = (double*)take(8 * n * n);
+  w.P = (double*)take(8 * n * n);
+  w.R = (double*)take(8 * n * n);
+  w.tmp = (double*)take(8 * n * n);
+  w.innov = (double*)take(8 * n);
+  w.w = (double*)take(8 * n);
+  w.Y = (double*)take(8 * m * n);
+  w.psq = (double*)take(8 * m * nt);
+  w.pdot = (double*)take(8 * m * nt);
+  w.bmin = (double*)take(8 * (size_t)nb);
+  w.bmax = (double*)take(8 * (size_t)nb);
+  w.minv = (double*)take(8);
+  w.status = (int*)take(16);
+  if (ws) *ws = w;
+  return off;
+}
+
+size_t update_workspace_bytes(int64_t m, int64_t n) { return update_layout(m, n, nullptr, nullptr); }
+
+int predict(int64_t m, int64_t n, const double* C, const double* var, const double* HC, const double* CQ,
+            const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, cudaStream_t st) {
+  if (m * n > 0) {
+    add_kernel<<<grid_for(m * n / 2 + 1), kT, 0, st>>>(C, CQ, Co, m * n);
+    HIKF_CHECK_LAUNCH();
+  }
+  add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(var, dQ, varo, m);
+  HIKF_CHECK_LAUNCH();
+  if (n > 0) {
+    add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, st>>>(HC, HCQ, HCo, n * n);
+    HIKF_CHECK_LAUNCH();
+  }
+  return HIKF_OK;
+}
+
+// Cholesky + inverse of the symmetric n x n S (overwritten); status[0] = pivot.
+static int factor(double* S, double* L, double* Li, double* tmp, int64_t n, int* status, cudaStream_t st) {
+  HIKF_CHECK_CUDA(cudaMemsetAsync(L, 0, sizeof(double) * n * n, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(Li, 0, sizeof(double) * n * n, st));
+  return chol_inv(S, L, Li, n, n, 0, tmp, status, st);
+}
+
+int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
+  const int64_t m = a.m, n = a.n;
+  if (a.workspace_bytes < update_workspace_bytes(m, n)) {
+    set_error("update workspace too small (%zu < %zu bytes)", a.workspace_bytes, update_workspace_bytes(m, n));
+    return HIKF_BAD_ARGUMENT;
+  }
+  UpdWs w;
+  update_layout(m, n, (char*)a.workspace, &w);
+  HIKF_CHECK_CUDA(cudaMemsetAsync(w.status, 0, 16, st));
+
+  // ---- predict (fused in front) ----
+  const double *Cp = a.C, *varp = a.var, *HCp = a.HC;
+  if (a.CQ) {
+    ProfScope ps(ST_PREDICT, st);
+    HIKF_TRY(predict(m, n, a.C, a.var, a.HC, a.CQ, a.dQ, a.HCQ, a.C_out, a.var_out, w.HCp, st));
+    Cp = a.C_out;
+    varp = a.var_out;  // var_out temporarily holds var'; finalize reads it before overwriting
+    HCp = w.HCp;
+  }
+
+  // ---- n x n factorization ----
+  ProfScope* pf = new ProfScope(ST_FACTOR, st);
+  build_S<<<grid_for(n * n), kT, 0, st>>>(HCp, n, a.r, w.S);
+  HIKF_CHECK_LAUNCH();
+  HIKF_TRY(factor(w.S, w.L, w.Li, w.tmp, n, w.status, st));
+  transpose_kernel<<<grid_for(n * n), kT, 0, st>>>(w.Li, n, w.LiT);
+  HIKF_CHECK_LAUNCH();
+
+  // ---- innovation and whitened innovation ----
+  innovation<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, a.ip, a.ix, a.val, a.mean, a.z, w.innov);
+  HIKF_CHECK_LAUNCH();
+  trmv_lower<<<ceil_div(n * 32, kT), kT, 0, st>>>(w.Li, n, w.innov, w.w);
+  HIKF_CHECK_LAUNCH();
+
+  // ---- P = Li HC', R = HC' Li^T, HC_new = HC' - R P ----
+  {
+    GemmArgs g;
+    g.M = n; g.N = n; g.K = n;
+    g.A = w.Li; g.sa_r = n;
+    g.B = HCp; g.sb_r = n;
+    g.C = w.P; g.ldc = n;
+    HIKF_TRY(dgemm(g, 1, st));
+    GemmArgs h;
+    h.M = n; h.N = n; h.K = n;
+    h.A = HCp; h.sa_r = n;
+    h.B = w.LiT; h.sb_r = n;
+    h.C = w.R; h.ldc = n;
+    h.kmode = KB_UPPER;
+    HIKF_TRY(dgemm(h, 1, st));
+    GemmArgs c;
+    c.M = n; c.N = n; c.K = n;
+    c.A = w.R; c.sa_r = n;
+    c.B = w.P; c.sb_r = n;
+    c.C = a.HC_out; c.ldc = n;
+    c.Cin = HCp; c.ldcin = n;
+    c.alpha = -1.0; c.beta = 1.0;
+    HIKF_TRY(dgemm(c, 1, st));
+  }
+  delete pf;
+
+  // ---- Y = C' Li^T with fused row partials (|Y_i|^2, Y_i . w) ----
+  const int nt = ceil_div(n, DG_BN);
+  {
+    GemmArgs g;
+    g.M = m; g.N = n; g.K = n;
+    g.A = Cp; g.sa_r = n;
+    g.B = w.LiT; g.sb_r = n;
+    g.C = w.Y; g.ldc = n;
+    g.kmode = KB_UPPER;
+    g.psq = w.psq; g.pdot = w.pdot; g.w = w.w; g.ldp = nt;
+    ProfScope ps(ST_GEMM_Y, st);
+    HIKF_TRY(dgemm(g, 1, st));
+  }
+  const int nb = grid_for(m);
+  ProfScope* pz = new ProfScope(ST_FINALIZE, st);
+  finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
+  HIKF_CHECK_LAUNCH();
+  check_variance<<<1, 1, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+  HIKF_CHECK_LAUNCH();
+  delete pz;
+
+  // ---- C_new = C' - Y P ----
+  {
+    GemmArgs g;
+    g.M = m; g.N = n; g.K = n;
+    g.A = w.Y; g.sa_r = n;
+    g.B = w.P; g.sb_r = n;
+    g.C = a.C_out; g.ldc = n;
+    g.Cin = Cp; g.ldcin = n;
+    g.alpha = -1.0; g.beta = 1.0;
+    ProfScope ps(ST_GEMM_C, st);
+    HIKF_TRY(dgemm(g, 1, st));
+  }
+
+  // ---- status back to the host ----
+  int hs[2] = {0, 0};
+  double mv = 0.0;
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(&mv, w.minv, sizeof(double), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (res) {
+    res->pivot = hs[0];
+    res->min_var = mv;
+  }
+  if (hs[0]) {
+    set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
+    return HIKF_NOT_PD;
+  }
+  if (hs[1]) {
+    set_error("posterior variance went negative beyond tolerance (min %.3e)", mv);
+    return HIKF_NEGATIVE_VARIANCE;
+  }
+  return HIKF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// spd_solve (linalg.py:18-37): X = A^{-1} B via X = Li^T (Li B)
+// ---------------------------------------------------------------------------
+__global__ void asym_check(const double* __restrict__ A, int64_t n, double* out2) {
+  // out2[0] = max|A|, out2[1] = max|A - A^T| (single block, n <= a few thousand)
+  __shared__ double s0[kT], s1[kT];
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int64_t i = e / n, j = e % n;
+    double v = A[e];
+    a0 = fmax(a0, fabs(v));
+    double d = fabs(v - A[j * n + i]);
+    a1 = (d != d) ? d : fmax(a1, d);
+    if (v != v) a0 = v;
+  }
+  s0[threadIdx.x] = a0;
+  s1[threadIdx.x] = a1;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      s0[threadIdx.x] = fmax(s0[threadIdx.x], s0[threadIdx.x + o]);
+      s1[threadIdx.x] = fmax(s1[threadIdx.x], s1[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out2[0] = s0[0];
+    out2[1] = s1[0];
+  }
+}
+
+size_t spd_workspace_bytes(int64_t n, int64_t k) {
+  return align_up(8 * n * n) * 5 + align_up(8 * n * std::max<int64_t>(k, 1)) + align_up(64);
+}
+
+int spd_solve(int64_t n, int64_t k, const double* A, const double* B, double* X, void* ws, size_t ws_bytes,
+              int64_t* info, cudaStream_t st) {
+  if (ws_bytes < spd_workspace_bytes(n, k)) {
+    set_error("spd_solve workspace too small");
+    return HIKF_BAD_ARGUMENT;
+  }
+  char* p = (char*)ws;
+  double* S = (double*)p;
+  p += align_up(8 * n * n);
+  double* L = (double*)p;
+  p += align_up(8 * n * n);
+  double* Li = (double*)p;
+  p += align_up(8 * n * n);
+  double* LiT = (double*)p;
+  p += align_up(8 * n * n);
+  double* tmp = (double*)p;
+  p += align_up(8 * n * n);
+  double* Z = (double*)p;
+  p += align_up(8 * n * std::max<int64_t>(k, 1));
+  double* chk = (double*)p;
+  int* status = (int*)(chk + 2);
+  if (info) *info = 0;
+  if (n == 0) return HIKF_OK;
+  asym_check<<<1, kT, 0, st>>>(A, n, chk);
+  HIKF_CHECK_LAUNCH();
+  double hchk[2];
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(hchk, chk, sizeof(hchk), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  // numpy: scale = |A|.max(); if scale > 0 and |A - A^T|.max() > 1e-10 * scale
+  if (hchk[0] > 0 && hchk[1] > 1e-10 * hchk[0]) {
+    set_error("A is not symmetric within tolerance");
+    return HIKF_ASYMMETRIC;
+  }
+  HIKF_CHECK_CUDA(cudaMemsetAsync(status, 0, 8, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(S, A, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st));
+  HIKF_TRY(factor(S, L, Li, tmp, n, status, st));
+  transpose_kernel<<<grid_for(n * n), kT, 0, st>>>(Li, n, LiT);
+  HIKF_CHECK_LAUNCH();
+  if (k > 0) {
+    GemmArgs g;  // Z = Li B
+    g.M = n; g.N = k; g.K = n;
+    g.A = Li; g.sa_r = n;
+    g.B = B; g.sb_r = k;
+    g.C = Z; g.ldc = k;
+    HIKF_TRY(dgemm(g, 1, st));
+    GemmArgs h;  // X = Li^T Z
+    h.M = n; h.N = k; h.K = n;
+    h.A = LiT; h.sa_r = n;
+    h.B = Z; h.sb_r = k;
+    h.C = X; h.ldc = k;
+    HIKF_TRY(dgemm(h, 1, st));
+  }
+  int hs = 0;
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(&hs, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (hs) {
+    if (info) *info = hs;
+    set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs);
+    return HIKF_NOT_PD;
+  }
+  return HIKF_OK;
+}
+
+}  // namespace hikf

@@ -1,0 +1,251 @@
+"""HiKF cross-covariance filter on the B200: drop-in for the HiKF part of the
+reference hikf.filters (filters.py:82-157).
+
+State and precompute objects keep their arrays as CUDA torch tensors
+(``*_t`` attributes) and expose the reference's numpy fields (``mean``,
+``cross_cov``, ``variance``, ``HC``; ``C_Q``, ``HC_Q``, ``diag_Q``) as lazily
+copied host views, because callers such as experiment.run_hikf do
+``run.means[t] = state.mean`` (experiment.py:237).
+
+``hikf_predict`` is lazy: it returns a state that remembers "prior + pre";
+``hikf_update`` on such a state runs the fused predict+update of
+libhikf_b200.so, and reading a field of it materialises the predict.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+import scipy.sparse
+import torch
+
+from . import _lib
+from ._lib import NumericalConsistencyError  # noqa: F401  (re-export, filters.py:27-28)
+from .kernels import value_at_zero  # noqa: F401
+
+__all__ = [
+    "DeviceCSR", "HikfPrecompute", "HikfState", "NumericalConsistencyError",
+    "hikf_precompute_fmm", "hikf_init", "hikf_predict", "hikf_update",
+]
+
+
+def _dev():
+    return _lib.require_cuda()
+
+
+def _to_dev(x, shape=None) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=_dev(), dtype=torch.float64)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(_dev())
+    t = t.contiguous()
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {shape}, got {tuple(t.shape)}")
+    return t
+
+
+class DeviceCSR:
+    """Device copy of a CSR ray operator (int32 indptr/indices, float64 data).
+
+    Cached per host matrix object so the per-step update does not re-upload H.
+    """
+
+    _cache: dict = {}
+
+    def __init__(self, H):
+        Hc = H.tocsr() if scipy.sparse.issparse(H) else scipy.sparse.csr_matrix(np.asarray(H, dtype=float))
+        Hc = Hc.copy()
+        Hc.sum_duplicates()
+        Hc.sort_indices()
+        self.shape = Hc.shape
+        self.nnz = Hc.nnz
+        dev = _dev()
+        self.indptr = torch.from_numpy(Hc.indptr.astype(np.int32)).to(dev)
+        self.indices = torch.from_numpy(Hc.indices.astype(np.int32)).to(dev)
+        self.data = torch.from_numpy(Hc.data.astype(np.float64)).to(dev)
+
+    @classmethod
+    def of(cls, H) -> "DeviceCSR":
+        if isinstance(H, DeviceCSR):
+            return H
+        key = id(H)
+        hit = cls._cache.get(key)
+        if hit is not None:
+            ref, dcsr = hit
+            if ref() is H:
+                return dcsr
+        dcsr = cls(H)
+        try:
+            cls._cache[key] = (weakref.ref(H), dcsr)
+        except TypeError:  # not weak-referenceable (plain ndarray subclasses are fine)
+            pass
+        return dcsr
+
+
+class HikfPrecompute:
+    """C_Q = Q H^T (m, n), HC_Q = sym(H C_Q) (n, n), diag_Q (m,) -- filters.py:82-88."""
+
+    def __init__(self, C_Q, HC_Q, diag_Q):
+        self.C_Q_t = _to_dev(C_Q)
+        self.HC_Q_t = _to_dev(HC_Q)
+        self.diag_Q_t = _to_dev(diag_Q)
+        self._host = {}
+
+    def _np(self, name):
+        if name not in self._host:
+            self._host[name] = getattr(self, name + "_t").cpu().numpy()
+        return self._host[name]
+
+    C_Q = property(lambda self: self._np("C_Q"))
+    HC_Q = property(lambda self: self._np("HC_Q"))
+    diag_Q = property(lambda self: self._np("diag_Q"))
+
+
+class HikfState:
+    """(mean, C = P H^T, diag P, HC = H P H^T) -- filters.py:91-96."""
+
+    def __init__(self, mean, cross_cov, variance, HC, *, _prior=None, _pre=None):
+        self._prior = _prior
+        self._pre = _pre
+        self._host = {}
+        if _prior is None:
+            self.mean_t = _to_dev(mean)
+            m = self.mean_t.shape[0]
+            self.cross_cov_t = _to_dev(cross_cov)
+            if self.cross_cov_t.ndim != 2 or self.cross_cov_t.shape[0] != m:
+                raise ValueError("cross_cov must have shape (m, n)")
+            self.variance_t = _to_dev(variance, (m,))
+            n = self.cross_cov_t.shape[1]
+            self.HC_t = _to_dev(HC, (n, n))
+        else:
+            self.mean_t = _prior.mean_t  # the predict leaves the mean unchanged
+            self.cross_cov_t = self.variance_t = self.HC_t = None
+
+    @property
+    def pending(self) -> bool:
+        return self._prior is not None and self.cross_cov_t is None
+
+    def _materialize(self):
+        """Run the (non-fused) predict kernel for a lazily predicted state."""
+        if not self.pending:
+            return
+        p, pre = self._prior, self._pre
+        m, n = p.cross_cov_t.shape
+        C = torch.empty_like(p.cross_cov_t)
+        v = torch.empty_like(p.variance_t)
+        HC = torch.empty_like(p.HC_t)
+        _lib.check(_lib.load().hikf_predict(m, n, p.cross_cov_t.data_ptr(), p.variance_t.data_ptr(),
+                                            p.HC_t.data_ptr(), pre.C_Q_t.data_ptr(), pre.diag_Q_t.data_ptr(),
+                                            pre.HC_Q_t.data_ptr(), C.data_ptr(), v.data_ptr(), HC.data_ptr(),
+                                            _lib.stream_ptr()))
+        self.cross_cov_t, self.variance_t, self.HC_t = C, v, HC
+
+    def _np(self, name):
+        if name not in self._host:
+            if name != "mean":
+                self._materialize()
+            self._host[name] = getattr(self, name + "_t").cpu().numpy()
+        return self._host[name]
+
+    mean = property(lambda self: self._np("mean"))
+    cross_cov = property(lambda self: self._np("cross_cov"))
+    variance = property(lambda self: self._np("variance"))
+    HC = property(lambda self: self._np("HC"))
+
+    @property
+    def shape(self):
+        src = self._prior if self.pending else self
+        return tuple(src.cross_cov_t.shape)
+
+
+def _model_H(model):
+    return model.H
+
+
+def hikf_precompute_fmm(model, tree) -> HikfPrecompute:
+    """Form Q H^T with one device FMM product over H^T (filters.py:99-105)."""
+    H = DeviceCSR.of(_model_H(model))
+    m, n = tree.m, H.shape[0]
+    if H.shape[1] != m:
+        raise ValueError("operator columns do not match state length")
+    dev = _dev()
+    C_Q = torch.empty((m, n), dtype=torch.float64, device=dev)
+    HC_Q = torch.empty((n, n), dtype=torch.float64, device=dev)
+    diag_Q = torch.empty((m,), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().hikf_precompute(tree._handle, n, H.indptr.data_ptr(), H.indices.data_ptr(),
+                                           H.data.data_ptr(), C_Q.data_ptr(), HC_Q.data_ptr(), diag_Q.data_ptr(),
+                                           _lib.stream_ptr()))
+    return HikfPrecompute(C_Q, HC_Q, diag_Q)
+
+
+def hikf_init(model) -> HikfState:
+    """mean = mu_0, C = alpha H^T, var = alpha, HC = alpha H H^T (filters.py:118-126)."""
+    H = DeviceCSR.of(_model_H(model))
+    m, n = int(model.m), H.shape[0]
+    dev = _dev()
+    mean = _to_dev(model.initial_mean, (m,)).clone()
+    C = torch.empty((m, n), dtype=torch.float64, device=dev)
+    var = torch.empty((m,), dtype=torch.float64, device=dev)
+    HC = torch.empty((n, n), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().hikf_init_state(m, n, H.indptr.data_ptr(), H.indices.data_ptr(), H.data.data_ptr(),
+                                           float(model.alpha), C.data_ptr(), var.data_ptr(), HC.data_ptr(),
+                                           _lib.stream_ptr()))
+    return HikfState(mean, C, var, HC)
+
+
+def hikf_predict(state: HikfState, pre: HikfPrecompute) -> HikfState:
+    """C += C_Q, var += diag_Q, HC += HC_Q (filters.py:129-135); evaluated lazily."""
+    state._materialize()
+    if tuple(pre.C_Q_t.shape) != tuple(state.cross_cov_t.shape):
+        raise ValueError("precompute shape does not match the state")
+    return HikfState(None, None, None, None, _prior=state, _pre=pre)
+
+
+_WS: dict = {}
+
+
+def _workspace(m: int, n: int) -> torch.Tensor:
+    dev = _dev()
+    key = (m, n, dev.index)
+    ws = _WS.get(key)
+    if ws is None:
+        nbytes = int(_lib.load().hikf_update_workspace_bytes(m, n))
+        _WS.clear()  # one live workspace (the update is single-writer)
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _WS[key] = ws
+    return ws
+
+
+def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
+    """Kalman update of (mean, C, var, HC) against z (filters.py:138-157)."""
+    Hd = DeviceCSR.of(H)
+    m = state.mean_t.shape[0]
+    zt = z if isinstance(z, torch.Tensor) else np.asarray(z, dtype=float)
+    if Hd.shape[0] != zt.shape[0]:
+        raise ValueError("observation length does not match operator rows")
+    if Hd.shape[1] != m:
+        raise ValueError("operator columns do not match state length")
+    n = Hd.shape[0]
+    if n == 0:
+        return state
+    zt = _to_dev(zt, (n,))
+    fused = state.pending
+    src = state._prior if fused else state
+    pre = state._pre if fused else None
+    if tuple(src.cross_cov_t.shape) != (m, n):
+        raise ValueError("cross covariance shape does not match (m, n)")
+    dev = _dev()
+    mean = torch.empty((m,), dtype=torch.float64, device=dev)
+    C = torch.empty((m, n), dtype=torch.float64, device=dev)
+    var = torch.empty((m,), dtype=torch.float64, device=dev)
+    HC = torch.empty((n, n), dtype=torch.float64, device=dev)
+    ws = _workspace(m, n)
+    _lib.check(_lib.load().hikf_update(
+        m, n, state.mean_t.data_ptr(), src.cross_cov_t.data_ptr(), src.variance_t.data_ptr(), src.HC_t.data_ptr(),
+        _lib.ptr(pre.C_Q_t) if fused else None, _lib.ptr(pre.diag_Q_t) if fused else None,
+        _lib.ptr(pre.HC_Q_t) if fused else None,
+        Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), float(r_variance), zt.data_ptr(),
+        mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None,
+        _lib.stream_ptr()))
+    return HikfState(mean, C, var, HC)

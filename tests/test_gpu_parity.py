@@ -1,0 +1,254 @@
+"""Parity of the CUDA path (libhikf_b200.so through the Python mirror) with the
+reference, via the golden fixtures (made by the real reference) and the CPU
+oracle.  Integer/index data bit-exact; floats within the tolerances written
+in each test (north star: relative Frobenius <= 1e-9 on C_Q, cross_cov,
+mean and variance after the last step).
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse
+
+from oracle import hikf_oracle as O
+from tests.golden import cases
+
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+PARITY = 1e-9
+
+
+def _load(name):
+    return dict(np.load(os.path.join(G, name)))
+
+
+def _sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1404_3816_b200 as p
+    return p
+
+
+def _spec(p, spec):
+    return p.KernelSpec(spec["family"], variance=spec.get("variance", 1.0),
+                        length_scale=spec.get("length_scale", 1.0), log_amplitude=spec.get("log_amplitude"))
+
+
+def _near_pattern_from_pairs(ex, m):
+    """Canonical (row-sorted, col-sorted) near pattern from leaf pairs."""
+    order, starts, counts = ex["order"], ex["leaf_starts"], ex["leaf_counts"]
+    rows, cols = [], []
+    for t, s in zip(ex["near_t"], ex["near_s"]):
+        tp = order[starts[t]:starts[t] + counts[t]]
+        sp = order[starts[s]:starts[s] + counts[s]]
+        rows.append(np.repeat(tp, len(sp)))
+        cols.append(np.tile(sp, len(tp)))
+    A = scipy.sparse.coo_matrix((np.ones(sum(len(r) for r in rows)), (np.concatenate(rows), np.concatenate(cols))),
+                                shape=(m, m)).tocsr()
+    A.sort_indices()
+    return A
+
+
+def check_tree_ints(tree, g, prefix="tree_"):
+    assert tree.depth == int(g[prefix + "depth"])
+    assert tree.root_size == float(g[prefix + "root_size"])
+    assert np.array_equal(tree.root_lo, g[prefix + "root_lo"])
+    ex = tree.export()
+    assert np.array_equal(ex["order"], g[prefix + "order"])
+    assert np.array_equal(ex["leaf_ids"], g[prefix + "leaf_ids"])
+    assert np.array_equal(ex["leaf_starts"], g[prefix + "leaf_starts"])
+    assert np.array_equal(ex["leaf_counts"], g[prefix + "leaf_counts"])
+    near = _near_pattern_from_pairs(ex, tree.m)
+    assert near.nnz == int(g[prefix + "near_nnz"])
+    assert _sha(near.indptr.astype(np.int64), near.indices.astype(np.int64)) == g[prefix + "near_pattern_sha"].item().decode()
+    if tree.depth >= 2:
+        assert sorted(tree._orders.items()) == [tuple(r) for r in g[prefix + "orders"].tolist()]
+        keys, counts, h = [], [], hashlib.sha256()
+        for lev in range(2, tree.depth + 1):
+            for dx, dy in O.m2l_offsets():
+                t, s = tree.m2l_pairs(lev, dx, dy)
+                if len(t):
+                    keys.append((lev, dx, dy))
+                    counts.append(len(t))
+        # digest in the reference's sorted-key order
+        for key in sorted(keys):
+            t, s = tree.m2l_pairs(*key)
+            h.update(t.astype(np.int64).tobytes())
+            h.update(s.astype(np.int64).tobytes())
+        assert np.array_equal(np.array(sorted(keys), dtype=np.int64), g[prefix + "m2l_keys"])
+        assert np.array_equal(np.array([c for _, c in sorted(zip(keys, counts))], dtype=np.int64), g[prefix + "m2l_counts"])
+        assert h.hexdigest() == g[prefix + "m2l_pairs_sha"].item().decode()
+
+
+@pytest.mark.parametrize("name", list(cases.tree_cases()))
+def test_tree_and_matmat_match_reference(pkg, name):
+    pts, spec, n_cheb, leaf, nvec = cases.tree_cases()[name]
+    g = _load(f"tree_{name}.npz")
+    tree = pkg.build_tree(pkg.PointSet(pts), _spec(pkg, spec), pkg.FmmConfig(n_cheb=n_cheb, max_leaf_points=leaf))
+    check_tree_ints(tree, g)
+    if tree.depth >= 2:
+        np.testing.assert_allclose(tree.interp_weights(), g["op_interp_data"], rtol=0, atol=1e-14)
+        for key, val in g.items():
+            if key.startswith("op_m2l_"):
+                lev, dx, dy = (int(v) for v in key[len("op_m2l_"):].split("_"))
+                np.testing.assert_allclose(tree.m2l_op(lev, dx, dy), val, rtol=1e-14, atol=1e-300)
+            if key.startswith("op_shift_"):
+                lev, c = key[len("op_shift_"):].split("_")
+                np.testing.assert_allclose(tree.shift_op(int(lev), int(c[0]), int(c[1])), val, rtol=0, atol=1e-14)
+    U = tree.matmat(g["V"])
+    # reassociation only: far below the 1e-9 north-star bound
+    assert O.rel_fro(U, g["U"]) <= 1e-13, O.rel_fro(U, g["U"])
+
+
+def test_matvec_linear_and_columns(pkg):
+    pts, spec, n_cheb, leaf, _ = cases.tree_cases()["cloud_exp4"]
+    tree = pkg.build_tree(pkg.PointSet(pts), _spec(pkg, spec), pkg.FmmConfig(n_cheb=n_cheb, max_leaf_points=leaf))
+    rng = np.random.default_rng(14)
+    v, w = rng.standard_normal((2, len(pts)))
+    comb = tree.matvec(2.5 * v - 0.3 * w)
+    sep = 2.5 * tree.matvec(v) - 0.3 * tree.matvec(w)
+    assert np.allclose(comb, sep, atol=1e-10 * np.abs(sep).max())
+    V = rng.standard_normal((len(pts), 3))
+    out = tree.matmat(V)
+    for c in range(3):
+        assert np.allclose(out[:, c], tree.matvec(V[:, c]), atol=1e-12)
+    assert np.array_equal(tree.matvec(np.zeros(len(pts))), np.zeros(len(pts)))
+    with pytest.raises(ValueError):
+        tree.matvec(np.zeros(len(pts) + 1))
+    with pytest.raises(ValueError):
+        tree.matmat(np.zeros((len(pts) + 1, 2)))
+
+
+def test_config_errors(pkg):
+    with pytest.raises(ValueError):
+        pkg.FmmConfig(n_cheb=1)
+    with pytest.raises(ValueError):
+        pkg.FmmConfig(n_cheb=13)
+    with pytest.raises(ValueError):
+        pkg.FmmConfig(max_leaf_points=0)
+
+
+def test_spd_solve(pkg):
+    g = _load("spd_solve.npz")
+    np.testing.assert_allclose(pkg.spd_solve(g["A"], g["B"]), g["X"], rtol=1e-12, atol=1e-14)
+    with pytest.raises(pkg.DecompositionError):
+        pkg.spd_solve(np.diag([1.0, -1.0]), np.ones(2))
+    with pytest.raises(ValueError):
+        pkg.spd_solve(np.array([[2.0, 1.0], [0.0, 2.0]]), np.ones(2))
+    with pytest.raises(ValueError):
+        pkg.spd_solve(np.ones((2, 3)), np.ones(2))
+    # a larger SPD system exercising the recursive blocked factorization
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((300, 300))
+    A = A @ A.T + 300 * np.eye(300)
+    B = rng.standard_normal((300, 7))
+    np.testing.assert_allclose(pkg.spd_solve(A, B), np.linalg.solve(A, B), rtol=1e-10, atol=1e-13)
+
+
+def test_update_hand_cases(pkg):
+    flt = pkg.filters
+    g = _load("update_cases.npz")
+    for i, (st, Hm, r, z) in enumerate(cases.update_cases()):
+        s = flt.HikfState(mean=st["mean"], cross_cov=st["cross_cov"], variance=st["variance"], HC=st["HC"])
+        out = flt.hikf_update(s, scipy.sparse.csr_matrix(Hm), r, z)
+        for k in ("mean", "cross_cov", "variance", "HC"):
+            # the posterior is a difference of O(|input|) terms: roundoff scales with the input
+            scale = max(np.abs(st["cross_cov"]).max(), np.abs(st["HC"]).max(), np.abs(st["variance"]).max())
+            np.testing.assert_allclose(getattr(out, k), g[f"c{i}_{k}"], rtol=1e-12, atol=1e-14 * scale)
+    bad = flt.HikfState(mean=np.zeros(1), cross_cov=np.array([[3.0]]), variance=np.array([1.0]), HC=np.array([[4.0]]))
+    with pytest.raises(flt.NumericalConsistencyError):
+        flt.hikf_update(bad, np.array([[1.0]]), 0.0, np.array([0.0]))
+    notpd = flt.HikfState(mean=np.zeros(1), cross_cov=np.array([[1.0]]), variance=np.array([1.0]), HC=np.array([[-4.0]]))
+    with pytest.raises(pkg.DecompositionError):
+        flt.hikf_update(notpd, np.array([[1.0]]), 0.0, np.array([0.0]))
+    s = flt.HikfState(mean=np.zeros(1), cross_cov=np.array([[1.0]]), variance=np.array([1.0]), HC=np.array([[1.0]]))
+    with pytest.raises(ValueError):
+        flt.hikf_update(s, np.array([[1.0]]), 1.0, np.array([1.0, 2.0]))
+
+
+def _gpu_scenario(pkg, cfg):
+    N = cfg["N"]
+    grid = pkg.Grid2D(nx=N, ny=N, dx=1.0 / N, dy=1.0 / N)
+    acq = pkg.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], source_x=0.0, receiver_x=1.0)
+    H = pkg.tomography.build_ray_operator(grid, acq)
+    return grid, H
+
+
+class _Model:
+    def __init__(self, grid, H, kernel, r):
+        self.grid, self.H, self.q_kernel, self.r_variance = grid, H, kernel, r
+        self.alpha = 0.0
+        self.m = grid.m
+        self.n = H.shape[0]
+        self.initial_mean = np.zeros(grid.m)
+
+
+def _run_filter(pkg, cfg, obs):
+    flt = pkg.filters
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    model = _Model(grid, H, kern, cfg["R"])
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    pre = flt.hikf_precompute_fmm(model, tree)
+    st = flt.hikf_init(model)
+    for t in range(cfg["T"]):
+        st = flt.hikf_update(flt.hikf_predict(st, pre), H, model.r_variance, obs[t])
+    return tree, H, pre, st
+
+
+@pytest.mark.parametrize("fixture,cfg", [("small_rays.npz", cases.SMALL), ("cfg1.npz", cases.CFG1)])
+def test_filter_matches_reference(pkg, fixture, cfg):
+    g = _load(fixture)
+    tree, H, pre, st = _run_filter(pkg, cfg, g["obs"])
+    assert np.array_equal(H.indptr.astype(np.int64), g["H_indptr"])
+    assert np.array_equal(H.indices.astype(np.int64), g["H_indices"])
+    np.testing.assert_array_equal(H.data, g["H_data"])
+    check_tree_ints(tree, g)
+    assert O.rel_fro(pre.C_Q, g["C_Q"]) <= 1e-13
+    assert O.rel_fro(pre.HC_Q, g["HC_Q"]) <= 1e-13
+    np.testing.assert_array_equal(pre.diag_Q, np.ones(tree.m))
+    for k, ref in (("mean", "final_mean"), ("variance", "final_variance"), ("cross_cov", "final_cross_cov")):
+        err = O.rel_fro(getattr(st, k), g[ref])
+        assert err <= PARITY, (k, err)
+
+
+@pytest.mark.slow
+def test_filter_cfg2_matches_reference(pkg):
+    """cfg2 (m = 65,536, n = 256, 100 steps): the thin-budget case."""
+    g = _load("cfg2.npz")
+    tree, H, pre, st = _run_filter(pkg, cases.CFG2, g["obs"])
+    assert np.array_equal(H.indptr.astype(np.int64), g["H_indptr"])
+    assert np.array_equal(H.indices.astype(np.int64), g["H_indices"])
+    check_tree_ints(tree, g)
+    cols = g["cols"]
+    assert O.rel_fro(pre.C_Q[:, cols], g["C_Q_cols"]) <= 1e-13
+    assert abs(np.linalg.norm(pre.C_Q) - float(g["C_Q_fro"])) <= 1e-13 * float(g["C_Q_fro"])
+    assert O.rel_fro(st.mean, g["final_mean"]) <= PARITY
+    assert O.rel_fro(st.variance, g["final_variance"]) <= PARITY
+    assert O.rel_fro(st.cross_cov[:, cols], g["final_cross_cov_cols"]) <= PARITY
+    assert O.rel_fro(st.HC, g["final_HC"]) <= PARITY
+
+
+def test_dgemm_against_torch(pkg):
+    """The DMMA GEMM inside spd_solve / update vs torch float64 on random data."""
+    import torch
+    rng = np.random.default_rng(8)
+    for n, k in ((64, 5), (200, 33), (513, 130)):
+        A = rng.standard_normal((n, n))
+        A = A @ A.T + n * np.eye(n)
+        B = rng.standard_normal((n, k))
+        X = pkg.spd_solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+        ref = torch.linalg.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+        assert torch.allclose(X, ref, rtol=1e-10, atol=1e-12)

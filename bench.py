@@ -318,6 +318,8 @@ def main():
         return float(t.item())
 
     # ---- tree build + Q H^T precompute (one-time; timed separately) ----
+    # (a tiny build first, so lazy CUDA module loading is not charged to the tree)
+    P.build_tree(P.PointSet(np.random.default_rng(0).random((256, 2))), kern)
     barrier_sync()
     t0 = time.perf_counter()
     tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
@@ -334,7 +336,9 @@ def main():
     barrier_sync()
     lib.hikf_prof_enable(0)
     t_qht = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-    fmm_stage = {s: _lib.prof_read(s) for s in ("densify", "p2p", "p2m", "m2m", "m2l", "l2p")}
+    fmm_stage = {s: _lib.prof_read(s) for s in ("densify", "p2p", "p2m", "m2m", "m2l", "l2l", "l2p")}
+    fmm_useful = {s: _lib.prof_flops(s) for s in ("p2p", "p2m", "m2m", "m2l", "l2l", "l2p")}
+    qht_useful = float(sum(fmm_useful.values()))
     ex = tree.export()
     cnt = ex["leaf_counts"]
     near_pts = float(np.sum(cnt[ex["near_t"]] * cnt[ex["near_s"]]))
@@ -410,10 +414,15 @@ def main():
         "qht": {"value": world * m * n / t_qht, "unit": "(m*n)/s", "ms": 1000.0 * t_qht, "tree_build_s": t_build,
                 "precompute_incl_build_mn_per_s": m * n / (t_qht + t_build),
                 "flops_dense_formulation": qht_flops,
+                "flops_performed": qht_useful,
                 "stage_ms": {k: v[0] for k, v in fmm_stage.items()},
-                "roofline": {"bound": "fp64", "achieved": qht_flops / t_qht / 1e12, "peak": FP64_PEAK_TFLOPS,
-                             "unit": "TFLOP/s", "frac": qht_flops / t_qht / 1e12 / FP64_PEAK_TFLOPS,
-                             "m2l": {"achieved": ff["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
+                "stage_gflop_performed": {k: v / 1e9 for k, v in fmm_useful.items()},
+                "roofline": {"bound": "fp64", "achieved": qht_useful / t_qht / 1e12, "peak": FP64_PEAK_TFLOPS,
+                             "unit": "TFLOP/s", "frac": qht_useful / t_qht / 1e12 / FP64_PEAK_TFLOPS,
+                             "note": "performed flops (H^T sparsity exploited: only nonzero charge columns are "
+                                     "multiplied); dense-formulation equivalent rate = "
+                                     f"{qht_flops / t_qht / 1e12:.1f} TFLOP/s",
+                             "m2l": {"achieved": fmm_useful["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
         "roofline": {"kernel": "dgemm_kernel (C_new = C' - Y P, 2 m n^2 flops per launch)", "bound": "fp64",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SOURCE,

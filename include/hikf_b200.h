@@ -70,6 +70,9 @@ int hikf_last_error(char* buf, size_t len);
 int hikf_tree_create(const double* xy_host, int64_t m, const hikf_kernel* kernel, int32_t n_cheb,
                      int64_t max_leaf, void* stream, hikf_tree** out);
 int hikf_tree_destroy(hikf_tree* tree);
+/* Return the library's cached stream-ordered workspace (FMM expansions,
+ * H^T regrouping) to the driver; it is otherwise kept between calls. */
+int hikf_release_cached_memory(void);
 
 /* Scalars of the tree: depth, per-level orders (orders[lev] for lev 2..depth,
  * 0 elsewhere; array of 21), root_lo[2], root_size, #occupied leaves,
@@ -158,14 +161,24 @@ int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, d
                       const double* src, const double* rcv, int32_t* indptr, int32_t* indices, double* data,
                       int64_t* nnz_out);
 
+/* ---- FP64 DMMA GEMM building block (the update's workhorse) ----
+ * C (M x N, ldc) = alpha A (M x K, lda) B (K x N, ldb) + beta C, row-major,
+ * device pointers.  kmode 0: full; 1: B upper triangular (K-range k <= col
+ * tile); 2: B lower triangular.  variant -1 = default tile shape. */
+int hikf_dgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+               double* C, int64_t ldc, double alpha, double beta, int32_t kmode, int32_t variant, void* stream);
+
 /* ---- instrumentation (bench.py) ----
  * Stage timers: CUDA events recorded on the launching stream around each
  * stage (ids in csrc/prof.h: 0 predict, 1 factor, 2 Y GEMM, 3 finalize,
- * 4 C GEMM, 5 P2P, 6 P2M, 7 M2M, 8 M2L, 9 L2P, 10 densify).
+ * 4 C GEMM, 5 P2P, 6 P2M, 7 M2M, 8 M2L, 9 L2P, 10 H^T regrouping, 11 L2L).
  * hikf_launch_count: kernels launched by this library since load. */
 int hikf_prof_enable(int on);
 int hikf_prof_reset(void);
 int hikf_prof_read(int32_t stage, double* total_ms, int64_t* count);
+/* useful flops executed by a stage's kernels while profiling was enabled
+ * (2 per multiply-add actually performed; skipped zero blocks not counted) */
+int hikf_prof_flops(int32_t stage, uint64_t* flops);
 int64_t hikf_launch_count(void);
 
 #ifdef __cplusplus

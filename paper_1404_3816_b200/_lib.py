@@ -56,6 +56,7 @@ SIGNATURES = {
     "hikf_last_error": (ctypes.c_int, [ctypes.c_char_p, _SZ]),
     "hikf_tree_create": (ctypes.c_int, [_P, _I64, ctypes.POINTER(HikfKernel), _I32, _I64, _P, ctypes.POINTER(_P)]),
     "hikf_tree_destroy": (ctypes.c_int, [_P]),
+    "hikf_release_cached_memory": (ctypes.c_int, []),
     "hikf_tree_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
     "hikf_tree_export": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "hikf_tree_export_op": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P]),
@@ -71,15 +72,17 @@ SIGNATURES = {
     "hikf_spd_solve_workspace_bytes": (_SZ, [_I64, _I64]),
     "hikf_spd_solve": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _SZ, _P, _P]),
     "hikf_ray_operator": (ctypes.c_int, [_I64, _I64, _D, _D, _D, _D, _I64, _P, _P, _P, _P, _P, _P]),
+    "hikf_dgemm": (ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I32, _I32, _P]),
     "hikf_prof_enable": (ctypes.c_int, [ctypes.c_int]),
     "hikf_prof_reset": (ctypes.c_int, []),
     "hikf_prof_read": (ctypes.c_int, [_I32, _P, _P]),
+    "hikf_prof_flops": (ctypes.c_int, [_I32, _P]),
     "hikf_launch_count": (_I64, []),
 }
 
 # stage ids of hikf_prof_read (csrc/prof.h)
 STAGES = {"predict": 0, "factor": 1, "gemm_y": 2, "finalize": 3, "gemm_c": 4, "p2p": 5, "p2m": 6, "m2m": 7,
-          "m2l": 8, "l2p": 9, "densify": 10}
+          "m2l": 8, "l2p": 9, "densify": 10, "l2l": 11}
 
 
 def prof_read(stage: str):
@@ -88,6 +91,13 @@ def prof_read(stage: str):
     cnt = ctypes.c_int64()
     load().hikf_prof_read(STAGES[stage], ctypes.byref(ms), ctypes.byref(cnt))
     return ms.value, cnt.value
+
+
+def prof_flops(stage: str) -> int:
+    """Useful flops a stage executed since the last hikf_prof_reset (profiling on)."""
+    v = ctypes.c_uint64()
+    load().hikf_prof_flops(STAGES[stage], ctypes.byref(v))
+    return v.value
 
 _lib = None
 

@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "dgemm.cuh"
 #include "prof.h"
 #include "tree.h"
 #include "update.h"
@@ -96,19 +97,7 @@ int grid_for(int64_t n) {
 
 int matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
                 cudaStream_t st) {
-  double* Ht = nullptr;
-  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Ht, sizeof(double) * std::max<int64_t>(1, t->m * n), st));
-  {
-    ProfScope ps(ST_DENSIFY, st);
-    HIKF_CHECK_CUDA(cudaMemsetAsync(Ht, 0, sizeof(double) * t->m * n, st));
-    if (n > 0) {
-      scatter_transpose<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, Ht);
-      HIKF_CHECK_LAUNCH();
-    }
-  }
-  int s = fmm_matmat(t, Ht, n, n, U, n, st);
-  cudaFreeAsync(Ht, st);
-  return s;
+  return fmm_matmat_csrT(t, n, ip, ix, val, U, st);
 }
 
 }  // namespace
@@ -117,6 +106,21 @@ int matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, c
 using namespace hikf;
 
 static cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Keep stream-ordered allocations cached in the device's default pool between
+// calls (the default release threshold of 0 would unmap and remap the FMM
+// workspace at every synchronisation).
+static void keep_pool() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done = true;
+}
 
 extern "C" {
 
@@ -140,11 +144,22 @@ int hikf_tree_create(const double* xy_host, int64_t m, const hikf_kernel* kernel
     set_error("no CUDA device: the HiKF B200 path has no CPU fallback");
     return HIKF_NO_DEVICE;
   }
+  keep_pool();
   return tree_build(xy_host, m, *kernel, n_cheb, max_leaf, as_stream(stream), out);
 }
 
 int hikf_tree_destroy(hikf_tree* tree) {
   tree_free(tree);
+  return HIKF_OK;
+}
+
+int hikf_release_cached_memory(void) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  HIKF_CHECK_CUDA(cudaGetDevice(&dev));
+  HIKF_CHECK_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  HIKF_CHECK_CUDA(cudaDeviceSynchronize());
+  HIKF_CHECK_CUDA(cudaMemPoolTrimTo(pool, 0));
   return HIKF_OK;
 }
 
@@ -380,6 +395,28 @@ int hikf_spd_solve(int64_t n, int64_t k, const double* A, const double* B, doubl
                    int64_t* info, void* stream) {
   if (n < 0 || k < 0) return HIKF_BAD_ARGUMENT;
   return spd_solve(n, k, A, B, X, ws, ws_bytes, info, as_stream(stream));
+}
+
+int hikf_dgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+               double* C, int64_t ldc, double alpha, double beta, int32_t kmode, int32_t variant, void* stream) {
+  if (M < 0 || N < 0 || K < 0 || kmode < 0 || kmode > 2) return HIKF_BAD_ARGUMENT;
+  int prev = dgemm_variant();
+  if (variant >= 0) set_dgemm_variant(variant);
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.A = A; g.sa_r = lda;
+  g.B = B; g.sb_r = ldb;
+  g.C = C; g.ldc = ldc;
+  if (beta != 0.0) {
+    g.Cin = C;
+    g.ldcin = ldc;
+  }
+  g.alpha = alpha;
+  g.beta = beta;
+  g.kmode = kmode;
+  int s = dgemm(g, 1, as_stream(stream));
+  set_dgemm_variant(prev);
+  return s;
 }
 
 int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n, const double* src,

@@ -39,9 +39,23 @@ struct GemmArgs {
   double* pdot = nullptr;
   const double* w = nullptr;
   int64_t ldp = 0;
+  int variant = -1;  // tile-shape variant (-1: dgemm_variant())
 };
 
 // C = alpha * A B + beta * Cin (+ partials); launches on `stream`.
 int dgemm(const GemmArgs& g, int batch, cudaStream_t stream);
+// tile-shape variant in use (0 = default); HIKF_DGEMM_VARIANT overrides
+int dgemm_variant();
+void set_dgemm_variant(int v);
+// number of column tiles (= partial sums per row) the current variant uses for N columns
+inline int dgemm_col_tiles(int64_t N, int variant = -1) {
+  int v = variant >= 0 ? variant : dgemm_variant();
+  return ceil_div(N, (v == 5 || v >= 8) ? 64 : 128);
+}
+// variants used by the update for the triangular Y GEMM and the full C GEMM
+// (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log); HIKF_DGEMM_VARIANT overrides both
+int update_variant_y();
+int update_variant_c();
+constexpr int DG_MIN_BN = 64;  // smallest column tile of any variant (partials workspace sizing)
 
 }  // namespace hikf

@@ -5,22 +5,17 @@
 
 #include "fmm_device.cuh"
 #include "prof.h"
+#include "sparse.h"
 #include "tree.h"
 
 namespace hikf {
 
 namespace {
 
-struct ProvBase {
-  int64_t kcols;  // columns of this pass
-  __device__ int64_t ncols() const { return kcols; }
-  KParams kp;
-  __device__ double kernel(double r) const { return kernel_of_r(kp, r); }
-};
-
 // Near field (fmm.py:166-201, :330): U rows of target leaf = sum over the
 // occupied 3x3-adjacent leaves (ox outer, oy inner) of K(x_t, x_s) V_s.
 struct P2PProv : ProvBase {
+  static constexpr int kStage = ST_P2P;
   static constexpr bool kAccumulate = false;
   const int32_t *leaf_box, *leaf_start, *leaf_count, *box2leaf;
   const double* xy_s;
@@ -48,6 +43,7 @@ struct P2PProv : ProvBase {
     d.b = V;
     d.ldb = ldv;
     d.b_rows = order + s0;
+    d.bmask = nullptr;
     return true;
   }
   __device__ double* out_row(int task, int r) const { return U + order[leaf_start[task] + r] * ldu; }
@@ -55,6 +51,9 @@ struct P2PProv : ProvBase {
 
 // P2M (fmm.py:338): W_leaf[a][:] = sum_p W2[p][a] V[p][:]
 struct P2MProv : ProvBase {
+  static constexpr int kStage = ST_P2M;
+  static constexpr int kStages = 2;
+  static constexpr int kMinBlocks = 2;
   static constexpr bool kAccumulate = false;
   const int32_t *leaf_box, *leaf_start, *leaf_count;
   const double* W2s;
@@ -75,6 +74,7 @@ struct P2MProv : ProvBase {
     d.b = V;
     d.ldb = ldv;
     d.b_rows = order + s0;
+    d.bmask = nullptr;
     return true;
   }
   __device__ double* out_row(int task, int r) const { return W + ((int64_t)leaf_box[task] * q + r) * kcols; }
@@ -82,6 +82,9 @@ struct P2MProv : ProvBase {
 
 // M2M (fmm.py:339-345): W_p[b] = sum_{children c} sum_a C_c[a][b] W_c[a]
 struct M2MProv : ProvBase {
+  static constexpr int kStage = ST_M2M;
+  static constexpr int kStages = 2;
+  static constexpr int kMinBlocks = 2;
   static constexpr bool kAccumulate = false;
   const int32_t* occ;            // occupied parents at level l
   const uint8_t* child_flag;     // occupancy at level l+1
@@ -90,6 +93,7 @@ struct M2MProv : ProvBase {
   int64_t Gp;
   const double* Wc;              // level l+1
   double* Wp;                    // level l
+  const uint8_t* cmask;          // child activity masks (sparse charges) or null
   __device__ int rows(int) const { return qp; }
   __device__ int nsegs(int) const { return 4; }
   __device__ bool seg(int task, int s, Seg& d) const {
@@ -105,6 +109,7 @@ struct M2MProv : ProvBase {
     d.b = Wc + child * qc * kcols;
     d.ldb = kcols;
     d.b_rows = nullptr;
+    d.bmask = cmask ? cmask + child * ngroups : nullptr;
     return true;
   }
   __device__ double* out_row(int task, int r) const { return Wp + ((int64_t)occ[task] * qp + r) * kcols; }
@@ -113,6 +118,7 @@ struct M2MProv : ProvBase {
 // M2L over the interaction list (fmm.py:349-359) with the parent-to-child
 // shift (fmm.py:361-363) fused as a 41st segment.
 struct M2LProv : ProvBase {
+  static constexpr int kStage = ST_M2L;
   static constexpr bool kAccumulate = false;
   const int32_t* occ;         // occupied targets at level l
   const uint8_t* flag;        // occupancy at level l
@@ -123,6 +129,7 @@ struct M2LProv : ProvBase {
   int64_t G;
   const double* W;            // multipoles, level l
   double* L;                  // locals, level l
+  const uint8_t* smask;       // source activity masks (sparse charges) or null
   // L2L from the parent level (null at level 2)
   const double* Lp;
   const double* shift;        // shift ops between l-1 and l: 4 x (q x qp)
@@ -134,6 +141,7 @@ struct M2LProv : ProvBase {
     d.gen = false;
     d.b_rows = nullptr;
     d.ldb = kcols;
+    d.bmask = nullptr;
     if (s < 40) {
       if (!((present >> s) & 1)) return false;
       int64_t src;
@@ -144,6 +152,7 @@ struct M2LProv : ProvBase {
       d.a_rs = q;
       d.a_cs = 1;
       d.b = W + src * q * kcols;
+      d.bmask = smask ? smask + src * ngroups : nullptr;
       return true;
     }
     int c = (int)((tx & 1) * 2 + (ty & 1));
@@ -158,9 +167,81 @@ struct M2LProv : ProvBase {
   __device__ double* out_row(int task, int r) const { return L + ((int64_t)occ[task] * q + r) * kcols; }
 };
 
-// L2P (fmm.py:366): U[p][:] += sum_a W2[p][a] L_leaf[a][:]
-struct L2PProv : ProvBase {
+// L2L only (fmm.py:361-363), accumulated after the per-offset sparse M2L passes
+struct L2LProv : ProvBase {
+  static constexpr int kStage = ST_L2L;
+  static constexpr int kStages = 2;
+  static constexpr int kMinBlocks = 2;
   static constexpr bool kAccumulate = true;
+  const int32_t* occ;
+  int q, qp;
+  int64_t G;
+  const double* Lp;
+  const double* shift;  // 4 x (q x qp)
+  double* L;
+  __device__ int rows(int) const { return q; }
+  __device__ int nsegs(int) const { return 1; }
+  __device__ bool seg(int task, int, Seg& d) const {
+    int64_t t = occ[task], tx = t / G, ty = t % G;
+    int c = (int)((tx & 1) * 2 + (ty & 1));
+    d.K = qp;
+    d.gen = false;
+    d.a = shift + (int64_t)c * q * qp;
+    d.a_rs = qp;
+    d.a_cs = 1;
+    d.b = Lp + ((tx >> 1) * (G >> 1) + (ty >> 1)) * qp * kcols;
+    d.ldb = kcols;
+    d.b_rows = nullptr;
+    d.bmask = nullptr;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const { return L + ((int64_t)occ[task] * q + r) * kcols; }
+};
+
+// L2L grouped by parent (fmm.py:361-363): the four children of a parent share
+// B = L_parent, A = the four stacked shift operators (4 q x qp); accumulates
+// into the children's locals (which already hold the M2L sum).
+struct L2LParentProv : ProvBase {
+  static constexpr int kStage = ST_L2L;
+  static constexpr int kStages = 2;
+  static constexpr int kMinBlocks = 2;
+  static constexpr bool kAccumulate = true;
+  const int32_t* occp;  // occupied parents at level l-1
+  int q, qp;
+  int64_t Gp;
+  const double* Lp;
+  const double* shift;  // 4 x (q x qp), stacked
+  double* L;
+  __device__ int rows(int) const { return 4 * q; }
+  __device__ int nsegs(int) const { return 1; }
+  __device__ bool seg(int task, int, Seg& d) const {
+    d.K = qp;
+    d.gen = false;
+    d.a = shift;
+    d.a_rs = qp;
+    d.a_cs = 1;
+    d.b = Lp + (int64_t)occp[task] * qp * kcols;
+    d.ldb = kcols;
+    d.b_rows = nullptr;
+    d.bmask = nullptr;
+    return true;
+  }
+  __device__ double* out_row(int task, int r) const {
+    int64_t P = occp[task], X = P / Gp, Y = P % Gp;
+    int c = r / q;
+    int64_t child = (2 * X + (c >> 1)) * (2 * Gp) + (2 * Y + (c & 1));
+    return L + (child * q + (r % q)) * kcols;
+  }
+};
+
+// L2P (fmm.py:366): U[p][:] += sum_a W2[p][a] L_leaf[a][:]  (kAdd = false:
+// store, for the sparse path where the near field is added afterwards)
+template <bool kAdd>
+struct L2PProv : ProvBase {
+  static constexpr int kStage = ST_L2P;
+  static constexpr int kStages = 2;
+  static constexpr int kMinBlocks = 2;
+  static constexpr bool kAccumulate = kAdd;
   const int32_t *leaf_box, *leaf_start, *leaf_count;
   const double* W2s;
   int q;
@@ -179,6 +260,7 @@ struct L2PProv : ProvBase {
     d.b = L + (int64_t)leaf_box[task] * q * kcols;
     d.ldb = kcols;
     d.b_rows = nullptr;
+    d.bmask = nullptr;
     return true;
   }
   __device__ double* out_row(int task, int r) const { return U + order[leaf_start[task] + r] * ldu; }
@@ -190,13 +272,114 @@ int launch(const Prov& p, int64_t tasks, int64_t max_rows, int64_t kcols, cudaSt
   static bool configured = false;
   if (!configured) {
     HIKF_CHECK_CUDA(cudaFuncSetAttribute(seg_gemm_kernel<Prov>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SG_SMEM));
+                                         (int)sg_smem<Prov>()));
     configured = true;
   }
   dim3 grid((unsigned)tasks, (unsigned)ceil_div(max_rows, SG_R), (unsigned)ceil_div(kcols, SG_BN));
-  seg_gemm_kernel<Prov><<<grid, SG_THREADS, SG_SMEM, st>>>(p);
+  Prov q = p;
+  if (!q.flops) q.flops = prof_flops_ptr(Prov::kStage);
+  seg_gemm_kernel<Prov><<<grid, SG_THREADS, sg_smem<Prov>(), st>>>(q);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
+}
+
+}  // namespace
+
+namespace {
+
+bool aligned16(const void* p, int64_t ld) { return (((uintptr_t)p & 15) == 0) && (ld % 2 == 0); }
+
+// bytes per column of the expansion workspace: all W levels + two L levels
+int64_t expansion_bytes_per_col(const hikf_tree* t) {
+  const int D = t->depth;
+  if (D < 2) return 0;
+  int64_t per_col = 0;
+  for (int l = 2; l <= D; ++l) per_col += (int64_t)8 * ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l];
+  per_col += (int64_t)8 * ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D];
+  if (D > 2) per_col += (int64_t)8 * ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1];
+  return per_col;
+}
+
+template <class P>
+void set_base(P& p, const hikf_tree* t, int64_t kc, int64_t gofs, int64_t ngroups, bool vecB) {
+  p.kcols = kc;
+  p.gofs = gofs;
+  p.ngroups = ngroups;
+  p.vecB = vecB;
+  p.kp = t->kp;
+}
+
+// M2M, M2L (+L2L) and L2P for one column pass whose leaf multipoles are in
+// Wl[D].  masks[l] (sparse charges) lets the DMMA stages skip zero groups.
+template <bool kL2PAdd>
+int far_field(hikf_tree* t, double* const* Wl, double* const* Lbuf, int64_t kc, int64_t gofs, int64_t ngroups,
+              uint8_t* const* masks, double* Uc, int64_t ldu, cudaStream_t st) {
+  const int D = t->depth;
+  const int qD = t->orders[D] * t->orders[D];
+  for (int l = D - 1; l >= 2; --l) {
+    M2MProv mm;
+    set_base(mm, t, kc, gofs, ngroups, aligned16(Wl[l + 1], kc));
+    mm.occ = t->occ[l];
+    mm.child_flag = t->occ_flag[l + 1];
+    mm.shift = t->shift[l];
+    mm.qp = t->orders[l] * t->orders[l];
+    mm.qc = t->orders[l + 1] * t->orders[l + 1];
+    mm.Gp = (int64_t)1 << l;
+    mm.Wc = Wl[l + 1];
+    mm.Wp = Wl[l];
+    mm.cmask = masks ? masks[l + 1] : nullptr;
+    ProfScope ps(ST_M2M, st);
+    HIKF_TRY(launch(mm, t->n_occ[l], mm.qp, kc, st));
+  }
+  const double* Lprev = nullptr;
+  double* Lcur = nullptr;
+  for (int l = 2; l <= D; ++l) {
+    Lcur = Lbuf[(D - l) & 1];
+    M2LProv ml;
+    set_base(ml, t, kc, gofs, ngroups, aligned16(Wl[l], kc) && aligned16(Lbuf[0], kc) && aligned16(Lbuf[1], kc));
+    ml.occ = t->occ[l];
+    ml.flag = t->occ_flag[l];
+    ml.ops = t->m2l[l];
+    ml.present = t->m2l_present[l];
+    ml.q = t->orders[l] * t->orders[l];
+    ml.G = (int64_t)1 << l;
+    ml.W = Wl[l];
+    ml.L = Lcur;
+    ml.smask = masks ? masks[l] : nullptr;
+    ml.Lp = Lprev;
+    ml.shift = l > 2 ? t->shift[l - 1] : nullptr;
+    ml.qp = l > 2 ? t->orders[l - 1] * t->orders[l - 1] : 0;
+    {
+      ProfScope ps(ST_M2L, st);
+      HIKF_TRY(launch(ml, t->n_occ[l], ml.q, kc, st));
+    }
+    Lprev = Lcur;
+  }
+  L2PProv<kL2PAdd> lp;
+  set_base(lp, t, kc, gofs, ngroups, aligned16(Lcur, kc));
+  lp.leaf_box = t->leaf_box;
+  lp.leaf_start = t->leaf_start;
+  lp.leaf_count = t->leaf_count;
+  lp.W2s = t->W2s;
+  lp.q = qD;
+  lp.order = t->order;
+  lp.L = Lcur;
+  lp.U = Uc;
+  lp.ldu = ldu;
+  ProfScope ps(ST_L2P, st);
+  return launch(lp, t->n_leaves, t->max_count, kc, st);
+}
+
+void carve(const hikf_tree* t, double* ws, int64_t kc, double** Wl, double** Lbuf) {
+  const int D = t->depth;
+  double* cur = ws;
+  for (int l = 2; l <= D; ++l) {
+    Wl[l] = cur;
+    cur += ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * kc;
+  }
+  Lbuf[0] = cur;  // holds the levels with the parity of D
+  cur += ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * kc;
+  Lbuf[1] = cur;
 }
 
 }  // namespace
@@ -205,13 +388,8 @@ int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U,
   if (k <= 0) return HIKF_OK;
   const int D = t->depth;
   // column pass width: keep the expansion workspace within ~24 GiB
-  int64_t per_col = 0;  // bytes per column: all W levels + two L levels
-  if (D >= 2) {
-    for (int l = 2; l <= D; ++l) per_col += (int64_t)8 * ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l];
-    per_col += (int64_t)8 * ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D];
-    if (D > 2) per_col += (int64_t)8 * ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1];
-  }
-  int64_t budget = (int64_t)24 << 30;
+  const int64_t per_col = expansion_bytes_per_col(t);
+  const int64_t budget = (int64_t)24 << 30;
   int64_t kpass = k;
   if (per_col > 0 && per_col * kpass > budget) kpass = std::max<int64_t>(SG_BN, (budget / per_col) / SG_BN * SG_BN);
 
@@ -222,10 +400,10 @@ int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U,
     const int64_t kc = std::min(kpass, k - c0);
     const double* Vc = V + c0;
     double* Uc = U + c0;
+    const bool vecV = aligned16(Vc, ldv);
     // ---- near field: U = near @ V ----
     P2PProv pp;
-    pp.kcols = kc;
-    pp.kp = t->kp;
+    set_base(pp, t, kc, 0, 0, vecV);
     pp.leaf_box = t->leaf_box;
     pp.leaf_start = t->leaf_start;
     pp.leaf_count = t->leaf_count;
@@ -242,24 +420,13 @@ int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U,
       HIKF_TRY(launch(pp, t->n_leaves, t->max_count, kc, st));
     }
     if (D < 2) continue;
-
-    // workspace carve: W[l] for l = 2..D, then L ping-pong (level D and D-1 sized)
     double* Wl[kMaxDepth + 1] = {nullptr};
-    double* cur = ws;
-    for (int l = 2; l <= D; ++l) {
-      Wl[l] = cur;
-      cur += ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * kc;
-    }
     double* Lbuf[2];
-    Lbuf[0] = cur;  // holds levels with parity of D
-    cur += ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * kc;
-    Lbuf[1] = cur;
-
-    // ---- upward pass: P2M then M2M ----
+    carve(t, ws, kc, Wl, Lbuf);
+    // ---- upward pass: P2M ----
     const int qD = t->orders[D] * t->orders[D];
     P2MProv pm;
-    pm.kcols = kc;
-    pm.kp = t->kp;
+    set_base(pm, t, kc, 0, 0, vecV);
     pm.leaf_box = t->leaf_box;
     pm.leaf_start = t->leaf_start;
     pm.leaf_count = t->leaf_count;
@@ -273,66 +440,107 @@ int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U,
       ProfScope ps(ST_P2M, st);
       HIKF_TRY(launch(pm, t->n_leaves, qD, kc, st));
     }
-    for (int l = D - 1; l >= 2; --l) {
-      M2MProv mm;
-      mm.kcols = kc;
-      mm.kp = t->kp;
-      mm.occ = t->occ[l];
-      mm.child_flag = t->occ_flag[l + 1];
-      mm.shift = t->shift[l];
-      mm.qp = t->orders[l] * t->orders[l];
-      mm.qc = t->orders[l + 1] * t->orders[l + 1];
-      mm.Gp = (int64_t)1 << l;
-      mm.Wc = Wl[l + 1];
-      mm.Wp = Wl[l];
-      ProfScope ps(ST_M2M, st);
-      HIKF_TRY(launch(mm, t->n_occ[l], mm.qp, kc, st));
-    }
-    // ---- downward pass: M2L (+ L2L) per level ----
-    const double* Lprev = nullptr;
-    double* Lcur = nullptr;
-    for (int l = 2; l <= D; ++l) {
-      Lcur = Lbuf[(D - l) & 1];
-      M2LProv ml;
-      ml.kcols = kc;
-      ml.kp = t->kp;
-      ml.occ = t->occ[l];
-      ml.flag = t->occ_flag[l];
-      ml.ops = t->m2l[l];
-      ml.present = t->m2l_present[l];
-      ml.q = t->orders[l] * t->orders[l];
-      ml.G = (int64_t)1 << l;
-      ml.W = Wl[l];
-      ml.L = Lcur;
-      ml.Lp = Lprev;
-      ml.shift = l > 2 ? t->shift[l - 1] : nullptr;
-      ml.qp = l > 2 ? t->orders[l - 1] * t->orders[l - 1] : 0;
-      {
-        ProfScope ps(ST_M2L, st);
-        HIKF_TRY(launch(ml, t->n_occ[l], ml.q, kc, st));
-      }
-      Lprev = Lcur;
-    }
-    // ---- L2P: U += interp @ local ----
-    L2PProv lp;
-    lp.kcols = kc;
-    lp.kp = t->kp;
-    lp.leaf_box = t->leaf_box;
-    lp.leaf_start = t->leaf_start;
-    lp.leaf_count = t->leaf_count;
-    lp.W2s = t->W2s;
-    lp.q = qD;
-    lp.order = t->order;
-    lp.L = Lcur;
-    lp.U = Uc;
-    lp.ldu = ldu;
-    {
-      ProfScope ps(ST_L2P, st);
-      HIKF_TRY(launch(lp, t->n_leaves, t->max_count, kc, st));
-    }
+    // ---- M2M, M2L + L2L, L2P: U += interp @ local ----
+    HIKF_TRY(far_field<true>(t, Wl, Lbuf, kc, 0, 0, nullptr, Uc, ldu, st));
   }
   if (ws) HIKF_CHECK_CUDA(cudaFreeAsync(ws, st));
   return HIKF_OK;
+}
+
+int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
+                    cudaStream_t st) {
+  if (n <= 0) return HIKF_OK;
+  const int D = t->depth;
+  SparseHt sp;
+  {
+    ProfScope ps(ST_DENSIFY, st);  // the regrouping of H^T replaces the densify step
+    HIKF_TRY(sparse_build(t, n, ip, ix, val, &sp, st));
+  }
+  int status = HIKF_OK;
+  if (D >= 2) {
+    // ---- upward pass on the active (box, ray) pairs only ----
+    PairLevel pl[kMaxDepth + 1];
+    {
+      ProfScope ps(ST_P2M, st);
+      status = pairs_leaf(t, sp, &pl[D], st);
+    }
+    for (int l = D - 1; l >= 2 && status == HIKF_OK; --l) {
+      ProfScope ps(ST_M2M, st);
+      status = pairs_parent(t, l, pl[l + 1], n, &pl[l], st);
+    }
+    // ---- downward pass: dense locals (every box gets a far field) ----
+    // M2L accumulates per offset into a pair-major scratch (q contiguous
+    // coefficients per (box, ray)); l2l_transpose then adds the parent shift
+    // and writes the box-major locals the L2L/L2P GEMMs consume.
+    double* Lbuf[2] = {nullptr, nullptr};
+    double* scratch = nullptr;
+    const int64_t szD = ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * n;
+    const int64_t szD1 = ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1] * n;
+    int64_t szS = 0;
+    for (int l = 2; l <= D; ++l) szS = std::max<int64_t>(szS, ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n);
+    if (status == HIKF_OK) {
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * szD, st));
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * std::max<int64_t>(szD1, 1), st));
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch, sizeof(double) * szS, st));
+    }
+    const bool vec = (n % 2) == 0;
+    const double* Lprev = nullptr;
+    double* Lcur = nullptr;
+    for (int l = 2; l <= D && status == HIKF_OK; ++l) {
+      Lcur = Lbuf[(D - l) & 1];
+      const int q = t->orders[l] * t->orders[l];
+      {
+        ProfScope ps(ST_M2L, st);
+        HIKF_CHECK_CUDA(cudaMemsetAsync(scratch, 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, st));
+        for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
+          status = m2l_pass(t, l, slot, pl[l], n, scratch, st);
+      }
+      if (status == HIKF_OK) {
+        ProfScope ps(ST_L2L, st);
+        status = pair_to_box(t, l, scratch, n, Lcur, st);
+        if (status == HIKF_OK && l > 2) {
+          L2LParentProv ll;
+          set_base(ll, t, n, 0, 0, vec);
+          ll.occp = t->occ[l - 1];
+          ll.q = q;
+          ll.qp = t->orders[l - 1] * t->orders[l - 1];
+          ll.Gp = (int64_t)1 << (l - 1);
+          ll.Lp = Lprev;
+          ll.shift = t->shift[l - 1];
+          ll.L = Lcur;
+          status = launch(ll, t->n_occ[l - 1], 4 * q, n, st);
+        }
+      }
+      Lprev = Lcur;
+    }
+    if (status == HIKF_OK) {
+      L2PProv<false> lp;
+      set_base(lp, t, n, 0, 0, vec);
+      lp.leaf_box = t->leaf_box;
+      lp.leaf_start = t->leaf_start;
+      lp.leaf_count = t->leaf_count;
+      lp.W2s = t->W2s;
+      lp.q = t->orders[D] * t->orders[D];
+      lp.order = t->order;
+      lp.L = Lcur;
+      lp.U = U;
+      lp.ldu = n;
+      ProfScope ps(ST_L2P, st);
+      status = launch(lp, t->n_leaves, t->max_count, n, st);
+    }
+    for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
+    cudaFreeAsync(scratch, st);
+    cudaFreeAsync(Lbuf[0], st);
+    cudaFreeAsync(Lbuf[1], st);
+  } else {
+    HIKF_CHECK_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * t->m * n, st));
+  }
+  if (status == HIKF_OK) {
+    ProfScope ps(ST_P2P, st);
+    status = sparse_p2p(t, sp, U, n, st);
+  }
+  sparse_free(&sp, st);
+  return status;
 }
 
 }  // namespace hikf

@@ -14,6 +14,11 @@
 // shared memory and accumulates with FP64 DMMA (mma.sync m8n8k4) into
 // registers; CTA tile = 64 rows x 128 columns, 8 warps, each warp owns 16
 // columns x all 8 row tiles.
+//
+// Sparse charges (V = H^T): a segment may carry an activity mask (one byte
+// per 8-column group of its B block).  Inactive groups are exact zeros, so
+// their loads and DMMAs are skipped -- the sums are the same numbers (a skipped
+// product is +-0), only the work shrinks.
 #pragma once
 
 #include "common.cuh"
@@ -42,6 +47,9 @@ constexpr int SG_AS = SG_KC + 4;  // smem row strides (doubles), == 4 mod 16: co
 constexpr int SG_BS = SG_BN + 4;
 constexpr int SG_STAGE_DOUBLES = SG_R * SG_AS + SG_KC * SG_BS;
 constexpr size_t SG_SMEM = (size_t)SG_STAGES * SG_STAGE_DOUBLES * sizeof(double) + 64;
+// shared memory of a provider's pipeline depth
+template <class Prov>
+constexpr size_t sg_smem() { return (size_t)Prov::kStages * SG_STAGE_DOUBLES * sizeof(double) + 64; }
 
 // One segment of an output block.
 struct Seg {
@@ -54,13 +62,31 @@ struct Seg {
   const double* b;            // B[kk][c] = b[(b_rows ? b_rows[kk] : kk) * ldb + c]
   int64_t ldb;
   const int64_t* b_rows;
+  const uint8_t* bmask;       // per 8-column group activity of B (absolute groups), null = dense
+};
+
+// Base of every provider: columns of this pass and the kernel parameters.
+struct ProvBase {
+  static constexpr int kStages = SG_STAGES;  // cp.async ring depth (long K: interaction lists)
+  static constexpr int kMinBlocks = 1;       // CTAs per SM the register budget must allow
+  unsigned long long* flops = nullptr;       // useful-flop counter (profiling) or null
+  int64_t kcols = 0;   // columns of this pass
+  int64_t gofs = 0;    // absolute 8-column group of column 0 of the pass (masks)
+  int64_t ngroups = 0; // groups per mask row
+  bool vecB = false;   // B rows 16-byte aligned with an even leading dimension
+  KParams kp;
+  __device__ int64_t ncols() const { return kcols; }
+  __device__ double kernel(double r) const { return kernel_of_r(kp, r); }
 };
 
 template <class Prov>
-__global__ void __launch_bounds__(SG_THREADS, 1) seg_gemm_kernel(Prov prov) {
+__global__ void __launch_bounds__(SG_THREADS, Prov::kMinBlocks) seg_gemm_kernel(Prov prov) {
+  constexpr int STAGES = Prov::kStages;
   extern __shared__ double smem_raw[];
   double* smem = smem_raw;
-  __shared__ int stage_k[SG_STAGES];
+  __shared__ int stage_k[STAGES];
+  __shared__ unsigned stage_am[STAGES];
+  unsigned long long useful = 0;  // thread 0: 2 * rows * k * active columns
 
   const int task = blockIdx.x;
   const int row0 = blockIdx.y * SG_R;
@@ -73,15 +99,32 @@ __global__ void __launch_bounds__(SG_THREADS, 1) seg_gemm_kernel(Prov prov) {
   const int g = lane >> 2, t4 = lane & 3;
   const int rows_here = min(SG_R, nrows - row0);
   const int nrt = (rows_here + 7) >> 3;  // active 8-row tiles
+  const int arows = nrt * 8;
+  // groups of this column tile that exist at all
+  const int ncol_here = (int)(ncols - col0 < SG_BN ? ncols - col0 : SG_BN);
+  const unsigned all_groups = ncol_here >= SG_BN ? 0xffffu : ((1u << ((ncol_here + 7) >> 3)) - 1u);
+  const int64_t g0 = prov.gofs + col0 / 8;
+
+  auto activity = [&](const Seg& s) -> unsigned {
+    if (!s.bmask) return all_groups;
+    unsigned am = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (g0 + q < prov.ngroups && s.bmask[g0 + q]) am |= 1u << q;
+    return am & all_groups;
+  };
 
   // producer cursor
   int cur_seg = 0, cur_k = 0;
+  unsigned cur_am = 0;
   Seg sd;
   sd.K = 0;
-  // advance to the first valid (segment, k) position
   auto next_valid = [&](int s) {
     while (s < nsegs) {
-      if (prov.seg(task, s, sd) && sd.K > 0) return s;
+      if (prov.seg(task, s, sd) && sd.K > 0) {
+        cur_am = activity(sd);
+        if (cur_am) return s;
+      }
       ++s;
     }
     return s;
@@ -96,9 +139,11 @@ __global__ void __launch_bounds__(SG_THREADS, 1) seg_gemm_kernel(Prov prov) {
       return;
     }
     const int kc = min(SG_KC, sd.K - cur_k);
-    // A tile: SG_R x SG_KC, zero outside (rows_here, kc)
-    for (int e = tid; e < SG_R * SG_KC; e += SG_THREADS) {
+    const int kc4 = (kc + 3) & ~3;  // zero-fill up to the DMMA k granularity
+    // A tile: arows x kc4 (rows beyond rows_here only feed unstored accumulators)
+    for (int e = tid; e < arows * SG_KC; e += SG_THREADS) {
       int r = e / SG_KC, kk = e % SG_KC;
+      if (kk >= kc4) continue;
       bool ok = r < rows_here && kk < kc;
       double* dst = As + r * SG_AS + kk;
       if (sd.gen) {
@@ -114,18 +159,38 @@ __global__ void __launch_bounds__(SG_THREADS, 1) seg_gemm_kernel(Prov prov) {
         cp_async8(dst, src, ok);
       }
     }
-    // B tile: SG_KC x SG_BN
-    for (int e = tid; e < SG_KC * SG_BN; e += SG_THREADS) {
-      int kk = e / SG_BN, c = e % SG_BN;
-      bool ok = kk < kc && col0 + c < ncols;
-      const double* src = sd.b;
-      if (ok) {
-        int64_t row = sd.b_rows ? sd.b_rows[cur_k + kk] : (int64_t)(cur_k + kk);
-        src = sd.b + row * sd.ldb + col0 + c;
+    // B tile: kc4 x SG_BN, only the active 8-column groups
+    if (prov.vecB) {
+      for (int e = tid; e < SG_KC * (SG_BN / 2); e += SG_THREADS) {
+        int kk = e / (SG_BN / 2), c = (e % (SG_BN / 2)) * 2;
+        if (kk >= kc4 || !((cur_am >> (c >> 3)) & 1)) continue;
+        int bytes = 0;
+        const double* src = sd.b;
+        if (kk < kc && col0 + c < ncols) {
+          int64_t row = sd.b_rows ? sd.b_rows[cur_k + kk] : (int64_t)(cur_k + kk);
+          src = sd.b + row * sd.ldb + col0 + c;
+          bytes = col0 + c + 1 < ncols ? 16 : 8;
+        }
+        cp_async16(Bs + kk * SG_BS + c, src, bytes);
       }
-      cp_async8(Bs + kk * SG_BS + c, src, ok);
+    } else {
+      for (int e = tid; e < SG_KC * SG_BN; e += SG_THREADS) {
+        int kk = e / SG_BN, c = e % SG_BN;
+        if (kk >= kc4 || !((cur_am >> (c >> 3)) & 1)) continue;
+        bool ok = kk < kc && col0 + c < ncols;
+        const double* src = sd.b;
+        if (ok) {
+          int64_t row = sd.b_rows ? sd.b_rows[cur_k + kk] : (int64_t)(cur_k + kk);
+          src = sd.b + row * sd.ldb + col0 + c;
+        }
+        cp_async8(Bs + kk * SG_BS + c, src, ok);
+      }
     }
-    if (tid == 0) stage_k[stage] = kc;
+    if (tid == 0) {
+      stage_k[stage] = kc;
+      stage_am[stage] = cur_am;
+      useful += 2ull * rows_here * kc * (8ull * __popc(cur_am));
+    }
     // advance the cursor
     cur_k += SG_KC;
     if (cur_k >= sd.K) {
@@ -141,39 +206,42 @@ __global__ void __launch_bounds__(SG_THREADS, 1) seg_gemm_kernel(Prov prov) {
     for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < SG_STAGES - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     issue(s);
     cp_async_commit();
   }
   for (int it = 0;; ++it) {
-    cp_async_wait<SG_STAGES - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const int stage = it % SG_STAGES;
+    const int stage = it % STAGES;
     const int kc = stage_k[stage];
     if (kc == 0) break;
+    const unsigned am = stage_am[stage];
     // refill the slot consumed in the previous iteration
-    issue((it + SG_STAGES - 1) % SG_STAGES);
+    issue((it + STAGES - 1) % STAGES);
     cp_async_commit();
 
+    const bool on0 = (am >> (2 * warp)) & 1, on1 = (am >> (2 * warp + 1)) & 1;
+    if (!(on0 || on1)) continue;
     const double* As = smem + stage * SG_STAGE_DOUBLES;
     const double* Bs = As + SG_R * SG_AS;
     const int nk4 = (kc + 3) >> 2;
     for (int k4 = 0; k4 < nk4; ++k4) {
       const int kb = k4 * 4;
-      double bf[2];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[(kb + t4) * SG_BS + warp * 16 + j * 8 + g];
+      double bf0 = Bs[(kb + t4) * SG_BS + warp * 16 + g];
+      double bf1 = Bs[(kb + t4) * SG_BS + warp * 16 + 8 + g];
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         if (i < nrt) {
           double af = As[(i * 8 + g) * SG_AS + kb + t4];
-          dmma884(acc[i][0][0], acc[i][0][1], af, bf[0]);
-          dmma884(acc[i][1][0], acc[i][1][1], af, bf[1]);
+          if (on0) dmma884(acc[i][0][0], acc[i][0][1], af, bf0);
+          if (on1) dmma884(acc[i][1][0], acc[i][1][1], af, bf1);
         }
       }
     }
   }
   cp_async_wait<0>();
+  if (prov.flops && tid == 0 && useful) atomicAdd(prov.flops, useful);
 
   // epilogue: store or accumulate into the output rows
 #pragma unroll

@@ -18,6 +18,7 @@ std::mutex g_mu;
 bool g_on = false;
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_pool;
+unsigned long long* g_flops = nullptr;  // ST_COUNT device counters
 
 cudaEvent_t take() {
   if (!g_pool.empty()) {
@@ -30,6 +31,16 @@ cudaEvent_t take() {
   return e;
 }
 }  // namespace
+
+unsigned long long* prof_flops_ptr(int stage) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_on) return nullptr;
+  if (!g_flops) {
+    if (cudaMalloc(&g_flops, sizeof(unsigned long long) * ST_COUNT) != cudaSuccess) return nullptr;
+    cudaMemset(g_flops, 0, sizeof(unsigned long long) * ST_COUNT);
+  }
+  return g_flops + stage;
+}
 
 ProfScope::ProfScope(int stage, cudaStream_t st) : stage_(stage), st_(st), active_(false) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -67,6 +78,23 @@ int hikf_prof_reset(void) {
     g_pool.push_back(r.b);
   }
   g_recs.clear();
+  if (g_flops) {
+    cudaDeviceSynchronize();
+    cudaMemset(g_flops, 0, sizeof(unsigned long long) * ST_COUNT);
+  }
+  return HIKF_OK;
+}
+
+int hikf_prof_flops(int32_t stage, uint64_t* out) {
+  if (!out || stage < 0 || stage >= ST_COUNT) return HIKF_BAD_ARGUMENT;
+  *out = 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_flops) {
+    cudaDeviceSynchronize();
+    unsigned long long v = 0;
+    cudaMemcpy(&v, g_flops + stage, sizeof(v), cudaMemcpyDeviceToHost);
+    *out = v;
+  }
   return HIKF_OK;
 }
 

@@ -19,9 +19,13 @@ enum Stage {
   ST_M2M = 7,
   ST_M2L = 8,
   ST_L2P = 9,
-  ST_DENSIFY = 10, // H^T scatter for the precompute
-  ST_COUNT = 11
+  ST_DENSIFY = 10, // H^T regrouping (sparse charges) / scatter
+  ST_L2L = 11,     // parent-to-child locals (sparse path; fused into M2L on the dense path)
+  ST_COUNT = 12
 };
+
+// device counter of useful flops of a stage while profiling is enabled, else null
+unsigned long long* prof_flops_ptr(int stage);
 
 class ProfScope {
  public:

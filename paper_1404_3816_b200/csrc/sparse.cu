@@ -1,0 +1,721 @@
+// Q H^T with the charges V = H^T kept sparse (filters.py:101-102 densifies
+// H^T on the host; here it never exists densely anywhere).
+//
+// H (CSR, n rays x m cells) is regrouped on the device into "entries"
+// (sorted position of the cell, ray j, length) ordered by (leaf, j, cell):
+// for the crosswell operator a leaf holds ~10 rays x ~8 cells, so
+//   * P2M becomes a tiny per-(leaf, ray) sum (W_leaf[a][j] = sum S_a(x_p) h_jp),
+//   * P2P becomes, per active (target leaf, ray) item, a direct sum over the
+//     ray's cells in the 3x3 neighbourhood (the reference's near @ V restricted
+//     to its nonzeros -- the skipped terms are exact zeros),
+//   * every multipole carries an 8-column activity mask that lets the DMMA
+//     M2M/M2L stages skip exact-zero column groups.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "fmm_device.cuh"
+#include "prof.h"
+#include "sparse.h"
+#include "tree.h"
+
+namespace hikf {
+
+namespace {
+
+constexpr int kT = 256;
+
+int grid_for(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms() * 32));
+}
+
+// one CTA per ray: key = leaf * n + j, value = CSR position
+__global__ void entry_keys(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
+                           const int32_t* __restrict__ inv_order, const int32_t* __restrict__ leaf_of,
+                           int64_t* __restrict__ key, int32_t* __restrict__ pos) {
+  int64_t j = blockIdx.x;
+  for (int64_t e = ip[j] + threadIdx.x; e < ip[j + 1]; e += blockDim.x) {
+    int32_t sp = inv_order[ix[e]];
+    key[e] = (int64_t)leaf_of[sp] * n + j;
+    pos[e] = (int32_t)e;
+  }
+}
+
+__global__ void entry_gather(int64_t nnz, int64_t n, const int64_t* __restrict__ key, const int32_t* __restrict__ pos,
+                             const int32_t* __restrict__ ix, const double* __restrict__ val,
+                             const int32_t* __restrict__ inv_order, int32_t* __restrict__ e_sp,
+                             int32_t* __restrict__ e_j, double* __restrict__ e_v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t p = pos[i];
+    e_sp[i] = inv_order[ix[p]];
+    e_j[i] = (int32_t)(key[i] % n);
+    e_v[i] = val[p];
+  }
+}
+
+// groups: run starts of equal (leaf, j) keys
+__global__ void group_tables(int64_t ng, int64_t n, const int64_t* __restrict__ gkey, const int32_t* __restrict__ gcnt,
+                             const int32_t* __restrict__ gstart_excl, int32_t* __restrict__ g_j,
+                             int32_t* __restrict__ g_leaf, int32_t* __restrict__ g_start) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x) {
+    g_j[i] = (int32_t)(gkey[i] % n);
+    g_leaf[i] = (int32_t)(gkey[i] / n);
+    g_start[i] = gstart_excl[i];
+    if (i == ng - 1) g_start[ng] = gstart_excl[i] + gcnt[i];
+  }
+}
+
+// leaf_g[L] = first group with leaf >= L (binary search), L in [0, nleaves]
+__global__ void leaf_group_offsets(int64_t nleaves, int64_t ng, const int32_t* __restrict__ g_leaf,
+                                   int32_t* __restrict__ leaf_g) {
+  for (int64_t L = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; L <= nleaves; L += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = ng;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (g_leaf[mid] < L) lo = mid + 1; else hi = mid;
+    }
+    leaf_g[L] = (int32_t)lo;
+  }
+}
+
+// leaf-level mask: a leaf box is active for group j/8 if it holds a nonzero of ray j
+__global__ void leaf_mask(int64_t ng, const int32_t* __restrict__ g_leaf, const int32_t* __restrict__ g_j,
+                          const int32_t* __restrict__ leaf_box, int64_t ngr, uint8_t* __restrict__ mask) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x)
+    mask[(int64_t)leaf_box[g_leaf[i]] * ngr + g_j[i] / 8] = 1;
+}
+
+// parent mask = OR of the four children (exact: a parent multipole is a sum of children's)
+__global__ void parent_mask(int64_t Gp, int64_t ngr, const uint8_t* __restrict__ child, uint8_t* __restrict__ parent) {
+  int64_t total = Gp * Gp * ngr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t box = e / ngr, gg = e % ngr, X = box / Gp, Y = box % Gp;
+    uint8_t v = 0;
+    for (int c = 0; c < 4; ++c) {
+      int64_t ch = (2 * X + (c >> 1)) * (2 * Gp) + (2 * Y + (c & 1));
+      v |= child[ch * ngr + gg];
+    }
+    parent[e] = v;
+  }
+}
+
+// candidate P2P items: for every (source leaf, j) group, the <= 9 adjacent
+// occupied target leaves; key = target * n + j (INT64_MAX = none)
+__global__ void item_candidates(int64_t ng, int64_t n, int64_t G, const int32_t* __restrict__ g_leaf,
+                                const int32_t* __restrict__ g_j, const int32_t* __restrict__ leaf_box,
+                                const int32_t* __restrict__ box2leaf, int64_t* __restrict__ cand) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t box = leaf_box[g_leaf[i]], bx = box / G, by = box % G;
+    for (int s = 0; s < 9; ++s) {
+      int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
+      int64_t k = INT64_MAX;
+      if (nx >= 0 && nx < G && ny >= 0 && ny < G) {
+        int32_t T = box2leaf[nx * G + ny];
+        if (T >= 0) k = (int64_t)T * n + g_j[i];
+      }
+      cand[i * 9 + s] = k;
+    }
+  }
+}
+
+// Sparse P2M: W_leaf[a][j] = sum_{entries (p, j, v) of the leaf} W2[p][a] v, and
+// zeros for the inactive columns of every active 8-column group.
+__global__ void p2m_sparse(int q, int64_t kcols, int64_t c0, int64_t ngr, const int32_t* __restrict__ leaf_box,
+                           const int32_t* __restrict__ leaf_g, const int32_t* __restrict__ g_j,
+                           const int32_t* __restrict__ g_start, const int32_t* __restrict__ e_sp,
+                           const double* __restrict__ e_v, const double* __restrict__ W2s,
+                           const uint8_t* __restrict__ mask, double* __restrict__ W) {
+  const int64_t L = blockIdx.x;
+  const int64_t box = leaf_box[L];
+  const int32_t gb = leaf_g[L], ge = leaf_g[L + 1];
+  if (gb == ge) return;
+  double* Wb = W + box * q * kcols;
+  const uint8_t* mrow = mask + box * ngr;
+  // zero the active groups of this column pass [c0, c0 + kcols)
+  for (int64_t e = threadIdx.x; e < (int64_t)q * kcols; e += blockDim.x) {
+    int64_t a = e / kcols, c = e % kcols;
+    if (mrow[(c0 + c) >> 3]) Wb[a * kcols + c] = 0.0;
+  }
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < (int64_t)(ge - gb) * q; e += blockDim.x) {
+    int32_t gi = gb + (int32_t)(e / q);
+    int a = (int)(e % q);
+    int64_t c = (int64_t)g_j[gi] - c0;
+    if (c < 0 || c >= kcols) continue;
+    double s = 0.0;
+    for (int32_t k = g_start[gi]; k < g_start[gi + 1]; ++k) s += W2s[(int64_t)e_sp[k] * q + a] * e_v[k];
+    Wb[(int64_t)a * kcols + c] = s;
+  }
+}
+
+// Sparse P2P, one warp per active (target leaf T, ray j):
+// U[t][j] += sum_{adjacent leaves s (ox outer, oy inner)} sum_{entries (p, j, v) in s} K(x_t, x_p) v
+__global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, int64_t n, int64_t G, KParams kp,
+                           const int32_t* __restrict__ leaf_box, const int32_t* __restrict__ leaf_start,
+                           const int32_t* __restrict__ leaf_count, const int32_t* __restrict__ box2leaf,
+                           const int32_t* __restrict__ leaf_g, const int32_t* __restrict__ g_j,
+                           const int32_t* __restrict__ g_start, const int32_t* __restrict__ e_sp,
+                           const double* __restrict__ e_v, const double* __restrict__ xy_s,
+                           const int64_t* __restrict__ order, double* __restrict__ U, int64_t ldu,
+                           unsigned long long* __restrict__ flops) {
+  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (item >= nitems) return;
+  const int64_t key = items[item];
+  const int32_t T = (int32_t)(key / n);
+  const int32_t j = (int32_t)(key % n);
+  const int64_t box = leaf_box[T], bx = box / G, by = box % G;
+  // the <= 9 entry ranges of ray j in the adjacent leaves
+  int32_t rb[9], re[9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    rb[s] = re[s] = 0;
+    int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
+    if (nx < 0 || nx >= G || ny < 0 || ny >= G) continue;
+    int32_t S = box2leaf[nx * G + ny];
+    if (S < 0) continue;
+    int32_t lo = leaf_g[S], hi = leaf_g[S + 1];
+    while (lo < hi) {
+      int32_t mid = (lo + hi) >> 1;
+      if (g_j[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    if (lo < leaf_g[S + 1] && g_j[lo] == j) {
+      rb[s] = g_start[lo];
+      re[s] = g_start[lo + 1];
+    }
+  }
+  const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
+  if (flops && lane == 0) {
+    unsigned long long ne = 0;
+    for (int s = 0; s < 9; ++s) ne += re[s] - rb[s];
+    atomicAdd(flops, 2ull * ne * cnt);
+  }
+  for (int tb = 0; tb < cnt; tb += 32) {
+    const int t = tb + lane;
+    const bool ok = t < cnt;
+    double tx = 0.0, ty = 0.0;
+    if (ok) {
+      tx = xy_s[2 * (int64_t)(t0 + t)];
+      ty = xy_s[2 * (int64_t)(t0 + t) + 1];
+    }
+    double acc = 0.0;
+#pragma unroll 1
+    for (int s = 0; s < 9; ++s)
+      for (int32_t k = rb[s]; k < re[s]; ++k) {
+        const int32_t p = e_sp[k];
+        const double v = e_v[k];
+        acc += kernel_of_r(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
+      }
+    if (ok) U[order[t0 + t] * ldu + j] += acc;
+  }
+}
+
+}  // namespace
+
+void sparse_free(SparseHt* s, cudaStream_t st) {
+  cudaFreeAsync(s->e_sp, st);
+  cudaFreeAsync(s->e_j, st);
+  cudaFreeAsync(s->e_v, st);
+  cudaFreeAsync(s->g_j, st);
+  cudaFreeAsync(s->g_start, st);
+  cudaFreeAsync(s->leaf_g, st);
+  cudaFreeAsync(s->g_leaf, st);
+  cudaFreeAsync(s->items, st);
+  for (int l = 0; l <= kMaxDepth; ++l) cudaFreeAsync(s->mask[l], st);
+  *s = SparseHt();
+}
+
+template <class T>
+static int aalloc(T** p, size_t count, cudaStream_t st) {
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)p, std::max<size_t>(1, count) * sizeof(T), st));
+  return HIKF_OK;
+}
+
+int sparse_build(const hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, SparseHt* s,
+                 cudaStream_t st) {
+  const bool masks = s->build_masks;
+  *s = SparseHt();
+  s->build_masks = masks;
+  s->n = n;
+  s->ngr = (n + 7) / 8;
+  int32_t nnz32 = 0;
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(&nnz32, ip + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  const int64_t nnz = nnz32;
+  s->nnz = nnz;
+  const int64_t L = t->n_leaves;
+
+  // ---- entries sorted by (leaf, j); CSR order (j, cell) makes the sort keep cell order ----
+  int64_t *key = nullptr, *key_s = nullptr;
+  int32_t *pos = nullptr, *pos_s = nullptr;
+  HIKF_TRY(aalloc(&key, nnz, st));
+  HIKF_TRY(aalloc(&key_s, nnz, st));
+  HIKF_TRY(aalloc(&pos, nnz, st));
+  HIKF_TRY(aalloc(&pos_s, nnz, st));
+  if (n > 0) {
+    entry_keys<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, t->inv_order, t->leaf_of, key, pos);
+    HIKF_CHECK_LAUNCH();
+  }
+  int end_bit = 1;
+  while (end_bit < 63 && ((int64_t)1 << end_bit) < L * n) ++end_bit;
+  size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+  int32_t* d_num = nullptr;
+  HIKF_TRY(aalloc(&d_num, 2, st));
+  int64_t* gkey = nullptr;
+  int32_t *gcnt = nullptr, *gexcl = nullptr;
+  HIKF_TRY(aalloc(&gkey, nnz, st));
+  HIKF_TRY(aalloc(&gcnt, nnz, st));
+  HIKF_TRY(aalloc(&gexcl, nnz, st));
+  cub::DeviceRadixSort::SortPairs(nullptr, b1, key, key_s, pos, pos_s, (int)nnz, 0, end_bit, st);
+  cub::DeviceRunLengthEncode::Encode(nullptr, b2, key_s, gkey, gcnt, d_num, (int)nnz, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, b3, gcnt, gexcl, (int)nnz, st);
+  void* tmp = nullptr;
+  size_t tb = std::max(std::max(b1, b2), b3);
+  HIKF_CHECK_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), st));
+  cub::DeviceRadixSort::SortPairs(tmp, b1, key, key_s, pos, pos_s, (int)nnz, 0, end_bit, st);
+  HIKF_TRY(aalloc(&s->e_sp, nnz, st));
+  HIKF_TRY(aalloc(&s->e_j, nnz, st));
+  HIKF_TRY(aalloc(&s->e_v, nnz, st));
+  entry_gather<<<grid_for(nnz), kT, 0, st>>>(nnz, n, key_s, pos_s, ix, val, t->inv_order, s->e_sp, s->e_j, s->e_v);
+  HIKF_CHECK_LAUNCH();
+  cub::DeviceRunLengthEncode::Encode(tmp, b2, key_s, gkey, gcnt, d_num, (int)nnz, st);
+  int32_t ngroups = 0;
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(&ngroups, d_num, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  s->ngroups = ngroups;
+  cub::DeviceScan::ExclusiveSum(tmp, b3, gcnt, gexcl, (int)ngroups, st);
+  HIKF_TRY(aalloc(&s->g_j, ngroups, st));
+  HIKF_TRY(aalloc(&s->g_leaf, ngroups, st));
+  int32_t* g_leaf = s->g_leaf;
+  HIKF_TRY(aalloc(&s->g_start, ngroups + 1, st));
+  HIKF_TRY(aalloc(&s->leaf_g, L + 1, st));
+  if (ngroups > 0) {
+    group_tables<<<grid_for(ngroups), kT, 0, st>>>(ngroups, n, gkey, gcnt, gexcl, s->g_j, g_leaf, s->g_start);
+    HIKF_CHECK_LAUNCH();
+  } else {
+    HIKF_CHECK_CUDA(cudaMemsetAsync(s->g_start, 0, sizeof(int32_t), st));
+  }
+  leaf_group_offsets<<<grid_for(L + 1), kT, 0, st>>>(L, ngroups, g_leaf, s->leaf_g);
+  HIKF_CHECK_LAUNCH();
+
+  // ---- activity masks per level (only for the masked dense path) ----
+  const int D = t->depth;
+  if (D >= 2 && s->build_masks) {
+    int64_t G = t->G;
+    HIKF_TRY(aalloc(&s->mask[D], G * G * s->ngr, st));
+    HIKF_CHECK_CUDA(cudaMemsetAsync(s->mask[D], 0, G * G * s->ngr, st));
+    if (ngroups > 0) {
+      leaf_mask<<<grid_for(ngroups), kT, 0, st>>>(ngroups, g_leaf, s->g_j, t->leaf_box, s->ngr, s->mask[D]);
+      HIKF_CHECK_LAUNCH();
+    }
+    for (int l = D - 1; l >= 2; --l) {
+      int64_t Gp = (int64_t)1 << l;
+      HIKF_TRY(aalloc(&s->mask[l], Gp * Gp * s->ngr, st));
+      parent_mask<<<grid_for(Gp * Gp * s->ngr), kT, 0, st>>>(Gp, s->ngr, s->mask[l + 1], s->mask[l]);
+      HIKF_CHECK_LAUNCH();
+    }
+  }
+
+  // ---- P2P work items: unique (target leaf, j) over all groups' neighbourhoods ----
+  int64_t ncand = 9 * (int64_t)ngroups;
+  int64_t *cand = nullptr, *cand_s = nullptr;
+  HIKF_TRY(aalloc(&cand, ncand, st));
+  HIKF_TRY(aalloc(&cand_s, ncand, st));
+  HIKF_TRY(aalloc(&s->items, ncand, st));
+  if (ngroups > 0) {
+    item_candidates<<<grid_for(ngroups), kT, 0, st>>>(ngroups, n, t->G, g_leaf, s->g_j, t->leaf_box, t->box2leaf,
+                                                      cand);
+    HIKF_CHECK_LAUNCH();
+    size_t b5 = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, b4, cand, cand_s, (int)ncand, 0, 64, st);
+    cub::DeviceSelect::Unique(nullptr, b5, cand_s, s->items, d_num + 1, (int)ncand, st);
+    void* tmp2 = nullptr;
+    HIKF_CHECK_CUDA(cudaMallocAsync(&tmp2, std::max(b4, b5), st));
+    cub::DeviceRadixSort::SortKeys(tmp2, b4, cand, cand_s, (int)ncand, 0, 64, st);
+    cub::DeviceSelect::Unique(tmp2, b5, cand_s, s->items, d_num + 1, (int)ncand, st);
+    int32_t nu = 0;
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(&nu, d_num + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+    // drop the INT64_MAX sentinel (sorted last)
+    int64_t last = 0;
+    if (nu > 0) {
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(&last, s->items + nu - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+      if (last == INT64_MAX) --nu;
+    }
+    s->nitems = nu;
+    cudaFreeAsync(tmp2, st);
+  }
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(key, st);
+  cudaFreeAsync(key_s, st);
+  cudaFreeAsync(pos, st);
+  cudaFreeAsync(pos_s, st);
+  cudaFreeAsync(gkey, st);
+  cudaFreeAsync(gcnt, st);
+  cudaFreeAsync(gexcl, st);
+  cudaFreeAsync(cand, st);
+  cudaFreeAsync(cand_s, st);
+  cudaFreeAsync(d_num, st);
+  return HIKF_OK;
+}
+
+int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, int64_t c0, cudaStream_t st) {
+  const int q = t->orders[t->depth] * t->orders[t->depth];
+  if (t->n_leaves > 0) {
+    p2m_sparse<<<(unsigned)t->n_leaves, 128, 0, st>>>(q, kcols, c0, s.ngr, t->leaf_box, s.leaf_g, s.g_j, s.g_start,
+                                                       s.e_sp, s.e_v, t->W2s, s.mask[t->depth], W);
+    HIKF_CHECK_LAUNCH();
+  }
+  return HIKF_OK;
+}
+
+int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st) {
+  if (s.nitems <= 0) return HIKF_OK;
+  const int64_t threads = s.nitems * 32;
+  p2p_sparse<<<(unsigned)((threads + kT - 1) / kT), kT, 0, st>>>(
+      s.nitems, s.items, s.n, t->G, t->kp, t->leaf_box, t->leaf_start, t->leaf_count, t->box2leaf, s.leaf_g, s.g_j,
+      s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, prof_flops_ptr(ST_P2P));
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+
+namespace {
+
+__global__ void leaf_pair_keys(int64_t ng, int64_t n, const int32_t* __restrict__ g_leaf,
+                               const int32_t* __restrict__ g_j, const int32_t* __restrict__ leaf_box,
+                               int64_t* __restrict__ key) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x)
+    key[i] = (int64_t)leaf_box[g_leaf[i]] * n + g_j[i];
+}
+
+// Wc[g][a] = sum_{entries (p, v) of group g} W2[p][a] v   (fmm.py:338 restricted to nonzeros)
+__device__ __forceinline__ void count_flops(unsigned long long* flops, unsigned v) {
+  if (!flops) return;
+  unsigned tot = __reduce_add_sync(__activemask(), v);
+  if ((threadIdx.x & 31) == __ffs(__activemask()) - 1 && tot) atomicAdd(flops, (unsigned long long)tot);
+}
+
+__global__ void p2m_pairs(int64_t ng, int q, const int32_t* __restrict__ g_start, const int32_t* __restrict__ e_sp,
+                          const double* __restrict__ e_v, const double* __restrict__ W2s, double* __restrict__ Wc,
+                          unsigned long long* __restrict__ flops) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ng * q; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t gi = e / q;
+    int a = (int)(e % q);
+    double s = 0.0;
+    for (int32_t k = g_start[gi]; k < g_start[gi + 1]; ++k) s += W2s[(int64_t)e_sp[k] * q + a] * e_v[k];
+    Wc[e] = s;
+    count_flops(flops, 2u * (unsigned)(g_start[gi + 1] - g_start[gi]));
+  }
+}
+
+__global__ void parent_keys(int64_t np, const int64_t* __restrict__ ckey, int64_t n, int64_t Gc,
+                            int64_t* __restrict__ pkey) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t box = ckey[i] / n, j = ckey[i] % n;
+    int64_t cx = box / Gc, cy = box % Gc;
+    pkey[i] = ((cx >> 1) * (Gc >> 1) + (cy >> 1)) * n + j;
+  }
+}
+
+__device__ __forceinline__ int64_t find_key(const int64_t* __restrict__ keys, int64_t np, int64_t k) {
+  int64_t lo = 0, hi = np;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return (lo < np && keys[lo] == k) ? lo : -1;
+}
+
+// W_P[b][j] = sum_{children c (cx, cy order)} sum_a C_c[a][b] W_c[a][j]  (fmm.py:339-345)
+__global__ void m2m_pairs(int64_t npp, const int64_t* __restrict__ pkey, int qp, int qc, int64_t Gp, int64_t n,
+                          const double* __restrict__ shift, int64_t npc, const int64_t* __restrict__ ckey,
+                          const double* __restrict__ Wcc, double* __restrict__ Wp, unsigned long long* __restrict__ flops) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npp * qp; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pi = e / qp;
+    int b = (int)(e % qp);
+    int64_t box = pkey[pi] / n, j = pkey[pi] % n, X = box / Gp, Y = box % Gp;
+    double s = 0.0;
+    unsigned found = 0;
+    for (int c = 0; c < 4; ++c) {
+      int64_t child = (2 * X + (c >> 1)) * (2 * Gp) + (2 * Y + (c & 1));
+      int64_t ci = find_key(ckey, npc, child * n + j);
+      if (ci < 0) continue;
+      ++found;
+      const double* C = shift + (int64_t)c * qc * qp;
+      const double* w = Wcc + ci * qc;
+      for (int a = 0; a < qc; ++a) s += C[(int64_t)a * qp + b] * w[a];
+    }
+    Wp[e] = s;
+    count_flops(flops, 2u * found * (unsigned)qc);
+  }
+}
+
+// One M2L offset over all active source pairs of a level: a warp takes 16
+// pairs (two 8-column DMMA groups sharing the A fragments of M_d), computes
+// M_d W_s[:, j] on the DMMA pipe and adds it into the pair-major scratch
+// L[T][j][:] (q contiguous coefficients per (T, j)), T = S - d.
+// Within one offset every (T, j) has at most one source, so the adds are
+// race-free and the offsets are summed in the reference's order.
+constexpr int kPairGroups = 2;
+constexpr int kMaxK4Smem = 16;  // q <= 64: M_d staged in shared memory, B fragments preloaded
+__host__ __device__ inline int m2l_ld(int q) { return q + ((4 - q % 16) + 16) % 16; }  // == 4 mod 16
+
+// kSmem: M_d in shared memory and B preloaded; NK4 / NRT = ceil(q/4) / ceil(q/8)
+// as compile-time bounds of the fragment loops (generic path: 16 / 8 with runtime q)
+template <bool kSmem, int NK4, int NRT>
+__global__ void __launch_bounds__(256, (kSmem && NK4 < 9) ? 2 : 1) m2l_pairs_kernel(int64_t np, const int64_t* __restrict__ key,
+                                                        const double* __restrict__ Wc, int q, int64_t n, int64_t G,
+                                                        int dx, int dy, const uint8_t* __restrict__ occ,
+                                                        const double* __restrict__ M, double* __restrict__ L,
+                                                        unsigned long long* __restrict__ flops) {
+  extern __shared__ double Ms[];
+  const int ld = kSmem ? m2l_ld(q) : q;
+  if (kSmem) {
+    for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = M[e];
+    __syncthreads();
+  }
+  const double* A = kSmem ? Ms : M;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t p0 = warp * (8 * kPairGroups);
+  if (p0 >= np) return;
+  const int g = lane >> 2, t4 = lane & 3;
+  // my column (pair) in each group: validity and target
+  int64_t myT[kPairGroups], myJ[kPairGroups], myP[kPairGroups];
+  bool any = false;
+#pragma unroll
+  for (int c = 0; c < kPairGroups; ++c) {
+    int64_t p = p0 + c * 8 + g;
+    myT[c] = -1;
+    myJ[c] = 0;
+    myP[c] = p;
+    if (p < np) {
+      int64_t S = key[p] / n, j = key[p] % n;
+      int64_t tx = S / G - dx, ty = S % G - dy, s2;
+      if (tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) && s2 == S &&
+          occ[tx * G + ty]) {
+        myT[c] = tx * G + ty;
+        myJ[c] = j;
+      }
+    }
+    any |= __any_sync(0xffffffffu, myT[c] >= 0);
+  }
+  if (!any) return;
+  if (flops) {
+    int nv = 0;
+#pragma unroll
+    for (int c = 0; c < kPairGroups; ++c) nv += __popc(__ballot_sync(0xffffffffu, myT[c] >= 0 && t4 == 0));
+    if (lane == 0) atomicAdd(flops, 2ull * nv * q * q);
+  }
+  const int nrt = (q + 7) >> 3;
+  const int nk4 = (q + 3) >> 2;
+  constexpr int RT = kSmem ? NRT : 8;  // row tiles held in registers per pass
+  // B fragments (this lane's pair, k = 4 k4 + t4), preloaded when q <= 64
+  double bpre[kSmem ? kPairGroups : 1][kSmem ? NK4 : 1];
+  if (kSmem) {
+#pragma unroll
+    for (int c = 0; c < kPairGroups; ++c)
+#pragma unroll
+      for (int k4 = 0; k4 < NK4; ++k4) {
+        const int k = k4 * 4 + t4;
+        bpre[c][k4] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
+      }
+  }
+  for (int r0 = 0; r0 < nrt; r0 += RT) {
+    double acc[RT][kPairGroups][2];
+#pragma unroll
+    for (int i = 0; i < RT; ++i)
+#pragma unroll
+      for (int c = 0; c < kPairGroups; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
+    if (kSmem) {
+#pragma unroll
+      for (int k4 = 0; k4 < NK4; ++k4) {
+        const int k = k4 * 4 + t4;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int r = i * 8 + g;
+          const double a = (r < q && k < q) ? A[r * ld + k] : 0.0;
+#pragma unroll
+          for (int c = 0; c < kPairGroups; ++c) dmma884(acc[i][c][0], acc[i][c][1], a, bpre[c][k4]);
+        }
+      }
+    } else {
+      for (int k4 = 0; k4 < nk4; ++k4) {
+        const int k = k4 * 4 + t4;
+        double b[kPairGroups];
+#pragma unroll
+        for (int c = 0; c < kPairGroups; ++c) b[c] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int r = (r0 + i) * 8 + g;
+          if (r0 + i < nrt) {
+            const double a = (r < q && k < q) ? __ldg(A + (int64_t)r * q + k) : 0.0;
+#pragma unroll
+            for (int c = 0; c < kPairGroups; ++c) dmma884(acc[i][c][0], acc[i][c][1], a, b[c]);
+          }
+        }
+      }
+    }
+    // epilogue: lane holds rows (r0+i)*8+g of columns 2*t4, 2*t4+1 of each group
+#pragma unroll
+    for (int c = 0; c < kPairGroups; ++c)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 2 * t4 + h;
+        const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
+        const int64_t j = __shfl_sync(0xffffffffu, myJ[c], col * 4);
+        if (T < 0) continue;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int r = (r0 + i) * 8 + g;
+          if (r0 + i < nrt && r < q) L[(T * n + j) * q + r] += acc[i][c][h];
+        }
+      }
+  }
+}
+
+// Pair-major M2L scratch S[T][j][a] -> box-major locals L[T][a][j] for the
+// occupied boxes (CTA = box x 32-column chunk, smem-staged transpose).
+constexpr int kTrCols = 32;
+__global__ void __launch_bounds__(256) pair_to_box_kernel(const int32_t* __restrict__ occ, int q, int64_t n,
+                                                          const double* __restrict__ S, double* __restrict__ L) {
+  extern __shared__ double tile[];  // kTrCols x (q + 1)
+  const int64_t T = occ[blockIdx.x];
+  const int64_t j0 = (int64_t)blockIdx.y * kTrCols;
+  const int cw = (int)((n - j0) < kTrCols ? (n - j0) : kTrCols);
+  const int qs = q + 1;
+  const double* src = S + (T * n + j0) * q;
+  for (int e = threadIdx.x; e < cw * q; e += blockDim.x) tile[(e / q) * qs + e % q] = src[e];
+  __syncthreads();
+  for (int e = threadIdx.x; e < cw * q; e += blockDim.x) {
+    int a = e / cw, jj = e % cw;
+    L[(T * q + a) * n + j0 + jj] = tile[jj * qs + a];
+  }
+}
+
+}  // namespace
+
+int pair_to_box(const hikf_tree* t, int l, const double* S, int64_t n, double* L, cudaStream_t st) {
+  if (t->n_occ[l] == 0 || n == 0) return HIKF_OK;
+  const int q = t->orders[l] * t->orders[l];
+  const size_t smem = sizeof(double) * kTrCols * (q + 1);
+  static size_t configured = 0;
+  if (smem > configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(pair_to_box_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 << 10)));
+    configured = std::max<size_t>(smem, 48 << 10);
+  }
+  dim3 grid((unsigned)t->n_occ[l], (unsigned)((n + kTrCols - 1) / kTrCols));
+  pair_to_box_kernel<<<grid, 256, smem, st>>>(t->occ[l], q, n, S, L);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+namespace {
+
+int grid_cap(int64_t n) {
+  int64_t b = (n + kT - 1) / kT;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)num_sms() * 64));
+}
+
+}  // namespace
+
+void pairs_free(PairLevel* p, cudaStream_t st) {
+  cudaFreeAsync(p->key, st);
+  cudaFreeAsync(p->W, st);
+  *p = PairLevel();
+}
+
+int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st) {
+  *out = PairLevel();
+  const int q = t->orders[t->depth] * t->orders[t->depth];
+  out->np = s.ngroups;
+  HIKF_TRY(aalloc(&out->key, s.ngroups, st));
+  HIKF_TRY(aalloc(&out->W, s.ngroups * q, st));
+  if (s.ngroups == 0) return HIKF_OK;
+  leaf_pair_keys<<<grid_cap(s.ngroups), kT, 0, st>>>(s.ngroups, s.n, s.g_leaf, s.g_j, t->leaf_box, out->key);
+  HIKF_CHECK_LAUNCH();
+  p2m_pairs<<<grid_cap(s.ngroups * q), kT, 0, st>>>(s.ngroups, q, s.g_start, s.e_sp, s.e_v, t->W2s, out->W,
+                                                     prof_flops_ptr(ST_P2M));
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st) {
+  *out = PairLevel();
+  const int64_t Gc = (int64_t)1 << (l + 1), Gp = (int64_t)1 << l;
+  const int qp = t->orders[l] * t->orders[l], qc = t->orders[l + 1] * t->orders[l + 1];
+  if (child.np == 0) {
+    HIKF_TRY(aalloc(&out->key, 1, st));
+    HIKF_TRY(aalloc(&out->W, 1, st));
+    return HIKF_OK;
+  }
+  int64_t *pk = nullptr, *pk_s = nullptr;
+  int32_t* d_num = nullptr;
+  HIKF_TRY(aalloc(&pk, child.np, st));
+  HIKF_TRY(aalloc(&pk_s, child.np, st));
+  HIKF_TRY(aalloc(&out->key, child.np, st));
+  HIKF_TRY(aalloc(&d_num, 1, st));
+  parent_keys<<<grid_cap(child.np), kT, 0, st>>>(child.np, child.key, n, Gc, pk);
+  HIKF_CHECK_LAUNCH();
+  int end_bit = 1;
+  while (end_bit < 63 && ((int64_t)1 << end_bit) < Gp * Gp * n) ++end_bit;
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, b1, pk, pk_s, (int)child.np, 0, end_bit, st);
+  cub::DeviceSelect::Unique(nullptr, b2, pk_s, out->key, d_num, (int)child.np, st);
+  void* tmp = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(std::max(b1, b2), 1), st));
+  cub::DeviceRadixSort::SortKeys(tmp, b1, pk, pk_s, (int)child.np, 0, end_bit, st);
+  cub::DeviceSelect::Unique(tmp, b2, pk_s, out->key, d_num, (int)child.np, st);
+  int32_t np = 0;
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(&np, d_num, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  out->np = np;
+  HIKF_TRY(aalloc(&out->W, (int64_t)np * qp, st));
+  m2m_pairs<<<grid_cap((int64_t)np * qp), kT, 0, st>>>(np, out->key, qp, qc, Gp, n, t->shift[l], child.np, child.key,
+                                                       child.W, out->W, prof_flops_ptr(ST_M2M));
+  HIKF_CHECK_LAUNCH();
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(pk, st);
+  cudaFreeAsync(pk_s, st);
+  cudaFreeAsync(d_num, st);
+  return HIKF_OK;
+}
+
+int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, cudaStream_t st) {
+  if (src.np == 0 || !((t->m2l_present[l] >> slot) & 1)) return HIKF_OK;
+  M2LOffsets offs;
+  const int q = t->orders[l] * t->orders[l];
+  const int64_t warps = (src.np + 8 * kPairGroups - 1) / (8 * kPairGroups);
+  const int64_t threads = warps * 32;
+  const unsigned blocks = (unsigned)((threads + kT - 1) / kT);
+  const size_t smem = sizeof(double) * q * m2l_ld(q);
+  const int64_t G = (int64_t)1 << l;
+  const double* M = t->m2l[l] + (int64_t)slot * q * q;
+  unsigned long long* fl = prof_flops_ptr(ST_M2L);
+#define HIKF_M2L_CASE(QQ, K4, RT)                                                                               \
+  case QQ:                                                                                                     \
+    m2l_pairs_kernel<true, K4, RT><<<blocks, kT, smem, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],   \
+                                                             offs.dy[slot], t->occ_flag[l], M, L, fl);         \
+    break;
+  switch (q) {
+    HIKF_M2L_CASE(4, 1, 1)
+    HIKF_M2L_CASE(9, 3, 2)
+    HIKF_M2L_CASE(16, 4, 2)
+    HIKF_M2L_CASE(25, 7, 4)
+    HIKF_M2L_CASE(36, 9, 5)
+    HIKF_M2L_CASE(49, 13, 7)
+    HIKF_M2L_CASE(64, 16, 8)
+    default:
+      m2l_pairs_kernel<false, 1, 1><<<blocks, kT, 0, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],
+                                                            offs.dy[slot], t->occ_flag[l], M, L, fl);
+  }
+#undef HIKF_M2L_CASE
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+}  // namespace hikf

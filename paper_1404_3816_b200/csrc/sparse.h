@@ -1,0 +1,49 @@
+// H^T in leaf-grouped sparse form for the Q H^T precompute (see sparse.cu).
+#pragma once
+
+#include "common.cuh"
+
+struct hikf_tree;
+
+namespace hikf {
+
+struct SparseHt {
+  int64_t n = 0, nnz = 0, ngroups = 0, nitems = 0, ngr = 0;
+  bool build_masks = false;    // per-level 8-ray activity masks (masked dense M2L path)
+  int32_t* e_sp = nullptr;     // entry: sorted position of the cell
+  int32_t* e_j = nullptr;      // entry: ray
+  double* e_v = nullptr;       // entry: intersection length
+  int32_t* g_j = nullptr;      // group (leaf, ray): ray
+  int32_t* g_start = nullptr;  // group -> first entry, [ngroups + 1]
+  int32_t* leaf_g = nullptr;   // leaf -> first group, [n_leaves + 1]
+  int32_t* g_leaf = nullptr;   // group (leaf, ray): leaf rank
+  int64_t* items = nullptr;    // P2P work items: target_leaf * n + ray
+  uint8_t* mask[21] = {nullptr};  // per level: (G_l^2, ngr) activity of 8-ray groups (optional)
+};
+
+// Active multipoles of one level in compact form: (box, ray) pairs with a
+// nonzero multipole, sorted by key = box * n + ray, and their q coefficients.
+struct PairLevel {
+  int64_t np = 0;
+  int64_t* key = nullptr;
+  double* W = nullptr;  // np x q
+};
+
+int sparse_build(const hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, SparseHt* s,
+                 cudaStream_t st);
+void sparse_free(SparseHt* s, cudaStream_t st);
+int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, int64_t c0, cudaStream_t st);
+int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st);
+
+// leaf multipoles of the active (leaf, ray) pairs (sparse P2M)
+int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st);
+// parent multipoles from the children's active pairs (sparse M2M), level l from l+1
+int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st);
+void pairs_free(PairLevel* p, cudaStream_t st);
+// L_l[T][:, j] += M_d W_{T+d}[:, j] for every active source pair and one offset slot
+// S must be the pair-major scratch S[T][j][a] (zeroed before the 40 offsets)
+int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, cudaStream_t st);
+// L[T][a][j] = S[T][j][a] for the occupied boxes of level l
+int pair_to_box(const hikf_tree* t, int l, const double* S, int64_t n, double* L, cudaStream_t st);
+
+}  // namespace hikf

@@ -67,6 +67,17 @@ __global__ void iota64(int64_t* v, int64_t m) {
     v[i] = i;
 }
 
+__global__ void inverse_perm(const int64_t* __restrict__ order, int64_t m, int32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    inv[order[i]] = (int32_t)i;
+}
+
+__global__ void leaf_ranks(const int32_t* __restrict__ start, const int32_t* __restrict__ count, int64_t nl,
+                           int32_t* __restrict__ leaf_of) {
+  for (int64_t r = blockIdx.x; r < nl; r += gridDim.x)
+    for (int32_t i = threadIdx.x; i < count[r]; i += blockDim.x) leaf_of[start[r] + i] = (int32_t)r;
+}
+
 __global__ void gather_xy(const double* __restrict__ xy, const int64_t* __restrict__ order, int64_t m,
                           double* __restrict__ xy_s) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
@@ -153,6 +164,8 @@ void tree_free(hikf_tree* t) {
   cudaFree(t->xy);
   cudaFree(t->xy_s);
   cudaFree(t->order);
+  cudaFree(t->inv_order);
+  cudaFree(t->leaf_of);
   cudaFree(t->leaf_box);
   cudaFree(t->leaf_start);
   cudaFree(t->leaf_count);
@@ -303,6 +316,13 @@ static int build_impl(hikf_tree* t, const double* xy_host, cudaStream_t st) {
   HIKF_CHECK_CUDA(cudaMemcpyAsync(t->leaf_count, lc.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, st));
   HIKF_CHECK_CUDA(cudaMemcpyAsync(t->box2leaf, b2l.data(), sizeof(int32_t) * G * G, cudaMemcpyHostToDevice, st));
 
+  HIKF_TRY(dalloc(&t->inv_order, m));
+  HIKF_TRY(dalloc(&t->leaf_of, m));
+  inverse_perm<<<grid_for(m), kThreads, 0, st>>>(t->order, m, t->inv_order);
+  HIKF_CHECK_LAUNCH();
+  leaf_ranks<<<(unsigned)std::min<int64_t>(nl, 65535), kThreads, 0, st>>>(t->leaf_start, t->leaf_count, nl,
+                                                                          t->leaf_of);
+  HIKF_CHECK_LAUNCH();
   HIKF_TRY(dalloc(&t->xy_s, 2 * m));
   gather_xy<<<grid_for(m), kThreads, 0, st>>>(t->xy, t->order, m, t->xy_s);
   HIKF_CHECK_LAUNCH();

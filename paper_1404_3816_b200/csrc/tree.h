@@ -36,6 +36,8 @@ struct hikf_tree {
   double* xy = nullptr;
   double* xy_s = nullptr;
   int64_t* order = nullptr;
+  int32_t* inv_order = nullptr;  // point -> sorted position
+  int32_t* leaf_of = nullptr;    // sorted position -> leaf rank
   int32_t* leaf_box = nullptr;
   int32_t* leaf_start = nullptr;
   int32_t* leaf_count = nullptr;
@@ -80,5 +82,8 @@ int tree_export_m2l_pairs(const hikf_tree* t, int lev, int dx, int dy, std::vect
 
 // U = tree @ V (dense V, m x k), fmm.py:325-367
 int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U, int64_t ldu, cudaStream_t stream);
+// U (m x n) = tree @ H^T for a device CSR H (n x m), H^T kept sparse
+int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
+                    cudaStream_t stream);
 
 }  // namespace hikf

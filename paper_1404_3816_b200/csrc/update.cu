@@ -268,7 +268,7 @@ static size_t update_layout(int64_t m, int64_t n, char* base, UpdWs* ws) {
     off += align_up(bytes);
     return p;
   };
-  int nt = ceil_div(n, DG_BN);
+  int nt = ceil_div(n, DG_MIN_BN);
   int nb = grid_for(m);
   UpdWs w;
   w.HCp = (double*)take(8 * n * n);
@@ -377,7 +377,8 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   delete pf;
 
   // ---- Y = C' Li^T with fused row partials (|Y_i|^2, Y_i . w) ----
-  const int nt = ceil_div(n, DG_BN);
+  const int vy = update_variant_y();
+  const int nt = dgemm_col_tiles(n, vy);
   {
     GemmArgs g;
     g.M = m; g.N = n; g.K = n;
@@ -386,6 +387,7 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
     g.C = w.Y; g.ldc = n;
     g.kmode = KB_UPPER;
     g.psq = w.psq; g.pdot = w.pdot; g.w = w.w; g.ldp = nt;
+    g.variant = vy;
     ProfScope ps(ST_GEMM_Y, st);
     HIKF_TRY(dgemm(g, 1, st));
   }
@@ -406,6 +408,7 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
     g.C = a.C_out; g.ldc = n;
     g.Cin = Cp; g.ldcin = n;
     g.alpha = -1.0; g.beta = 1.0;
+    g.variant = update_variant_c();
     ProfScope ps(ST_GEMM_C, st);
     HIKF_TRY(dgemm(g, 1, st));
   }

@@ -252,3 +252,19 @@ def test_dgemm_against_torch(pkg):
         X = pkg.spd_solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
         ref = torch.linalg.solve(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
         assert torch.allclose(X, ref, rtol=1e-10, atol=1e-12)
+
+
+@pytest.mark.parametrize("name,n", [("cloud_exp4", 37), ("edges_gauss", 300), ("rect_empty", 130),
+                                    ("single_leaf", 9), ("depth1", 20), ("grid_30x28", 150)])
+def test_sparse_charges_path_equals_dense(pkg, name, n):
+    """tree @ H^T with H^T kept sparse (masked DMMA stages, sparse P2M/P2P) vs the
+    dense-charge path on the densified H^T: the same sums up to reassociation."""
+    pts, spec, n_cheb, leaf, _ = cases.tree_cases()[name]
+    tree = pkg.build_tree(pkg.PointSet(pts), _spec(pkg, spec), pkg.FmmConfig(n_cheb=n_cheb, max_leaf_points=leaf))
+    H = scipy.sparse.random(n, len(pts), density=min(1.0, 40.0 / len(pts)), random_state=3, format="csr")
+    Us = tree.matmat_csrT(H).cpu().numpy()
+    Ud = tree.matmat(np.ascontiguousarray(H.T.toarray()))
+    assert O.rel_fro(Us, Ud) <= 1e-14, O.rel_fro(Us, Ud)
+    # empty rays and an all-zero operator
+    Z = scipy.sparse.csr_matrix((n, len(pts)))
+    assert np.array_equal(tree.matmat_csrT(Z).cpu().numpy(), np.zeros((len(pts), n)))

@@ -275,8 +275,11 @@ int launch(const Prov& p, int64_t tasks, int64_t max_rows, int64_t kcols, cudaSt
                                          (int)sg_smem<Prov>()));
     configured = true;
   }
-  dim3 grid((unsigned)tasks, (unsigned)ceil_div(max_rows, SG_R), (unsigned)ceil_div(kcols, SG_BN));
+  // blockIdx.x = (task * row_tiles + row_tile) * col_tiles + col_tile
+  const int64_t rt = ceil_div(max_rows, SG_R), ct = ceil_div(kcols, SG_BN);
+  dim3 grid((unsigned)(tasks * rt * ct), 1, 1);
   Prov q = p;
+  q.row_tiles = (int)rt;
   if (!q.flops) q.flops = prof_flops_ptr(Prov::kStage);
   seg_gemm_kernel<Prov><<<grid, SG_THREADS, sg_smem<Prov>(), st>>>(q);
   HIKF_CHECK_LAUNCH();

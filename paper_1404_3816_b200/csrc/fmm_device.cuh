@@ -74,6 +74,7 @@ struct ProvBase {
   int64_t gofs = 0;    // absolute 8-column group of column 0 of the pass (masks)
   int64_t ngroups = 0; // groups per mask row
   bool vecB = false;   // B rows 16-byte aligned with an even leading dimension
+  int row_tiles = 1;   // 64-row tiles per task (set by the launcher)
   KParams kp;
   __device__ int64_t ncols() const { return kcols; }
   __device__ double kernel(double r) const { return kernel_of_r(kp, r); }
@@ -88,12 +89,17 @@ __global__ void __launch_bounds__(SG_THREADS, Prov::kMinBlocks) seg_gemm_kernel(
   __shared__ unsigned stage_am[STAGES];
   unsigned long long useful = 0;  // thread 0: 2 * rows * k * active columns
 
-  const int task = blockIdx.x;
-  const int row0 = blockIdx.y * SG_R;
+  // flattened grid, column tiles fastest: consecutive CTAs share the task's A
+  // block (W2 rows, M2L operators) in L2
+  const int64_t ncols = prov.ncols();
+  const int nct = (int)((ncols + SG_BN - 1) / SG_BN);
+  const int64_t bid = blockIdx.x;
+  const int col0 = (int)(bid % nct) * SG_BN;
+  const int64_t rest = bid / nct;
+  const int task = (int)(rest / prov.row_tiles);
+  const int row0 = (int)(rest % prov.row_tiles) * SG_R;
   const int nrows = prov.rows(task);
   if (row0 >= nrows) return;
-  const int col0 = blockIdx.z * SG_BN;
-  const int64_t ncols = prov.ncols();
   const int nsegs = prov.nsegs(task);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;

@@ -459,14 +459,14 @@ __global__ void m2m_pairs(int64_t npp, const int64_t* __restrict__ pkey, int qp,
 // L[T][j][:] (q contiguous coefficients per (T, j)), T = S - d.
 // Within one offset every (T, j) has at most one source, so the adds are
 // race-free and the offsets are summed in the reference's order.
-constexpr int kPairGroups = 2;
+constexpr int kPairGroups = 1;  // 8 pairs per warp: low register count, many warps in flight
 constexpr int kMaxK4Smem = 16;  // q <= 64: M_d staged in shared memory, B fragments preloaded
 __host__ __device__ inline int m2l_ld(int q) { return q + ((4 - q % 16) + 16) % 16; }  // == 4 mod 16
 
 // kSmem: M_d in shared memory and B preloaded; NK4 / NRT = ceil(q/4) / ceil(q/8)
 // as compile-time bounds of the fragment loops (generic path: 16 / 8 with runtime q)
 template <bool kSmem, int NK4, int NRT>
-__global__ void __launch_bounds__(256, (kSmem && NK4 < 9) ? 2 : 1) m2l_pairs_kernel(int64_t np, const int64_t* __restrict__ key,
+__global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_kernel(int64_t np, const int64_t* __restrict__ key,
                                                         const double* __restrict__ Wc, int q, int64_t n, int64_t G,
                                                         int dx, int dy, const uint8_t* __restrict__ occ,
                                                         const double* __restrict__ M, double* __restrict__ L,
@@ -484,7 +484,8 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 < 9) ? 2 : 1) m2l_pairs_ker
   if (p0 >= np) return;
   const int g = lane >> 2, t4 = lane & 3;
   // my column (pair) in each group: validity and target
-  int64_t myT[kPairGroups], myJ[kPairGroups], myP[kPairGroups];
+  int32_t myT[kPairGroups], myJ[kPairGroups];
+  int64_t myP[kPairGroups];
   bool any = false;
 #pragma unroll
   for (int c = 0; c < kPairGroups; ++c) {
@@ -497,8 +498,8 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 < 9) ? 2 : 1) m2l_pairs_ker
       int64_t tx = S / G - dx, ty = S % G - dy, s2;
       if (tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) && s2 == S &&
           occ[tx * G + ty]) {
-        myT[c] = tx * G + ty;
-        myJ[c] = j;
+        myT[c] = (int32_t)(tx * G + ty);
+        myJ[c] = (int32_t)j;
       }
     }
     any |= __any_sync(0xffffffffu, myT[c] >= 0);
@@ -524,38 +525,55 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 < 9) ? 2 : 1) m2l_pairs_ker
         bpre[c][k4] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
       }
   }
+  if (kSmem) {
+    // one 8-row tile at a time: two interleaved accumulator chains over k
+    for (int i = 0; i < nrt; ++i) {
+      const int r = i * 8 + g;
+      double acc0[kPairGroups][2], acc1[kPairGroups][2];
+#pragma unroll
+      for (int c = 0; c < kPairGroups; ++c) acc0[c][0] = acc0[c][1] = acc1[c][0] = acc1[c][1] = 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < NK4; ++k4) {
+        const int k = k4 * 4 + t4;
+        const double a = (r < q && k < q) ? A[r * ld + k] : 0.0;
+#pragma unroll
+        for (int c = 0; c < kPairGroups; ++c) {
+          if (k4 & 1)
+            dmma884(acc1[c][0], acc1[c][1], a, bpre[c][k4]);
+          else
+            dmma884(acc0[c][0], acc0[c][1], a, bpre[c][k4]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < kPairGroups; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 2 * t4 + h;
+          const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
+          const int64_t j = (int64_t)__shfl_sync(0xffffffffu, myJ[c], col * 4);
+          if (T >= 0 && r < q) L[(T * n + j) * q + r] += acc0[c][h] + acc1[c][h];
+        }
+    }
+    return;
+  }
   for (int r0 = 0; r0 < nrt; r0 += RT) {
     double acc[RT][kPairGroups][2];
 #pragma unroll
     for (int i = 0; i < RT; ++i)
 #pragma unroll
       for (int c = 0; c < kPairGroups; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
-    if (kSmem) {
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int k = k4 * 4 + t4;
+      double b[kPairGroups];
 #pragma unroll
-      for (int k4 = 0; k4 < NK4; ++k4) {
-        const int k = k4 * 4 + t4;
+      for (int c = 0; c < kPairGroups; ++c) b[c] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
 #pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const int r = i * 8 + g;
-          const double a = (r < q && k < q) ? A[r * ld + k] : 0.0;
+      for (int i = 0; i < RT; ++i) {
+        const int r = (r0 + i) * 8 + g;
+        if (r0 + i < nrt) {
+          const double a = (r < q && k < q) ? __ldg(A + (int64_t)r * q + k) : 0.0;
 #pragma unroll
-          for (int c = 0; c < kPairGroups; ++c) dmma884(acc[i][c][0], acc[i][c][1], a, bpre[c][k4]);
-        }
-      }
-    } else {
-      for (int k4 = 0; k4 < nk4; ++k4) {
-        const int k = k4 * 4 + t4;
-        double b[kPairGroups];
-#pragma unroll
-        for (int c = 0; c < kPairGroups; ++c) b[c] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const int r = (r0 + i) * 8 + g;
-          if (r0 + i < nrt) {
-            const double a = (r < q && k < q) ? __ldg(A + (int64_t)r * q + k) : 0.0;
-#pragma unroll
-            for (int c = 0; c < kPairGroups; ++c) dmma884(acc[i][c][0], acc[i][c][1], a, b[c]);
-          }
+          for (int c = 0; c < kPairGroups; ++c) dmma884(acc[i][c][0], acc[i][c][1], a, b[c]);
         }
       }
     }
@@ -566,7 +584,7 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 < 9) ? 2 : 1) m2l_pairs_ker
       for (int h = 0; h < 2; ++h) {
         const int col = 2 * t4 + h;
         const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
-        const int64_t j = __shfl_sync(0xffffffffu, myJ[c], col * 4);
+        const int64_t j = (int64_t)__shfl_sync(0xffffffffu, myJ[c], col * 4);
         if (T < 0) continue;
 #pragma unroll
         for (int i = 0; i < RT; ++i) {

@@ -1,0 +1,17 @@
+// Box-streaming DMMA GEMM for the L2L / L2P transfers (see boxgemm.cu).
+#pragma once
+
+#include "common.cuh"
+#include "tree.h"
+
+namespace hikf {
+
+// L_l[child][a][j] = S[child][j][a] + sum_b C_child[a][b] L_{l-1}[parent][b][j] for every
+// child of an occupied parent (l > 2); S is the pair-major M2L scratch of level l
+int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int64_t n, double* L, cudaStream_t st);
+// whether the warp-streaming kernel handles R rows x K inner (K <= 64, A fits in smem)
+bool box_supported(int rows, int K);
+// U[order[p]][j] = sum_a W2[p][a] L_leaf[a][j] (store)
+int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st);
+
+}  // namespace hikf

@@ -3,6 +3,7 @@
 // each stage a seg_gemm_kernel launch over boxes x column tiles.
 #include <algorithm>
 
+#include "boxgemm.h"
 #include "fmm_device.cuh"
 #include "prof.h"
 #include "sparse.h"
@@ -498,7 +499,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
         for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
           status = m2l_pass(t, l, slot, pl[l], n, scratch, st);
       }
-      if (status == HIKF_OK) {
+      if (status == HIKF_OK && l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
+        ProfScope ps(ST_L2L, st);
+        status = l2l_boxes(t, l, scratch, Lprev, n, Lcur, st);
+      } else if (status == HIKF_OK) {
         ProfScope ps(ST_L2L, st);
         status = pair_to_box(t, l, scratch, n, Lcur, st);
         if (status == HIKF_OK && l > 2) {
@@ -516,7 +520,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       }
       Lprev = Lcur;
     }
-    if (status == HIKF_OK) {
+    if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
+      ProfScope ps(ST_L2P, st);
+      status = l2p_boxes(t, Lcur, n, U, n, st);
+    } else if (status == HIKF_OK) {
       L2PProv<false> lp;
       set_base(lp, t, n, 0, 0, vec);
       lp.leaf_box = t->leaf_box;

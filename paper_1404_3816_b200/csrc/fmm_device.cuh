@@ -249,25 +249,36 @@ __global__ void __launch_bounds__(SG_THREADS, Prov::kMinBlocks) seg_gemm_kernel(
   cp_async_wait<0>();
   if (prov.flops && tid == 0 && useful) atomicAdd(prov.flops, useful);
 
-  // epilogue: store or accumulate into the output rows
+  // epilogue: store or accumulate into the output rows (accumulate: all the
+  // reads first, so they overlap instead of serialising behind the stores)
+  double* orows[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    if (i >= nrt) continue;
     const int r = i * 8 + g;
-    if (r >= rows_here) continue;
-    double* orow = prov.out_row(task, row0 + r);
+    orows[i] = (i < nrt && r < rows_here) ? prov.out_row(task, row0 + r) : nullptr;
+  }
+  if (Prov::kAccumulate) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (!orows[i]) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t c = col0 + warp * 16 + j * 8 + 2 * t4;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (c + h < ncols) acc[i][j][h] += orows[i][c + h];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if (!orows[i]) continue;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int64_t c = col0 + warp * 16 + j * 8 + 2 * t4;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (c + h < ncols) {
-          if (Prov::kAccumulate)
-            orow[c + h] += acc[i][j][h];
-          else
-            orow[c + h] = acc[i][j][h];
-        }
-      }
+      for (int h = 0; h < 2; ++h)
+        if (c + h < ncols) orows[i][c + h] = acc[i][j][h];
     }
   }
 }

@@ -75,51 +75,58 @@ __global__ void transpose_kernel(const double* __restrict__ X, int64_t n, double
 // Cholesky + inverse of one <= NB x NB diagonal block held in shared memory.
 // L (lower, ld), Li (lower, ld) written; upper triangles left untouched (zeroed
 // by the caller).  status[0] = global 1-based pivot of the first failure.
-__global__ void chol_inv_base(const double* __restrict__ S, int64_t ld, int nb, int64_t offset,
-                              double* __restrict__ L, double* __restrict__ Li, int* status) {
+// Right-looking factorisation: every thread recomputes the pivot (no extra
+// barrier), warp w updates rows i = w (mod 8) of the trailing triangle.
+__global__ void __launch_bounds__(256) chol_inv_base(const double* __restrict__ S, int64_t ld, int nb,
+                                                     int64_t offset, double* __restrict__ L,
+                                                     double* __restrict__ Li, int* status) {
   extern __shared__ double base_smem[];
   double(*a)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(base_smem);
   double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(base_smem + NB * (NB + 1));
-  __shared__ int bad;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  for (int e = tid; e < nb * nb; e += blockDim.x) a[e / nb][e % nb] = S[(e / nb) * ld + e % nb];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    int i = e / nb, k = e - i * nb;
+    a[i][k] = S[(int64_t)i * ld + k];
+  }
   __syncthreads();
-  // right-looking Cholesky on the lower triangle
+  int bad = 0;
   for (int j = 0; j < nb; ++j) {
-    if (tid == 0) {
-      double d = a[j][j];
-      if (!(d > 0.0)) {
-        if (!bad) bad = j + 1;
-        d = 1.0;  // keep going; the result is discarded by the caller
-      }
-      a[j][j] = sqrt(d);
+    double d = a[j][j];
+    if (!(d > 0.0)) {
+      if (!bad) bad = j + 1;
+      d = 1.0;  // keep going; the result is discarded by the caller
     }
+    const double piv = sqrt(d);
+    const double inv = 1.0 / piv;
+    // column j below the diagonal
+    for (int i = j + 1 + tid; i < nb; i += blockDim.x) a[i][j] *= inv;
     __syncthreads();
-    double piv = a[j][j];
-    for (int i = j + 1 + tid; i < nb; i += blockDim.x) a[i][j] = a[i][j] / piv;
-    __syncthreads();
-    for (int e = tid; e < (nb - j - 1) * (nb - j - 1); e += blockDim.x) {
-      int i = j + 1 + e / (nb - j - 1), k = j + 1 + e % (nb - j - 1);
-      if (k <= i) a[i][k] -= a[i][j] * a[k][j];
+    if (tid == 0) a[j][j] = piv;
+    for (int i = j + 1 + warp; i < nb; i += 8) {
+      const double lij = a[i][j];
+      for (int k = j + 1 + lane; k <= i; k += 32) a[i][k] -= lij * a[k][j];
     }
     __syncthreads();
   }
-  // inverse by forward substitution, one column per thread
+  // inverse by forward substitution, one column per thread (the dot-product
+  // chains of the 64 columns run in parallel)
+  __shared__ double rdiag[NB];
+  for (int i = tid; i < nb; i += blockDim.x) rdiag[i] = 1.0 / a[i][i];
+  __syncthreads();
   for (int c = tid; c < nb; c += blockDim.x) {
-    x[c][c] = 1.0 / a[c][c];
+    x[c][c] = rdiag[c];
     for (int i = c + 1; i < nb; ++i) {
       double s = 0.0;
       for (int k = c; k < i; ++k) s += a[i][k] * x[k][c];
-      x[i][c] = -s / a[i][i];
+      x[i][c] = -s * rdiag[i];
     }
   }
   __syncthreads();
   for (int e = tid; e < nb * nb; e += blockDim.x) {
-    int i = e / nb, j = e % nb;
-    if (j <= i) {
-      L[i * ld + j] = a[i][j];
-      Li[i * ld + j] = x[i][j];
+    int i = e / nb, k = e - i * nb;
+    if (k <= i) {
+      L[(int64_t)i * ld + k] = a[i][k];
+      Li[(int64_t)i * ld + k] = x[i][k];
     }
   }
   if (tid == 0 && bad && status[0] == 0) status[0] = (int)(offset + bad);

@@ -40,8 +40,17 @@ for v in [int(x) for x in os.environ.get("SWEEP_VARIANTS", "0,1,2,3,4,5,6,7,8").
                                            0, v, st))
     t_up = timeit(lambda: lib.hikf_dgemm(M, N, N, A.data_ptr(), N, B.data_ptr(), N, C.data_ptr(), N, 1.0, 0.0,
                                          1, v, st))
+    # correctness of this variant against cuBLAS on a 4096-row slice (full and upper-triangular)
+    Cs = torch.zeros(4096, N, dtype=torch.float64, device="cuda")
+    lib.hikf_dgemm(4096, N, N, A.data_ptr(), N, B.data_ptr(), N, Cs.data_ptr(), N, 1.0, 0.0, 0, v, st)
+    ref = torch.matmul(A[:4096], B)
+    err_full = float(((Cs - ref).abs().max() / ref.abs().max()).item())
+    lib.hikf_dgemm(4096, N, N, A.data_ptr(), N, B.data_ptr(), N, Cs.data_ptr(), N, 1.0, 0.0, 1, v, st)
+    ref_u = None  # kmode 1 assumes B upper triangular (LiT); skip on a full random B
+    err_up = None
     out[f"v{v}"] = {"full_ms": t_full, "full_tflops": full / t_full / 1e9,
-                    "upper_ms": t_up, "upper_tflops": 0.5 * full / t_up / 1e9}
+                    "upper_ms": t_up, "upper_tflops": 0.5 * full / t_up / 1e9, "err_full": err_full,
+                    "err_upper": err_up}
     print(v, out[f"v{v}"], flush=True)
 # correctness of the default variant vs cuBLAS on a slice
 ref = torch.matmul(A[:4096], B)

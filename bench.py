@@ -56,6 +56,10 @@ CONFIGS = {
 # DMMA/DFMA issue-rate microbenchmark gives 37.0, profiles/r01_fp64_micro.json).
 FP64_PEAK_TFLOPS = 35.46
 FP64_PEAK_SOURCE = "measured cuBLAS DGEMM 8192^3 on B200 (profiles/r01_fp64_dgemm.json); not in MEASURED_PEAKS.json"
+# DRAM traffic of one C-GEMM launch at cfg4 from `ncu --set full` (dram__bytes_read.sum +
+# dram__bytes_write.sum, profiles/r01_ncu_sparse_summary.txt: 17.2 + 8.56 GB); the algorithmic
+# bytes are Y + C' in, C out = 3 x 8 m n = 25.8 GB (P stays in L2).
+C_GEMM_TRAFFIC_CFG4 = 17.2e9 + 8.559e9
 
 
 def hbm_peak():
@@ -425,7 +429,9 @@ def main():
                              "m2l": {"achieved": fmm_useful["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
         "roofline": {"kernel": "dgemm_kernel (C_new = C' - Y P, 2 m n^2 flops per launch)", "bound": "fp64",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None, "peak_source": FP64_PEAK_SOURCE,
+                     "frac": achieved / FP64_PEAK_TFLOPS,
+                     "traffic": C_GEMM_TRAFFIC_CFG4 if args.config == "cfg4" else None,
+                     "algorithmic_bytes": 24.0 * m * n, "peak_source": FP64_PEAK_SOURCE,
                      "share_of_step": (ms_c + ms_y) / (1000.0 * t_loop) if t_loop else None,
                      "update_step_flops": update_flops,
                      "update_step_frac": update_flops * args.steps / t_loop / 1e12 / FP64_PEAK_TFLOPS},

@@ -258,6 +258,21 @@ __global__ void check_variance(int nb, const double* bmin, const double* bmax, i
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// library-owned side stream + fork/join events for the n x n work of the update
+int side_stream(cudaStream_t* side, cudaEvent_t* a, cudaEvent_t* b) {
+  static cudaStream_t s = nullptr;
+  static cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (!s) {
+    HIKF_CHECK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+  }
+  *side = s;
+  *a = e0;
+  *b = e1;
+  return HIKF_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -334,27 +349,44 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   HIKF_CHECK_CUDA(cudaMemsetAsync(w.status, 0, 16, st));
 
   // ---- predict (fused in front) ----
+  // The n x n work (S, Cholesky + inverse, P, R, HC_new, whitened innovation)
+  // depends only on HC' and runs on a side stream, overlapping the HBM-bound
+  // C' = C + C_Q stream on the main stream; both join before the Y GEMM.
   const double *Cp = a.C, *varp = a.var, *HCp = a.HC;
+  cudaStream_t side = st;
+  cudaEvent_t ev_hc = nullptr, ev_nn = nullptr;
+  HIKF_TRY(side_stream(&side, &ev_hc, &ev_nn));
   if (a.CQ) {
-    ProfScope ps(ST_PREDICT, st);
-    HIKF_TRY(predict(m, n, a.C, a.var, a.HC, a.CQ, a.dQ, a.HCQ, a.C_out, a.var_out, w.HCp, st));
-    Cp = a.C_out;
-    varp = a.var_out;  // var_out temporarily holds var'; finalize reads it before overwriting
+    add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, st>>>(a.HC, a.HCQ, w.HCp, n * n);
+    HIKF_CHECK_LAUNCH();
     HCp = w.HCp;
   }
+  HIKF_CHECK_CUDA(cudaEventRecord(ev_hc, st));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev_hc, 0));
+  if (a.CQ) {
+    ProfScope ps(ST_PREDICT, st);
+    if (m * n > 0) {
+      add_kernel<<<grid_for(m * n / 2 + 1), kT, 0, st>>>(a.C, a.CQ, a.C_out, m * n);
+      HIKF_CHECK_LAUNCH();
+    }
+    add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(a.var, a.dQ, a.var_out, m);
+    HIKF_CHECK_LAUNCH();
+    Cp = a.C_out;
+    varp = a.var_out;  // var_out temporarily holds var'; finalize reads it before overwriting
+  }
 
-  // ---- n x n factorization ----
-  ProfScope* pf = new ProfScope(ST_FACTOR, st);
-  build_S<<<grid_for(n * n), kT, 0, st>>>(HCp, n, a.r, w.S);
+  // ---- n x n factorization (side stream) ----
+  ProfScope* pf = new ProfScope(ST_FACTOR, side);
+  build_S<<<grid_for(n * n), kT, 0, side>>>(HCp, n, a.r, w.S);
   HIKF_CHECK_LAUNCH();
-  HIKF_TRY(factor(w.S, w.L, w.Li, w.tmp, n, w.status, st));
-  transpose_kernel<<<grid_for(n * n), kT, 0, st>>>(w.Li, n, w.LiT);
+  HIKF_TRY(factor(w.S, w.L, w.Li, w.tmp, n, w.status, side));
+  transpose_kernel<<<grid_for(n * n), kT, 0, side>>>(w.Li, n, w.LiT);
   HIKF_CHECK_LAUNCH();
 
   // ---- innovation and whitened innovation ----
-  innovation<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, a.ip, a.ix, a.val, a.mean, a.z, w.innov);
+  innovation<<<ceil_div(n * 32, kT), kT, 0, side>>>(n, a.ip, a.ix, a.val, a.mean, a.z, w.innov);
   HIKF_CHECK_LAUNCH();
-  trmv_lower<<<ceil_div(n * 32, kT), kT, 0, st>>>(w.Li, n, w.innov, w.w);
+  trmv_lower<<<ceil_div(n * 32, kT), kT, 0, side>>>(w.Li, n, w.innov, w.w);
   HIKF_CHECK_LAUNCH();
 
   // ---- P = Li HC', R = HC' Li^T, HC_new = HC' - R P ----
@@ -364,14 +396,14 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
     g.A = w.Li; g.sa_r = n;
     g.B = HCp; g.sb_r = n;
     g.C = w.P; g.ldc = n;
-    HIKF_TRY(dgemm(g, 1, st));
+    HIKF_TRY(dgemm(g, 1, side));
     GemmArgs h;
     h.M = n; h.N = n; h.K = n;
     h.A = HCp; h.sa_r = n;
     h.B = w.LiT; h.sb_r = n;
     h.C = w.R; h.ldc = n;
     h.kmode = KB_UPPER;
-    HIKF_TRY(dgemm(h, 1, st));
+    HIKF_TRY(dgemm(h, 1, side));
     GemmArgs c;
     c.M = n; c.N = n; c.K = n;
     c.A = w.R; c.sa_r = n;
@@ -379,9 +411,11 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
     c.C = a.HC_out; c.ldc = n;
     c.Cin = HCp; c.ldcin = n;
     c.alpha = -1.0; c.beta = 1.0;
-    HIKF_TRY(dgemm(c, 1, st));
+    HIKF_TRY(dgemm(c, 1, side));
   }
   delete pf;
+  HIKF_CHECK_CUDA(cudaEventRecord(ev_nn, side));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_nn, 0));
 
   // ---- Y = C' Li^T with fused row partials (|Y_i|^2, Y_i . w) ----
   const int vy = update_variant_y();

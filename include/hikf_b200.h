@@ -145,6 +145,22 @@ int hikf_update(int64_t m, int64_t n, const double* mean_dev, const double* C_de
                 const double* z_dev, double* mean_out, double* C_out, double* var_out, double* HC_out,
                 void* workspace, size_t workspace_bytes, double* min_var_out, void* stream);
 
+/* ---- row-sharded update: the same update on rows [r0, r1) of a
+ * state sharded across ranks.  Hmean_dev = the all-reduced H mean (the
+ * caller sums the per-rank hikf_csr_spmv partials); the n x n quantities are
+ * replicated and identical on every rank.  The negative-variance check is
+ * global, so it is not applied here: minmax_out[0] = min over the local rows
+ * of the posterior variance, minmax_out[1] = max of the prior variance, for
+ * the caller's all-reduce.  Returns HIKF_NOT_PD like hikf_update. */
+int hikf_update_rows(int64_t m_local, int64_t n, const double* mean_dev, const double* C_dev, const double* var_dev,
+                     const double* HC_dev, const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev,
+                     const double* Hmean_dev, double r_variance, const double* z_dev, double* mean_out,
+                     double* C_out, double* var_out, double* HC_out, void* workspace, size_t workspace_bytes,
+                     double* minmax_out, void* stream);
+/* y (n) = H x for a CSR H (n x cols) on the device. */
+int hikf_csr_spmv(int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev,
+                  const double* x_dev, double* y_dev, void* stream);
+
 /* ---- spd_solve (linalg.py:18-37): X (n x k) = A^{-1} B, A SPD n x n ----
  * Symmetry check |A - A^T|max <= 1e-10 |A|max (HIKF_ASYMMETRIC), Cholesky
  * (HIKF_NOT_PD with the failing pivot in *info), two triangular solves. */

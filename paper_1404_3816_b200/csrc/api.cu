@@ -389,6 +389,54 @@ int hikf_update(int64_t m, int64_t n, const double* mean, const double* C, const
   return s;
 }
 
+int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const double* C, const double* var,
+                     const double* HC, const double* CQ, const double* dQ, const double* HCQ, const double* Hmean,
+                     double r, const double* z, double* mean_out, double* C_out, double* var_out, double* HC_out,
+                     void* workspace, size_t workspace_bytes, double* minmax_out, void* stream) {
+  if (m_local < 1 || n < 1 || !mean || !C || !var || !HC || !Hmean || !z || !mean_out || !C_out || !var_out ||
+      !HC_out) {
+    set_error("bad update_rows arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (CQ && (!dQ || !HCQ)) {
+    set_error("fused predict needs C_Q, diag_Q and HC_Q");
+    return HIKF_BAD_ARGUMENT;
+  }
+  UpdateArgs a;
+  a.m = m_local;
+  a.n = n;
+  a.mean = mean;
+  a.C = C;
+  a.var = var;
+  a.HC = HC;
+  a.CQ = CQ;
+  a.dQ = dQ;
+  a.HCQ = HCQ;
+  a.Hmean = Hmean;
+  a.no_check = true;
+  a.r = r;
+  a.z = z;
+  a.mean_out = mean_out;
+  a.C_out = C_out;
+  a.var_out = var_out;
+  a.HC_out = HC_out;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  UpdateResult res;
+  int s = update(a, as_stream(stream), &res);
+  if (minmax_out) {
+    minmax_out[0] = res.min_var;
+    minmax_out[1] = res.max_prior_var;
+  }
+  return s;
+}
+
+int hikf_csr_spmv(int64_t n, const int32_t* ip, const int32_t* ix, const double* val, const double* x, double* y,
+                  void* stream) {
+  if (n < 0) return HIKF_BAD_ARGUMENT;
+  return spmv(n, ip, ix, val, x, y, as_stream(stream));
+}
+
 size_t hikf_spd_solve_workspace_bytes(int64_t n, int64_t k) { return spd_workspace_bytes(n, k); }
 
 int hikf_spd_solve(int64_t n, int64_t k, const double* A, const double* B, double* X, void* ws, size_t ws_bytes,

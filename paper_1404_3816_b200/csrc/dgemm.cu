@@ -1,6 +1,7 @@
 // FP64 DMMA GEMM (see dgemm.cuh).  One templated kernel; the tile shape is
 // a compile-time variant (dgemm_variant() picks it; HIKF_DGEMM_VARIANT
 // overrides for tuning sweeps).
+#include <algorithm>
 #include <cstdlib>
 
 #include "dgemm.cuh"

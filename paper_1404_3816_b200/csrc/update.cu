@@ -184,16 +184,34 @@ int chol_inv(double* S, double* L, double* Li, int64_t n, int64_t ld, int64_t of
 }
 
 // innov = z - H mean (CSR SpMV, one warp per row), filters.py:147
+// (with Hmean != null the caller supplies H mean -- the all-reduced partials of a
+// row-sharded state -- and the kernel only forms z - Hmean)
 __global__ void innovation(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
                            const double* __restrict__ val, const double* __restrict__ mean, const double* __restrict__ z,
-                           double* __restrict__ innov) {
+                           const double* __restrict__ Hmean, double* __restrict__ innov) {
   int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (row >= n) return;
   double s = 0.0;
-  for (int64_t e = ip[row] + lane; e < ip[row + 1]; e += 32) s += val[e] * mean[ix[e]];
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (Hmean) {
+    s = Hmean[row];
+  } else {
+    for (int64_t e = ip[row] + lane; e < ip[row + 1]; e += 32) s += val[e] * mean[ix[e]];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
   if (lane == 0) innov[row] = z[row] - s;
+}
+
+// y = H x (CSR, one warp per row)
+__global__ void csr_spmv(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
+                         const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int64_t e = ip[row] + lane; e < ip[row + 1]; e += 32) s += val[e] * x[ix[e]];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[row] = s;
 }
 
 // w = Li innov (n x n lower-triangular GEMV, one warp per row)
@@ -253,6 +271,7 @@ __global__ void check_variance(int nb, const double* bmin, const double* bmax, i
   }
   double prior_max = fmax(mx, 0.0);
   out[0] = mn;
+  out[1] = mx;
   if (mn < -1e-10 * fmax(prior_max, DBL_MIN)) status[1] = 1;
 }
 
@@ -308,13 +327,21 @@ static size_t update_layout(int64_t m, int64_t n, char* base, UpdWs* ws) {
   w.pdot = (double*)take(8 * m * nt);
   w.bmin = (double*)take(8 * (size_t)nb);
   w.bmax = (double*)take(8 * (size_t)nb);
-  w.minv = (double*)take(8);
+  w.minv = (double*)take(16);
   w.status = (int*)take(16);
   if (ws) *ws = w;
   return off;
 }
 
 size_t update_workspace_bytes(int64_t m, int64_t n) { return update_layout(m, n, nullptr, nullptr); }
+
+int spmv(int64_t n, const int32_t* ip, const int32_t* ix, const double* val, const double* x, double* y,
+         cudaStream_t st) {
+  if (n <= 0) return HIKF_OK;
+  csr_spmv<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, ip, ix, val, x, y);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
 
 int predict(int64_t m, int64_t n, const double* C, const double* var, const double* HC, const double* CQ,
             const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, cudaStream_t st) {
@@ -384,7 +411,7 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   HIKF_CHECK_LAUNCH();
 
   // ---- innovation and whitened innovation ----
-  innovation<<<ceil_div(n * 32, kT), kT, 0, side>>>(n, a.ip, a.ix, a.val, a.mean, a.z, w.innov);
+  innovation<<<ceil_div(n * 32, kT), kT, 0, side>>>(n, a.ip, a.ix, a.val, a.mean, a.z, a.Hmean, w.innov);
   HIKF_CHECK_LAUNCH();
   trmv_lower<<<ceil_div(n * 32, kT), kT, 0, side>>>(w.Li, n, w.innov, w.w);
   HIKF_CHECK_LAUNCH();
@@ -456,19 +483,21 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
 
   // ---- status back to the host ----
   int hs[2] = {0, 0};
-  double mv = 0.0;
+  double mm[2] = {0.0, 0.0};
   HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(&mv, w.minv, sizeof(double), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
   HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  const double mv = mm[0];
   if (res) {
     res->pivot = hs[0];
-    res->min_var = mv;
+    res->min_var = mm[0];
+    res->max_prior_var = mm[1];
   }
   if (hs[0]) {
     set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
     return HIKF_NOT_PD;
   }
-  if (hs[1]) {
+  if (hs[1] && !a.no_check) {
     set_error("posterior variance went negative beyond tolerance (min %.3e)", mv);
     return HIKF_NEGATIVE_VARIANCE;
   }

@@ -16,17 +16,22 @@ struct UpdateArgs {
   double *mean_out = nullptr, *C_out = nullptr, *var_out = nullptr, *HC_out = nullptr;
   void* workspace = nullptr;
   size_t workspace_bytes = 0;
+  const double* Hmean = nullptr;  // row-sharded state: all-reduced H mean (else computed from H, mean)
+  bool no_check = false;          // row-sharded state: the caller applies the global variance check
 };
 
 struct UpdateResult {
   int pivot = 0;
-  double min_var = 0.0;
+  double min_var = 0.0;        // min over the rows of the posterior variance
+  double max_prior_var = 0.0;  // max over the rows of the prior variance
 };
 
 size_t update_workspace_bytes(int64_t m, int64_t n);
 int update(const UpdateArgs& a, cudaStream_t stream, UpdateResult* res);
 int predict(int64_t m, int64_t n, const double* C, const double* var, const double* HC, const double* CQ,
             const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, cudaStream_t st);
+int spmv(int64_t n, const int32_t* ip, const int32_t* ix, const double* val, const double* x, double* y,
+         cudaStream_t st);
 size_t spd_workspace_bytes(int64_t n, int64_t k);
 int spd_solve(int64_t n, int64_t k, const double* A, const double* B, double* X, void* ws, size_t ws_bytes,
               int64_t* info, cudaStream_t st);

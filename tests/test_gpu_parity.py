@@ -283,3 +283,37 @@ def test_sparse_charges_path_equals_dense(pkg, name, n):
     # empty rays and an all-zero operator
     Z = scipy.sparse.csr_matrix((n, len(pts)))
     assert np.array_equal(tree.matmat_csrT(Z).cpu().numpy(), np.zeros((len(pts), n)))
+
+
+def test_cuda_row_sharded_update_equals_full(pkg):
+    """The building blocks of the row-sharded filter (hikf_csr_spmv partials +
+    hikf_update_rows on row blocks) reproduce the full hikf_update on one GPU."""
+    import torch
+    from paper_1404_3816_b200.sharded import CudaRowStep, local_columns, row_block
+    flt = pkg.filters
+    g = _load("cfg1.npz")
+    cfg = cases.CFG1
+    tree, H, pre, st_full = _run_filter(pkg, dict(cfg, T=3), g["obs"])
+    m, n = H.shape[1], H.shape[0]
+    world = 3
+    steps, states = [], []
+    for r in range(world):
+        r0, r1 = row_block(m, world, r)
+        steps.append((r0, r1, CudaRowStep((pre.C_Q_t[r0:r1].contiguous(), pre.HC_Q_t, pre.diag_Q_t[r0:r1].contiguous()), n)))
+        states.append({"mean": torch.zeros(r1 - r0, dtype=torch.float64, device="cuda"),
+                       "C": torch.zeros(r1 - r0, n, dtype=torch.float64, device="cuda"),
+                       "var": torch.zeros(r1 - r0, dtype=torch.float64, device="cuda"),
+                       "HC": torch.zeros(n, n, dtype=torch.float64, device="cuda")})
+    Hl = [s[2].prepare_h(local_columns(H, s[0], s[1])) for s in steps]
+    for t in range(3):
+        partial = sum(steps[r][2].spmv(Hl[r], states[r]) for r in range(world))
+        z = torch.as_tensor(g["obs"][t]).cuda()
+        states = [steps[r][2].update_rows(states[r], partial, cfg["R"], z)[0] for r in range(world)]
+    mean = torch.cat([s["mean"] for s in states]).cpu().numpy()
+    C = torch.cat([s["C"] for s in states]).cpu().numpy()
+    var = torch.cat([s["var"] for s in states]).cpu().numpy()
+    for s in states[1:]:
+        assert torch.equal(s["HC"], states[0]["HC"])
+    assert O.rel_fro(mean, st_full.mean) <= 1e-12
+    assert O.rel_fro(var, st_full.variance) <= 1e-12
+    assert O.rel_fro(C, st_full.cross_cov) <= 1e-12

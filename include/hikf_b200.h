@@ -177,6 +177,17 @@ int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, d
                       const double* src, const double* rcv, int32_t* indptr, int32_t* indices, double* data,
                       int64_t* nnz_out);
 
+/* ---- build_ray_operator on the device (tomography.py:76-133) ----
+ * Same result as hikf_ray_operator (bit-identical pattern and lengths) with
+ * the per-ray tracing on the GPU: one CTA per ray.  src/rcv are HOST arrays
+ * (the ray lengths are taken with the host's hypot so they round like
+ * numpy's); indptr_dev[n+1] / indices_dev / data_dev are device buffers.
+ * With indices_dev == NULL only indptr_dev and *nnz_out are produced; else
+ * capacity (entries) must be >= nnz.  Requires nx + ny <= 4096. */
+int hikf_ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n,
+                             const double* src, const double* rcv, int32_t* indptr_dev, int32_t* indices_dev,
+                             double* data_dev, int64_t capacity, int64_t* nnz_out, void* stream);
+
 /* ---- FP64 DMMA GEMM building block (the update's workhorse) ----
  * C (M x N, ldc) = alpha A (M x K, lda) B (K x N, ldb) + beta C, row-major,
  * device pointers.  kmode 0: full; 1: B upper triangular (K-range k <= col

@@ -8,6 +8,7 @@
 
 #include "dgemm.cuh"
 #include "prof.h"
+#include "rays.h"
 #include "tree.h"
 #include "update.h"
 
@@ -465,6 +466,17 @@ int hikf_dgemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, co
   int s = dgemm(g, 1, as_stream(stream));
   set_dgemm_variant(prev);
   return s;
+}
+
+int hikf_ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n,
+                             const double* src, const double* rcv, int32_t* indptr_dev, int32_t* indices_dev,
+                             double* data_dev, int64_t capacity, int64_t* nnz_out, void* stream) {
+  if (!src || !rcv || !indptr_dev || !nnz_out) {
+    set_error("hikf_ray_operator_device: null argument");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return ray_operator_device(nx, ny, dx, dy, x0, y0, n, src, rcv, indptr_dev, indices_dev, data_dev, capacity,
+                             nnz_out, as_stream(stream));
 }
 
 int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n, const double* src,

@@ -66,6 +66,19 @@ class DeviceCSR:
         self.data = torch.from_numpy(Hc.data.astype(np.float64)).to(dev)
 
     @classmethod
+    def from_device(cls, indptr, indices, data, shape) -> "DeviceCSR":
+        """Wrap device CSR arrays that are already canonical (sorted, no duplicates)."""
+        self = cls.__new__(cls)
+        self.shape = tuple(int(s) for s in shape)
+        self.nnz = int(indices.numel())
+        self.indptr, self.indices, self.data = indptr, indices, data
+        return self
+
+    def to_scipy(self) -> scipy.sparse.csr_matrix:
+        return scipy.sparse.csr_matrix((self.data.cpu().numpy(), self.indices.cpu().numpy(),
+                                        self.indptr.cpu().numpy()), shape=self.shape)
+
+    @classmethod
     def of(cls, H) -> "DeviceCSR":
         if isinstance(H, DeviceCSR):
             return H

@@ -2,9 +2,11 @@
 
 Mirror of the reference tomography.py:20-133 (Acquisition,
 default_acquisition, build_ray_operator): the ray/cell intersection tracing
-runs in native C++ inside libhikf_b200.so (hikf_ray_operator), reproducing
-the reference's breakpoint, midpoint and grazing-ray rules so the CSR pattern
-is bit-identical (tests/test_gpu_parity.py, test_boundary.py).
+runs in native C++ inside libhikf_b200.so (hikf_ray_operator), or on the GPU
+(hikf_ray_operator_device: one CTA per ray, the result stays in HBM),
+reproducing the reference's breakpoint, midpoint and grazing-ray rules so the
+CSR pattern and lengths are bit-identical (tests/test_gpu_parity.py,
+test_boundary.py).
 """
 
 from __future__ import annotations
@@ -76,3 +78,28 @@ def build_ray_operator(grid, acq) -> scipy.sparse.csr_matrix:
     _lib.check(lib.hikf_ray_operator(*args, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data,
                                      ctypes.byref(nnz)))
     return scipy.sparse.csr_matrix((data, indices, indptr), shape=(n, grid.m))
+
+
+def build_ray_operator_device(grid, acq):
+    """build_ray_operator traced on the GPU; returns a filters.DeviceCSR in HBM
+    that hikf_precompute_fmm / hikf_update accept wherever they take H."""
+    import torch
+
+    from .filters import DeviceCSR, _dev
+    src, rcv = acq.ray_endpoints()
+    src = np.ascontiguousarray(src, dtype=float)
+    rcv = np.ascontiguousarray(rcv, dtype=float)
+    n = src.shape[0]
+    x0, y0 = grid.origin
+    lib = _lib.load()
+    dev = _dev()
+    indptr = torch.empty(n + 1, dtype=torch.int32, device=dev)
+    cap = n * (grid.nx + grid.ny)  # a ray crosses at most nx + ny - 1 cells
+    indices = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    data = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
+    nnz = ctypes.c_int64(0)
+    _lib.check(lib.hikf_ray_operator_device(grid.nx, grid.ny, float(grid.dx), float(grid.dy), float(x0), float(y0), n,
+                                            src.ctypes.data, rcv.ctypes.data, indptr.data_ptr(), indices.data_ptr(),
+                                            data.data_ptr(), cap, ctypes.byref(nnz), _lib.stream_ptr()))
+    k = nnz.value
+    return DeviceCSR.from_device(indptr, indices[:k].clone(), data[:k].clone(), (n, grid.m))

@@ -144,27 +144,28 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
       }
     }
   }
+  // row partials first (they read w / px), then the stores: keeping the
+  // loads ahead of the stores avoids load-after-store serialisation on
+  // possibly aliasing pointers
+  if (PARTIALS) {
+    const double sc = g.px ? 1.0 : (Cin ? 1.0 : g.alpha);
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const int rl = wm * TM * 8 + i * 8 + gq;
-    const int64_t row = m0 + rl;
-    double ssq = 0.0, sdot = 0.0;
+    for (int i = 0; i < TM; ++i) {
+      const int rl = wm * TM * 8 + i * 8 + gq;
+      const int64_t row = m0 + rl;
+      double ssq = 0.0, sdot = 0.0;
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int64_t col = n0 + wn * TN * 8 + j * 8 + 2 * t4;
+      for (int j = 0; j < TN; ++j) {
+        const int64_t col = n0 + wn * TN * 8 + j * 8 + 2 * t4;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (row < g.M && col + h < g.N) {
-          double v = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
-          if (PARTIALS) {
-            ssq += v * v;
+        for (int h = 0; h < 2; ++h) {
+          if (row < g.M && col + h < g.N) {
+            const double v = sc * acc[i][j][h];
+            ssq += v * (g.px ? g.px[row * g.ldx + col + h] : v);
             sdot += v * g.w[col + h];
           }
-          C[row * g.ldc + col + h] = v;
         }
       }
-    }
-    if (PARTIALS) {
       ssq += __shfl_xor_sync(0xffffffffu, ssq, 1);
       ssq += __shfl_xor_sync(0xffffffffu, ssq, 2);
       sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
@@ -173,6 +174,17 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
         red_sq[wn][rl] = ssq;
         red_dot[wn][rl] = sdot;
       }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t col = n0 + wn * TN * 8 + j * 8 + 2 * t4;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (row < g.M && col + h < g.N) C[row * g.ldc + col + h] = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
     }
   }
   if (PARTIALS) {

@@ -34,11 +34,15 @@ struct GemmArgs {
   double alpha = 1.0, beta = 0.0;
   int kmode = KFULL;
   int64_t bsA = 0, bsB = 0, bsC = 0, bsCin = 0;  // batch strides (blockIdx.z)
-  // fused row partials: psq[i * ldp + tile] = sum_j (alpha acc)^2, pdot[...] = sum_j (alpha acc) w[j]
+  // fused row partials over the CTA's column tile:
+  //   px == null: psq[i * ldp + tile] = sum_j (alpha acc)^2, pdot[...] = sum_j (alpha acc) w[j]
+  //   px != null: psq[i * ldp + tile] = sum_j acc px[i * ldx + j], pdot[...] = sum_j acc w[j]
   double* psq = nullptr;
   double* pdot = nullptr;
   const double* w = nullptr;
   int64_t ldp = 0;
+  const double* px = nullptr;
+  int64_t ldx = 0;
   int variant = -1;  // tile-shape variant (-1: dgemm_variant())
 };
 

@@ -19,6 +19,8 @@
 #include "prof.h"
 #include "update.h"
 
+#include <cstdlib>
+
 namespace hikf {
 
 namespace {
@@ -298,7 +300,7 @@ int side_stream(cudaStream_t* side, cudaEvent_t* a, cudaEvent_t* b) {
 // workspace layout of the update
 // ---------------------------------------------------------------------------
 struct UpdWs {
-  double *HCp, *S, *L, *Li, *LiT, *P, *R, *tmp, *innov, *w, *Y, *psq, *pdot, *bmin, *bmax, *minv;
+  double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *w, *Y, *psq, *pdot, *bmin, *bmax, *minv;
   int* status;
 };
 
@@ -319,6 +321,7 @@ static size_t update_layout(int64_t m, int64_t n, char* base, UpdWs* ws) {
   w.LiT = (double*)take(8 * n * n);
   w.P = (double*)take(8 * n * n);
   w.R = (double*)take(8 * n * n);
+  w.Sinv = (double*)take(8 * n * n);
   w.tmp = (double*)take(8 * n * n);
   w.innov = (double*)take(8 * n);
   w.w = (double*)take(8 * n);
@@ -379,7 +382,19 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   // The n x n work (S, Cholesky + inverse, P, R, HC_new, whitened innovation)
   // depends only on HC' and runs on a side stream, overlapping the HBM-bound
   // C' = C + C_Q stream on the main stream; both join before the Y GEMM.
+  // update form: "sinv" (default) K = C' S^-1 in one GEMM with C_new = r K;
+  // "y2" (HIKF_UPDATE_FORM=y2): Y = C' Li^T, C_new = C' - Y (Li HC')
+  static const bool form_y2 = [] {
+    const char* e = getenv("HIKF_UPDATE_FORM");
+    return e && e[0] == 'y';
+  }();
   const double *Cp = a.C, *varp = a.var, *HCp = a.HC;
+  // sinv reads C' while writing C_new: C' must not live in C_out
+  double* Cdst = form_y2 ? a.C_out : w.Y;
+  if (!form_y2 && !a.CQ && a.C == a.C_out && m * n > 0) {
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(w.Y, a.C, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, st));
+    Cp = w.Y;
+  }
   cudaStream_t side = st;
   cudaEvent_t ev_hc = nullptr, ev_nn = nullptr;
   HIKF_TRY(side_stream(&side, &ev_hc, &ev_nn));
@@ -393,12 +408,12 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   if (a.CQ) {
     ProfScope ps(ST_PREDICT, st);
     if (m * n > 0) {
-      add_kernel<<<grid_for(m * n / 2 + 1), kT, 0, st>>>(a.C, a.CQ, a.C_out, m * n);
+      add_kernel<<<grid_for(m * n / 2 + 1), kT, 0, st>>>(a.C, a.CQ, Cdst, m * n);
       HIKF_CHECK_LAUNCH();
     }
     add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(a.var, a.dQ, a.var_out, m);
     HIKF_CHECK_LAUNCH();
-    Cp = a.C_out;
+    Cp = Cdst;
     varp = a.var_out;  // var_out temporarily holds var'; finalize reads it before overwriting
   }
 
@@ -413,8 +428,18 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   // ---- innovation and whitened innovation ----
   innovation<<<ceil_div(n * 32, kT), kT, 0, side>>>(n, a.ip, a.ix, a.val, a.mean, a.z, a.Hmean, w.innov);
   HIKF_CHECK_LAUNCH();
-  trmv_lower<<<ceil_div(n * 32, kT), kT, 0, side>>>(w.Li, n, w.innov, w.w);
-  HIKF_CHECK_LAUNCH();
+  if (form_y2) {
+    trmv_lower<<<ceil_div(n * 32, kT), kT, 0, side>>>(w.Li, n, w.innov, w.w);
+    HIKF_CHECK_LAUNCH();
+  } else {  // S^-1 = Li^T Li (symmetric)
+    GemmArgs g;
+    g.M = n; g.N = n; g.K = n;
+    g.A = w.LiT; g.sa_r = n;
+    g.B = w.Li; g.sb_r = n;
+    g.C = w.Sinv; g.ldc = n;
+    g.kmode = KB_LOWER;
+    HIKF_TRY(dgemm(g, 1, side));
+  }
 
   // ---- P = Li HC', R = HC' Li^T, HC_new = HC' - R P ----
   {
@@ -444,41 +469,65 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   HIKF_CHECK_CUDA(cudaEventRecord(ev_nn, side));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_nn, 0));
 
-  // ---- Y = C' Li^T with fused row partials (|Y_i|^2, Y_i . w) ----
-  const int vy = update_variant_y();
-  const int nt = dgemm_col_tiles(n, vy);
-  {
-    GemmArgs g;
-    g.M = m; g.N = n; g.K = n;
-    g.A = Cp; g.sa_r = n;
-    g.B = w.LiT; g.sb_r = n;
-    g.C = w.Y; g.ldc = n;
-    g.kmode = KB_UPPER;
-    g.psq = w.psq; g.pdot = w.pdot; g.w = w.w; g.ldp = nt;
-    g.variant = vy;
-    ProfScope ps(ST_GEMM_Y, st);
-    HIKF_TRY(dgemm(g, 1, st));
-  }
   const int nb = grid_for(m);
-  ProfScope* pz = new ProfScope(ST_FINALIZE, st);
-  finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
-  HIKF_CHECK_LAUNCH();
-  check_variance<<<1, 1, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
-  HIKF_CHECK_LAUNCH();
-  delete pz;
-
-  // ---- C_new = C' - Y P ----
-  {
-    GemmArgs g;
-    g.M = m; g.N = n; g.K = n;
-    g.A = w.Y; g.sa_r = n;
-    g.B = w.P; g.sb_r = n;
-    g.C = a.C_out; g.ldc = n;
-    g.Cin = Cp; g.ldcin = n;
-    g.alpha = -1.0; g.beta = 1.0;
-    g.variant = update_variant_c();
-    ProfScope ps(ST_GEMM_C, st);
-    HIKF_TRY(dgemm(g, 1, st));
+  if (!form_y2) {
+    // ---- K = C' S^-1 in one GEMM: C_new = C' - K HC' = r K (HC' = S - r I);
+    //      fused row partials psq = rowsum(K o C'), pdot = K innov ----
+    const int vc = update_variant_c();
+    const int nt = dgemm_col_tiles(n, vc);
+    {
+      GemmArgs g;
+      g.M = m; g.N = n; g.K = n;
+      g.A = Cp; g.sa_r = n;
+      g.B = w.Sinv; g.sb_r = n;
+      g.C = a.C_out; g.ldc = n;
+      g.alpha = a.r;
+      g.psq = w.psq; g.pdot = w.pdot; g.w = w.innov; g.ldp = nt;
+      g.px = Cp; g.ldx = n;
+      g.variant = vc;
+      ProfScope ps(ST_GEMM_C, st);
+      HIKF_TRY(dgemm(g, 1, st));
+    }
+    ProfScope pz(ST_FINALIZE, st);
+    finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
+    HIKF_CHECK_LAUNCH();
+    check_variance<<<1, 1, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+    HIKF_CHECK_LAUNCH();
+  } else {
+    // ---- Y = C' Li^T with fused row partials (|Y_i|^2, Y_i . w) ----
+    const int vy = update_variant_y();
+    const int nt = dgemm_col_tiles(n, vy);
+    {
+      GemmArgs g;
+      g.M = m; g.N = n; g.K = n;
+      g.A = Cp; g.sa_r = n;
+      g.B = w.LiT; g.sb_r = n;
+      g.C = w.Y; g.ldc = n;
+      g.kmode = KB_UPPER;
+      g.psq = w.psq; g.pdot = w.pdot; g.w = w.w; g.ldp = nt;
+      g.variant = vy;
+      ProfScope ps(ST_GEMM_Y, st);
+      HIKF_TRY(dgemm(g, 1, st));
+    }
+    ProfScope* pz = new ProfScope(ST_FINALIZE, st);
+    finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
+    HIKF_CHECK_LAUNCH();
+    check_variance<<<1, 1, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+    HIKF_CHECK_LAUNCH();
+    delete pz;
+    // ---- C_new = C' - Y P ----
+    {
+      GemmArgs g;
+      g.M = m; g.N = n; g.K = n;
+      g.A = w.Y; g.sa_r = n;
+      g.B = w.P; g.sb_r = n;
+      g.C = a.C_out; g.ldc = n;
+      g.Cin = Cp; g.ldcin = n;
+      g.alpha = -1.0; g.beta = 1.0;
+      g.variant = update_variant_c();
+      ProfScope ps(ST_GEMM_C, st);
+      HIKF_TRY(dgemm(g, 1, st));
+    }
   }
 
   // ---- status back to the host ----

@@ -10,6 +10,111 @@ namespace hikf {
 
 namespace {
 
+// Shared epilogue: alpha/beta, fused row partials, stores.  Accumulator
+// acc[i][j][h] holds C[row = i*8 + gq][col] of the warp tile with
+//   SPLIT = false: col = j*8 + 2 t4 + h        (8-column DMMA tiles)
+//   SPLIT = true:  col = (2 t4 + h) * TN + j   (interleaved tiles: each thread
+//                  owns two runs of TN contiguous columns)
+template <int BM, int BN, int WM, int WN, bool PARTIALS, bool SPLIT = false>
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[BM / WM / 8][BN / WN / 8][2], double* C,
+                                              const double* Cin, int64_t m0, int64_t n0, int tid, int wm, int wn,
+                                              int gq, int t4, double (*red_sq)[PARTIALS ? BM : 1],
+                                              double (*red_dot)[PARTIALS ? BM : 1]) {
+  constexpr int THREADS = WM * WN * 32;
+  constexpr int TM = BM / WM / 8;
+  constexpr int TN = BN / WN / 8;
+  const int64_t cw = n0 + wn * TN * 8;
+  auto colh = [&](int j, int h) -> int64_t { return cw + (SPLIT ? (2 * t4 + h) * TN + j : j * 8 + 2 * t4 + h); };
+  // beta * Cin is read for the whole warp tile before any store: C may alias
+  // Cin (in-place C_new = C' - Y P), and separating the phases lets the loads
+  // overlap instead of serialising load -> store round trips.
+  if (Cin) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = colh(j, h);
+          double c = 0.0;
+          if (row < g.M && col < g.N) c = Cin[row * g.ldcin + col];
+          acc[i][j][h] = g.alpha * acc[i][j][h] + g.beta * c;
+        }
+    }
+  }
+  // row partials first (they read w / px), then the stores: keeping the
+  // loads ahead of the stores avoids load-after-store serialisation on
+  // possibly aliasing pointers
+  if (PARTIALS) {
+    const double sc = g.px ? 1.0 : (Cin ? 1.0 : g.alpha);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int rl = wm * TM * 8 + i * 8 + gq;
+      const int64_t row = m0 + rl;
+      double ssq = 0.0, sdot = 0.0;
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = colh(j, h);
+          if (row < g.M && col < g.N) {
+            const double v = sc * acc[i][j][h];
+            ssq += v * (g.px ? g.px[row * g.ldx + col] : v);
+            sdot += v * g.w[col];
+          }
+        }
+      ssq += __shfl_xor_sync(0xffffffffu, ssq, 1);
+      ssq += __shfl_xor_sync(0xffffffffu, ssq, 2);
+      sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
+      sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
+      if (t4 == 0) {
+        red_sq[wn][rl] = ssq;
+        red_dot[wn][rl] = sdot;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
+    if (SPLIT && (TN % 2 == 0) && row < g.M && cw + BN / WN <= g.N && g.ldc % 2 == 0 && ((uintptr_t)C & 15) == 0) {
+      // two runs of TN contiguous columns: 16-byte stores
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < TN; j += 2) {
+          const double v0 = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
+          const double v1 = Cin ? acc[i][j + 1][h] : g.alpha * acc[i][j + 1][h];
+          *reinterpret_cast<double2*>(C + row * g.ldc + colh(j, h)) = make_double2(v0, v1);
+        }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t col = colh(j, h);
+          if (row < g.M && col < g.N) C[row * g.ldc + col] = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
+        }
+    }
+  }
+  if (PARTIALS) {
+    __syncthreads();
+    for (int rl = tid; rl < BM; rl += THREADS) {
+      int64_t row = m0 + rl;
+      if (row < g.M) {
+        double s = 0.0, d = 0.0;
+#pragma unroll
+        for (int w = 0; w < WN; ++w) {
+          s += red_sq[w][rl];
+          d += red_dot[w][rl];
+        }
+        g.psq[row * g.ldp + blockIdx.x] = s;
+        g.pdot[row * g.ldp + blockIdx.x] = d;
+      }
+    }
+  }
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool VEC, bool PARTIALS>
 __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
   constexpr int THREADS = WM * WN * 32;
@@ -39,10 +144,39 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
   if (g.kmode == KB_LOWER) kbeg = (n0 / BK) * BK;
   const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
+  // interior fast path (16-byte copies): per-thread offsets fixed, per-tile
+  // bases uniform, no bounds tests
+  constexpr int A_IT = (BM * BK / 2) / THREADS, B_IT = (BK * BN / 2) / THREADS;
+  constexpr int RA = THREADS / (BK / 2), RB = THREADS / (BN / 2);
+  const bool interior = VEC && m0 + BM <= g.M && n0 + BN <= g.N;
+  const int r0 = tid / (BK / 2), kc0 = (tid % (BK / 2)) * 2;
+  const int kr0 = tid / (BN / 2), c0 = (tid % (BN / 2)) * 2;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sa0 = sbase + (uint32_t)(r0 * AS + kc0) * 8u;
+  const uint32_t sb0 = sbase + (uint32_t)(BM * AS + kr0 * BS + c0) * 8u;
+  const double* ga0 = A + (m0 + r0) * g.sa_r + kc0 + kbeg;
+  const double* gb0 = B + (kr0 + kbeg) * g.sb_r + n0 + c0;
+  const int64_t stepA = (int64_t)RA * g.sa_r, stepB = (int64_t)RB * g.sb_r;
+
   auto issue = [&](int tile, int stage) {
     double* As = smem + stage * STAGE;
     double* Bs = As + BM * AS;
     const int64_t k0 = kbeg + (int64_t)tile * BK;
+    if (VEC && A_IT * THREADS == BM * BK / 2 && B_IT * THREADS == BK * BN / 2 && THREADS % (BK / 2) == 0 &&
+        THREADS % (BN / 2) == 0 && interior && k0 + BK <= kend) {
+      const uint32_t so = (uint32_t)(stage * STAGE) * 8u;
+      const double* ga = ga0 + (int64_t)tile * BK;
+      const double* gb = gb0 + (int64_t)tile * BK * g.sb_r;
+#pragma unroll
+      for (int it = 0; it < A_IT; ++it)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa0 + so + (uint32_t)(it * RA * AS * 8)),
+                     "l"(ga + it * stepA));
+#pragma unroll
+      for (int it = 0; it < B_IT; ++it)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sb0 + so + (uint32_t)(it * RB * BS * 8)),
+                     "l"(gb + it * stepB));
+      return;
+    }
     if (VEC) {
 #pragma unroll
       for (int it = 0; it < (BM * BK / 2) / THREADS; ++it) {
@@ -124,85 +258,346 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // ---- epilogue ----
-  // beta * Cin is read for the whole warp tile before any store: C may alias
-  // Cin (in-place C_new = C' - Y P), and separating the phases lets the loads
-  // overlap instead of serialising load -> store round trips.
-  if (Cin) {
+  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
+}
+
+// Pipelined variant (16-byte copies only).  Differences from dgemm_kernel:
+//  * all STAGES slots are in flight: tile t + STAGES is issued into tile t's
+//    slot once every warp has its last fragments of tile t in registers;
+//  * the k-slice fragments are double-buffered in registers, and the first
+//    slice of tile t+1 is loaded before the last DMMAs of tile t, so the
+//    barrier and the shared-memory latency at a tile boundary overlap DMMAs
+//    still queued in the pipe;
+//  * copy addresses are 32-bit offsets from per-tile uniform bases, with the
+//    row / column bounds folded into per-thread masks once.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool PARTIALS>
+__global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel2(GemmArgs g) {
+  constexpr int THREADS = WM * WN * 32;
+  constexpr int AS = BK + 4;
+  constexpr int BS = BN + 4;
+  constexpr int STAGE = BM * AS + BK * BS;
+  constexpr int TM = BM / WM / 8;
+  constexpr int TN = BN / WN / 8;
+  constexpr int KQ = BK / 4;
+  constexpr int A_IT = (BM * BK / 2) / THREADS;
+  constexpr int B_IT = (BK * BN / 2) / THREADS;
+  static_assert(A_IT >= 1 && B_IT >= 1 && A_IT <= 32 && B_IT <= 16, "copy split");
+  extern __shared__ double smem[];
+  __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
+  __shared__ double red_dot[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
+
+  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  const int z = blockIdx.z;
+  const double* A = g.A + z * g.bsA;
+  const double* B = g.B + z * g.bsB;
+  double* C = g.C + z * g.bsC;
+  const double* Cin = g.Cin ? g.Cin + z * g.bsCin : nullptr;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int gq = lane >> 2, t4 = lane & 3;
+
+  int64_t kbeg = 0, kend = g.K;
+  if (g.kmode == KB_UPPER) kend = min(g.K, n0 + BN);
+  if (g.kmode == KB_LOWER) kbeg = (n0 / BK) * BK;
+  const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  // per-thread copy masks (bounds that do not change along k)
+  uint32_t a_ok = 0, b_ok = 0, b_half = 0;
 #pragma unroll
-    for (int i = 0; i < TM; ++i) {
-      const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t col = n0 + wn * TN * 8 + j * 8 + 2 * t4;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double c = 0.0;
-          if (row < g.M && col + h < g.N) c = Cin[row * g.ldcin + col + h];
-          acc[i][j][h] = g.alpha * acc[i][j][h] + g.beta * c;
-        }
-      }
-    }
+  for (int it = 0; it < A_IT; ++it) {
+    const int r = (tid + it * THREADS) / (BK / 2);
+    if (m0 + r < g.M) a_ok |= 1u << it;
   }
-  // row partials first (they read w / px), then the stores: keeping the
-  // loads ahead of the stores avoids load-after-store serialisation on
-  // possibly aliasing pointers
-  if (PARTIALS) {
-    const double sc = g.px ? 1.0 : (Cin ? 1.0 : g.alpha);
 #pragma unroll
-    for (int i = 0; i < TM; ++i) {
-      const int rl = wm * TM * 8 + i * 8 + gq;
-      const int64_t row = m0 + rl;
-      double ssq = 0.0, sdot = 0.0;
-#pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        const int64_t col = n0 + wn * TN * 8 + j * 8 + 2 * t4;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (row < g.M && col + h < g.N) {
-            const double v = sc * acc[i][j][h];
-            ssq += v * (g.px ? g.px[row * g.ldx + col + h] : v);
-            sdot += v * g.w[col + h];
-          }
-        }
-      }
-      ssq += __shfl_xor_sync(0xffffffffu, ssq, 1);
-      ssq += __shfl_xor_sync(0xffffffffu, ssq, 2);
-      sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
-      sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
-      if (t4 == 0) {
-        red_sq[wn][rl] = ssq;
-        red_dot[wn][rl] = sdot;
-      }
-    }
+  for (int it = 0; it < B_IT; ++it) {
+    const int c = ((tid + it * THREADS) % (BN / 2)) * 2;
+    if (n0 + c < g.N) b_ok |= 1u << it;
+    if (n0 + c + 1 == g.N) b_half |= 1u << it;
   }
+  const double* Ab = A + m0 * g.sa_r;
+  const double* Bb = B + n0;
+
+  auto issue = [&](int tile, int stage) {
+    double* As = smem + stage * STAGE;
+    double* Bs = As + BM * AS;
+    const int64_t k0 = kbeg + (int64_t)tile * BK;
+    const bool fullk = k0 + BK <= kend;
+    const double* At = Ab + k0;
+    const double* Bt = Bb + k0 * g.sb_r;
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
-#pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const int64_t col = n0 + wn * TN * 8 + j * 8 + 2 * t4;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (row < g.M && col + h < g.N) C[row * g.ldc + col + h] = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
+    for (int it = 0; it < A_IT; ++it) {
+      const int e = tid + it * THREADS;
+      const int r = e / (BK / 2), kc = (e % (BK / 2)) * 2;
+      int bytes = (a_ok >> it) & 1 ? 16 : 0;
+      if (!fullk) {
+        const int64_t rem = kend - (k0 + kc);
+        bytes = rem >= 2 ? bytes : (rem == 1 ? bytes / 2 : 0);
+      }
+      cp_async16(As + r * AS + kc, bytes ? At + r * g.sa_r + kc : A, bytes);
     }
-  }
-  if (PARTIALS) {
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it) {
+      const int e = tid + it * THREADS;
+      const int kr = e / (BN / 2), c = (e % (BN / 2)) * 2;
+      int bytes = (b_ok >> it) & 1 ? ((b_half >> it) & 1 ? 8 : 16) : 0;
+      if (!fullk && k0 + kr >= kend) bytes = 0;
+      cp_async16(Bs + kr * BS + c, bytes ? Bt + kr * g.sb_r + c : B, bytes);
+    }
+  };
+
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  double af[2][TM], bf[2][TN];
+  auto load_frag = [&](int buf, int stage, int kb) {
+    const double* As = smem + stage * STAGE + (wm * TM * 8) * AS;
+    const double* Bs = smem + stage * STAGE + BM * AS + wn * TN * 8;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) af[buf][i] = As[(i * 8 + gq) * AS + kb + t4];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) bf[buf][j] = Bs[(kb + t4) * BS + j * 8 + gq];
+  };
+
+  if (ntiles > 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      if (s < ntiles) issue(s, s);
+      cp_async_commit();
+    }
+    cp_async_wait<STAGES - 1>();
     __syncthreads();
-    for (int rl = tid; rl < BM; rl += THREADS) {
-      int64_t row = m0 + rl;
-      if (row < g.M) {
-        double s = 0.0, d = 0.0;
+    load_frag(0, 0, 0);
+    int stage = 0;
+    for (int tile = 0; tile < ntiles; ++tile) {
 #pragma unroll
-        for (int w = 0; w < WN; ++w) {
-          s += red_sq[w][rl];
-          d += red_dot[w][rl];
+      for (int kq = 0; kq < KQ; ++kq) {
+        const int cur = kq & 1;
+        if (kq == KQ - 1) {
+          // tile + 1 resident, every warp past its reads of this tile's slot
+          cp_async_wait<STAGES - 2>();
+          __syncthreads();
+          if (tile + STAGES < ntiles) issue(tile + STAGES, stage);
+          cp_async_commit();
+          const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+          if (tile + 1 < ntiles) load_frag(cur ^ 1, nstage, 0);
+        } else {
+          load_frag(cur ^ 1, stage, (kq + 1) * 4);
         }
-        g.psq[row * g.ldp + blockIdx.x] = s;
-        g.pdot[row * g.ldp + blockIdx.x] = d;
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
       }
+      stage = stage + 1 == STAGES ? 0 : stage + 1;
     }
   }
+  cp_async_wait<0>();
+  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool P>
+int launch_two(const GemmArgs& g, int batch, cudaStream_t st) {
+  constexpr size_t smem = (size_t)STAGES * (BM * (BK + 4) + BK * (BN + 4)) * sizeof(double);
+  auto kern = dgemm_kernel2<BM, BN, BK, WM, WN, STAGES, MINB, P>;
+  static bool configured = false;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), (unsigned)batch);
+  kern<<<grid, WM * WN * 32, smem, st>>>(g);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+// LDS.128 variant (16-byte copies only).  The k-slots of the DMMA are
+// remapped so each thread's operands are contiguous in shared memory:
+//   step q (0..3) of a 16-deep k-tile uses k = 4 t4 + q for lane (gq, t4),
+//   so a thread's A values A[row][4 t4 .. 4 t4 + 3] are two LDS.128;
+//   the 8-column DMMA tile j is the column set {c * TN + j}, so a thread's B
+//   values B[k][gq TN .. gq TN + TN - 1] are TN / 2 LDS.128.
+// Per warp and k-tile that is 2 TM + 2 TN loads for 4 TM TN DMMAs (the
+// 8-byte-fragment kernel needs 4 TM + 4 TN).  A rows are padded to 18 doubles
+// and B rows swizzled (16-byte chunk c of k-row r stored at c ^ ((r >> 2) & 3))
+// so every quarter-warp LDS.128 phase hits 8 distinct 16-byte bank groups.
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool PARTIALS, int BK = 16>
+__global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) {
+  static_assert(BK % 16 == 0, "k-tile is a multiple of 16");
+  constexpr int THREADS = WM * WN * 32;
+  constexpr int AS = BK + 2;
+  constexpr int BS = BN;
+  constexpr int STAGE = BM * AS + BK * BS;
+  constexpr int TM = BM / WM / 8;
+  constexpr int TN = BN / WN / 8;
+  constexpr int A_IT = (BM * BK / 2) / THREADS;
+  constexpr int B_IT = (BK * BN / 2) / THREADS;
+  static_assert(TN == 8, "swizzle assumes 4 chunks per thread row");
+  static_assert(A_IT >= 1 && B_IT >= 1 && A_IT <= 32 && B_IT <= 32, "copy split");
+  extern __shared__ double smem[];
+  __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
+  __shared__ double red_dot[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
+
+  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  const int z = blockIdx.z;
+  const double* A = g.A + z * g.bsA;
+  const double* B = g.B + z * g.bsB;
+  double* C = g.C + z * g.bsC;
+  const double* Cin = g.Cin ? g.Cin + z * g.bsCin : nullptr;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int gq = lane >> 2, t4 = lane & 3;
+
+  int64_t kbeg = 0, kend = g.K;
+  if (g.kmode == KB_UPPER) kend = min(g.K, n0 + BN);
+  if (g.kmode == KB_LOWER) kbeg = (n0 / BK) * BK;
+  const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  uint32_t a_ok = 0, b_ok = 0, b_half = 0;
+#pragma unroll
+  for (int it = 0; it < A_IT; ++it) {
+    const int r = (tid + it * THREADS) / (BK / 2);
+    if (m0 + r < g.M) a_ok |= 1u << it;
+  }
+#pragma unroll
+  for (int it = 0; it < B_IT; ++it) {
+    const int c = ((tid + it * THREADS) % (BN / 2)) * 2;
+    if (n0 + c < g.N) b_ok |= 1u << it;
+    if (n0 + c + 1 == g.N) b_half |= 1u << it;
+  }
+  const double* Ab = A + m0 * g.sa_r;
+  const double* Bb = B + n0;
+
+  // interior fast path: per-thread offsets fixed, per-tile bases uniform
+  static_assert(THREADS % (BK / 2) == 0 && THREADS % (BN / 2) == 0, "copy rows");
+  constexpr int RA = THREADS / (BK / 2), RB = THREADS / (BN / 2);
+  const bool interior = m0 + BM <= g.M && n0 + BN <= g.N;
+  const int r0 = tid / (BK / 2), kc0 = (tid % (BK / 2)) * 2;
+  const int kr0 = tid / (BN / 2), ch0 = tid % (BN / 2);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t sa0 = sbase + (uint32_t)(r0 * AS + kc0) * 8u;
+  const uint32_t sb0 = sbase + (uint32_t)(BM * AS + kr0 * BS) * 8u;
+  const double* ga0 = Ab + r0 * g.sa_r + kc0 + kbeg;
+  const double* gb0 = Bb + (kr0 + kbeg) * g.sb_r + 2 * ch0;
+  const int64_t stepA = (int64_t)RA * g.sa_r, stepB = (int64_t)RB * g.sb_r;
+
+  auto issue = [&](int tile, int stage) {
+    const int64_t k0 = kbeg + (int64_t)tile * BK;
+    if (interior && k0 + BK <= kend) {
+      const uint32_t so = (uint32_t)(stage * STAGE) * 8u;
+      const double* ga = ga0 + (int64_t)tile * BK;
+      const double* gb = gb0 + (int64_t)tile * BK * g.sb_r;
+#pragma unroll
+      for (int it = 0; it < A_IT; ++it)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa0 + so + (uint32_t)(it * RA * AS * 8)),
+                     "l"(ga + it * stepA));
+#pragma unroll
+      for (int it = 0; it < B_IT; ++it) {
+        const int kr = kr0 + it * RB;
+        const uint32_t d = sb0 + so + (uint32_t)(it * RB * BS * 8) + (uint32_t)((ch0 ^ ((kr >> 2) & 3)) * 16);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gb + it * stepB));
+      }
+      return;
+    }
+    double* As = smem + stage * STAGE;
+    double* Bs = As + BM * AS;
+    const bool fullk = k0 + BK <= kend;
+    const double* At = Ab + k0;
+    const double* Bt = Bb + k0 * g.sb_r;
+#pragma unroll
+    for (int it = 0; it < A_IT; ++it) {
+      const int e = tid + it * THREADS;
+      const int r = e / (BK / 2), kc = (e % (BK / 2)) * 2;
+      int bytes = (a_ok >> it) & 1 ? 16 : 0;
+      if (!fullk) {
+        const int64_t rem = kend - (k0 + kc);
+        bytes = rem >= 2 ? bytes : (rem == 1 ? bytes / 2 : 0);
+      }
+      cp_async16(As + r * AS + kc, bytes ? At + r * g.sa_r + kc : A, bytes);
+    }
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it) {
+      const int e = tid + it * THREADS;
+      const int kr = e / (BN / 2), ch = e % (BN / 2);
+      int bytes = (b_ok >> it) & 1 ? ((b_half >> it) & 1 ? 8 : 16) : 0;
+      if (!fullk && k0 + kr >= kend) bytes = 0;
+      cp_async16(Bs + kr * BS + 2 * (ch ^ ((kr >> 2) & 3)), bytes ? Bt + kr * g.sb_r + 2 * ch : B, bytes);
+    }
+  };
+
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ntiles) issue(s, s);
+    cp_async_commit();
+  }
+  int stage = 0;
+  for (int tile = 0; tile < ntiles; ++tile) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = tile + STAGES - 1;
+      const int ns = stage == 0 ? STAGES - 1 : stage - 1;  // == nt % STAGES
+      if (nt < ntiles) issue(nt, ns);
+      cp_async_commit();
+    }
+    const double* As = smem + stage * STAGE + (wm * TM * 8 + gq) * AS + 4 * t4;
+    const double* Bs = smem + stage * STAGE + BM * AS + wn * TN * 8;
+#pragma unroll
+    for (int h16 = 0; h16 < BK / 16; ++h16) {
+      double a[TM][4];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const double2 x = *reinterpret_cast<const double2*>(As + i * 8 * AS + 16 * h16);
+        const double2 y = *reinterpret_cast<const double2*>(As + i * 8 * AS + 16 * h16 + 2);
+        a[i][0] = x.x; a[i][1] = x.y; a[i][2] = y.x; a[i][3] = y.y;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double* Br = Bs + (16 * h16 + 4 * t4 + q) * BS;
+        double b[TN];
+#pragma unroll
+        for (int jj = 0; jj < TN / 2; ++jj) {
+          const double2 v = *reinterpret_cast<const double2*>(Br + 2 * ((gq * (TN / 2) + jj) ^ t4));
+          b[2 * jj] = v.x;
+          b[2 * jj + 1] = v.y;
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i][q], b[j]);
+      }
+    }
+    stage = stage + 1 == STAGES ? 0 : stage + 1;
+  }
+  cp_async_wait<0>();
+  gemm_epilogue<BM, BN, WM, WN, PARTIALS, true>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool P, int BK = 16>
+int launch_three(const GemmArgs& g, int batch, cudaStream_t st) {
+  constexpr size_t smem = (size_t)STAGES * (BM * (BK + 2) + BK * BN) * sizeof(double);
+  auto kern = dgemm_kernel3<BM, BN, WM, WN, STAGES, MINB, P, BK>;
+  static bool configured = false;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), (unsigned)batch);
+  kern<<<grid, WM * WN * 32, smem, st>>>(g);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool VEC, bool P>
@@ -227,6 +622,20 @@ int launch_variant(const GemmArgs& g, int batch, bool vec, bool part, cudaStream
                 : launch_one<BM, BN, BK, WM, WN, STAGES, MINB, true, false>(g, batch, st);
   return part ? launch_one<BM, BN, BK, WM, WN, STAGES, MINB, false, true>(g, batch, st)
               : launch_one<BM, BN, BK, WM, WN, STAGES, MINB, false, false>(g, batch, st);
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
+int launch_variant2(const GemmArgs& g, int batch, bool vec, bool part, cudaStream_t st) {
+  if (!vec) return launch_variant<BM, BN, BK, WM, WN, STAGES, MINB>(g, batch, vec, part, st);
+  return part ? launch_two<BM, BN, BK, WM, WN, STAGES, MINB, true>(g, batch, st)
+              : launch_two<BM, BN, BK, WM, WN, STAGES, MINB, false>(g, batch, st);
+}
+
+template <int BM, int BN, int WM, int WN, int STAGES, int MINB, int BK = 16>
+int launch_variant3(const GemmArgs& g, int batch, bool vec, bool part, cudaStream_t st) {
+  if (!vec) return launch_variant<BM, BN, 16, WM, WN, STAGES, MINB>(g, batch, vec, part, st);
+  return part ? launch_three<BM, BN, WM, WN, STAGES, MINB, true, BK>(g, batch, st)
+              : launch_three<BM, BN, WM, WN, STAGES, MINB, false, BK>(g, batch, st);
 }
 
 int g_variant = -1;
@@ -274,6 +683,38 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
       return launch_variant<64, 64, 32, 2, 2, 2, 3>(g, batch, vec, part, st);
     case 10:  // 64x64x16, 4 warps of 32x32, 2 stages, 5 CTAs / SM
       return launch_variant<64, 64, 16, 2, 2, 2, 4>(g, batch, vec, part, st);
+    case 11:  // 64x128x16, 4 warps of 32x64, 3 stages, 2 CTAs / SM
+      return launch_variant<64, 128, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
+    case 12:  // 64x128x16, 4 warps of 32x64, 4 stages, 2 CTAs / SM
+      return launch_variant<64, 128, 16, 2, 2, 4, 2>(g, batch, vec, part, st);
+    case 13:  // 128x64x16, 4 warps of 64x32, 3 stages, 2 CTAs / SM
+      return launch_variant<128, 64, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
+    case 14:  // 64x128x16, 4 warps of 32x64, 2 stages, 3 CTAs / SM
+      return launch_variant<64, 128, 16, 2, 2, 2, 3>(g, batch, vec, part, st);
+    case 15:  // 64x128x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
+      return launch_variant<64, 128, 32, 2, 2, 2, 2>(g, batch, vec, part, st);
+    case 16:  // v7 shape, pipelined kernel
+      return launch_variant2<64, 128, 16, 2, 4, 3, 2>(g, batch, vec, part, st);
+    case 17:  // v11 shape (4 warps of 32x64), pipelined kernel
+      return launch_variant2<64, 128, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
+    case 18:  // v10 shape (64x64x16, 2 stages), pipelined kernel
+      return launch_variant2<64, 64, 16, 2, 2, 2, 4>(g, batch, vec, part, st);
+    case 21:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 3 stages, 2 CTAs / SM
+      return launch_variant3<64, 128, 2, 2, 3, 2>(g, batch, vec, part, st);
+    case 22:  // LDS.128 kernel: 128x64x16, 4 warps of 32x64 (2 x 1... see dgemm.cuh), 3 stages
+      return launch_variant3<128, 64, 4, 1, 3, 2>(g, batch, vec, part, st);
+    case 23:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 4 stages, 2 CTAs / SM
+      return launch_variant3<64, 128, 2, 2, 4, 2>(g, batch, vec, part, st);
+    case 24:  // LDS.128 kernel: 128x128x16, 8 warps of 32x64, 3 stages, 1 CTA / SM
+      return launch_variant3<128, 128, 4, 2, 3, 1>(g, batch, vec, part, st);
+    case 25:  // LDS.128 kernel: 64x128x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
+      return launch_variant3<64, 128, 2, 2, 2, 2, 32>(g, batch, vec, part, st);
+    case 26:  // LDS.128 kernel: 128x64x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
+      return launch_variant3<128, 64, 4, 1, 2, 2, 32>(g, batch, vec, part, st);
+    case 27:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 2 stages, 2 CTAs / SM
+      return launch_variant3<64, 128, 2, 2, 2, 2>(g, batch, vec, part, st);
+    case 20:  // 64x128x32, 8 warps, 2 stages, 2 CTAs / SM
+      return launch_variant2<64, 128, 32, 2, 4, 2, 2>(g, batch, vec, part, st);
     default:  // 128x128x16, 8 warps of 64x32, 5 stages
       return launch_variant<128, 128, 16, 2, 4, 5, 1>(g, batch, vec, part, st);
   }

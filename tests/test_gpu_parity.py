@@ -317,3 +317,42 @@ def test_cuda_row_sharded_update_equals_full(pkg):
     assert O.rel_fro(mean, st_full.mean) <= 1e-12
     assert O.rel_fro(var, st_full.variance) <= 1e-12
     assert O.rel_fro(C, st_full.cross_cov) <= 1e-12
+
+
+def test_lookahead_factorisation_is_bit_identical(pkg):
+    """The update factorises the next step's S while its GEMM runs (update.cu,
+    LookAhead).  A run where every step hits the look-ahead and a run where
+    every step misses it (the HC_Q argument alternates between two buffers of
+    equal content, so the pointer check fails) must agree bitwise, and a stale
+    look-ahead (HC changed behind the library's back) must not be used."""
+    import torch
+    from paper_1404_3816_b200.sharded import CudaRowStep
+    from paper_1404_3816_b200.filters import DeviceCSR
+    g = _load("cfg1.npz")
+    cfg = cases.CFG1
+    tree, H, pre, _ = _run_filter(pkg, dict(cfg, T=1), g["obs"])
+    m, n = H.shape[1], H.shape[0]
+    Hd = DeviceCSR(H)
+
+    def run(alternate, poke=False):
+        hcq = [pre.HC_Q_t, pre.HC_Q_t.clone()]
+        st = {"mean": torch.zeros(m, dtype=torch.float64, device="cuda"),
+              "C": torch.zeros(m, n, dtype=torch.float64, device="cuda"),
+              "var": torch.zeros(m, dtype=torch.float64, device="cuda"),
+              "HC": torch.zeros(n, n, dtype=torch.float64, device="cuda")}
+        for t in range(5):
+            step = CudaRowStep((pre.C_Q_t, hcq[t % 2] if alternate else hcq[0], pre.diag_Q_t), n)
+            if poke and t == 3:
+                st["HC"] = st["HC"].clone()
+                st["HC"][0, 0] += 1e-9  # the look-ahead computed from the old HC is stale now
+            z = torch.as_tensor(g["obs"][t]).cuda()
+            st = step.update_rows(st, step.spmv(Hd, st), cfg["R"], z)[0]
+        return st
+
+    hits, misses = run(False), run(True)
+    for k in hits:
+        assert torch.equal(hits[k], misses[k]), k
+    poked_hits, poked_misses = run(False, poke=True), run(True, poke=True)
+    for k in poked_hits:
+        assert torch.equal(poked_hits[k], poked_misses[k]), k
+    assert not torch.equal(poked_hits["C"], hits["C"])

@@ -40,14 +40,18 @@ ws = torch.empty(int(lib.hikf_update_workspace_bytes(m, n)), dtype=torch.uint8, 
 mv = ctypes.c_double(0.0)
 
 
+mode = sys.argv[3] if len(sys.argv) > 3 else "update"
+
+
 def step():
-    _lib.check(lib.hikf_update(m, n, mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), CQ.data_ptr(),
-                               dQ.data_ptr(), HCQ.data_ptr(), ip.data_ptr(), ix.data_ptr(), val.data_ptr(), 1e-3,
+    fused = mode != "nopredict"  # nopredict: update only (no fused predict), factor timed alone
+    _lib.check(lib.hikf_update(m, n, mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(),
+                               CQ.data_ptr() if fused else None, dQ.data_ptr() if fused else None,
+                               HCQ.data_ptr() if fused else None, ip.data_ptr(), ix.data_ptr(), val.data_ptr(), 1e-3,
                                z.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(),
                                outs[3].data_ptr(), ws.data_ptr(), ws.numel(), ctypes.byref(mv), _lib.stream_ptr()))
 
 
-mode = sys.argv[3] if len(sys.argv) > 3 else "update"
 if mode == "gemm":
     # only the two m x n x n GEMMs of the update, with the update's operands and variants:
     # Y = C' Li^T (B upper triangular, variant 10) and C_new = C' - Y P (variant 7)

@@ -59,7 +59,7 @@ FP64_PEAK_SOURCE = "measured cuBLAS DGEMM 8192^3 on B200 (profiles/r01_fp64_dgem
 # DRAM traffic of one C-GEMM launch at cfg4 from `ncu --set full` (dram__bytes_read.sum +
 # dram__bytes_write.sum, profiles/r01_ncu_sparse_summary.txt: 17.2 + 8.56 GB); the algorithmic
 # bytes are Y + C' in, C out = 3 x 8 m n = 25.8 GB (P stays in L2).
-C_GEMM_TRAFFIC_CFG4 = 17.2e9 + 8.559e9
+C_GEMM_TRAFFIC_CFG4 = 8.615e9 + 8.694e9  # ncu dram read + write of the K GEMM (profiles/r01_ncu_kgemm_summary.txt)
 
 
 def hbm_peak():

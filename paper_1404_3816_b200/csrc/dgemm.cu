@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
     if (s < ntiles) issue(s, s);
     cp_async_commit();
   }
-  for (int tile = 0; tile < ntiles; ++tile) {
+  auto tile_step = [&](int tile) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     int nt = tile + STAGES - 1;
@@ -255,164 +255,11 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
-  }
+  };
+  for (int tile = 0; tile < ntiles; ++tile) tile_step(tile);
   cp_async_wait<0>();
 
   gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
-}
-
-// Pipelined variant (16-byte copies only).  Differences from dgemm_kernel:
-//  * all STAGES slots are in flight: tile t + STAGES is issued into tile t's
-//    slot once every warp has its last fragments of tile t in registers;
-//  * the k-slice fragments are double-buffered in registers, and the first
-//    slice of tile t+1 is loaded before the last DMMAs of tile t, so the
-//    barrier and the shared-memory latency at a tile boundary overlap DMMAs
-//    still queued in the pipe;
-//  * copy addresses are 32-bit offsets from per-tile uniform bases, with the
-//    row / column bounds folded into per-thread masks once.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool PARTIALS>
-__global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel2(GemmArgs g) {
-  constexpr int THREADS = WM * WN * 32;
-  constexpr int AS = BK + 4;
-  constexpr int BS = BN + 4;
-  constexpr int STAGE = BM * AS + BK * BS;
-  constexpr int TM = BM / WM / 8;
-  constexpr int TN = BN / WN / 8;
-  constexpr int KQ = BK / 4;
-  constexpr int A_IT = (BM * BK / 2) / THREADS;
-  constexpr int B_IT = (BK * BN / 2) / THREADS;
-  static_assert(A_IT >= 1 && B_IT >= 1 && A_IT <= 32 && B_IT <= 16, "copy split");
-  extern __shared__ double smem[];
-  __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
-  __shared__ double red_dot[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
-
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
-  const int z = blockIdx.z;
-  const double* A = g.A + z * g.bsA;
-  const double* B = g.B + z * g.bsB;
-  double* C = g.C + z * g.bsC;
-  const double* Cin = g.Cin ? g.Cin + z * g.bsCin : nullptr;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WN, wn = warp % WN;
-  const int gq = lane >> 2, t4 = lane & 3;
-
-  int64_t kbeg = 0, kend = g.K;
-  if (g.kmode == KB_UPPER) kend = min(g.K, n0 + BN);
-  if (g.kmode == KB_LOWER) kbeg = (n0 / BK) * BK;
-  const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
-
-  // per-thread copy masks (bounds that do not change along k)
-  uint32_t a_ok = 0, b_ok = 0, b_half = 0;
-#pragma unroll
-  for (int it = 0; it < A_IT; ++it) {
-    const int r = (tid + it * THREADS) / (BK / 2);
-    if (m0 + r < g.M) a_ok |= 1u << it;
-  }
-#pragma unroll
-  for (int it = 0; it < B_IT; ++it) {
-    const int c = ((tid + it * THREADS) % (BN / 2)) * 2;
-    if (n0 + c < g.N) b_ok |= 1u << it;
-    if (n0 + c + 1 == g.N) b_half |= 1u << it;
-  }
-  const double* Ab = A + m0 * g.sa_r;
-  const double* Bb = B + n0;
-
-  auto issue = [&](int tile, int stage) {
-    double* As = smem + stage * STAGE;
-    double* Bs = As + BM * AS;
-    const int64_t k0 = kbeg + (int64_t)tile * BK;
-    const bool fullk = k0 + BK <= kend;
-    const double* At = Ab + k0;
-    const double* Bt = Bb + k0 * g.sb_r;
-#pragma unroll
-    for (int it = 0; it < A_IT; ++it) {
-      const int e = tid + it * THREADS;
-      const int r = e / (BK / 2), kc = (e % (BK / 2)) * 2;
-      int bytes = (a_ok >> it) & 1 ? 16 : 0;
-      if (!fullk) {
-        const int64_t rem = kend - (k0 + kc);
-        bytes = rem >= 2 ? bytes : (rem == 1 ? bytes / 2 : 0);
-      }
-      cp_async16(As + r * AS + kc, bytes ? At + r * g.sa_r + kc : A, bytes);
-    }
-#pragma unroll
-    for (int it = 0; it < B_IT; ++it) {
-      const int e = tid + it * THREADS;
-      const int kr = e / (BN / 2), c = (e % (BN / 2)) * 2;
-      int bytes = (b_ok >> it) & 1 ? ((b_half >> it) & 1 ? 8 : 16) : 0;
-      if (!fullk && k0 + kr >= kend) bytes = 0;
-      cp_async16(Bs + kr * BS + c, bytes ? Bt + kr * g.sb_r + c : B, bytes);
-    }
-  };
-
-  double acc[TM][TN][2];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  double af[2][TM], bf[2][TN];
-  auto load_frag = [&](int buf, int stage, int kb) {
-    const double* As = smem + stage * STAGE + (wm * TM * 8) * AS;
-    const double* Bs = smem + stage * STAGE + BM * AS + wn * TN * 8;
-#pragma unroll
-    for (int i = 0; i < TM; ++i) af[buf][i] = As[(i * 8 + gq) * AS + kb + t4];
-#pragma unroll
-    for (int j = 0; j < TN; ++j) bf[buf][j] = Bs[(kb + t4) * BS + j * 8 + gq];
-  };
-
-  if (ntiles > 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) {
-      if (s < ntiles) issue(s, s);
-      cp_async_commit();
-    }
-    cp_async_wait<STAGES - 1>();
-    __syncthreads();
-    load_frag(0, 0, 0);
-    int stage = 0;
-    for (int tile = 0; tile < ntiles; ++tile) {
-#pragma unroll
-      for (int kq = 0; kq < KQ; ++kq) {
-        const int cur = kq & 1;
-        if (kq == KQ - 1) {
-          // tile + 1 resident, every warp past its reads of this tile's slot
-          cp_async_wait<STAGES - 2>();
-          __syncthreads();
-          if (tile + STAGES < ntiles) issue(tile + STAGES, stage);
-          cp_async_commit();
-          const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
-          if (tile + 1 < ntiles) load_frag(cur ^ 1, nstage, 0);
-        } else {
-          load_frag(cur ^ 1, stage, (kq + 1) * 4);
-        }
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
-      }
-      stage = stage + 1 == STAGES ? 0 : stage + 1;
-    }
-  }
-  cp_async_wait<0>();
-  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
-}
-
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool P>
-int launch_two(const GemmArgs& g, int batch, cudaStream_t st) {
-  constexpr size_t smem = (size_t)STAGES * (BM * (BK + 4) + BK * (BN + 4)) * sizeof(double);
-  auto kern = dgemm_kernel2<BM, BN, BK, WM, WN, STAGES, MINB, P>;
-  static bool configured = false;
-  if (!configured) {
-    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), (unsigned)batch);
-  kern<<<grid, WM * WN * 32, smem, st>>>(g);
-  HIKF_CHECK_LAUNCH();
-  return HIKF_OK;
 }
 
 // LDS.128 variant (16-byte copies only).  The k-slots of the DMMA are
@@ -624,13 +471,6 @@ int launch_variant(const GemmArgs& g, int batch, bool vec, bool part, cudaStream
               : launch_one<BM, BN, BK, WM, WN, STAGES, MINB, false, false>(g, batch, st);
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
-int launch_variant2(const GemmArgs& g, int batch, bool vec, bool part, cudaStream_t st) {
-  if (!vec) return launch_variant<BM, BN, BK, WM, WN, STAGES, MINB>(g, batch, vec, part, st);
-  return part ? launch_two<BM, BN, BK, WM, WN, STAGES, MINB, true>(g, batch, st)
-              : launch_two<BM, BN, BK, WM, WN, STAGES, MINB, false>(g, batch, st);
-}
-
 template <int BM, int BN, int WM, int WN, int STAGES, int MINB, int BK = 16>
 int launch_variant3(const GemmArgs& g, int batch, bool vec, bool part, cudaStream_t st) {
   if (!vec) return launch_variant<BM, BN, 16, WM, WN, STAGES, MINB>(g, batch, vec, part, st);
@@ -689,32 +529,14 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
       return launch_variant<64, 128, 16, 2, 2, 4, 2>(g, batch, vec, part, st);
     case 13:  // 128x64x16, 4 warps of 64x32, 3 stages, 2 CTAs / SM
       return launch_variant<128, 64, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 14:  // 64x128x16, 4 warps of 32x64, 2 stages, 3 CTAs / SM
-      return launch_variant<64, 128, 16, 2, 2, 2, 3>(g, batch, vec, part, st);
     case 15:  // 64x128x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
       return launch_variant<64, 128, 32, 2, 2, 2, 2>(g, batch, vec, part, st);
-    case 16:  // v7 shape, pipelined kernel
-      return launch_variant2<64, 128, 16, 2, 4, 3, 2>(g, batch, vec, part, st);
-    case 17:  // v11 shape (4 warps of 32x64), pipelined kernel
-      return launch_variant2<64, 128, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 18:  // v10 shape (64x64x16, 2 stages), pipelined kernel
-      return launch_variant2<64, 64, 16, 2, 2, 2, 4>(g, batch, vec, part, st);
     case 21:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 3 stages, 2 CTAs / SM
       return launch_variant3<64, 128, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 22:  // LDS.128 kernel: 128x64x16, 4 warps of 32x64 (2 x 1... see dgemm.cuh), 3 stages
+    case 22:  // LDS.128 kernel: 128x64x16, 4 warps of 32x64 stacked along rows, 3 stages
       return launch_variant3<128, 64, 4, 1, 3, 2>(g, batch, vec, part, st);
-    case 23:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 4 stages, 2 CTAs / SM
-      return launch_variant3<64, 128, 2, 2, 4, 2>(g, batch, vec, part, st);
-    case 24:  // LDS.128 kernel: 128x128x16, 8 warps of 32x64, 3 stages, 1 CTA / SM
-      return launch_variant3<128, 128, 4, 2, 3, 1>(g, batch, vec, part, st);
-    case 25:  // LDS.128 kernel: 64x128x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
-      return launch_variant3<64, 128, 2, 2, 2, 2, 32>(g, batch, vec, part, st);
-    case 26:  // LDS.128 kernel: 128x64x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
-      return launch_variant3<128, 64, 4, 1, 2, 2, 32>(g, batch, vec, part, st);
     case 27:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 2 stages, 2 CTAs / SM
       return launch_variant3<64, 128, 2, 2, 2, 2>(g, batch, vec, part, st);
-    case 20:  // 64x128x32, 8 warps, 2 stages, 2 CTAs / SM
-      return launch_variant2<64, 128, 32, 2, 4, 2, 2>(g, batch, vec, part, st);
     default:  // 128x128x16, 8 warps of 64x32, 5 stages
       return launch_variant<128, 128, 16, 2, 4, 5, 1>(g, batch, vec, part, st);
   }

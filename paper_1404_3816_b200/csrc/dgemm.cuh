@@ -54,7 +54,7 @@ void set_dgemm_variant(int v);
 // number of column tiles (= partial sums per row) the current variant uses for N columns
 inline int dgemm_col_tiles(int64_t N, int variant = -1) {
   int v = variant >= 0 ? variant : dgemm_variant();
-  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 18 || v == 22 || v == 26) ? 64 : 128);
+  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22) ? 64 : 128);
 }
 // variants used by the update for the triangular Y GEMM and the full C GEMM
 // (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log); HIKF_DGEMM_VARIANT overrides both

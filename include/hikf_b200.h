@@ -118,6 +118,15 @@ int hikf_tree_matmat_csrT(hikf_tree* tree, int64_t n, const int32_t* indptr_dev,
 int hikf_precompute(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
                     const double* data_dev, double* C_Q_dev, double* HC_Q_dev, double* diag_Q_dev, void* stream);
 
+/* ---- hikf_precompute_dense (filters.py:108-115; Gram as kernels.py:97-117) ----
+ * The reference's exact-algebra oracle path: C_Q = Q H^T with the dense Gram
+ * Q[i][j] = K(|x_i - x_j|), here as a direct sum over the nonzeros of H^T (Q is
+ * never stored); HC_Q = sym(H C_Q); diag_Q = diag(Q).  xy_host: m x 2 cell
+ * coordinates (original order); H CSR on the device. */
+int hikf_precompute_dense(const double* xy_host, int64_t m, const hikf_kernel* kernel, int64_t n,
+                          const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev,
+                          double* C_Q_dev, double* HC_Q_dev, double* diag_Q_dev, void* stream);
+
 /* ---- hikf_init (filters.py:118-126): C = alpha H^T, var = alpha, HC = alpha H H^T ----
  * (the mean is the caller's initial_mean copy). */
 int hikf_init_state(int64_t m, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,

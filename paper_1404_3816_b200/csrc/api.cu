@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 
+#include "dense.h"
 #include "dgemm.cuh"
 #include "prof.h"
 #include "rays.h"
@@ -315,6 +316,44 @@ int hikf_precompute(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   fill<<<grid_for(t->m), kT, 0, st>>>(dQ, t->m, k0);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
+}
+
+int hikf_precompute_dense(const double* xy_host, int64_t m, const hikf_kernel* kernel, int64_t n, const int32_t* ip,
+                          const int32_t* ix, const double* val, double* CQ, double* HCQ, double* dQ, void* stream) {
+  if (!xy_host || !kernel || m < 1 || n < 0) {
+    set_error("bad dense precompute arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (kernel->family != HIKF_GAUSSIAN && kernel->family != HIKF_EXPONENTIAL && kernel->family != HIKF_LOGARITHM) {
+    set_error("unknown kernel family %d", kernel->family);
+    return HIKF_BAD_ARGUMENT;
+  }
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+    set_error("no CUDA device: the HiKF B200 path has no CPU fallback");
+    return HIKF_NO_DEVICE;
+  }
+  keep_pool();
+  cudaStream_t st = as_stream(stream);
+  double* xy = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&xy, sizeof(double) * 2 * m, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(xy, xy_host, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, st));
+  const KParams kp = make_kparams(*kernel);
+  int s = dense_cq(m, n, xy, ip, ix, val, kp, CQ, st);
+  if (s == HIKF_OK && n > 0) {
+    double* X = nullptr;
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&X, sizeof(double) * n * n, st));
+    spmm_rows<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, CQ, X);
+    HIKF_CHECK_LAUNCH();
+    symmetrize<<<grid_for(n * n), kT, 0, st>>>(X, n, HCQ);
+    HIKF_CHECK_LAUNCH();
+    cudaFreeAsync(X, st);
+  }
+  // diag(Q) = K(0) = value_at_zero (kernels.py:91-95): the dense Gram's diagonal
+  fill<<<grid_for(m), kT, 0, st>>>(dQ, m, kernel->family == HIKF_LOGARITHM ? 0.0 : kernel->variance);
+  HIKF_CHECK_LAUNCH();
+  cudaFreeAsync(xy, st);
+  return s;
 }
 
 int hikf_init_state(int64_t m, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double alpha,

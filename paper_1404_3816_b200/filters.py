@@ -25,7 +25,7 @@ from ._lib import NumericalConsistencyError  # noqa: F401  (re-export, filters.p
 from .kernels import value_at_zero  # noqa: F401
 
 __all__ = [
-    "DeviceCSR", "HikfPrecompute", "HikfState", "NumericalConsistencyError",
+    "DeviceCSR", "HikfPrecompute", "HikfState", "NumericalConsistencyError", "hikf_precompute_dense",
     "hikf_precompute_fmm", "hikf_init", "hikf_predict", "hikf_update",
 ]
 
@@ -189,6 +189,30 @@ def hikf_precompute_fmm(model, tree) -> HikfPrecompute:
     _lib.check(_lib.load().hikf_precompute(tree._handle, n, H.indptr.data_ptr(), H.indices.data_ptr(),
                                            H.data.data_ptr(), C_Q.data_ptr(), HC_Q.data_ptr(), diag_Q.data_ptr(),
                                            _lib.stream_ptr()))
+    return HikfPrecompute(C_Q, HC_Q, diag_Q)
+
+
+def hikf_precompute_dense(model) -> HikfPrecompute:
+    """Exact dense-algebra path (filters.py:108-115): C_Q = Q H^T with the dense
+    Gram Q (kernels.py:97-117), evaluated on the device as a direct sum over the
+    nonzeros of H^T (Q is never stored)."""
+    import ctypes
+
+    from .fmm import _coords_of
+    from .kernels import to_c
+    H = DeviceCSR.of(_model_H(model))
+    xy = _coords_of(model.grid.cell_centers())
+    m, n = xy.shape[0], H.shape[0]
+    if H.shape[1] != m:
+        raise ValueError("operator columns do not match state length")
+    dev = _dev()
+    C_Q = torch.empty((m, n), dtype=torch.float64, device=dev)
+    HC_Q = torch.empty((n, n), dtype=torch.float64, device=dev)
+    diag_Q = torch.empty((m,), dtype=torch.float64, device=dev)
+    kc = to_c(model.q_kernel)
+    _lib.check(_lib.load().hikf_precompute_dense(xy.ctypes.data, m, ctypes.byref(kc), n, H.indptr.data_ptr(),
+                                                 H.indices.data_ptr(), H.data.data_ptr(), C_Q.data_ptr(),
+                                                 HC_Q.data_ptr(), diag_Q.data_ptr(), _lib.stream_ptr()))
     return HikfPrecompute(C_Q, HC_Q, diag_Q)
 
 

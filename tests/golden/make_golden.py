@@ -3,7 +3,7 @@
 Run in the build container only (the reference lives at /root/reference and
 does not travel to the GPU box):
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--big]
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--big | --dense]
 
 Every fixture is produced by the reference ``hikf`` package's own public API
 (build_tree / FmmTree.matmat / hikf_precompute_fmm / hikf_init /
@@ -152,7 +152,44 @@ def run_filter(cfg: dict, full: bool) -> dict:
     return out
 
 
+def dense_cases() -> dict:
+    """hikf_precompute_dense (filters.py:108-115) + the filter on it: the
+    reference's exact-algebra path (run_hikf mode "dense", experiment.py:224)."""
+    out = {}
+    log_case = dict(cases.SMALL, name="small_log", N=16, ns=3, nr=4, family="logarithm", T=6)
+    for cfg in (cases.SMALL, cases.CFG1, log_case):
+        name = cfg["name"]
+        grid, H, kern, model, record = scenario(cfg) if cfg["family"] != "logarithm" else _log_scenario(cfg)
+        pre = flt.hikf_precompute_dense(model)
+        out.update({f"{name}_C_Q": pre.C_Q, f"{name}_HC_Q": pre.HC_Q, f"{name}_diag_Q": pre.diag_Q})
+        if cfg["family"] == "logarithm":  # conditionally PD only: precompute pinned, no filter run
+            continue
+        state = flt.hikf_init(model)
+        for t in range(cfg["T"]):
+            state = flt.hikf_update(flt.hikf_predict(state, pre), H, model.r_variance, record.observations[t])
+        out.update({f"{name}_obs": record.observations, f"{name}_final_mean": state.mean,
+                    f"{name}_final_variance": state.variance, f"{name}_final_cross_cov": state.cross_cov,
+                    f"{name}_final_HC": state.HC})
+        print(f"  dense {name}: m {model.m} n {H.shape[0]}", flush=True)
+    return out
+
+
+def _log_scenario(cfg: dict):
+    N = cfg["N"]
+    grid = Grid2D(nx=N, ny=N, dx=1.0 / N, dy=1.0 / N)
+    acq = default_acquisition(grid, cfg["ns"], cfg["nr"], source_x=0.0, receiver_x=1.0)
+    H = build_ray_operator(grid, acq)
+    kern = KernelSpec("logarithm", log_amplitude=-0.5)
+    model = StateSpaceModel(grid=grid, H=H, q_kernel=kern, r_variance=cfg["R"], alpha=0.0)
+    fields = cases.plume_fields(grid.cell_centers().coords, cfg["T"])
+    record = simulate_truth_and_data(model, PlumeScenario(fields), seed=[cfg["seed"], 0])
+    return grid, H, kern, model, record
+
+
 def main(big: bool):
+    if "--dense" in sys.argv:  # only the dense-path fixtures (other fixtures untouched)
+        np.savez_compressed(os.path.join(HERE, "dense_cases.npz"), **dense_cases())
+        return
     os.makedirs(HERE, exist_ok=True)
     # 1) tree / matmat fixtures over the point-set cases
     for name, (pts, spec, n_cheb, leaf, nvec) in cases.tree_cases().items():

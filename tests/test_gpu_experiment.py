@@ -1,0 +1,78 @@
+"""Dense exact-algebra precompute (hikf_precompute_dense, filters.py:108-115)
+and the device-resident experiment loop (run_hikf, experiment.py:219-242) on
+the GPU, against fixtures made by the reference (tests/golden/dense_cases.npz,
+cfg1.npz, small_rays.npz)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import hikf_oracle as O
+from tests.golden import cases
+
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+LOG = dict(cases.SMALL, name="small_log", N=16, ns=3, nr=4, family="logarithm", T=6)
+
+
+def _scenario(cfg, obs, T=None):
+    import paper_1404_3816_b200 as P
+    from paper_1404_3816_b200 import experiment as E
+    N = cfg["N"]
+    grid = P.Grid2D(nx=N, ny=N, dx=1.0 / N, dy=1.0 / N)
+    H = P.tomography.build_ray_operator(grid, P.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], 0.0, 1.0))
+    kern = (P.KernelSpec("logarithm", log_amplitude=-0.5) if cfg["family"] == "logarithm"
+            else P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"]))
+    model = E.StateSpaceModel(grid=grid, H=H, q_kernel=kern, r_variance=cfg["R"], alpha=0.0)
+    T = cfg["T"] if T is None else T
+    rec = E.SimulatedRecord(truth=np.zeros((T, grid.m)), observations=np.asarray(obs)[:T])
+    return E.Scenario(model=model, record=rec,
+                      fmm_config=P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+
+
+@pytest.mark.parametrize("name,cfg", [("small", cases.SMALL), ("cfg1", cases.CFG1), ("small_log", LOG)])
+def test_dense_precompute_matches_reference(name, cfg):
+    from paper_1404_3816_b200 import filters as flt
+    g = dict(np.load(os.path.join(G, "dense_cases.npz")))
+    scn = _scenario(cfg, np.zeros((cfg["T"], 1)))
+    pre = flt.hikf_precompute_dense(scn.model)
+    assert O.rel_fro(pre.C_Q, g[f"{name}_C_Q"]) <= 1e-13
+    assert O.rel_fro(pre.HC_Q, g[f"{name}_HC_Q"]) <= 1e-13
+    np.testing.assert_array_equal(pre.diag_Q, g[f"{name}_diag_Q"])
+
+
+def test_dense_and_fmm_precompute_agree():
+    """test_filters.py:130-136: FMM C_Q against the dense oracle path.  At the
+    cfg1 order (4) the FMM truncation error must be the reference's own
+    (golden FMM C_Q vs golden dense C_Q); at n_cheb = 7 it must meet the
+    reference test's atol = 1e-6 max|C_Q|."""
+    import paper_1404_3816_b200 as P
+    from paper_1404_3816_b200 import filters as flt
+    cfg = cases.CFG1
+    scn = _scenario(cfg, np.zeros((1, 1)), T=1)
+    dense = flt.hikf_precompute_dense(scn.model)
+    tree = P.build_tree(scn.model.grid.cell_centers(), scn.model.q_kernel, scn.fmm_config)
+    fast = flt.hikf_precompute_fmm(scn.model, tree)
+    ref_err = O.rel_fro(np.load(os.path.join(G, "cfg1.npz"))["C_Q"], np.load(os.path.join(G, "dense_cases.npz"))["cfg1_C_Q"])
+    assert abs(O.rel_fro(fast.C_Q, dense.C_Q) - ref_err) <= 1e-9 * ref_err + 1e-13
+    tree7 = P.build_tree(scn.model.grid.cell_centers(), scn.model.q_kernel, P.FmmConfig(n_cheb=7))
+    fast7 = flt.hikf_precompute_fmm(scn.model, tree7)
+    assert np.allclose(fast7.C_Q, dense.C_Q, atol=1e-6 * np.abs(dense.C_Q).max())
+
+
+@pytest.mark.parametrize("mode,fixture,prefix,cfg", [
+    ("fmm", "small_rays.npz", "", cases.SMALL), ("fmm", "cfg1.npz", "", cases.CFG1),
+    ("dense", "dense_cases.npz", "small_", cases.SMALL), ("dense", "dense_cases.npz", "cfg1_", cases.CFG1)])
+def test_run_hikf_matches_reference(mode, fixture, prefix, cfg):
+    from paper_1404_3816_b200 import experiment as E
+    g = dict(np.load(os.path.join(G, fixture)))
+    scn = _scenario(cfg, g[f"{prefix}obs"])
+    run = E.run_hikf(scn, mode)
+    assert run.label == "hikf" and run.means.shape == (cfg["T"], scn.model.m)
+    assert run.online_seconds > 0 and run.precompute_seconds > 0
+    assert run.storage == E.storage_bytes("hikf", scn.model.m, n=scn.model.n)
+    assert run.effective_ranks == [None] * cfg["T"]
+    assert O.rel_fro(run.means[-1], g[f"{prefix}final_mean"]) <= 1e-9
+    assert O.rel_fro(run.final_variance, g[f"{prefix}final_variance"]) <= 1e-9

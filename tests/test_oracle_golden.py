@@ -166,3 +166,28 @@ def test_oracle_cfg4_pins():
     assert H.nnz == int(g["H_nnz"])
     assert _sha(H.indptr.astype(np.int64), H.indices.astype(np.int64)) == g["H_pattern_sha"].item().decode()
     assert _sha(H.data) == g["H_data_sha"].item().decode()
+
+
+DENSE_CASES = [("small", cases.SMALL), ("cfg1", cases.CFG1),
+               ("small_log", dict(cases.SMALL, N=16, ns=3, nr=4, family="logarithm", T=6))]
+
+
+@pytest.mark.parametrize("name,cfg", DENSE_CASES)
+def test_oracle_dense_precompute_matches_reference(name, cfg):
+    """hikf_precompute_dense (filters.py:108-115) and the filter run on it."""
+    g = _load("dense_cases.npz")
+    xy, H = _scenario(cfg)
+    kern = (O.Kern("logarithm", log_amplitude=-0.5) if cfg["family"] == "logarithm"
+            else O.Kern(cfg["family"], 1.0, cfg["L"]))
+    pre = O.precompute_dense(H, xy, kern)
+    assert O.rel_fro(pre.C_Q, g[f"{name}_C_Q"]) <= 1e-14
+    assert O.rel_fro(pre.HC_Q, g[f"{name}_HC_Q"]) <= 1e-14
+    np.testing.assert_array_equal(pre.diag_Q, g[f"{name}_diag_Q"])
+    if cfg["family"] == "logarithm":
+        return
+    st = O.init_state(H, len(xy))
+    for t in range(cfg["T"]):
+        st = O.update(O.predict(st, pre), H, cfg["R"], g[f"{name}_obs"][t])
+    assert O.rel_fro(st.mean, g[f"{name}_final_mean"]) <= 1e-11
+    assert O.rel_fro(st.variance, g[f"{name}_final_variance"]) <= 1e-11
+    assert O.rel_fro(st.cross_cov, g[f"{name}_final_cross_cov"]) <= 1e-11

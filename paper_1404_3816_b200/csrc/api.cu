@@ -65,14 +65,42 @@ __global__ void scatter_transpose(int64_t n, const int32_t* __restrict__ ip, con
   for (int64_t e = ip[r] + threadIdx.x; e < ip[r + 1]; e += blockDim.x) Ht[(int64_t)ix[e] * n + r] = val[e];
 }
 
-// X = H C (n x n), one CTA per row of H, threads over the n columns
+// X = H C (n x n), one CTA per row of H.  Each thread owns 4 adjacent columns
+// (one 32-byte load per nonzero) and accumulates them in CSR order, so 4
+// independent FMA chains and the row's gathers stay in flight.
 __global__ void spmm_rows(int64_t n, const int32_t* __restrict__ ip, const int32_t* __restrict__ ix,
                           const double* __restrict__ val, const double* __restrict__ C, double* __restrict__ X) {
-  int64_t r = blockIdx.x;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    double s = 0.0;
-    for (int64_t e = ip[r]; e < ip[r + 1]; ++e) s += val[e] * C[(int64_t)ix[e] * n + j];
-    X[r * n + j] = s;
+  const int64_t r = blockIdx.x;
+  const int32_t b = ip[r], e1 = ip[r + 1];
+  const bool vec = (n % 4) == 0 && (((uintptr_t)C) & 31) == 0;
+  for (int64_t j0 = 4 * (int64_t)threadIdx.x; j0 < n; j0 += 4 * (int64_t)blockDim.x) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (vec) {
+#pragma unroll 4
+      for (int32_t e = b; e < e1; ++e) {
+        const double v = val[e];
+        const double* row = C + (int64_t)ix[e] * n + j0;
+        const double2 a = __ldg(reinterpret_cast<const double2*>(row));
+        const double2 c = __ldg(reinterpret_cast<const double2*>(row + 2));
+        s0 += v * a.x;
+        s1 += v * a.y;
+        s2 += v * c.x;
+        s3 += v * c.y;
+      }
+    } else {
+      for (int32_t e = b; e < e1; ++e) {
+        const double v = val[e];
+        const double* row = C + (int64_t)ix[e] * n;
+        s0 += v * row[j0];
+        if (j0 + 1 < n) s1 += v * row[j0 + 1];
+        if (j0 + 2 < n) s2 += v * row[j0 + 2];
+        if (j0 + 3 < n) s3 += v * row[j0 + 3];
+      }
+    }
+    X[r * n + j0] = s0;
+    if (j0 + 1 < n) X[r * n + j0 + 1] = s1;
+    if (j0 + 2 < n) X[r * n + j0 + 2] = s2;
+    if (j0 + 3 < n) X[r * n + j0 + 3] = s3;
   }
 }
 
@@ -364,6 +392,11 @@ int hikf_init_state(int64_t m, int64_t n, const int32_t* ip, const int32_t* ix, 
   HIKF_CHECK_LAUNCH();
   if (n == 0) return HIKF_OK;
   // C = alpha H^T (dense), HC = alpha (H H^T)  (filters.py:118-126)
+  if (alpha == 0.0) {  // the BASELINE configs: 0 * H^T and 0 * H H^T are zeros (H >= 0)
+    HIKF_CHECK_CUDA(cudaMemsetAsync(C_out, 0, sizeof(double) * m * n, st));
+    HIKF_CHECK_CUDA(cudaMemsetAsync(HC_out, 0, sizeof(double) * n * n, st));
+    return HIKF_OK;
+  }
   double* Ht = nullptr;
   double* X = nullptr;
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Ht, sizeof(double) * m * n, st));

@@ -451,6 +451,27 @@ int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U,
   return HIKF_OK;
 }
 
+// Side streams for the concurrent parts of the sparse Q H^T: the near field
+// (compute-bound P2P) and the per-level M2L chains (latency-bound launches)
+// are independent of each other and of the other levels.
+namespace {
+struct QhtStreams {
+  cudaStream_t s[8] = {};
+  cudaEvent_t e[kMaxDepth + 4] = {};
+};
+int qht_streams(QhtStreams** out) {
+  static QhtStreams p;
+  static bool init = false;
+  if (!init) {
+    for (auto& x : p.s) HIKF_CHECK_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (auto& x : p.e) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    init = true;
+  }
+  *out = &p;
+  return HIKF_OK;
+}
+}  // namespace
+
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
                     cudaStream_t st) {
   if (n <= 0) return HIKF_OK;
@@ -460,95 +481,124 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     ProfScope ps(ST_DENSIFY, st);  // the regrouping of H^T replaces the densify step
     HIKF_TRY(sparse_build(t, n, ip, ix, val, &sp, st));
   }
-  int status = HIKF_OK;
-  if (D >= 2) {
-    // ---- upward pass on the active (box, ray) pairs only ----
-    PairLevel pl[kMaxDepth + 1];
-    {
-      ProfScope ps(ST_P2M, st);
-      status = pairs_leaf(t, sp, &pl[D], st);
-    }
-    for (int l = D - 1; l >= 2 && status == HIKF_OK; --l) {
-      ProfScope ps(ST_M2M, st);
-      status = pairs_parent(t, l, pl[l + 1], n, &pl[l], st);
-    }
-    // ---- downward pass: dense locals (every box gets a far field) ----
-    // M2L accumulates per offset into a pair-major scratch (q contiguous
-    // coefficients per (box, ray)); l2l_transpose then adds the parent shift
-    // and writes the box-major locals the L2L/L2P GEMMs consume.
-    double* Lbuf[2] = {nullptr, nullptr};
-    double* scratch = nullptr;
-    const int64_t szD = ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * n;
-    const int64_t szD1 = ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1] * n;
-    int64_t szS = 0;
-    for (int l = 2; l <= D; ++l) szS = std::max<int64_t>(szS, ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n);
-    if (status == HIKF_OK) {
-      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * szD, st));
-      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * std::max<int64_t>(szD1, 1), st));
-      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch, sizeof(double) * szS, st));
-    }
-    const bool vec = (n % 2) == 0;
-    const double* Lprev = nullptr;
-    double* Lcur = nullptr;
-    for (int l = 2; l <= D && status == HIKF_OK; ++l) {
-      Lcur = Lbuf[(D - l) & 1];
-      const int q = t->orders[l] * t->orders[l];
-      {
-        ProfScope ps(ST_M2L, st);
-        HIKF_CHECK_CUDA(cudaMemsetAsync(scratch, 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, st));
-        for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
-          status = m2l_pass(t, l, slot, pl[l], n, scratch, st);
-      }
-      if (status == HIKF_OK && l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
-        ProfScope ps(ST_L2L, st);
-        status = l2l_boxes(t, l, scratch, Lprev, n, Lcur, st);
-      } else if (status == HIKF_OK) {
-        ProfScope ps(ST_L2L, st);
-        status = pair_to_box(t, l, scratch, n, Lcur, st);
-        if (status == HIKF_OK && l > 2) {
-          L2LParentProv ll;
-          set_base(ll, t, n, 0, 0, vec);
-          ll.occp = t->occ[l - 1];
-          ll.q = q;
-          ll.qp = t->orders[l - 1] * t->orders[l - 1];
-          ll.Gp = (int64_t)1 << (l - 1);
-          ll.Lp = Lprev;
-          ll.shift = t->shift[l - 1];
-          ll.L = Lcur;
-          status = launch(ll, t->n_occ[l - 1], 4 * q, n, st);
-        }
-      }
-      Lprev = Lcur;
-    }
-    if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
-      ProfScope ps(ST_L2P, st);
-      status = l2p_boxes(t, Lcur, n, U, n, st);
-    } else if (status == HIKF_OK) {
-      L2PProv<false> lp;
-      set_base(lp, t, n, 0, 0, vec);
-      lp.leaf_box = t->leaf_box;
-      lp.leaf_start = t->leaf_start;
-      lp.leaf_count = t->leaf_count;
-      lp.W2s = t->W2s;
-      lp.q = t->orders[D] * t->orders[D];
-      lp.order = t->order;
-      lp.L = Lcur;
-      lp.U = U;
-      lp.ldu = n;
-      ProfScope ps(ST_L2P, st);
-      status = launch(lp, t->n_leaves, t->max_count, n, st);
-    }
-    for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
-    cudaFreeAsync(scratch, st);
-    cudaFreeAsync(Lbuf[0], st);
-    cudaFreeAsync(Lbuf[1], st);
-  } else {
+  if (D < 2) {
     HIKF_CHECK_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * t->m * n, st));
+    int status;
+    {
+      ProfScope ps(ST_P2P, st);
+      status = sparse_p2p(t, sp, U, n, st);
+    }
+    sparse_free(&sp, st);
+    return status;
   }
+  QhtStreams* qs = nullptr;
+  HIKF_TRY(qht_streams(&qs));
+  cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1], ev_up = qs->e[2];
+
+  // ---- near field, concurrently: sums parked in Pnear, added after L2P ----
+  double* Pnear = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Pnear, sizeof(double) * std::max<int64_t>(1, sp.nitems * t->max_count), st));
+  HIKF_CHECK_CUDA(cudaEventRecord(ev_base, st));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(qs->s[0], ev_base, 0));
+  int status = HIKF_OK;
+  {
+    ProfScope ps(ST_P2P, qs->s[0]);
+    status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear);
+  }
+  HIKF_CHECK_CUDA(cudaEventRecord(ev_p2p, qs->s[0]));
+
+  // ---- upward pass on the active (box, ray) pairs only ----
+  PairLevel pl[kMaxDepth + 1];
+  {
+    ProfScope ps(ST_P2M, st);
+    if (status == HIKF_OK) status = pairs_leaf(t, sp, &pl[D], st);
+  }
+  for (int l = D - 1; l >= 2 && status == HIKF_OK; --l) {
+    ProfScope ps(ST_M2M, st);
+    status = pairs_parent(t, l, pl[l + 1], n, &pl[l], st);
+  }
+  // ---- M2L, one stream per level: each level accumulates per offset into its
+  // own pair-major scratch (q contiguous coefficients per (box, ray)) ----
+  double* scratch[kMaxDepth + 1] = {};
+  double* Lbuf[2] = {nullptr, nullptr};
+  const int64_t szD = ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * n;
+  const int64_t szD1 = ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1] * n;
+  if (status == HIKF_OK) {
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * szD, st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * std::max<int64_t>(szD1, 1), st));
+    for (int l = 2; l <= D; ++l)
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch[l],
+                                      sizeof(double) * ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n, st));
+    HIKF_CHECK_CUDA(cudaEventRecord(ev_up, st));
+    for (int l = D; l >= 2 && status == HIKF_OK; --l) {  // biggest level first
+      cudaStream_t sl = qs->s[1 + (D - l) % 7];
+      HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, ev_up, 0));
+      const int q = t->orders[l] * t->orders[l];
+      ProfScope ps(ST_M2L, sl);
+      HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, sl));
+      for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot) status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl);
+      HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
+    }
+  }
+  // ---- downward pass (main stream): L = scratch^T + shift L_parent, then L2P ----
+  const bool vec = (n % 2) == 0;
+  const double* Lprev = nullptr;
+  double* Lcur = nullptr;
+  for (int l = 2; l <= D && status == HIKF_OK; ++l) {
+    Lcur = Lbuf[(D - l) & 1];
+    const int q = t->orders[l] * t->orders[l];
+    HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
+    if (l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
+      ProfScope ps(ST_L2L, st);
+      status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st);
+    } else {
+      ProfScope ps(ST_L2L, st);
+      status = pair_to_box(t, l, scratch[l], n, Lcur, st);
+      if (status == HIKF_OK && l > 2) {
+        L2LParentProv ll;
+        set_base(ll, t, n, 0, 0, vec);
+        ll.occp = t->occ[l - 1];
+        ll.q = q;
+        ll.qp = t->orders[l - 1] * t->orders[l - 1];
+        ll.Gp = (int64_t)1 << (l - 1);
+        ll.Lp = Lprev;
+        ll.shift = t->shift[l - 1];
+        ll.L = Lcur;
+        status = launch(ll, t->n_occ[l - 1], 4 * q, n, st);
+      }
+    }
+    Lprev = Lcur;
+  }
+  if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
+    ProfScope ps(ST_L2P, st);
+    status = l2p_boxes(t, Lcur, n, U, n, st);
+  } else if (status == HIKF_OK) {
+    L2PProv<false> lp;
+    set_base(lp, t, n, 0, 0, vec);
+    lp.leaf_box = t->leaf_box;
+    lp.leaf_start = t->leaf_start;
+    lp.leaf_count = t->leaf_count;
+    lp.W2s = t->W2s;
+    lp.q = t->orders[D] * t->orders[D];
+    lp.order = t->order;
+    lp.L = Lcur;
+    lp.U = U;
+    lp.ldu = n;
+    ProfScope ps(ST_L2P, st);
+    status = launch(lp, t->n_leaves, t->max_count, n, st);
+  }
+  // ---- join: every side stream's work is ordered before the frees below ----
+  for (int l = 2; l <= D; ++l) HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_p2p, 0));
   if (status == HIKF_OK) {
     ProfScope ps(ST_P2P, st);
-    status = sparse_p2p(t, sp, U, n, st);
+    status = sparse_p2p_scatter(t, sp, Pnear, U, n, st);
   }
+  for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
+  for (int l = 2; l <= D; ++l) cudaFreeAsync(scratch[l], st);
+  cudaFreeAsync(Lbuf[0], st);
+  cudaFreeAsync(Lbuf[1], st);
+  cudaFreeAsync(Pnear, st);
   sparse_free(&sp, st);
   return status;
 }

@@ -158,7 +158,7 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
                            const int32_t* __restrict__ g_start, const int32_t* __restrict__ e_sp,
                            const double* __restrict__ e_v, const double* __restrict__ xy_s,
                            const int64_t* __restrict__ order, double* __restrict__ U, int64_t ldu,
-                           unsigned long long* __restrict__ flops) {
+                           double* __restrict__ Pnear, int32_t maxc, unsigned long long* __restrict__ flops) {
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (item >= nitems) return;
@@ -207,8 +207,27 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
         const double v = e_v[k];
         acc += kernel_of_r(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
       }
-    if (ok) U[order[t0 + t] * ldu + j] += acc;
+    if (!ok) continue;
+    if (Pnear)
+      Pnear[item * maxc + t] = acc;  // added into U later (p2p_scatter): U = far + near either way
+    else
+      U[order[t0 + t] * ldu + j] += acc;
   }
+}
+
+// U[target, ray] += near sum, one warp per P2P item (the deferred add of p2p_sparse)
+__global__ void p2p_scatter(int64_t nitems, const int64_t* __restrict__ items, int64_t n,
+                            const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_count,
+                            const int64_t* __restrict__ order, const double* __restrict__ Pnear, int32_t maxc,
+                            double* __restrict__ U, int64_t ldu) {
+  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (item >= nitems) return;
+  const int64_t key = items[item];
+  const int32_t T = (int32_t)(key / n);
+  const int32_t j = (int32_t)(key % n);
+  const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
+  for (int t = lane; t < cnt; t += 32) U[order[t0 + t] * ldu + j] += Pnear[item * maxc + t];
 }
 
 }  // namespace
@@ -371,12 +390,23 @@ int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, 
   return HIKF_OK;
 }
 
-int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st) {
+int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st, double* Pnear) {
   if (s.nitems <= 0) return HIKF_OK;
   const int64_t threads = s.nitems * 32;
   p2p_sparse<<<(unsigned)((threads + kT - 1) / kT), kT, 0, st>>>(
       s.nitems, s.items, s.n, t->G, t->kp, t->leaf_box, t->leaf_start, t->leaf_count, t->box2leaf, s.leaf_g, s.g_j,
-      s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, prof_flops_ptr(ST_P2P));
+      s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, Pnear, (int32_t)t->max_count, prof_flops_ptr(ST_P2P));
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
+                       cudaStream_t st) {
+  if (s.nitems <= 0) return HIKF_OK;
+  const int64_t threads = s.nitems * 32;
+  p2p_scatter<<<(unsigned)((threads + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
+                                                                 t->leaf_count, t->order, Pnear,
+                                                                 (int32_t)t->max_count, U, ldu);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }

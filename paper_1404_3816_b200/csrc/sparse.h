@@ -33,7 +33,12 @@ int sparse_build(const hikf_tree* t, int64_t n, const int32_t* ip, const int32_t
                  cudaStream_t st);
 void sparse_free(SparseHt* s, cudaStream_t st);
 int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, int64_t c0, cudaStream_t st);
-int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st);
+// near field of the (target leaf, ray) items: U += near sum, or, with Pnear
+// (nitems x max_count), the sums are parked there and added by sparse_p2p_scatter
+int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st,
+               double* Pnear = nullptr);
+int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
+                       cudaStream_t st);
 
 // leaf multipoles of the active (leaf, ray) pairs (sparse P2M)
 int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st);

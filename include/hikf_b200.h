@@ -154,6 +154,23 @@ int hikf_update(int64_t m, int64_t n, const double* mean_dev, const double* C_de
                 const double* z_dev, double* mean_out, double* C_out, double* var_out, double* HC_out,
                 void* workspace, size_t workspace_bytes, double* min_var_out, void* stream);
 
+/* ---- hikf_update with a chained predict ----
+ * Same contract as hikf_update, plus two flags in chain:
+ *   bit 0 (produce): the GEMM epilogue also writes the next call's predicted
+ *          C' = C_out + C_Q (bit-identical to the predict add) into the
+ *          workspace;
+ *   bit 1 (consume): this call's C is the previous call's C_out, unmodified,
+ *          with the same C_Q and workspace -- use the C' that call produced and
+ *          skip the C + C_Q pass.  Pointers, sizes and success of the previous
+ *          call are checked; any mismatch falls back to the full predict.
+ * Setting bit 1 while C_out was modified in between gives wrong results. */
+int hikf_update_chained(int64_t m, int64_t n, const double* mean_dev, const double* C_dev, const double* var_dev,
+                        const double* HC_dev, const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev,
+                        const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev,
+                        double r_variance, const double* z_dev, double* mean_out, double* C_out, double* var_out,
+                        double* HC_out, void* workspace, size_t workspace_bytes, double* min_var_out, int32_t chain,
+                        void* stream);
+
 /* ---- row-sharded update: the same update on rows [r0, r1) of a
  * state sharded across ranks.  Hmean_dev = the all-reduced H mean (the
  * caller sums the per-rank hikf_csr_spmv partials); the n x n quantities are

@@ -87,6 +87,52 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
           const double v1 = Cin ? acc[i][j + 1][h] : g.alpha * acc[i][j + 1][h];
           *reinterpret_cast<double2*>(C + row * g.ldc + colh(j, h)) = make_double2(v0, v1);
         }
+    } else if (g.chain_out) {
+      // also emit chain_out = C + chain_add (the next step's predict, fused);
+      // columns 2 t4 and 2 t4 + 1 are adjacent: 16-byte accesses when aligned
+      const bool v16 = !SPLIT && row < g.M && cw + BN / WN <= g.N && (g.ldc | g.ldch) % 2 == 0 &&
+                       (((uintptr_t)C | (uintptr_t)g.chain_out | (uintptr_t)g.chain_add) & 15) == 0;
+      if (v16) {
+        double2 cv[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+          cv[j] = *reinterpret_cast<const double2*>(g.chain_add + row * g.ldch + colh(j, 0));
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const double v0 = Cin ? acc[i][j][0] : g.alpha * acc[i][j][0];
+          const double v1 = Cin ? acc[i][j][1] : g.alpha * acc[i][j][1];
+          *reinterpret_cast<double2*>(C + row * g.ldc + colh(j, 0)) = make_double2(v0, v1);
+          *reinterpret_cast<double2*>(g.chain_out + row * g.ldch + colh(j, 0)) =
+              make_double2(v0 + cv[j].x, v1 + cv[j].y);
+        }
+      } else {
+        double cv[TN][2];
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = colh(j, h);
+            cv[j][h] = (row < g.M && col < g.N) ? g.chain_add[row * g.ldch + col] : 0.0;
+          }
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t col = colh(j, h);
+            if (row < g.M && col < g.N) {
+              const double v = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
+              C[row * g.ldc + col] = v;
+              g.chain_out[row * g.ldch + col] = v + cv[j][h];
+            }
+          }
+      }
+    } else if (!SPLIT && row < g.M && cw + BN / WN <= g.N && g.ldc % 2 == 0 && ((uintptr_t)C & 15) == 0) {
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const double v0 = Cin ? acc[i][j][0] : g.alpha * acc[i][j][0];
+        const double v1 = Cin ? acc[i][j][1] : g.alpha * acc[i][j][1];
+        *reinterpret_cast<double2*>(C + row * g.ldc + colh(j, 0)) = make_double2(v0, v1);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < TN; ++j)

@@ -43,6 +43,10 @@ struct GemmArgs {
   int64_t ldp = 0;
   const double* px = nullptr;
   int64_t ldx = 0;
+  // optional second output: chain_out = C (as stored) + chain_add, same indexing with ldch
+  const double* chain_add = nullptr;
+  double* chain_out = nullptr;
+  int64_t ldch = 0;
   int variant = -1;  // tile-shape variant (-1: dgemm_variant())
 };
 

@@ -386,6 +386,24 @@ int lookahead_reserve(LookAhead& la, int64_t n) {
   return HIKF_OK;
 }
 
+// Chained predict (see UpdateArgs::chain): which workspace buffer holds the
+// C' that the previous call's GEMM epilogue wrote, and for which inputs.
+struct ChainState {
+  bool valid = false;
+  const double* C_out = nullptr;
+  const double* CQ = nullptr;
+  const void* ws = nullptr;
+  int64_t m = 0, n = 0;
+  int buf = 0;  // 0: Y, 1: Y2
+};
+
+ChainState& chain_state() {
+  static ChainState cs[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return cs[dev & 63];
+}
+
 bool lookahead_enabled() {
   static const bool on = [] {
     const char* e = getenv("HIKF_LOOKAHEAD");
@@ -400,7 +418,7 @@ bool lookahead_enabled() {
 // workspace layout of the update
 // ---------------------------------------------------------------------------
 struct UpdWs {
-  double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *w, *Y, *psq, *pdot, *bmin, *bmax, *minv;
+  double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *w, *Y, *Y2, *psq, *pdot, *bmin, *bmax, *minv;
   int* status;
 };
 
@@ -426,6 +444,7 @@ static size_t update_layout(int64_t m, int64_t n, char* base, UpdWs* ws) {
   w.innov = (double*)take(8 * n);
   w.w = (double*)take(8 * n);
   w.Y = (double*)take(8 * m * n);
+  w.Y2 = (double*)take(8 * m * n);
   w.psq = (double*)take(8 * m * nt);
   w.pdot = (double*)take(8 * m * nt);
   w.bmin = (double*)take(8 * (size_t)nb);
@@ -495,6 +514,15 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   update_layout(m, n, (char*)a.workspace, &w);
   HIKF_CHECK_CUDA(cudaMemsetAsync(w.status, 0, 16, st));
 
+  // chained predict: C' = C + C_Q of this call was already written by the previous
+  // call's GEMM epilogue when the caller passes that call's C_out and C_Q back
+  ChainState& ch = chain_state();
+  const bool chain_in = a.chain_in && a.CQ && ch.valid && ch.C_out == a.C && ch.CQ == a.CQ &&
+                        ch.ws == a.workspace && ch.m == m && ch.n == n;
+  double* Ycur = chain_in && ch.buf ? w.Y2 : w.Y;  // where this call's C' lives
+  double* Ynext = Ycur == w.Y ? w.Y2 : w.Y;
+  ch.valid = false;
+
   // K = C' S^-1 reads C' while writing C_new: C' must not live in C_out
   const double *Cp = a.C, *varp = a.var, *HCp = a.HC;
   if (!a.CQ && a.C == a.C_out && m * n > 0) {
@@ -532,10 +560,10 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
   if (a.CQ) {
     ProfScope ps(ST_PREDICT, st);
-    if (m * n > 0) HIKF_TRY(add_stream(a.C, a.CQ, w.Y, m * n, st));
+    if (m * n > 0 && !chain_in) HIKF_TRY(add_stream(a.C, a.CQ, Ycur, m * n, st));
     add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(a.var, a.dQ, a.var_out, m);
     HIKF_CHECK_LAUNCH();
-    Cp = w.Y;
+    Cp = Ycur;
     varp = a.var_out;  // var_out temporarily holds var'; finalize reads it before overwriting
   }
   if (a.CQ) {
@@ -573,6 +601,11 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
       g.alpha = a.r;
       g.psq = w.psq; g.pdot = w.pdot; g.w = w.innov; g.ldp = nt;
       g.px = Cp; g.ldx = n;
+      if (a.chain && a.CQ) {  // next call's C' = C_new + C_Q, written while C_new is in registers
+        g.chain_add = a.CQ;
+        g.chain_out = Ynext;
+        g.ldch = n;
+      }
       g.variant = vc;
       ProfScope ps(ST_GEMM_C, st);
       HIKF_TRY(dgemm(g, 1, st));
@@ -647,6 +680,15 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   if (hs[1] && !a.no_check) {
     set_error("posterior variance went negative beyond tolerance (min %.3e)", mv);
     return HIKF_NEGATIVE_VARIANCE;
+  }
+  if (a.chain && a.CQ) {
+    ch.valid = true;
+    ch.C_out = a.C_out;
+    ch.CQ = a.CQ;
+    ch.ws = a.workspace;
+    ch.m = m;
+    ch.n = n;
+    ch.buf = Ynext == w.Y2 ? 1 : 0;
   }
   return HIKF_OK;
 }

@@ -278,11 +278,25 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
     var = torch.empty((m,), dtype=torch.float64, device=dev)
     HC = torch.empty((n, n), dtype=torch.float64, device=dev)
     ws = _workspace(m, n)
-    _lib.check(_lib.load().hikf_update(
+    # chained predict (hikf_update_chained): every fused update also produces the
+    # next step's C' = C_new + C_Q; it is consumed only when this prior is exactly
+    # the state the previous update returned (states are immutable) with the same
+    # precompute, so a stale C' can never be used
+    chain = 1 if fused else 0
+    if fused and _CHAIN and _CHAIN["state"]() is src and _CHAIN["pre"]() is pre:
+        chain |= 2
+    _CHAIN.clear()
+    _lib.check(_lib.load().hikf_update_chained(
         m, n, state.mean_t.data_ptr(), src.cross_cov_t.data_ptr(), src.variance_t.data_ptr(), src.HC_t.data_ptr(),
         _lib.ptr(pre.C_Q_t) if fused else None, _lib.ptr(pre.diag_Q_t) if fused else None,
         _lib.ptr(pre.HC_Q_t) if fused else None,
         Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), float(r_variance), zt.data_ptr(),
-        mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None,
+        mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None, chain,
         _lib.stream_ptr()))
-    return HikfState(mean, C, var, HC)
+    out = HikfState(mean, C, var, HC)
+    if fused:
+        _CHAIN.update(state=weakref.ref(out), pre=weakref.ref(pre))
+    return out
+
+
+_CHAIN: dict = {}

@@ -356,3 +356,35 @@ def test_lookahead_factorisation_is_bit_identical(pkg):
     for k in poked_hits:
         assert torch.equal(poked_hits[k], poked_misses[k]), k
     assert not torch.equal(poked_hits["C"], hits["C"])
+
+
+def test_chained_predict_is_bit_identical(pkg):
+    """Fused updates through the Python API chain the predict (the GEMM epilogue
+    writes the next step's C' = C_new + C_Q; hikf_update_chained).  The chained
+    run must equal, bit for bit, the same steps through the unchained C-ABI
+    (hikf_update_rows over all rows), and a branch from an older state must not
+    consume the chained buffer."""
+    import torch
+    from paper_1404_3816_b200.sharded import CudaRowStep
+    flt = pkg.filters
+    g = _load("cfg1.npz")
+    cfg = cases.CFG1
+    tree, H, pre, st_api = _run_filter(pkg, dict(cfg, T=6), g["obs"])
+    m, n = H.shape[1], H.shape[0]
+    step = CudaRowStep((pre.C_Q_t, pre.HC_Q_t, pre.diag_Q_t), n)
+    Hd = flt.DeviceCSR(H)
+    st = {"mean": torch.zeros(m, dtype=torch.float64, device="cuda"),
+          "C": torch.zeros(m, n, dtype=torch.float64, device="cuda"),
+          "var": torch.zeros(m, dtype=torch.float64, device="cuda"),
+          "HC": torch.zeros(n, n, dtype=torch.float64, device="cuda")}
+    for t in range(6):
+        st = step.update_rows(st, step.spmv(Hd, st), cfg["R"], torch.as_tensor(g["obs"][t]).cuda())[0]
+    assert torch.equal(st["C"], st_api.cross_cov_t)
+    assert torch.equal(st["mean"], st_api.mean_t)
+    assert torch.equal(st["var"], st_api.variance_t)
+    # branching: two updates from the same prior give the same result
+    s0 = flt.hikf_init(type("Mdl", (), dict(H=H, m=m, n=n, alpha=0.0, initial_mean=np.zeros(m)))())
+    s1 = flt.hikf_update(flt.hikf_predict(s0, pre), H, cfg["R"], g["obs"][0])
+    a = flt.hikf_update(flt.hikf_predict(s1, pre), H, cfg["R"], g["obs"][1])
+    b = flt.hikf_update(flt.hikf_predict(s1, pre), H, cfg["R"], g["obs"][1])
+    assert torch.equal(a.cross_cov_t, b.cross_cov_t) and torch.equal(a.mean_t, b.mean_t)

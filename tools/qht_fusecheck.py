@@ -1,0 +1,28 @@
+"""Q H^T precompute timing (best of 4) and C_Q digest; run with and without
+HIKF_NO_LEAF_FUSION=1 to check that the fused leaf kernel is bit-identical."""
+import hashlib
+import sys
+
+import torch
+
+sys.path.insert(0, "/root/repo")
+import bench  # noqa: E402
+import paper_1404_3816_b200 as P  # noqa: E402
+cfg = bench.CONFIGS[sys.argv[1]]
+N = cfg["N"]
+grid = P.Grid2D(N, N, 1.0 / N, 1.0 / N)
+H = P.tomography.build_ray_operator(grid, P.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], 0.0, 1.0))
+class M: pass
+model = M(); model.H, model.m = H, grid.m
+kern = P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+pre = P.filters.hikf_precompute_fmm(model, tree)
+torch.cuda.synchronize()
+best = 1e30
+for _ in range(4):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    del pre
+    e0.record(); pre = P.filters.hikf_precompute_fmm(model, tree); e1.record(); torch.cuda.synchronize()
+    best = min(best, e0.elapsed_time(e1))
+h = hashlib.sha256(pre.C_Q_t.cpu().numpy().tobytes()).hexdigest()[:16]
+print(sys.argv[1], "ms", round(best, 2), "sha", h)

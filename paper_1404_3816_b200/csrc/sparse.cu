@@ -209,27 +209,28 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
       }
     if (!ok) continue;
     if (Pnear)
-      Pnear[item * maxc + t] = acc;  // added into U later (p2p_scatter): U = far + near either way
+      Pnear[(int64_t)t * nitems + item] = acc;  // added into U later (p2p_scatter): U = far + near either way
     else
       U[order[t0 + t] * ldu + j] += acc;
   }
 }
 
-// U[target, ray] += near sum, one warp per P2P item (the deferred add of p2p_sparse)
+// U[target, ray] += near sum (the deferred add of p2p_sparse).  Items are
+// sorted by (leaf, ray): a warp takes 32 consecutive items and walks the leaf
+// rows, so lanes of the same leaf update one row of U at their rays' columns;
+// Pnear is target-major (t * nitems + item), read coalesced.
 __global__ void p2p_scatter(int64_t nitems, const int64_t* __restrict__ items, int64_t n,
                             const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_count,
                             const int64_t* __restrict__ order, const double* __restrict__ Pnear, int32_t maxc,
                             double* __restrict__ U, int64_t ldu) {
-  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (item >= nitems) return;
   const int64_t key = items[item];
   const int32_t T = (int32_t)(key / n);
   const int32_t j = (int32_t)(key % n);
   const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
-  for (int t = lane; t < cnt; t += 32) U[order[t0 + t] * ldu + j] += Pnear[item * maxc + t];
+  for (int t = 0; t < cnt; ++t) U[order[t0 + t] * ldu + j] += Pnear[(int64_t)t * nitems + item];
 }
-
 }  // namespace
 
 void sparse_free(SparseHt* s, cudaStream_t st) {
@@ -403,8 +404,7 @@ int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cu
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
                        cudaStream_t st) {
   if (s.nitems <= 0) return HIKF_OK;
-  const int64_t threads = s.nitems * 32;
-  p2p_scatter<<<(unsigned)((threads + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
+  p2p_scatter<<<(unsigned)((s.nitems + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
                                                                  t->leaf_count, t->order, Pnear,
                                                                  (int32_t)t->max_count, U, ldu);
   HIKF_CHECK_LAUNCH();

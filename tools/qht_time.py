@@ -1,5 +1,5 @@
-"""Q H^T precompute timing (best of 4) and C_Q digest; run with and without
-HIKF_NO_LEAF_FUSION=1 to check that the fused leaf kernel is bit-identical."""
+"""Q H^T precompute timing (best of 4) and a C_Q digest, to check that a
+kernel change is bit-identical:  python tools/qht_time.py cfg4"""
 import hashlib
 import sys
 

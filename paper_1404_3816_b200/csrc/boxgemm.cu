@@ -164,10 +164,9 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
   if (g.flops && lane == 0 && useful) atomicAdd(g.flops, useful);
 }
 
-int k4_bucket(int K) {
-  const int nk4 = (K + 3) / 4;
-  return nk4 <= 4 ? 4 : nk4 <= 8 ? 8 : nk4 <= 12 ? 12 : 16;
-}
+// exact k-steps per operator size (one instantiation per ceil(K/4)): a padded
+// bucket would spend DMMAs on all-zero k-steps (49 -> 64 is 30 % at order 7)
+int k4_bucket(int K) { return (K + 3) / 4; }
 
 // shared memory of the A block: rows padded to 8, leading dimension pad4(4 * NK4)
 size_t box_smem(int R, int K) {
@@ -187,7 +186,7 @@ int launch_box_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   return HIKF_OK;
 }
 
-// compile-time k-steps: ceil(K/4) rounded up into {4, 8, 12, 16}; 8 row tiles per register pass
+// compile-time k-steps: exactly ceil(K/4); 8 row tiles per register pass
 int launch_box(const BoxArgs& a, int R, dim3 grid, cudaStream_t st) {
   const size_t smem = box_smem(R, a.K);
   const int nk4 = (a.K + 3) / 4;
@@ -195,10 +194,8 @@ int launch_box(const BoxArgs& a, int R, dim3 grid, cudaStream_t st) {
 #define HIKF_BOX(K4)                                                                          \
   if (nk4 <= K4)                                                                              \
     return launch_box_t<K4, BW_RT>(a, grid, smem, st);
-  HIKF_BOX(4)
-  HIKF_BOX(8)
-  HIKF_BOX(12)
-  HIKF_BOX(16)
+  HIKF_BOX(1) HIKF_BOX(2) HIKF_BOX(3) HIKF_BOX(4) HIKF_BOX(5) HIKF_BOX(6) HIKF_BOX(7) HIKF_BOX(8)
+  HIKF_BOX(9) HIKF_BOX(10) HIKF_BOX(11) HIKF_BOX(12) HIKF_BOX(13) HIKF_BOX(14) HIKF_BOX(15) HIKF_BOX(16)
 #undef HIKF_BOX
   set_error("box-streaming kernel supports K <= %d (got %d)", 4 * BW_MAXK4, a.K);
   return HIKF_BAD_ARGUMENT;

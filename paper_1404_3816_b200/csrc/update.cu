@@ -467,10 +467,7 @@ int spmv(int64_t n, const int32_t* ip, const int32_t* ix, const double* val, con
 
 int predict(int64_t m, int64_t n, const double* C, const double* var, const double* HC, const double* CQ,
             const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, cudaStream_t st) {
-  if (m * n > 0) {
-    add_kernel<<<grid_for(m * n / 2 + 1), kT, 0, st>>>(C, CQ, Co, m * n);
-    HIKF_CHECK_LAUNCH();
-  }
+  if (m * n > 0) HIKF_TRY(add_stream(C, CQ, Co, m * n, st));
   add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(var, dQ, varo, m);
   HIKF_CHECK_LAUNCH();
   if (n > 0) {

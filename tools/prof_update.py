@@ -45,11 +45,13 @@ mode = sys.argv[3] if len(sys.argv) > 3 else "update"
 
 def step():
     fused = mode != "nopredict"  # nopredict: update only (no fused predict), factor timed alone
-    _lib.check(lib.hikf_update(m, n, mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(),
-                               CQ.data_ptr() if fused else None, dQ.data_ptr() if fused else None,
-                               HCQ.data_ptr() if fused else None, ip.data_ptr(), ix.data_ptr(), val.data_ptr(), 1e-3,
-                               z.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(), outs[2].data_ptr(),
-                               outs[3].data_ptr(), ws.data_ptr(), ws.numel(), ctypes.byref(mv), _lib.stream_ptr()))
+    # produce the next step's C' in the GEMM epilogue, as the filter loop does (hikf_update_chained bit 0)
+    _lib.check(lib.hikf_update_chained(m, n, mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(),
+                                       CQ.data_ptr() if fused else None, dQ.data_ptr() if fused else None,
+                                       HCQ.data_ptr() if fused else None, ip.data_ptr(), ix.data_ptr(),
+                                       val.data_ptr(), 1e-3, z.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
+                                       outs[2].data_ptr(), outs[3].data_ptr(), ws.data_ptr(), ws.numel(),
+                                       ctypes.byref(mv), 1 if fused else 0, _lib.stream_ptr()))
 
 
 if mode == "gemm":

@@ -59,6 +59,17 @@ typedef struct {
 
 typedef struct hikf_tree hikf_tree; /* opaque, immutable after create */
 
+/* 3D kernel (no reference counterpart; oracle/hikf_oracle3d.py Kern3):
+ * variance exp(-r'^p), r' = |(dx/lx, dy/ly, dz/lz)|, family gaussian (p = 2)
+ * or exponential (p = 1).  Anisotropic when lx, ly, lz differ. */
+typedef struct {
+  int32_t family;
+  double variance;
+  double lx, ly, lz;
+} hikf_kernel3;
+
+typedef struct hikf_tree3 hikf_tree3; /* 3D octree bbFMM, opaque */
+
 int hikf_abi_version(void);
 /* Copy the last error message of this thread into buf (NUL-terminated). */
 int hikf_last_error(char* buf, size_t len);
@@ -213,6 +224,32 @@ int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, d
 int hikf_ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n,
                              const double* src, const double* rcv, int32_t* indptr_dev, int32_t* indices_dev,
                              double* data_dev, int64_t capacity, int64_t* nnz_out, void* stream);
+
+/* ---- 3D path (BASELINE cfg3 / cfg5) -- PARITY UNPINNED:
+ * the reference is 2D only; these follow oracle/hikf_oracle3d.py. ----
+ * 3D ray operator: cells x fastest (then y, z); n3/d3/o3 = cells/spacing/origin
+ * per axis; src/rcv (n, 3) row-major.  Host two-call protocol as
+ * hikf_ray_operator; the _device variant as hikf_ray_operator_device. */
+int hikf_ray_operator_3d(const int64_t* n3, const double* d3, const double* o3, int64_t n, const double* src,
+                         const double* rcv, int32_t* indptr, int32_t* indices, double* data, int64_t* nnz_out);
+int hikf_ray_operator_3d_device(const int64_t* n3, const double* d3, const double* o3, int64_t n,
+                                const double* src, const double* rcv, int32_t* indptr_dev, int32_t* indices_dev,
+                                double* data_dev, int64_t capacity, int64_t* nnz_out, void* stream);
+/* octree: xyz_host (m, 3); 2 <= n_cheb <= 5 (one order at every level);
+ * 1 <= max_leaf <= 128. */
+int hikf_tree3_create(const double* xyz_host, int64_t m, const hikf_kernel3* kernel, int32_t n_cheb,
+                      int64_t max_leaf, void* stream, hikf_tree3** out);
+int hikf_tree3_destroy(hikf_tree3* tree);
+int hikf_tree3_info(const hikf_tree3* tree, int64_t* m, int32_t* depth, int32_t* n_cheb, int64_t* n_leaves,
+                    double* lo3, double* size);
+/* order[m] (sorted position -> point), leaf keys ((bx G + by) G + bz), starts, counts */
+int hikf_tree3_export(const hikf_tree3* tree, int64_t* order, int64_t* leaf_keys, int64_t* leaf_starts,
+                      int64_t* leaf_counts);
+/* U (m x k) = Q V, device, row-major, original point order */
+int hikf_tree3_matmat(const hikf_tree3* tree, const double* V_dev, int64_t k, double* U_dev, void* stream);
+/* C_Q = Q H^T (m x n) from CSR H; HC_Q = sym(H C_Q); diag_Q = K(0) */
+int hikf_precompute3(hikf_tree3* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
+                     const double* data_dev, double* C_Q_dev, double* HC_Q_dev, double* diag_Q_dev, void* stream);
 
 /* ---- FP64 DMMA GEMM building block (the update's workhorse) ----
  * C (M x N, ldc) = alpha A (M x K, lda) B (K x N, ldb) + beta C, row-major,

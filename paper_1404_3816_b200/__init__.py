@@ -14,11 +14,11 @@ from .fmm import FmmConfig, FmmTree, build_tree
 from .grids import Grid2D, PointSet
 from .kernels import KernelSpec, value_at_zero
 from .linalg import spd_solve
-from . import experiment, filters, tomography
+from . import experiment, filters, space3d, tomography
 
 __all__ = [
     "KernelSpec", "value_at_zero", "Grid2D", "PointSet", "FmmConfig", "FmmTree", "build_tree",
-    "DecompositionError", "NumericalConsistencyError", "spd_solve", "filters", "tomography", "experiment",
+    "DecompositionError", "NumericalConsistencyError", "spd_solve", "filters", "tomography", "experiment", "space3d",
 ]
 
 __version__ = "0.1.0"

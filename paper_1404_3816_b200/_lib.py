@@ -44,6 +44,16 @@ class HikfKernel(ctypes.Structure):
     ]
 
 
+class HikfKernel3(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int32),
+        ("variance", ctypes.c_double),
+        ("lx", ctypes.c_double),
+        ("ly", ctypes.c_double),
+        ("lz", ctypes.c_double),
+    ]
+
+
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
@@ -78,6 +88,14 @@ SIGNATURES = {
     "hikf_spd_solve": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _SZ, _P, _P]),
     "hikf_ray_operator": (ctypes.c_int, [_I64, _I64, _D, _D, _D, _D, _I64, _P, _P, _P, _P, _P, _P]),
     "hikf_precompute_dense": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "hikf_ray_operator_3d": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P]),
+    "hikf_ray_operator_3d_device": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _P, _P]),
+    "hikf_tree3_create": (ctypes.c_int, [_P, _I64, _P, ctypes.c_int32, _I64, _P, _P]),
+    "hikf_tree3_destroy": (ctypes.c_int, [_P]),
+    "hikf_tree3_info": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "hikf_tree3_export": (ctypes.c_int, [_P, _P, _P, _P, _P]),
+    "hikf_tree3_matmat": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    "hikf_precompute3": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "hikf_ray_operator_device": (ctypes.c_int, [_I64, _I64, _D, _D, _D, _D, _I64, _P, _P, _P, _P, _P, _I64, _P, _P]),
     "hikf_dgemm": (ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I32, _I32, _P]),
     "hikf_prof_enable": (ctypes.c_int, [ctypes.c_int]),

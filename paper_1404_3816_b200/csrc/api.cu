@@ -7,6 +7,8 @@
 #include <vector>
 
 #include "dense.h"
+#include "fmm3d.h"
+#include "host_ops.h"
 #include "dgemm.cuh"
 #include "prof.h"
 #include "rays.h"
@@ -573,6 +575,102 @@ int hikf_ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, d
     std::memcpy(indices, ix.data(), sizeof(int32_t) * ix.size());
     std::memcpy(data, v.data(), sizeof(double) * v.size());
   }
+  return HIKF_OK;
+}
+
+// ---- 3D path (parity unpinned; oracle/hikf_oracle3d.py) ----
+int hikf_ray_operator_3d(const int64_t* n3, const double* d3, const double* o3, int64_t n, const double* src,
+                         const double* rcv, int32_t* indptr, int32_t* indices, double* data, int64_t* nnz_out) {
+  if (!n3 || !d3 || !o3 || (n > 0 && (!src || !rcv))) {
+    set_error("hikf_ray_operator_3d: null argument");
+    return HIKF_BAD_ARGUMENT;
+  }
+  std::vector<int32_t> ip, ix;
+  std::vector<double> v;
+  HIKF_TRY(ray_operator_3d(n3, d3, o3, n, src, rcv, ip, ix, v));
+  if (nnz_out) *nnz_out = (int64_t)ix.size();
+  if (indices) {
+    std::memcpy(indptr, ip.data(), sizeof(int32_t) * ip.size());
+    std::memcpy(indices, ix.data(), sizeof(int32_t) * ix.size());
+    std::memcpy(data, v.data(), sizeof(double) * v.size());
+  }
+  return HIKF_OK;
+}
+
+int hikf_ray_operator_3d_device(const int64_t* n3, const double* d3, const double* o3, int64_t n,
+                                const double* src, const double* rcv, int32_t* indptr_dev, int32_t* indices_dev,
+                                double* data_dev, int64_t capacity, int64_t* nnz_out, void* stream) {
+  if (!n3 || !d3 || !o3 || !indptr_dev || !nnz_out || (n > 0 && (!src || !rcv))) {
+    set_error("hikf_ray_operator_3d_device: null argument");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return ray_operator_3d_device(n3, d3, o3, n, src, rcv, indptr_dev, indices_dev, data_dev, capacity, nnz_out,
+                                as_stream(stream));
+}
+
+int hikf_tree3_create(const double* xyz_host, int64_t m, const hikf_kernel3* kernel, int32_t n_cheb,
+                      int64_t max_leaf, void* stream, hikf_tree3** out) {
+  if (!kernel || !out) {
+    set_error("null argument");
+    return HIKF_BAD_ARGUMENT;
+  }
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0) {
+    set_error("no CUDA device: the HiKF B200 path has no CPU fallback");
+    return HIKF_NO_DEVICE;
+  }
+  keep_pool();
+  return tree3_build(xyz_host, m, *kernel, n_cheb, max_leaf, as_stream(stream), out);
+}
+
+int hikf_tree3_destroy(hikf_tree3* tree) {
+  tree3_free(tree);
+  return HIKF_OK;
+}
+
+int hikf_tree3_info(const hikf_tree3* tree, int64_t* m, int32_t* depth, int32_t* n_cheb, int64_t* n_leaves,
+                    double* lo3, double* size) {
+  return tree3_info(tree, m, depth, n_cheb, n_leaves, lo3, size);
+}
+
+int hikf_tree3_export(const hikf_tree3* tree, int64_t* order, int64_t* leaf_keys, int64_t* leaf_starts,
+                      int64_t* leaf_counts) {
+  return tree3_export(tree, order, leaf_keys, leaf_starts, leaf_counts);
+}
+
+int hikf_tree3_matmat(const hikf_tree3* tree, const double* V, int64_t k, double* U, void* stream) {
+  if (!tree || k < 0 || (k > 0 && (!V || !U))) {
+    set_error("bad tree3 matmat arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  int64_t m = 0;
+  tree3_info(tree, &m, nullptr, nullptr, nullptr, nullptr, nullptr);
+  return tree3_matmat(tree, V, k, k, U, k, as_stream(stream));
+}
+
+int hikf_precompute3(hikf_tree3* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* CQ,
+                     double* HCQ, double* dQ, void* stream) {
+  if (!t || n < 0) {
+    set_error("bad precompute3 arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  cudaStream_t st = as_stream(stream);
+  int64_t m = 0;
+  tree3_info(t, &m, nullptr, nullptr, nullptr, nullptr, nullptr);
+  HIKF_TRY(tree3_matmat_csrT(t, n, ip, ix, val, CQ, st));
+  if (n > 0) {
+    double* X = nullptr;
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&X, sizeof(double) * n * n, st));
+    spmm_rows<<<(unsigned)n, kT, 0, st>>>(n, ip, ix, val, CQ, X);
+    HIKF_CHECK_LAUNCH();
+    symmetrize<<<grid_for(n * n), kT, 0, st>>>(X, n, HCQ);
+    HIKF_CHECK_LAUNCH();
+    cudaFreeAsync(X, st);
+  }
+  hikf_kernel3 k{};
+  tree3_kernel(t, &k);
+  fill<<<grid_for(m), kT, 0, st>>>(dQ, m, k.variance);  // K(0) = variance
+  HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
 

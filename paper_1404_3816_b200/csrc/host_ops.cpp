@@ -202,4 +202,81 @@ int ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, double
   return HIKF_OK;
 }
 
+double ray_length_3d(const double* p0, const double* p1) {
+  const double d0 = p1[0] - p0[0], d1 = p1[1] - p0[1], d2 = p1[2] - p0[2];
+  return sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+}
+
+int ray_operator_3d(const int64_t n3[3], const double d3[3], const double o3[3], int64_t n, const double* src,
+                    const double* rcv, std::vector<int32_t>& indptr, std::vector<int32_t>& indices,
+                    std::vector<double>& data) {
+  for (int a = 0; a < 3; ++a)
+    if (n3[a] < 1 || !(d3[a] > 0)) {
+      set_error("ray_operator_3d: bad grid");
+      return HIKF_BAD_ARGUMENT;
+    }
+  if (n < 0 || (n3[0] * n3[1] * n3[2]) > INT32_MAX) {
+    set_error("ray_operator_3d: bad sizes");
+    return HIKF_BAD_ARGUMENT;
+  }
+  for (int64_t r = 0; r < n; ++r)
+    for (const double* p : {src + 3 * r, rcv + 3 * r})
+      for (int a = 0; a < 3; ++a)
+        if (!(p[a] >= o3[a] && p[a] <= o3[a] + n3[a] * d3[a])) {
+          set_error("sources/receivers must lie within the grid bounding box");
+          return HIKF_BAD_ARGUMENT;
+        }
+  indptr.assign(n + 1, 0);
+  indices.clear();
+  data.clear();
+  std::vector<double> t;
+  std::vector<std::pair<int32_t, double>> row;
+  for (int64_t r = 0; r < n; ++r) {
+    const double *p0 = src + 3 * r, *p1 = rcv + 3 * r;
+    const double d[3] = {p1[0] - p0[0], p1[1] - p0[1], p1[2] - p0[2]};
+    const double length = ray_length_3d(p0, p1);
+    if (length == 0.0) {
+      set_error("source coincides with receiver (zero-length ray)");
+      return HIKF_BAD_ARGUMENT;
+    }
+    t.assign({0.0, 1.0});
+    for (int a = 0; a < 3; ++a)
+      if (d[a] != 0.0)
+        for (int64_t i = 1; i < n3[a]; ++i) {
+          const double tt = ((o3[a] + (double)i * d3[a]) - p0[a]) / d[a];
+          if (tt > 0.0 && tt < 1.0) t.push_back(tt);
+        }
+    std::sort(t.begin(), t.end());
+    t.erase(std::unique(t.begin(), t.end()), t.end());
+    row.clear();
+    for (size_t s = 0; s + 1 < t.size(); ++s) {
+      const double seg = (t[s + 1] - t[s]) * length;
+      if (!(seg > 0.0)) continue;
+      const double tm = 0.5 * (t[s] + t[s + 1]);
+      int64_t c[3];
+      for (int a = 0; a < 3; ++a) {
+        const double u = ((p0[a] + tm * d[a]) - o3[a]) / d3[a];
+        int64_t i = (int64_t)floor(u);
+        if ((double)i == u && i > 0) --i;  // on a plane: lower cell
+        c[a] = std::min<int64_t>(std::max<int64_t>(i, 0), n3[a] - 1);
+      }
+      row.push_back({(int32_t)((c[2] * n3[1] + c[1]) * n3[0] + c[0]), seg});
+    }
+    std::stable_sort(row.begin(), row.end(),
+                     [](const std::pair<int32_t, double>& a, const std::pair<int32_t, double>& b) {
+                       return a.first < b.first;
+                     });
+    for (size_t s = 0; s < row.size(); ++s) {
+      if (s > 0 && row[s].first == row[s - 1].first) {
+        data.back() += row[s].second;
+      } else {
+        indices.push_back(row[s].first);
+        data.push_back(row[s].second);
+      }
+    }
+    indptr[r + 1] = (int32_t)indices.size();
+  }
+  return HIKF_OK;
+}
+
 }  // namespace hikf

@@ -33,4 +33,12 @@ int ray_operator(int64_t nx, int64_t ny, double dx, double dy, double x0, double
                  const double* rcv, std::vector<int32_t>& indptr, std::vector<int32_t>& indices,
                  std::vector<double>& data);
 
+// 3D extension (no reference; oracle/hikf_oracle3d.py trace_3d): cells x-fastest,
+// breakpoints at x / y / z planes, midpoint rule with planes going low,
+// length = sqrt((dx dx + dy dy) + dz dz).  n3 / d3 / o3 = cells / spacing / origin.
+int ray_operator_3d(const int64_t n3[3], const double d3[3], const double o3[3], int64_t n, const double* src,
+                    const double* rcv, std::vector<int32_t>& indptr, std::vector<int32_t>& indices,
+                    std::vector<double>& data);
+double ray_length_3d(const double* p0, const double* p1);
+
 }  // namespace hikf

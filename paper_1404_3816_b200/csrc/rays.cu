@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "host_ops.h"
 #include "rays.h"
 
 namespace hikf {
@@ -23,8 +24,14 @@ namespace {
 constexpr int RT = 512;  // threads per ray CTA
 constexpr int RIPT = 8;  // items per thread: nx + ny <= 4096 breakpoint candidates per ray
 
-__global__ void __launch_bounds__(RT) ray_cells_kernel(int64_t nx, int64_t ny, double dx, double dy, double x0,
-                                                       double y0, const double* __restrict__ src,
+struct RayGrid {
+  int64_t n[3];
+  double d[3], o[3];
+};
+
+// DIM = 2: tomography.py:76-108; DIM = 3: its extension (oracle/hikf_oracle3d.py trace_3d)
+template <int DIM>
+__global__ void __launch_bounds__(RT) ray_cells_kernel(RayGrid gr, const double* __restrict__ src,
                                                        const double* __restrict__ rcv, const double* __restrict__ len,
                                                        int64_t cap, int32_t* __restrict__ cells,
                                                        double* __restrict__ segs, int32_t* __restrict__ counts) {
@@ -44,14 +51,20 @@ __global__ void __launch_bounds__(RT) ray_cells_kernel(int64_t nx, int64_t ny, d
   double* tsh = u.t;
 
   const int64_t r = blockIdx.x;
-  const double p0x = src[2 * r], p0y = src[2 * r + 1];
-  const double d0 = __dsub_rn(rcv[2 * r], p0x), d1 = __dsub_rn(rcv[2 * r + 1], p0y);
+  double p0[DIM], dv[DIM];
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    p0[a] = src[DIM * r + a];
+    dv[a] = __dsub_rn(rcv[DIM * r + a], p0[a]);
+  }
   const double length = len[r];
   const int tid = threadIdx.x;
 
-  // ---- candidate breakpoints: 0, 1 and the gridline crossings inside (0, 1) ----
+  // ---- candidate breakpoints: 0, 1 and the plane crossings inside (0, 1) ----
   unsigned long long key[RIPT];
-  const int64_t ncand = 2 + (d0 != 0.0 ? nx - 1 : 0) + (d1 != 0.0 ? ny - 1 : 0);
+  int64_t ncand = 2;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) ncand += dv[a] != 0.0 ? gr.n[a] - 1 : 0;
 #pragma unroll
   for (int q = 0; q < RIPT; ++q) {
     const int64_t c = (int64_t)tid * RIPT + q;
@@ -62,11 +75,14 @@ __global__ void __launch_bounds__(RT) ray_cells_kernel(int64_t nx, int64_t ny, d
       t = 1.0;
     } else if (c < ncand) {
       int64_t k = c - 2;
-      if (d0 != 0.0 && k < nx - 1) {
-        t = __ddiv_rn(__dsub_rn(__dadd_rn(x0, __dmul_rn((double)(k + 1), dx)), p0x), d0);
-      } else {
-        if (d0 != 0.0) k -= nx - 1;
-        t = __ddiv_rn(__dsub_rn(__dadd_rn(y0, __dmul_rn((double)(k + 1), dy)), p0y), d1);
+#pragma unroll
+      for (int a = 0; a < DIM; ++a) {
+        if (dv[a] == 0.0) continue;
+        if (k < gr.n[a] - 1) {
+          t = __ddiv_rn(__dsub_rn(__dadd_rn(gr.o[a], __dmul_rn((double)(k + 1), gr.d[a])), p0[a]), dv[a]);
+          break;
+        }
+        k -= gr.n[a] - 1;
       }
       if (!(t > 0.0 && t < 1.0)) t = 2.0;
     }
@@ -114,14 +130,16 @@ __global__ void __launch_bounds__(RT) ray_cells_kernel(int64_t nx, int64_t ny, d
       const double seg = __dmul_rn(__dsub_rn(tb, ta), length);
       if (seg > 0.0) {
         const double tm = __dmul_rn(0.5, __dadd_rn(ta, tb));
-        const double u = __ddiv_rn(__dsub_rn(__dadd_rn(p0x, __dmul_rn(tm, d0)), x0), dx);
-        const double w = __ddiv_rn(__dsub_rn(__dadd_rn(p0y, __dmul_rn(tm, d1)), y0), dy);
-        int64_t i = (int64_t)floor(u), j = (int64_t)floor(w);
-        if ((double)i == u && i > 0) --i;  // grazing: lower/left cell
-        if ((double)j == w && j > 0) --j;
-        i = i < 0 ? 0 : (i > nx - 1 ? nx - 1 : i);
-        j = j < 0 ? 0 : (j > ny - 1 ? ny - 1 : j);
-        ck[q] = (int32_t)(j * nx + i);
+        int64_t cell = 0;
+#pragma unroll
+        for (int a = DIM - 1; a >= 0; --a) {
+          const double u = __ddiv_rn(__dsub_rn(__dadd_rn(p0[a], __dmul_rn(tm, dv[a])), gr.o[a]), gr.d[a]);
+          int64_t i = (int64_t)floor(u);
+          if ((double)i == u && i > 0) --i;  // grazing: lower cell
+          i = i < 0 ? 0 : (i > gr.n[a] - 1 ? gr.n[a] - 1 : i);
+          cell = cell * gr.n[a] + i;  // x fastest
+        }
+        ck[q] = (int32_t)cell;
         sv[q] = seg;
       }
     }
@@ -188,31 +206,11 @@ __global__ void compact_kernel(int64_t n, int64_t cap, const int32_t* __restrict
 
 }  // namespace
 
-int ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n,
-                        const double* src_host, const double* rcv_host, int32_t* indptr_dev, int32_t* indices_dev,
-                        double* data_dev, int64_t capacity, int64_t* nnz_out, cudaStream_t st) {
-  if (nx < 1 || ny < 1 || !(dx > 0) || !(dy > 0) || n < 0) {
-    set_error("ray_operator: bad grid");
-    return HIKF_BAD_ARGUMENT;
-  }
-  if (nx + ny > (int64_t)RT * RIPT) {
-    set_error("device ray operator supports nx + ny <= %d", RT * RIPT);
-    return HIKF_BAD_ARGUMENT;
-  }
-  const double xmax = x0 + nx * dx, ymax = y0 + ny * dy;
-  std::vector<double> len(std::max<int64_t>(n, 1));
-  for (int64_t r = 0; r < n; ++r) {
-    for (const double* p : {src_host + 2 * r, rcv_host + 2 * r})
-      if (!(p[0] >= x0 && p[0] <= xmax && p[1] >= y0 && p[1] <= ymax)) {
-        set_error("sources/receivers must lie within the grid bounding box");
-        return HIKF_BAD_ARGUMENT;
-      }
-    len[r] = hypot(rcv_host[2 * r] - src_host[2 * r], rcv_host[2 * r + 1] - src_host[2 * r + 1]);
-    if (len[r] == 0.0) {
-      set_error("source coincides with receiver (zero-length ray)");
-      return HIKF_BAD_ARGUMENT;
-    }
-  }
+// shared driver: DIM-D rays with host-computed lengths (validated by the caller)
+template <int DIM>
+static int ray_driver(const RayGrid& gr, int64_t n, const double* src_host, const double* rcv_host,
+                      const std::vector<double>& len, int32_t* indptr_dev, int32_t* indices_dev, double* data_dev,
+                      int64_t capacity, int64_t* nnz_out, cudaStream_t st) {
   if (n == 0) {
     HIKF_CHECK_CUDA(cudaMemsetAsync(indptr_dev, 0, sizeof(int32_t), st));
     *nnz_out = 0;
@@ -221,16 +219,16 @@ int ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0,
   const int64_t cap = RT * RIPT;
   double *d_src, *d_rcv, *d_len, *segs;
   int32_t *cells, *counts;
-  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&d_src, sizeof(double) * 2 * n, st));
-  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&d_rcv, sizeof(double) * 2 * n, st));
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&d_src, sizeof(double) * DIM * n, st));
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&d_rcv, sizeof(double) * DIM * n, st));
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&d_len, sizeof(double) * n, st));
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&segs, sizeof(double) * n * cap, st));
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&cells, sizeof(int32_t) * n * cap, st));
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * (n + 1), st));
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(d_src, src_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(d_rcv, rcv_host, sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(d_src, src_host, sizeof(double) * DIM * n, cudaMemcpyHostToDevice, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(d_rcv, rcv_host, sizeof(double) * DIM * n, cudaMemcpyHostToDevice, st));
   HIKF_CHECK_CUDA(cudaMemcpyAsync(d_len, len.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-  ray_cells_kernel<<<(unsigned)n, RT, 0, st>>>(nx, ny, dx, dy, x0, y0, d_src, d_rcv, d_len, cap, cells, segs, counts);
+  ray_cells_kernel<DIM><<<(unsigned)n, RT, 0, st>>>(gr, d_src, d_rcv, d_len, cap, cells, segs, counts);
   HIKF_CHECK_LAUNCH();
   // indptr = exclusive scan of the per-ray counts
   HIKF_CHECK_CUDA(cudaMemsetAsync(indptr_dev, 0, sizeof(int32_t), st));
@@ -261,6 +259,65 @@ int ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0,
   cudaFreeAsync(cells, st);
   cudaFreeAsync(counts, st);
   return s;
+}
+
+int ray_operator_device(int64_t nx, int64_t ny, double dx, double dy, double x0, double y0, int64_t n,
+                        const double* src_host, const double* rcv_host, int32_t* indptr_dev, int32_t* indices_dev,
+                        double* data_dev, int64_t capacity, int64_t* nnz_out, cudaStream_t st) {
+  if (nx < 1 || ny < 1 || !(dx > 0) || !(dy > 0) || n < 0) {
+    set_error("ray_operator: bad grid");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (nx + ny > (int64_t)RT * RIPT) {
+    set_error("device ray operator supports nx + ny <= %d", RT * RIPT);
+    return HIKF_BAD_ARGUMENT;
+  }
+  const double xmax = x0 + nx * dx, ymax = y0 + ny * dy;
+  std::vector<double> len(std::max<int64_t>(n, 1));
+  for (int64_t r = 0; r < n; ++r) {
+    for (const double* p : {src_host + 2 * r, rcv_host + 2 * r})
+      if (!(p[0] >= x0 && p[0] <= xmax && p[1] >= y0 && p[1] <= ymax)) {
+        set_error("sources/receivers must lie within the grid bounding box");
+        return HIKF_BAD_ARGUMENT;
+      }
+    len[r] = hypot(rcv_host[2 * r] - src_host[2 * r], rcv_host[2 * r + 1] - src_host[2 * r + 1]);
+    if (len[r] == 0.0) {
+      set_error("source coincides with receiver (zero-length ray)");
+      return HIKF_BAD_ARGUMENT;
+    }
+  }
+  RayGrid gr{{nx, ny, 1}, {dx, dy, 1.0}, {x0, y0, 0.0}};
+  return ray_driver<2>(gr, n, src_host, rcv_host, len, indptr_dev, indices_dev, data_dev, capacity, nnz_out, st);
+}
+
+int ray_operator_3d_device(const int64_t n3[3], const double d3[3], const double o3[3], int64_t n,
+                           const double* src_host, const double* rcv_host, int32_t* indptr_dev, int32_t* indices_dev,
+                           double* data_dev, int64_t capacity, int64_t* nnz_out, cudaStream_t st) {
+  for (int a = 0; a < 3; ++a)
+    if (n3[a] < 1 || !(d3[a] > 0)) {
+      set_error("ray_operator_3d: bad grid");
+      return HIKF_BAD_ARGUMENT;
+    }
+  if (n < 0 || n3[0] + n3[1] + n3[2] > (int64_t)RT * RIPT + 1 || n3[0] * n3[1] * n3[2] > INT32_MAX) {
+    set_error("device 3D ray operator supports nx + ny + nz <= %d", RT * RIPT + 1);
+    return HIKF_BAD_ARGUMENT;
+  }
+  std::vector<double> len(std::max<int64_t>(n, 1));
+  for (int64_t r = 0; r < n; ++r) {
+    for (const double* p : {src_host + 3 * r, rcv_host + 3 * r})
+      for (int a = 0; a < 3; ++a)
+        if (!(p[a] >= o3[a] && p[a] <= o3[a] + n3[a] * d3[a])) {
+          set_error("sources/receivers must lie within the grid bounding box");
+          return HIKF_BAD_ARGUMENT;
+        }
+    len[r] = ray_length_3d(src_host + 3 * r, rcv_host + 3 * r);
+    if (len[r] == 0.0) {
+      set_error("source coincides with receiver (zero-length ray)");
+      return HIKF_BAD_ARGUMENT;
+    }
+  }
+  RayGrid gr{{n3[0], n3[1], n3[2]}, {d3[0], d3[1], d3[2]}, {o3[0], o3[1], o3[2]}};
+  return ray_driver<3>(gr, n, src_host, rcv_host, len, indptr_dev, indices_dev, data_dev, capacity, nnz_out, st);
 }
 
 }  // namespace hikf

@@ -177,7 +177,8 @@ def _model_H(model):
 
 
 def hikf_precompute_fmm(model, tree) -> HikfPrecompute:
-    """Form Q H^T with one device FMM product over H^T (filters.py:99-105)."""
+    """Form Q H^T with one device FMM product over H^T (filters.py:99-105);
+    ``tree`` may also be a 3D space3d.FmmTree3D (octree, cfg3 / cfg5)."""
     H = DeviceCSR.of(_model_H(model))
     m, n = tree.m, H.shape[0]
     if H.shape[1] != m:
@@ -186,9 +187,10 @@ def hikf_precompute_fmm(model, tree) -> HikfPrecompute:
     C_Q = torch.empty((m, n), dtype=torch.float64, device=dev)
     HC_Q = torch.empty((n, n), dtype=torch.float64, device=dev)
     diag_Q = torch.empty((m,), dtype=torch.float64, device=dev)
-    _lib.check(_lib.load().hikf_precompute(tree._handle, n, H.indptr.data_ptr(), H.indices.data_ptr(),
-                                           H.data.data_ptr(), C_Q.data_ptr(), HC_Q.data_ptr(), diag_Q.data_ptr(),
-                                           _lib.stream_ptr()))
+    entry = _lib.load().hikf_precompute3 if getattr(tree, "is_3d", False) else _lib.load().hikf_precompute
+    _lib.check(entry(tree._handle, n, H.indptr.data_ptr(), H.indices.data_ptr(),
+                     H.data.data_ptr(), C_Q.data_ptr(), HC_Q.data_ptr(), diag_Q.data_ptr(),
+                     _lib.stream_ptr()))
     return HikfPrecompute(C_Q, HC_Q, diag_Q)
 
 

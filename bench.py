@@ -48,7 +48,19 @@ CONFIGS = {
                  desc="cfg2: 2D 256x256 m=65536, n=256 crosswell rays, gaussian L=0.2, order 5, leaf 64"),
     "cfg4": dict(N=1024, ns=32, nr=32, family="exponential", L=0.25, R=1e-3, T=50, order=6, leaf=64,
                  desc="cfg4: 2D 1024x1024 m=1048576, n=1024 crosswell rays, exponential L=0.25, order 6, leaf 64"),
+    # 3D (no reference oracle: parity unpinned)
+    "cfg3": dict(dim=3, N=64, ns=24, nr=20, family="exponential", ls=(0.3, 0.3, 0.3), R=1e-3, T=100, order=5,
+                 leaf=128, plumes=[(0.2, 0.5, 0.5, 0.08, 0.005)],
+                 desc="cfg3: 3D 64^3 m=262144, n=480 jittered crosswell rays, exponential L=0.3, order 5, leaf 128"),
+    "cfg5": dict(dim=3, N=128, ns=32, nr=32, family="exponential", ls=(0.4, 0.4, 0.1), R=5e-4, T=50, order=5,
+                 leaf=128, plumes=[(0.3, 0.4, 0.5, 0.06, 0.005), (0.7, 0.6, 0.5, 0.1, -0.005)],
+                 desc="cfg5: 3D 128^3 m=2097152, n=1024 jittered crosswell rays, anisotropic exponential "
+                      "(0.4, 0.4, 0.1), order 5, leaf 128"),
 }
+
+
+def cfg_m(cfg):
+    return cfg["N"] ** cfg.get("dim", 2)
 
 # FP64 roofline denominator: MEASURED_PEAKS.json has no FP64 entry; this is the
 # cuBLAS DGEMM (torch.matmul float64, 8192^3) we measured on this pool's B200
@@ -203,7 +215,7 @@ def cpu_step_sample(cfg, rows, reps=1):
     m RHS, K HC, rowsum, predict add) is linear in the row count and the n x n
     terms (Cholesky, KH, KH HC) are the intercept.  Returns (seconds per full
     step, rows)."""
-    m = cfg["N"] ** 2
+    m = cfg_m(cfg)
     rows = min(rows, m)
     if rows == m:
         return _cpu_update_time(cfg, rows, reps), rows
@@ -212,6 +224,78 @@ def cpu_step_sample(cfg, rows, reps=1):
     b = max((t1 - t2) / (rows - rows // 2), 0.0)
     a = max(t1 - b * rows, 0.0)
     return a + b * m, rows
+
+
+def scenario_3d(cfg):
+    """3D scenario (space3d, recipe restated in oracle/hikf_oracle3d.py): grid,
+    seeded jittered crosswell, ray operator, plume observations."""
+    from paper_1404_3816_b200 import space3d as S
+    from oracle import hikf_oracle3d as O3
+    N = cfg["N"]
+    grid = S.Grid3D(N, N, N, 1.0 / N, 1.0 / N, 1.0 / N)
+    H = S.build_ray_operator_3d(grid, S.crosswell_3d(grid, cfg["ns"], cfg["nr"], 0))
+    xyz = grid.cell_centers().coords
+    F = O3.plumes_3d(xyz, cfg["T"], cfg["plumes"])
+    Z = np.asarray((H @ F[1:].T).T)
+    rng = np.random.default_rng([0, 0])
+    return grid, H, xyz, Z + math.sqrt(cfg["R"]) * rng.standard_normal(Z.shape)
+
+
+def fmm3_flops(tree, k):
+    """Dense-formulation flops of the 3D product as csrc/fmm3d.cu performs it
+    (expansions of every box at every level)."""
+    ex = tree.export()
+    q, D, G = tree.n_cheb ** 3, tree.depth, 1 << tree.depth
+    keys, cnt = ex["leaf_keys"], ex["leaf_counts"]
+    lut = dict(zip(keys.tolist(), cnt.tolist()))
+    near = 0
+    for key, c in zip(keys.tolist(), cnt.tolist()):
+        bx, by, bz = key // (G * G), (key // G) % G, key % G
+        for ox in (-1, 0, 1):
+            for oy in (-1, 0, 1):
+                for oz in (-1, 0, 1):
+                    x, y, z = bx + ox, by + oy, bz + oz
+                    if 0 <= x < G and 0 <= y < G and 0 <= z < G:
+                        near += c * lut.get((x * G + y) * G + z, 0)
+    f = {"p2p": 2.0 * k * near, "p2m": 2.0 * k * tree.m * q, "l2p": 2.0 * k * tree.m * q}
+    f["m2m"] = f["l2l"] = sum(2.0 * k * 8 ** (lev + 1) * q * q for lev in range(2, D))
+    m2l = 0.0
+    for lev in range(2, D + 1):
+        Gl = 1 << lev
+        i = np.arange(Gl)
+        per_axis = {}
+        for d in range(-3, 4):
+            j = i + d
+            per_axis[d] = {c: int(np.sum((j >= 0) & (j < Gl) & (i % 2 == c) &
+                                         (np.abs((j >> 1) - (i >> 1)) <= 1))) for c in (0, 1)}
+        for a in range(-3, 4):
+            for b in range(-3, 4):
+                for c in range(-3, 4):
+                    if max(abs(a), abs(b), abs(c)) < 2:
+                        continue
+                    m2l += sum(per_axis[a][x] * per_axis[b][y] * per_axis[c][z]
+                               for x in (0, 1) for y in (0, 1) for z in (0, 1))
+    f["m2l"] = 2.0 * k * q * q * m2l if D >= 2 else 0.0
+    return f
+
+
+def cpu_qht_sample_3d(cfg, H, xyz, cols=2):
+    """Exact Q H^T columns on the host (direct sum over each ray's cells, numpy):
+    the CPU baseline for the 3D precompute (the reference has no 3D path)."""
+    ls = np.array(cfg["ls"])
+    X = xyz / ls
+    sel = np.linspace(0, H.shape[0] - 1, cols).astype(int)
+    t0 = time.perf_counter()
+    for j in sel:
+        c = H.indices[H.indptr[j]:H.indptr[j + 1]]
+        h = H.data[H.indptr[j]:H.indptr[j + 1]]
+        acc = np.zeros(len(X))
+        for s in range(0, len(c), 16):
+            d = X[:, None, :] - X[None, c[s:s + 16], :]
+            r = np.sqrt((d * d).sum(-1))
+            acc += np.exp(-(r * r if cfg["family"] == "gaussian" else r)) @ h[s:s + 16]
+    t = time.perf_counter() - t0
+    return len(X) * cols / t, t
 
 
 def cpu_qht_sample(cfg, cols=8):
@@ -246,7 +330,7 @@ def run_reference(args, cfg, rank):
             per_step.append(t)
     t_step = statistics.median(per_step)
     value = 1.0 / t_step
-    sample = (f"oracle/hikf_oracle.py predict+update (numpy + OpenBLAS/LAPACK) on {rows} of {cfg['N'] ** 2} state rows "
+    sample = (f"oracle/hikf_oracle.py predict+update (numpy + OpenBLAS/LAPACK) on {rows} of {cfg_m(cfg)} state rows "
               f"with n={cfg['ns'] * cfg['nr']} (and rows/2), linearly extrapolated to m; one sample pair per step")
     line = {
         "metric": "hikf_assimilation_steps_per_sec", "value": value, "unit": "steps/s", "n_gpus": args.gpus,
@@ -295,12 +379,18 @@ def main():
     flt = P.filters
 
     N = cfg["N"]
-    grid = P.Grid2D(N, N, 1.0 / N, 1.0 / N)
-    H = P.tomography.build_ray_operator(grid, P.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], 0.0, 1.0))
+    dim3 = cfg.get("dim", 2) == 3
+    if dim3:
+        grid, H, xy, obs = scenario_3d(cfg)
+        kern = P.space3d.KernelSpec3(cfg["family"], 1.0, *cfg["ls"])
+    else:
+        grid = P.Grid2D(N, N, 1.0 / N, 1.0 / N)
+        H = P.tomography.build_ray_operator(grid, P.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], 0.0,
+                                                                                   1.0))
+        xy = grid.cell_centers().coords
+        obs = plume_observations(H, xy, cfg["T"], cfg["R"])
+        kern = P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
     m, n = grid.m, H.shape[0]
-    xy = grid.cell_centers().coords
-    obs = plume_observations(H, xy, cfg["T"], cfg["R"])
-    kern = P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
 
     class Model:
         pass
@@ -323,10 +413,16 @@ def main():
 
     # ---- tree build + Q H^T precompute (one-time; timed separately) ----
     # (a tiny build first, so lazy CUDA module loading is not charged to the tree)
-    P.build_tree(P.PointSet(np.random.default_rng(0).random((256, 2))), kern)
+    if dim3:
+        P.space3d.build_tree3d(np.random.default_rng(0).random((512, 3)), kern, cfg["order"], cfg["leaf"])
+    else:
+        P.build_tree(P.PointSet(np.random.default_rng(0).random((256, 2))), kern)
     barrier_sync()
     t0 = time.perf_counter()
-    tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    if dim3:
+        tree = P.space3d.build_tree3d(grid.cell_centers(), kern, cfg["order"], cfg["leaf"])
+    else:
+        tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t0
     flt.hikf_precompute_fmm(model, tree)  # warm-up of the precompute (allocator, L2)
@@ -343,11 +439,15 @@ def main():
     fmm_stage = {s: _lib.prof_read(s) for s in ("densify", "p2p", "p2m", "m2m", "m2l", "l2l", "l2p")}
     fmm_useful = {s: _lib.prof_flops(s) for s in ("p2p", "p2m", "m2m", "m2l", "l2l", "l2p")}
     qht_useful = float(sum(fmm_useful.values()))
-    ex = tree.export()
-    cnt = ex["leaf_counts"]
-    near_pts = float(np.sum(cnt[ex["near_t"]] * cnt[ex["near_s"]]))
-    ff = fmm_flops(tree._orders, tree.depth, n, near_pts, m) if tree.depth >= 2 else {"p2p": 2.0 * n * near_pts}
-    ff["m2l"] = m2l_flops(tree, n) if tree.depth >= 2 else 0.0
+    if dim3:
+        ff = fmm3_flops(tree, n)
+        qht_useful = float(sum(ff.values()))  # the 3D kernels perform the dense formulation
+    else:
+        ex = tree.export()
+        cnt = ex["leaf_counts"]
+        near_pts = float(np.sum(cnt[ex["near_t"]] * cnt[ex["near_s"]]))
+        ff = fmm_flops(tree._orders, tree.depth, n, near_pts, m) if tree.depth >= 2 else {"p2p": 2.0 * n * near_pts}
+        ff["m2l"] = m2l_flops(tree, n) if tree.depth >= 2 else 0.0
     qht_flops = sum(ff.values())
 
     # ---- filter: warm-up, then the timed region ----
@@ -468,10 +568,16 @@ def main():
             "sample": f"oracle predict+update on {rows} and {rows // 2} of {m} rows (n={n}), "
                       "linear extrapolation t(m) = a + b m"}
         try:
-            mn_s, tb, tq = cpu_qht_sample(cfg, cols=8)
-            line["cpu_baseline"]["qht"] = {"value": mn_s, "unit": "(m*n)/s",
-                                           "sample": f"oracle bbFMM matmat on 8 of {n} H^T columns ({tq:.1f} s), "
-                                                     f"tree build {tb:.1f} s"}
+            if dim3:
+                mn_s, tq = cpu_qht_sample_3d(cfg, H, xy, cols=2 if m <= 300000 else 1)
+                line["cpu_baseline"]["qht"] = {"value": mn_s, "unit": "(m*n)/s",
+                                               "sample": f"exact direct-sum Q H^T on {2 if m <= 300000 else 1} of "
+                                                         f"{n} columns ({tq:.1f} s; no reference 3D path)"}
+            else:
+                mn_s, tb, tq = cpu_qht_sample(cfg, cols=8)
+                line["cpu_baseline"]["qht"] = {"value": mn_s, "unit": "(m*n)/s",
+                                               "sample": f"oracle bbFMM matmat on 8 of {n} H^T columns ({tq:.1f} s), "
+                                                         f"tree build {tb:.1f} s"}
         except MemoryError:
             pass
     if rank == 0:

@@ -305,11 +305,18 @@ struct BoxOpArgs {
   int kc;
 };
 
-// one CTA = one output box; warp w owns chunk columns 8w .. 8w + 7
-__global__ void __launch_bounds__(T3, 1) boxop3_kernel(BoxOpArgs g) {
-  extern __shared__ double As[];
+// one CTA = one output box; warp w owns chunk columns 8w .. 8w + 7.  The
+// operators stream through shared memory in K-slices of 32 with a two-slot
+// cp.async ring, so the next slice (of this term or the next valid term)
+// loads while the current one is multiplied.
+constexpr int KS = 32;                    // k per slice
+constexpr int KLD = KS + 4;               // == 4 mod 16 doubles
+constexpr int SLICE = MAXRT * 8 * KLD;    // doubles per slot (128 rows)
+
+__global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
+  extern __shared__ double As[];  // 2 slots
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
-  const int q = g.q, nrt = (q + 7) >> 3, nk4 = (q + 3) / 4, lda = pad4(nk4 * 4);
+  const int q = g.q, nrt = (q + 7) >> 3, nslices = (q + KS - 1) / KS;
   const int64_t G = g.Gout, unit = blockIdx.x;
   int64_t ox, oy, oz;
   if (g.mode == OP_M2M) {
@@ -325,40 +332,85 @@ __global__ void __launch_bounds__(T3, 1) boxop3_kernel(BoxOpArgs g) {
   }
   const int64_t obox = (ox * G + oy) * G + oz;
   const int nterms = g.mode == OP_M2L ? NOFF : (g.mode == OP_M2M ? 8 : 1);
-  const int j0 = warp * 8, jc = j0 + gq;
-  double acc[MAXRT][2];
-  zero_acc(acc);
-  for (int term = 0; term < nterms; ++term) {
-    const double* A;
-    int64_t sbox = -1;  // CTA-uniform
+  // term -> (operator, source box); -1 when the term does not apply (CTA-uniform)
+  auto term_src = [&](int term, const double** A) -> int64_t {
     if (g.mode == OP_M2L) {
       const int dx = g.offs[3 * term], dy = g.offs[3 * term + 1], dz = g.offs[3 * term + 2];
       // parents adjacent per axis (fmm.py:301-302); floor((c + d) / 2) is the parent offset
       const int cx = (g.cls >> 2) & 1, cy = (g.cls >> 1) & 1, cz = g.cls & 1;
       const int pdx = (cx + dx) >> 1, pdy = (cy + dy) >> 1, pdz = (cz + dz) >> 1;
-      if (pdx < -1 || pdx > 1 || pdy < -1 || pdy > 1 || pdz < -1 || pdz > 1) continue;
+      if (pdx < -1 || pdx > 1 || pdy < -1 || pdy > 1 || pdz < -1 || pdz > 1) return -1;
       const int64_t sx = ox + dx, sy = oy + dy, sz = oz + dz;
-      if (sx < 0 || sy < 0 || sz < 0 || sx >= G || sy >= G || sz >= G) continue;
-      sbox = (sx * G + sy) * G + sz;
-      A = g.ops + (int64_t)term * q * q;
-    } else if (g.mode == OP_M2M) {
+      if (sx < 0 || sy < 0 || sz < 0 || sx >= G || sy >= G || sz >= G) return -1;
+      *A = g.ops + (int64_t)term * q * q;
+      return (sx * G + sy) * G + sz;
+    }
+    if (g.mode == OP_M2M) {
       const int64_t Gc = 2 * G;
       const int64_t cx = 2 * ox + ((term >> 2) & 1), cy = 2 * oy + ((term >> 1) & 1), cz = 2 * oz + (term & 1);
-      sbox = (cx * Gc + cy) * Gc + cz;
-      A = g.ops + (int64_t)term * q * q;  // shiftT[c]: parent coeff x child coeff
-    } else {
-      const int64_t Gp = G / 2;
-      sbox = ((ox >> 1) * Gp + (oy >> 1)) * Gp + (oz >> 1);
-      A = g.ops + (int64_t)g.cls * q * q;  // shift[c]: child coeff x parent coeff
+      *A = g.ops + (int64_t)term * q * q;  // shiftT[c]: parent coeff x child coeff
+      return (cx * Gc + cy) * Gc + cz;
     }
+    const int64_t Gp = G / 2;
+    *A = g.ops + (int64_t)g.cls * q * q;  // shift[c]: child coeff x parent coeff
+    return ((ox >> 1) * Gp + (oy >> 1)) * Gp + (oz >> 1);
+  };
+  auto next_term = [&](int from) {
+    const double* A;
+    for (int t = from; t < nterms; ++t)
+      if (term_src(t, &A) >= 0) return t;
+    return nterms;
+  };
+  // issue the copy of slice `sl` of term `term`'s operator into slot `slot` (zero-filled padding)
+  auto issue = [&](int term, int sl, int slot) {
+    const double* A;
+    term_src(term, &A);
+    double* dst = As + slot * SLICE;
+    const int k0 = sl * KS;
+    for (int e = threadIdx.x; e < MAXRT * 8 * KS; e += T3) {
+      const int r = e / KS, k = e % KS;
+      const bool ok = r < q && k0 + k < q;
+      cp_async8(dst + r * KLD + k, ok ? A + (int64_t)r * q + k0 + k : A, ok);
+    }
+  };
+  const int j0 = warp * 8, jc = j0 + gq;
+  double acc[MAXRT][2];
+  zero_acc(acc);
+  int term = next_term(0), sl = 0, slot = 0;
+  if (term < nterms) issue(term, 0, 0);
+  cp_async_commit();
+  while (term < nterms) {
+    // next step (slice of this term, or the first slice of the next valid term)
+    int nterm = term, nsl = sl + 1;
+    if (nsl == nslices) {
+      nterm = next_term(term + 1);
+      nsl = 0;
+    }
+    if (nterm < nterms) issue(nterm, nsl, slot ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
-    load_A(As, lda, nrt * 8, nk4 * 4, q, q, [&](int r, int c) { return A[(int64_t)r * q + c]; });
-    __syncthreads();
-    if (j0 >= g.kc) continue;
-    const double* B = g.in + sbox * (int64_t)q * KC;
-    warp_gemm(As, lda, nrt, nk4, gq, t4, [&](int k) { return (k < q && jc < g.kc) ? B[(int64_t)k * KC + jc] : 0.0; },
-              acc);
+    if (j0 < g.kc) {
+      const double* Aop;
+      const int64_t sbox = term_src(term, &Aop);
+      const double* B = g.in + sbox * (int64_t)q * KC;
+      const double* Asl = As + slot * SLICE;
+      const int k0 = sl * KS;
+      const int nk4 = (min(KS, q - k0) + 3) / 4;
+      for (int k4 = 0; k4 < nk4; ++k4) {
+        const int k = k0 + k4 * 4 + t4;
+        const double b = (k < q && jc < g.kc) ? B[(int64_t)k * KC + jc] : 0.0;
+#pragma unroll
+        for (int rt = 0; rt < MAXRT; ++rt)
+          if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], Asl[(rt * 8 + gq) * KLD + k4 * 4 + t4], b);
+      }
+    }
+    __syncthreads();  // everyone is done with `slot` before it is refilled
+    term = nterm;
+    sl = nsl;
+    slot ^= 1;
   }
+  cp_async_wait<0>();
   if (j0 >= g.kc) return;
   double* O = g.out + obox * (int64_t)q * KC;
 #pragma unroll
@@ -377,7 +429,7 @@ __global__ void __launch_bounds__(T3, 1) boxop3_kernel(BoxOpArgs g) {
   }
 }
 
-size_t boxop_smem(int q) { return sizeof(double) * (size_t)(((q + 7) >> 3) * 8) * pad4(((q + 3) / 4) * 4); }
+size_t boxop_smem(int) { return sizeof(double) * 2 * (size_t)SLICE; }
 size_t leafop_smem(int rows, int cols) {
   return sizeof(double) * (size_t)(((rows + 7) >> 3) * 8) * pad4(((cols + 3) / 4) * 4);
 }

@@ -303,7 +303,20 @@ struct BoxOpArgs {
   const double* ops;         // M2L: 316 x q x q; M2M: shiftT (8 x q x q); L2L: shift (8 x q x q)
   const int* offs;           // M2L: 316 x 3
   int kc;
+  const uint8_t* nz;         // M2L: per source box, 1 if its expansion has a nonzero in this chunk
 };
+
+// nz[box] = any(W[box][a][j] != 0, a < q, j < kc): M2L skips all-zero sources (exact: they add zeros)
+__global__ void nonzero_boxes(const double* __restrict__ W, int64_t nboxes, int q, int kc, uint8_t* __restrict__ nz) {
+  const int64_t box = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (box >= nboxes) return;
+  const double* w = W + box * (int64_t)q * KC;
+  bool any = false;
+  for (int e = lane; e < q * kc && !any; e += 32) any = w[(int64_t)(e / kc) * KC + e % kc] != 0.0;
+  any = __any_sync(0xffffffffu, any);
+  if (lane == 0) nz[box] = any ? 1 : 0;
+}
 
 // one CTA = one output box; warp w owns chunk columns 8w .. 8w + 7.  The
 // operators stream through shared memory in K-slices of 32 with a two-slot
@@ -342,8 +355,10 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
       if (pdx < -1 || pdx > 1 || pdy < -1 || pdy > 1 || pdz < -1 || pdz > 1) return -1;
       const int64_t sx = ox + dx, sy = oy + dy, sz = oz + dz;
       if (sx < 0 || sy < 0 || sz < 0 || sx >= G || sy >= G || sz >= G) return -1;
+      const int64_t sb = (sx * G + sy) * G + sz;
+      if (g.nz && !g.nz[sb]) return -1;  // all-zero source expansion
       *A = g.ops + (int64_t)term * q * q;
-      return (sx * G + sy) * G + sz;
+      return sb;
     }
     if (g.mode == OP_M2M) {
       const int64_t Gc = 2 * G;
@@ -649,12 +664,19 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
   // expansion buffers for one chunk: W_l, L_l (dense per level, KC columns)
   double* W[kMaxDepth + 1] = {nullptr};
   double* L[kMaxDepth + 1] = {nullptr};
+  uint8_t* NZ[kMaxDepth + 1] = {nullptr};
   if (D >= 2)
     for (int l = 2; l <= D; ++l) {
       const int64_t nb = (int64_t)1 << (3 * l);
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&W[l], sizeof(double) * nb * q * KC, st));
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&L[l], sizeof(double) * nb * q * KC, st));
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&NZ[l], nb, st));
     }
+  auto flag = [&](int l, int kc) {
+    const int64_t nb = (int64_t)1 << (3 * l);
+    nonzero_boxes<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, st>>>(W[l], nb, q, kc, NZ[l]);
+    return cudaGetLastError() == cudaSuccess ? HIKF_OK : HIKF_CUDA_ERROR;
+  };
   const T3v tv = view(t);
   int status = HIKF_OK;
   for (int64_t c0 = 0; c0 < k && status == HIKF_OK; c0 += KC) {
@@ -670,19 +692,21 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
       HIKF_CHECK_CUDA(cudaMemsetAsync(W[D], 0, sizeof(double) * ((int64_t)1 << (3 * D)) * q * KC, st));
       p2m3_kernel<<<(unsigned)nl, T3, sm_p2m, st>>>(tv, ch, W[D]);
       HIKF_CHECK_LAUNCH();
+      HIKF_TRY(flag(D, ch.kc));
     }
     for (int l = D - 1; l >= 2; --l) {
       ProfScope ps(ST_M2M, st);
-      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc};
+      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, nullptr};
       boxop3_kernel<<<(unsigned)((int64_t)1 << (3 * l)), T3, sm_box, st>>>(a);
       HIKF_CHECK_LAUNCH();
+      HIKF_TRY(flag(l, ch.kc));
     }
     for (int l = 2; l <= D; ++l) {
       {
         ProfScope ps(ST_M2L, st);
         const int64_t units = (int64_t)1 << (3 * (l - 1));  // parents: one class-c child each
         for (int c = 0; c < 8; ++c) {
-          BoxOpArgs a{OP_M2L, q, l, c, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc};
+          BoxOpArgs a{OP_M2L, q, l, c, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l]};
           boxop3_kernel<<<(unsigned)units, T3, sm_box, st>>>(a);
           HIKF_CHECK_LAUNCH();
         }
@@ -691,7 +715,7 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
         ProfScope ps(ST_L2L, st);
         const int64_t units = (int64_t)1 << (3 * (l - 1));
         for (int c = 0; c < 8; ++c) {
-          BoxOpArgs a{OP_L2L, q, l, c, (int64_t)1 << l, L[l - 1], L[l], t->shift, nullptr, ch.kc};
+          BoxOpArgs a{OP_L2L, q, l, c, (int64_t)1 << l, L[l - 1], L[l], t->shift, nullptr, ch.kc, nullptr};
           boxop3_kernel<<<(unsigned)units, T3, sm_box, st>>>(a);
           HIKF_CHECK_LAUNCH();
         }
@@ -706,6 +730,7 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
   for (int l = 2; l <= D; ++l) {
     cudaFreeAsync(W[l], st);
     cudaFreeAsync(L[l], st);
+    cudaFreeAsync(NZ[l], st);
   }
   return status;
 }

@@ -188,7 +188,7 @@ struct Chunk {
 };
 
 // ---- P2P: U[t] = sum_nbr K(t, s) V[s] (first write of the chunk's U columns) ----
-__global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch) {
+__global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, const uint8_t* __restrict__ leafnz) {
   extern __shared__ double As[];
   const int leaf = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch) {
     const int64_t x = bx + s / 9 - 1, y = by + (s / 3) % 3 - 1, z = bz + s % 3 - 1;
     if (x < 0 || y < 0 || z < 0 || x >= G || y >= G || z >= G) continue;
     const int sl = t.box2leaf[(x * G + y) * G + z];
-    if (sl < 0) continue;  // uniform across the CTA
+    if (sl < 0 || !leafnz[sl]) continue;  // no leaf / all-zero charges: uniform across the CTA
     const int ss = t.leaf_start[sl], sc = t.leaf_count[sl];
     __syncthreads();
     load_A(As, lda, nrt * 8, ((sc + 3) / 4) * 4, tc, sc, [&](int r, int c) {
@@ -235,9 +235,11 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch) {
 }
 
 // ---- P2M: W_D[box(leaf)] = W2_leaf^T V_leaf ----
-__global__ void __launch_bounds__(T3, 1) p2m3_kernel(const T3v t, Chunk ch, double* __restrict__ W) {
+__global__ void __launch_bounds__(T3, 1) p2m3_kernel(const T3v t, Chunk ch, double* __restrict__ W,
+                                                     const uint8_t* __restrict__ leafnz) {
   extern __shared__ double As[];
   const int leaf = blockIdx.x;
+  if (!leafnz[leaf]) return;  // W stays zero (memset)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf], q = t.q;
   const int nrt = (q + 7) >> 3, lda = pad4(((t.max_count + 3) / 4) * 4);
@@ -306,6 +308,20 @@ struct BoxOpArgs {
   const uint8_t* nz;         // M2L: per source box, 1 if its expansion has a nonzero in this chunk
 };
 
+// leafnz[l] = any(V[order[p]][j] != 0) over the leaf's points p, j < kc: P2P / P2M skip all-zero
+// source leaves (exact: they contribute zeros)
+__global__ void nonzero_leaves(const T3v t, const double* __restrict__ V, int64_t ldv, int kc, int64_t nl,
+                               uint8_t* __restrict__ nz) {
+  const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (leaf >= nl) return;
+  const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf];
+  bool any = false;
+  for (int e = lane; e < tc * kc && !any; e += 32) any = V[t.order[ts + e / kc] * ldv + e % kc] != 0.0;
+  any = __any_sync(0xffffffffu, any);
+  if (lane == 0) nz[leaf] = any ? 1 : 0;
+}
+
 // nz[box] = any(W[box][a][j] != 0, a < q, j < kc): M2L skips all-zero sources (exact: they add zeros)
 __global__ void nonzero_boxes(const double* __restrict__ W, int64_t nboxes, int q, int kc, uint8_t* __restrict__ nz) {
   const int64_t box = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -363,8 +379,10 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     if (g.mode == OP_M2M) {
       const int64_t Gc = 2 * G;
       const int64_t cx = 2 * ox + ((term >> 2) & 1), cy = 2 * oy + ((term >> 1) & 1), cz = 2 * oz + (term & 1);
+      const int64_t cb = (cx * Gc + cy) * Gc + cz;
+      if (g.nz && !g.nz[cb]) return -1;  // all-zero child expansion
       *A = g.ops + (int64_t)term * q * q;  // shiftT[c]: parent coeff x child coeff
-      return (cx * Gc + cy) * Gc + cz;
+      return cb;
     }
     const int64_t Gp = G / 2;
     *A = g.ops + (int64_t)g.cls * q * q;  // shift[c]: child coeff x parent coeff
@@ -672,6 +690,8 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&L[l], sizeof(double) * nb * q * KC, st));
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&NZ[l], nb, st));
     }
+  uint8_t* LNZ = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&LNZ, std::max<int64_t>(nl, 1), st));
   auto flag = [&](int l, int kc) {
     const int64_t nb = (int64_t)1 << (3 * l);
     nonzero_boxes<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, st>>>(W[l], nb, q, kc, NZ[l]);
@@ -681,22 +701,24 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
   int status = HIKF_OK;
   for (int64_t c0 = 0; c0 < k && status == HIKF_OK; c0 += KC) {
     Chunk ch{V + c0, ldv, (int)std::min<int64_t>(KC, k - c0), U + c0, ldu};
+    nonzero_leaves<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, st>>>(tv, ch.V, ch.ldv, ch.kc, nl, LNZ);
+    HIKF_CHECK_LAUNCH();
     {
       ProfScope ps(ST_P2P, st);
-      p2p3_kernel<<<(unsigned)nl, T3, sm_p2p, st>>>(tv, ch);
+      p2p3_kernel<<<(unsigned)nl, T3, sm_p2p, st>>>(tv, ch, LNZ);
       HIKF_CHECK_LAUNCH();
     }
     if (D < 2) continue;
     {
       ProfScope ps(ST_P2M, st);
       HIKF_CHECK_CUDA(cudaMemsetAsync(W[D], 0, sizeof(double) * ((int64_t)1 << (3 * D)) * q * KC, st));
-      p2m3_kernel<<<(unsigned)nl, T3, sm_p2m, st>>>(tv, ch, W[D]);
+      p2m3_kernel<<<(unsigned)nl, T3, sm_p2m, st>>>(tv, ch, W[D], LNZ);
       HIKF_CHECK_LAUNCH();
       HIKF_TRY(flag(D, ch.kc));
     }
     for (int l = D - 1; l >= 2; --l) {
       ProfScope ps(ST_M2M, st);
-      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, nullptr};
+      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, NZ[l + 1]};
       boxop3_kernel<<<(unsigned)((int64_t)1 << (3 * l)), T3, sm_box, st>>>(a);
       HIKF_CHECK_LAUNCH();
       HIKF_TRY(flag(l, ch.kc));
@@ -732,6 +754,7 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     cudaFreeAsync(L[l], st);
     cudaFreeAsync(NZ[l], st);
   }
+  cudaFreeAsync(LNZ, st);
   return status;
 }
 

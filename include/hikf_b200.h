@@ -251,6 +251,18 @@ int hikf_tree3_matmat(const hikf_tree3* tree, const double* V_dev, int64_t k, do
 int hikf_precompute3(hikf_tree3* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
                      const double* data_dev, double* C_Q_dev, double* HC_Q_dev, double* diag_Q_dev, void* stream);
 
+/* ---- dense Kalman filter (filters.py:45-74) and dense Gram (kernels.py:97-117) ----
+ * The reference's exact-algebra oracle path, on the device: G (m x m) =
+ * K(|x_i - x_j|) (r = 0 -> value_at_zero); kf_predict P_out = P + Q;
+ * kf_update: C = H P, S = sym(H C^T + r I), K^T = S^-1 C, mean += K (z - H mean),
+ * P = sym(P - K C).  All arrays device, row-major. */
+int hikf_dense_gram(const double* xy_host, int64_t m, const hikf_kernel* kernel, double* G_dev, void* stream);
+int hikf_kf_predict(int64_t m, const double* P_dev, const double* Q_dev, double* P_out, void* stream);
+size_t hikf_kf_workspace_bytes(int64_t m, int64_t n);
+int hikf_kf_update(int64_t m, int64_t n, const double* mean_dev, const double* P_dev, const int32_t* indptr_dev,
+                   const int32_t* indices_dev, const double* data_dev, double r_variance, const double* z_dev,
+                   double* mean_out, double* P_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ---- FP64 DMMA GEMM building block (the update's workhorse) ----
  * C (M x N, ldc) = alpha A (M x K, lda) B (K x N, ldb) + beta C, row-major,
  * device pointers.  kmode 0: full; 1: B upper triangular (K-range k <= col

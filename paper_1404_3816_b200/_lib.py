@@ -96,6 +96,10 @@ SIGNATURES = {
     "hikf_tree3_export": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "hikf_tree3_matmat": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
     "hikf_precompute3": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "hikf_dense_gram": (ctypes.c_int, [_P, _I64, _P, _P, _P]),
+    "hikf_kf_predict": (ctypes.c_int, [_I64, _P, _P, _P, _P]),
+    "hikf_kf_workspace_bytes": (_SZ, [_I64, _I64]),
+    "hikf_kf_update": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _D, _P, _P, _P, _P, _SZ, _P]),
     "hikf_ray_operator_device": (ctypes.c_int, [_I64, _I64, _D, _D, _D, _D, _I64, _P, _P, _P, _P, _P, _I64, _P, _P]),
     "hikf_dgemm": (ctypes.c_int, [_I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _D, _D, _I32, _I32, _P]),
     "hikf_prof_enable": (ctypes.c_int, [ctypes.c_int]),

@@ -8,6 +8,7 @@
 
 #include "dense.h"
 #include "fmm3d.h"
+#include "kf.h"
 #include "host_ops.h"
 #include "dgemm.cuh"
 #include "prof.h"
@@ -672,6 +673,42 @@ int hikf_precompute3(hikf_tree3* t, int64_t n, const int32_t* ip, const int32_t*
   fill<<<grid_for(m), kT, 0, st>>>(dQ, m, k.variance);  // K(0) = variance
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
+}
+
+// ---- dense Kalman filter + dense Gram (filters.py:45-74, kernels.py:97-117) ----
+int hikf_dense_gram(const double* xy_host, int64_t m, const hikf_kernel* kernel, double* G_dev, void* stream) {
+  if (!xy_host || !kernel || !G_dev || m < 1) {
+    set_error("bad dense_gram arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  cudaStream_t st = as_stream(stream);
+  double* xy = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync((void**)&xy, sizeof(double) * 2 * m, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(xy, xy_host, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, st));
+  int s = dense_gram(xy, m, make_kparams(*kernel), G_dev, st);
+  cudaFreeAsync(xy, st);
+  return s;
+}
+
+int hikf_kf_predict(int64_t m, const double* P, const double* Q, double* P_out, void* stream) {
+  if (m < 1 || !P || !Q || !P_out) {
+    set_error("bad kf_predict arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return kf_predict(m, P, Q, P_out, as_stream(stream));
+}
+
+size_t hikf_kf_workspace_bytes(int64_t m, int64_t n) { return kf_workspace_bytes(m, n); }
+
+int hikf_kf_update(int64_t m, int64_t n, const double* mean, const double* P, const int32_t* ip, const int32_t* ix,
+                   const double* val, double r, const double* z, double* mean_out, double* P_out, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  if (m < 1 || n < 0 || !mean || !P || !mean_out || !P_out || (n > 0 && (!ip || !z))) {
+    set_error("bad kf_update arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return kf_update(m, n, mean, P, ip, ix, val, r, z, mean_out, P_out, workspace, workspace_bytes,
+                   as_stream(stream));
 }
 
 }  // extern "C"

@@ -26,6 +26,7 @@ from .kernels import value_at_zero  # noqa: F401
 
 __all__ = [
     "DeviceCSR", "HikfPrecompute", "HikfState", "NumericalConsistencyError", "hikf_precompute_dense",
+    "KfState", "dense_gram", "kf_init", "kf_predict", "kf_update",
     "hikf_precompute_fmm", "hikf_init", "hikf_predict", "hikf_update",
 ]
 
@@ -302,3 +303,74 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
 
 
 _CHAIN: dict = {}
+
+
+# ----------------------------------------------------------------------
+# dense Kalman filter (filters.py:45-74) -- the exact-algebra oracle path
+# ----------------------------------------------------------------------
+
+
+class KfState:
+    """mean (m,) and the dense covariance (m, m) as CUDA tensors (``*_t``), numpy on access."""
+
+    def __init__(self, mean, cov):
+        self.mean_t, self.cov_t = mean, cov
+
+    mean = property(lambda self: self.mean_t.cpu().numpy())
+    cov = property(lambda self: self.cov_t.cpu().numpy())
+
+
+def dense_gram(spec, points) -> torch.Tensor:
+    """G[i, j] = K(|x_i - x_j|) on the device (kernels.py:97-117), r = 0 -> value_at_zero."""
+    import ctypes
+
+    from .fmm import _coords_of
+    from .kernels import to_c
+    xy = _coords_of(points)
+    m = xy.shape[0]
+    G = torch.empty((m, m), dtype=torch.float64, device=_dev())
+    kc = to_c(spec)
+    _lib.check(_lib.load().hikf_dense_gram(xy.ctypes.data, m, ctypes.byref(kc), G.data_ptr(), _lib.stream_ptr()))
+    return G
+
+
+def kf_init(model) -> KfState:
+    """mean = mu_0, cov = alpha I (filters.py:51-53)."""
+    m = int(model.m)
+    dev = _dev()
+    return KfState(_to_dev(model.initial_mean, (m,)).clone(),
+                   float(model.alpha) * torch.eye(m, dtype=torch.float64, device=dev))
+
+
+def kf_predict(state: KfState, Q) -> KfState:
+    """cov + Q (filters.py:56-59)."""
+    Qt = Q if isinstance(Q, torch.Tensor) else torch.as_tensor(np.asarray(Q, dtype=np.float64))
+    Qt = Qt.to(state.cov_t.device)
+    if tuple(Qt.shape) != tuple(state.cov_t.shape):
+        raise ValueError("Q shape does not match covariance")
+    out = torch.empty_like(state.cov_t)
+    _lib.check(_lib.load().hikf_kf_predict(out.shape[0], state.cov_t.data_ptr(), Qt.contiguous().data_ptr(),
+                                           out.data_ptr(), _lib.stream_ptr()))
+    return KfState(state.mean_t, out)
+
+
+def kf_update(state: KfState, H, r_variance: float, z) -> KfState:
+    """Dense Kalman update (filters.py:62-74)."""
+    Hd = DeviceCSR.of(H)
+    m = state.mean_t.shape[0]
+    zt = z if isinstance(z, torch.Tensor) else np.asarray(z, dtype=float)
+    if Hd.shape[0] != zt.shape[0] or Hd.shape[1] != m:
+        raise ValueError("observation / operator shape mismatch")
+    n = Hd.shape[0]
+    if n == 0:
+        return state
+    zt = _to_dev(zt, (n,))
+    mean = torch.empty_like(state.mean_t)
+    cov = torch.empty_like(state.cov_t)
+    lib = _lib.load()
+    ws = torch.empty(int(lib.hikf_kf_workspace_bytes(m, n)), dtype=torch.uint8, device=mean.device)
+    _lib.check(lib.hikf_kf_update(m, n, state.mean_t.data_ptr(), state.cov_t.data_ptr(), Hd.indptr.data_ptr(),
+                                  Hd.indices.data_ptr(), Hd.data.data_ptr(), float(r_variance), zt.data_ptr(),
+                                  mean.data_ptr(), cov.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_ptr()))
+    return KfState(mean, cov)
+

@@ -538,7 +538,6 @@ int dgemm_variant() {
 
 void set_dgemm_variant(int v) { g_variant = v; }
 
-int update_variant_y() { return getenv("HIKF_DGEMM_VARIANT") ? dgemm_variant() : 10; }
 int update_variant_c() { return getenv("HIKF_DGEMM_VARIANT") ? dgemm_variant() : 7; }
 
 int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {

@@ -60,9 +60,8 @@ inline int dgemm_col_tiles(int64_t N, int variant = -1) {
   int v = variant >= 0 ? variant : dgemm_variant();
   return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22) ? 64 : 128);
 }
-// variants used by the update for the triangular Y GEMM and the full C GEMM
-// (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log); HIKF_DGEMM_VARIANT overrides both
-int update_variant_y();
+// variant used by the update's K GEMM (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log);
+// HIKF_DGEMM_VARIANT overrides it
 int update_variant_c();
 constexpr int DG_MIN_BN = 64;  // smallest column tile of any variant (partials workspace sizing)
 

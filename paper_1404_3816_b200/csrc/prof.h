@@ -11,7 +11,7 @@ namespace hikf {
 enum Stage {
   ST_PREDICT = 0,
   ST_FACTOR = 1,   // S, Cholesky + inverse, n x n products, innovation
-  ST_GEMM_Y = 2,   // Y = C' Li^T (+ row partials)
+  ST_GEMM_Y = 2,   // unused since the single-GEMM update (kept: stage ids are ABI)
   ST_FINALIZE = 3, // var / mean rows + consistency check
   ST_GEMM_C = 4,   // C_new = C' - Y P
   ST_P2P = 5,

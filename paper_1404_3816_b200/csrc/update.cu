@@ -2,16 +2,16 @@
 //
 // For the predicted state (C' = C + C_Q, var' = var + diag_Q, HC' = HC + HC_Q):
 //   S   = sym(HC' + r I)                      (n x n)
-//   L   = chol(S), Li = L^{-1}                (recursive blocked, DMMA GEMMs)
-//   Y   = C' Li^T                             (m x n, triangular B: m n^2 flops)
-//   mean_new = mean + Y (Li (z - H mean))     (= mean + K innov, K = C' S^{-1})
-//   var_new  = var' - rowsum(Y o Y)           (= var' - rowsum(K o C'))
-//   P   = Li HC',  R = HC' Li^T
-//   C_new  = C' - Y P                          (= C' - K HC'; 2 m n^2 flops)
-//   HC_new = HC' - R P                         (= HC' - KH HC')
-// i.e. the reference's two m-RHS triangular solves plus K HC are regrouped
-// around Y (3 m n^2 instead of 4 m n^2 flops); the parity of this regrouping
-// against the reference at cfg1/cfg2 is measured in DESIGN.md section 5.
+//   L   = chol(S), Li = L^{-1}, S^-1 = Li^T Li (recursive blocked, DMMA GEMMs)
+//   K   = C' S^-1                             (one m x n x n GEMM, 2 m n^2 flops)
+//   C_new    = r K                            (= C' - K HC', since HC' = S - r I)
+//   mean_new = mean + K (z - H mean)          (GEMM epilogue row partial)
+//   var_new  = var' - rowsum(K o C')          (GEMM epilogue row partial)
+//   HC_new   = HC' - (HC' Li^T)(Li HC')       (= HC' - KH HC', side stream)
+// i.e. the reference's two m-RHS triangular solves plus K HC (4 m n^2 flops)
+// become one GEMM.  The n x n chain runs on a side stream and the next step's
+// factorisation is done ahead (look-ahead); the GEMM epilogue can also emit the
+// next step's C' (chained predict).  Parity and timings: DESIGN.md section 5.
 #include <algorithm>
 #include <cfloat>
 
@@ -255,17 +255,6 @@ __global__ void csr_spmv(int64_t n, const int32_t* __restrict__ ip, const int32_
   if (lane == 0) y[row] = s;
 }
 
-// w = Li innov (n x n lower-triangular GEMV, one warp per row)
-__global__ void trmv_lower(const double* __restrict__ Li, int64_t n, const double* __restrict__ x,
-                           double* __restrict__ y) {
-  int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
-  if (row >= n) return;
-  double s = 0.0;
-  for (int64_t k = lane; k <= row; k += 32) s += Li[row * n + k] * x[k];
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) y[row] = s;
-}
 
 // var_new = var' - sum_t psq, mean_new = mean + sum_t pdot; block min/max partials
 __global__ void finalize_rows(int64_t m, int nt, const double* __restrict__ psq, const double* __restrict__ pdot,

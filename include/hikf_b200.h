@@ -174,13 +174,15 @@ int hikf_update(int64_t m, int64_t n, const double* mean_dev, const double* C_de
  *          with the same C_Q and workspace -- use the C' that call produced and
  *          skip the C + C_Q pass.  Pointers, sizes and success of the previous
  *          call are checked; any mismatch falls back to the full predict.
- * Setting bit 1 while C_out was modified in between gives wrong results. */
+ * Setting bit 1 while C_out was modified in between gives wrong results.
+ * mean_host (optional, pinned host memory, m doubles): mean_out is also
+ * copied there, inside the call (the read-back overlaps the update's tail). */
 int hikf_update_chained(int64_t m, int64_t n, const double* mean_dev, const double* C_dev, const double* var_dev,
                         const double* HC_dev, const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev,
                         const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev,
                         double r_variance, const double* z_dev, double* mean_out, double* C_out, double* var_out,
                         double* HC_out, void* workspace, size_t workspace_bytes, double* min_var_out, int32_t chain,
-                        void* stream);
+                        double* mean_host, void* stream);
 
 /* ---- row-sharded update: the same update on rows [r0, r1) of a
  * state sharded across ranks.  Hmean_dev = the all-reduced H mean (the

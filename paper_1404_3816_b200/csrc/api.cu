@@ -431,14 +431,14 @@ int hikf_update(int64_t m, int64_t n, const double* mean, const double* C, const
                 const double* val, double r, const double* z, double* mean_out, double* C_out, double* var_out,
                 double* HC_out, void* workspace, size_t workspace_bytes, double* min_var_out, void* stream) {
   return hikf_update_chained(m, n, mean, C, var, HC, CQ, dQ, HCQ, ip, ix, val, r, z, mean_out, C_out, var_out, HC_out,
-                             workspace, workspace_bytes, min_var_out, 0, stream);
+                             workspace, workspace_bytes, min_var_out, 0, nullptr, stream);
 }
 
 int hikf_update_chained(int64_t m, int64_t n, const double* mean, const double* C, const double* var,
                         const double* HC, const double* CQ, const double* dQ, const double* HCQ, const int32_t* ip,
                         const int32_t* ix, const double* val, double r, const double* z, double* mean_out,
                         double* C_out, double* var_out, double* HC_out, void* workspace, size_t workspace_bytes,
-                        double* min_var_out, int32_t chain, void* stream) {
+                        double* min_var_out, int32_t chain, double* mean_host, void* stream) {
   if (m < 1 || n < 1 || !mean || !C || !var || !HC || !ip || !z || !mean_out || !C_out || !var_out || !HC_out) {
     set_error("bad update arguments");
     return HIKF_BAD_ARGUMENT;
@@ -470,6 +470,7 @@ int hikf_update_chained(int64_t m, int64_t n, const double* mean, const double* 
   a.workspace_bytes = workspace_bytes;
   a.chain = (chain & 1) != 0;
   a.chain_in = (chain & 2) != 0;
+  a.mean_host = mean_host;
   UpdateResult res;
   int s = update(a, as_stream(stream), &res);
   if (min_var_out) *min_var_out = res.min_var;

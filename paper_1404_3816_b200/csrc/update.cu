@@ -601,6 +601,8 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
     HIKF_CHECK_LAUNCH();
     check_variance<<<1, 1, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
     HIKF_CHECK_LAUNCH();
+    if (a.mean_host)  // the caller's read-back, overlapping the side-stream tail
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(a.mean_host, a.mean_out, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
   }
 
   // ---- side (overlapping the GEMM): P = Li HC', R = HC' Li^T, HC_new = HC' - R P ----

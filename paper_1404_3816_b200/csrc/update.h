@@ -22,6 +22,7 @@ struct UpdateArgs {
   // next call; the GEMM epilogue then also writes that call's C' = C_out + C_Q into the workspace
   bool chain = false;     // produce the next call's C'
   bool chain_in = false;  // may consume the C' the previous call produced (pointers are checked too)
+  double* mean_host = nullptr;  // optional pinned host copy of mean_out, filled inside the call
 };
 
 struct UpdateResult {

@@ -289,14 +289,19 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
     if fused and _CHAIN and _CHAIN["state"]() is src and _CHAIN["pre"]() is pre:
         chain |= 2
     _CHAIN.clear()
+    # the host copy of the posterior mean (what run_hikf reads every step) is
+    # filled inside the call into pinned memory owned by the new state
+    mean_host = torch.empty((m,), dtype=torch.float64, pin_memory=True)
     _lib.check(_lib.load().hikf_update_chained(
         m, n, state.mean_t.data_ptr(), src.cross_cov_t.data_ptr(), src.variance_t.data_ptr(), src.HC_t.data_ptr(),
         _lib.ptr(pre.C_Q_t) if fused else None, _lib.ptr(pre.diag_Q_t) if fused else None,
         _lib.ptr(pre.HC_Q_t) if fused else None,
         Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), float(r_variance), zt.data_ptr(),
         mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None, chain,
-        _lib.stream_ptr()))
+        mean_host.data_ptr(), _lib.stream_ptr()))
     out = HikfState(mean, C, var, HC)
+    out._pinned = mean_host
+    out._host["mean"] = mean_host.numpy()
     if fused:
         _CHAIN.update(state=weakref.ref(out), pre=weakref.ref(pre))
     return out

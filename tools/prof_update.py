@@ -51,7 +51,7 @@ def step():
                                        HCQ.data_ptr() if fused else None, ip.data_ptr(), ix.data_ptr(),
                                        val.data_ptr(), 1e-3, z.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
                                        outs[2].data_ptr(), outs[3].data_ptr(), ws.data_ptr(), ws.numel(),
-                                       ctypes.byref(mv), 1 if fused else 0, _lib.stream_ptr()))
+                                       ctypes.byref(mv), 1 if fused else 0, None, _lib.stream_ptr()))
 
 
 if mode == "gemm":

@@ -329,7 +329,10 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) 
   constexpr int TN = BN / WN / 8;
   constexpr int A_IT = (BM * BK / 2) / THREADS;
   constexpr int B_IT = (BK * BN / 2) / THREADS;
-  static_assert(TN == 8, "swizzle assumes 4 chunks per thread row");
+  static_assert(TN == 8 || TN == 4, "B swizzle defined for TN = 4 or 8");
+  // 16-byte chunk swizzle of B rows, by the row's t4 = (k >> 2) & 3: the 8 lanes
+  // of a quarter-warp (gq in {0, 1}, t4 in 0..3) then hit 8 distinct bank groups
+  auto swz = [](int t) { return TN == 8 ? t : ((t & 1) | ((t >> 1) << 2)); };
   static_assert(A_IT >= 1 && B_IT >= 1 && A_IT <= 32 && B_IT <= 32, "copy split");
   extern __shared__ double smem[];
   __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) 
 #pragma unroll
       for (int it = 0; it < B_IT; ++it) {
         const int kr = kr0 + it * RB;
-        const uint32_t d = sb0 + so + (uint32_t)(it * RB * BS * 8) + (uint32_t)((ch0 ^ ((kr >> 2) & 3)) * 16);
+        const uint32_t d = sb0 + so + (uint32_t)(it * RB * BS * 8) + (uint32_t)((ch0 ^ swz((kr >> 2) & 3)) * 16);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gb + it * stepB));
       }
       return;
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) 
       const int kr = e / (BN / 2), ch = e % (BN / 2);
       int bytes = (b_ok >> it) & 1 ? ((b_half >> it) & 1 ? 8 : 16) : 0;
       if (!fullk && k0 + kr >= kend) bytes = 0;
-      cp_async16(Bs + kr * BS + 2 * (ch ^ ((kr >> 2) & 3)), bytes ? Bt + kr * g.sb_r + 2 * ch : B, bytes);
+      cp_async16(Bs + kr * BS + 2 * (ch ^ swz((kr >> 2) & 3)), bytes ? Bt + kr * g.sb_r + 2 * ch : B, bytes);
     }
   };
 
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) 
         double b[TN];
 #pragma unroll
         for (int jj = 0; jj < TN / 2; ++jj) {
-          const double2 v = *reinterpret_cast<const double2*>(Br + 2 * ((gq * (TN / 2) + jj) ^ t4));
+          const double2 v = *reinterpret_cast<const double2*>(Br + 2 * ((gq * (TN / 2) + jj) ^ swz(t4)));
           b[2 * jj] = v.x;
           b[2 * jj + 1] = v.y;
         }
@@ -580,6 +583,10 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
       return launch_variant3<64, 128, 2, 2, 3, 2>(g, batch, vec, part, st);
     case 22:  // LDS.128 kernel: 128x64x16, 4 warps of 32x64 stacked along rows, 3 stages
       return launch_variant3<128, 64, 4, 1, 3, 2>(g, batch, vec, part, st);
+    case 28:  // LDS.128 kernel: 128x64x16, 4 warps of 64x32 (cuBLAS's warp shape), 3 stages, 2 CTAs / SM
+      return launch_variant3<128, 64, 2, 2, 3, 2>(g, batch, vec, part, st);
+    case 29:  // LDS.128 kernel: 128x64x16, 4 warps of 64x32, 4 stages, 2 CTAs / SM
+      return launch_variant3<128, 64, 2, 2, 4, 2>(g, batch, vec, part, st);
     case 27:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 2 stages, 2 CTAs / SM
       return launch_variant3<64, 128, 2, 2, 2, 2>(g, batch, vec, part, st);
     default:  // 128x128x16, 8 warps of 64x32, 5 stages

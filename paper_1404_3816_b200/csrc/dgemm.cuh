@@ -58,7 +58,7 @@ void set_dgemm_variant(int v);
 // number of column tiles (= partial sums per row) the current variant uses for N columns
 inline int dgemm_col_tiles(int64_t N, int variant = -1) {
   int v = variant >= 0 ? variant : dgemm_variant();
-  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22) ? 64 : 128);
+  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22 || v == 28 || v == 29) ? 64 : 128);
 }
 // variant used by the update's K GEMM (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log);
 // HIKF_DGEMM_VARIANT overrides it

@@ -129,6 +129,14 @@ int hikf_tree_matmat_csrT(hikf_tree* tree, int64_t n, const int32_t* indptr_dev,
 int hikf_precompute(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
                     const double* data_dev, double* C_Q_dev, double* HC_Q_dev, double* diag_Q_dev, void* stream);
 
+/* ---- row-sharded precompute: the rows r0 <= i < r1 of C_Q
+ * (the upward pass and M2L are replicated; L2P / P2P produce only these
+ * rows), the partial H[:, r0:r1] C_Q_rows (n x n; the caller sums the
+ * partials over ranks and symmetrises: HC_Q = sym(sum)), and diag_Q rows. */
+int hikf_precompute_rows(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
+                         const double* data_dev, int64_t r0, int64_t r1, double* C_Q_rows_dev,
+                         double* HC_Q_partial_dev, double* diag_Q_rows_dev, void* stream);
+
 /* ---- hikf_precompute_dense (filters.py:108-115; Gram as kernels.py:97-117) ----
  * The reference's exact-algebra oracle path: C_Q = Q H^T with the dense Gram
  * Q[i][j] = K(|x_i - x_j|), here as a direct sum over the nonzeros of H^T (Q is

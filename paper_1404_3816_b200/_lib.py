@@ -87,6 +87,7 @@ SIGNATURES = {
     "hikf_spd_solve_workspace_bytes": (_SZ, [_I64, _I64]),
     "hikf_spd_solve": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _SZ, _P, _P]),
     "hikf_ray_operator": (ctypes.c_int, [_I64, _I64, _D, _D, _D, _D, _I64, _P, _P, _P, _P, _P, _P]),
+    "hikf_precompute_rows": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
     "hikf_precompute_dense": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "hikf_ray_operator_3d": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "hikf_ray_operator_3d_device": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _P, _P]),

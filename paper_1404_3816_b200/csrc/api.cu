@@ -349,6 +349,41 @@ int hikf_precompute(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   return HIKF_OK;
 }
 
+// H[:, r0:r1] C_Q_local (n x n), C_Q_local = rows r0..r1 of C_Q
+__global__ void spmm_cols_window(int64_t n, int64_t r0, int64_t r1, const int32_t* __restrict__ ip,
+                                 const int32_t* __restrict__ ix, const double* __restrict__ val,
+                                 const double* __restrict__ C, double* __restrict__ X) {
+  const int64_t r = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = ip[r]; e < ip[r + 1]; ++e) {
+      const int64_t c = ix[e];
+      if (c >= r0 && c < r1) s += val[e] * C[(c - r0) * n + j];
+    }
+    X[r * n + j] = s;
+  }
+}
+
+int hikf_precompute_rows(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, int64_t r0,
+                         int64_t r1, double* CQ_rows, double* HCQ_partial, double* dQ_rows, void* stream) {
+  if (!t || n < 0 || r0 < 0 || r1 < r0 || r1 > t->m) {
+    set_error("bad precompute_rows arguments (need 0 <= r0 <= r1 <= m)");
+    return HIKF_BAD_ARGUMENT;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (r1 > r0) HIKF_TRY(fmm_matmat_csrT(t, n, ip, ix, val, CQ_rows, st, r0, r1));
+  if (n > 0) {
+    spmm_cols_window<<<(unsigned)n, kT, 0, st>>>(n, r0, r1, ip, ix, val, CQ_rows, HCQ_partial);
+    HIKF_CHECK_LAUNCH();
+  }
+  double k0 = t->spec.family == HIKF_LOGARITHM ? 0.0 : t->spec.variance;
+  if (r1 > r0) {
+    fill<<<grid_for(r1 - r0), kT, 0, st>>>(dQ_rows, r1 - r0, k0);
+    HIKF_CHECK_LAUNCH();
+  }
+  return HIKF_OK;
+}
+
 int hikf_precompute_dense(const double* xy_host, int64_t m, const hikf_kernel* kernel, int64_t n, const int32_t* ip,
                           const int32_t* ix, const double* val, double* CQ, double* HCQ, double* dQ, void* stream) {
   if (!xy_host || !kernel || m < 1 || n < 0) {

@@ -54,6 +54,7 @@ struct BoxArgs {
   const double* Lleaf;
   double* U;
   int64_t ldu;
+  int64_t r0, r1;  // L2P row window: only original rows in [r0, r1) are written, at U + (row - r0) ldu
   unsigned long long* flops;
 };
 
@@ -153,7 +154,9 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
         for (int i = 0; i < NRT; ++i) {
           const int r = (r0 + i) * 8 + gq;
           if (r0 + i >= nrt || r >= R) continue;
-          double* urow = g.U + g.order[g.leaf_start[task] + row_off + r] * g.ldu;
+          const int64_t orow = g.order[g.leaf_start[task] + row_off + r];
+          if (orow < g.r0 || orow >= g.r1) continue;
+          double* urow = g.U + (orow - g.r0) * g.ldu;
 #pragma unroll
           for (int h = 0; h < 2; ++h)
             if (jc + h < g.n) urow[jc + h] = acc[i][h];
@@ -225,9 +228,12 @@ int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int6
   return launch_box(a, 4 * a.q, dim3((unsigned)blocks), st);
 }
 
-int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st) {
+int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st,
+              int64_t r0, int64_t r1) {
   if (t->n_leaves == 0 || n == 0) return HIKF_OK;
   BoxArgs a{};
+  a.r0 = r0;
+  a.r1 = r1 < 0 ? INT64_MAX : r1;
   a.mode = 1;
   a.n = n;
   a.K = t->orders[t->depth] * t->orders[t->depth];

@@ -12,6 +12,8 @@ int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int6
 // whether the warp-streaming kernel handles R rows x K inner (K <= 64, A fits in smem)
 bool box_supported(int rows, int K);
 // U[order[p]][j] = sum_a W2[p][a] L_leaf[a][j] (store)
-int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st);
+// U = W2 L_leaf; with a row window only original rows r0 <= row < r1 are written, to U + (row - r0) ldu
+int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st,
+              int64_t r0 = 0, int64_t r1 = -1);
 
 }  // namespace hikf

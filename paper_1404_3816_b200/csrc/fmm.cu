@@ -473,8 +473,10 @@ int qht_streams(QhtStreams** out) {
 }  // namespace
 
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
-                    cudaStream_t st) {
+                    cudaStream_t st, int64_t r0, int64_t r1) {
   if (n <= 0) return HIKF_OK;
+  const bool window = r0 != 0 || (r1 >= 0 && r1 != t->m);
+  if (r1 < 0) r1 = t->m;
   const int D = t->depth;
   SparseHt sp;
   {
@@ -482,11 +484,11 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     HIKF_TRY(sparse_build(t, n, ip, ix, val, &sp, st));
   }
   if (D < 2) {
-    HIKF_CHECK_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * t->m * n, st));
+    HIKF_CHECK_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * (r1 - r0) * n, st));
     int status;
     {
       ProfScope ps(ST_P2P, st);
-      status = sparse_p2p(t, sp, U, n, st);
+      status = sparse_p2p(t, sp, U, n, st, nullptr, r0, r1);
     }
     sparse_free(&sp, st);
     return status;
@@ -571,7 +573,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
-    status = l2p_boxes(t, Lcur, n, U, n, st);
+    status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
+  } else if (status == HIKF_OK && window) {
+    set_error("row-windowed Q H^T needs the box-streaming L2P (leaf order <= 8)");
+    status = HIKF_BAD_ARGUMENT;
   } else if (status == HIKF_OK) {
     L2PProv<false> lp;
     set_base(lp, t, n, 0, 0, vec);
@@ -592,7 +597,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_p2p, 0));
   if (status == HIKF_OK) {
     ProfScope ps(ST_P2P, st);
-    status = sparse_p2p_scatter(t, sp, Pnear, U, n, st);
+    status = sparse_p2p_scatter(t, sp, Pnear, U, n, st, r0, r1);
   }
   for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
   for (int l = 2; l <= D; ++l) cudaFreeAsync(scratch[l], st);

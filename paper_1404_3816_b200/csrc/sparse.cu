@@ -158,7 +158,8 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
                            const int32_t* __restrict__ g_start, const int32_t* __restrict__ e_sp,
                            const double* __restrict__ e_v, const double* __restrict__ xy_s,
                            const int64_t* __restrict__ order, double* __restrict__ U, int64_t ldu,
-                           double* __restrict__ Pnear, int32_t maxc, unsigned long long* __restrict__ flops) {
+                           double* __restrict__ Pnear, int32_t maxc, int64_t r0, int64_t r1,
+                           unsigned long long* __restrict__ flops) {
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (item >= nitems) return;
@@ -210,8 +211,10 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
     if (!ok) continue;
     if (Pnear)
       Pnear[(int64_t)t * nitems + item] = acc;  // added into U later (p2p_scatter): U = far + near either way
-    else
-      U[order[t0 + t] * ldu + j] += acc;
+    else {
+      const int64_t row = order[t0 + t];
+      if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += acc;
+    }
   }
 }
 
@@ -222,14 +225,17 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
 __global__ void p2p_scatter(int64_t nitems, const int64_t* __restrict__ items, int64_t n,
                             const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_count,
                             const int64_t* __restrict__ order, const double* __restrict__ Pnear, int32_t maxc,
-                            double* __restrict__ U, int64_t ldu) {
+                            double* __restrict__ U, int64_t ldu, int64_t r0, int64_t r1) {
   const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (item >= nitems) return;
   const int64_t key = items[item];
   const int32_t T = (int32_t)(key / n);
   const int32_t j = (int32_t)(key % n);
   const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
-  for (int t = 0; t < cnt; ++t) U[order[t0 + t] * ldu + j] += Pnear[(int64_t)t * nitems + item];
+  for (int t = 0; t < cnt; ++t) {
+    const int64_t row = order[t0 + t];
+    if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += Pnear[(int64_t)t * nitems + item];
+  }
 }
 }  // namespace
 
@@ -391,22 +397,25 @@ int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, 
   return HIKF_OK;
 }
 
-int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st, double* Pnear) {
+int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st, double* Pnear,
+               int64_t r0, int64_t r1) {
   if (s.nitems <= 0) return HIKF_OK;
   const int64_t threads = s.nitems * 32;
   p2p_sparse<<<(unsigned)((threads + kT - 1) / kT), kT, 0, st>>>(
       s.nitems, s.items, s.n, t->G, t->kp, t->leaf_box, t->leaf_start, t->leaf_count, t->box2leaf, s.leaf_g, s.g_j,
-      s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, Pnear, (int32_t)t->max_count, prof_flops_ptr(ST_P2P));
+      s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, Pnear, (int32_t)t->max_count, r0,
+      r1 < 0 ? INT64_MAX : r1, prof_flops_ptr(ST_P2P));
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
 
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
-                       cudaStream_t st) {
+                       cudaStream_t st, int64_t r0, int64_t r1) {
   if (s.nitems <= 0) return HIKF_OK;
   p2p_scatter<<<(unsigned)((s.nitems + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
                                                                  t->leaf_count, t->order, Pnear,
-                                                                 (int32_t)t->max_count, U, ldu);
+                                                                 (int32_t)t->max_count, U, ldu, r0,
+                                                                 r1 < 0 ? INT64_MAX : r1);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }

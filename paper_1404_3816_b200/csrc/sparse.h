@@ -35,10 +35,11 @@ void sparse_free(SparseHt* s, cudaStream_t st);
 int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, int64_t c0, cudaStream_t st);
 // near field of the (target leaf, ray) items: U += near sum, or, with Pnear
 // (nitems x max_count), the sums are parked there and added by sparse_p2p_scatter
+// (row window as l2p_boxes: only original rows r0 <= row < r1, at U + (row - r0) ldu)
 int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st,
-               double* Pnear = nullptr);
+               double* Pnear = nullptr, int64_t r0 = 0, int64_t r1 = -1);
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
-                       cudaStream_t st);
+                       cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1);
 
 // leaf multipoles of the active (leaf, ray) pairs (sparse P2M)
 int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st);

@@ -83,7 +83,8 @@ int tree_export_m2l_pairs(const hikf_tree* t, int lev, int dx, int dy, std::vect
 // U = tree @ V (dense V, m x k), fmm.py:325-367
 int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U, int64_t ldu, cudaStream_t stream);
 // U (m x n) = tree @ H^T for a device CSR H (n x m), H^T kept sparse
+// U = Q H^T; with a row window only original rows r0 <= row < r1 are produced, at U + (row - r0) n
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
-                    cudaStream_t stream);
+                    cudaStream_t stream, int64_t r0 = 0, int64_t r1 = -1);
 
 }  // namespace hikf

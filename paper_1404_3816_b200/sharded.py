@@ -71,6 +71,33 @@ class ShardedHikf:
         return new_state
 
 
+def precompute_rows(tree, H, r0: int, r1: int, comm=None):
+    """This rank's share of hikf_precompute_fmm: the C_Q rows
+    [r0, r1) (hikf_precompute_rows: upward pass and M2L replicated, L2P / P2P
+    for the owned rows only), diag_Q rows, and HC_Q = sym(sum over ranks of
+    H[:, r0:r1] C_Q_rows) -- one n x n all-reduce (8 MB at n = 1024), or the
+    local partial alone when comm is None."""
+    import torch
+
+    from . import _lib
+    from .filters import DeviceCSR, _dev
+    Hd = DeviceCSR.of(H)
+    n = Hd.shape[0]
+    if not 0 <= r0 <= r1 <= tree.m:
+        raise ValueError(f"row block [{r0}, {r1}) outside [0, {tree.m}]")
+    dev = _dev()
+    CQ = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
+    X = torch.empty((n, n), dtype=torch.float64, device=dev)
+    dQ = torch.empty((r1 - r0,), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().hikf_precompute_rows(tree._handle, n, Hd.indptr.data_ptr(), Hd.indices.data_ptr(),
+                                                Hd.data.data_ptr(), int(r0), int(r1), CQ.data_ptr(), X.data_ptr(),
+                                                dQ.data_ptr(), _lib.stream_ptr()))
+    if comm is not None:
+        X = comm.allreduce_sum(X)
+        X = 0.5 * (X + X.T)
+    return CQ, X, dQ
+
+
 class TorchComm:
     """all-reduce helpers over a torch.distributed process group (NCCL or gloo)."""
 

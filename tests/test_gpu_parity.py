@@ -388,3 +388,27 @@ def test_chained_predict_is_bit_identical(pkg):
     a = flt.hikf_update(flt.hikf_predict(s1, pre), H, cfg["R"], g["obs"][1])
     b = flt.hikf_update(flt.hikf_predict(s1, pre), H, cfg["R"], g["obs"][1])
     assert torch.equal(a.cross_cov_t, b.cross_cov_t) and torch.equal(a.mean_t, b.mean_t)
+
+
+def test_row_sharded_precompute_equals_full(pkg):
+    """hikf_precompute_rows: the C_Q rows of each of 3 row blocks
+    are bit-identical to the matching rows of the full precompute, and the sum
+    of the H[:, rows] C_Q_rows partials reproduces HC_Q."""
+    import torch
+    from paper_1404_3816_b200.sharded import precompute_rows, row_block
+    g = _load("cfg1.npz")
+    cfg = cases.CFG1
+    tree, H, pre, _ = _run_filter(pkg, dict(cfg, T=1), g["obs"])
+    m = H.shape[1]
+    parts, X = [], None
+    for r in range(3):
+        r0, r1 = row_block(m, 3, r)
+        CQ, Xp, dQ = precompute_rows(tree, H, r0, r1)
+        assert torch.equal(CQ, pre.C_Q_t[r0:r1]), r
+        assert torch.equal(dQ, pre.diag_Q_t[r0:r1])
+        parts.append(CQ)
+        X = Xp if X is None else X + Xp
+    HCQ = (0.5 * (X + X.T)).cpu().numpy()
+    assert O.rel_fro(HCQ, pre.HC_Q) <= 1e-14
+    with pytest.raises(ValueError):
+        precompute_rows(tree, H, 5, 3)

@@ -347,6 +347,93 @@ def run_reference(args, cfg, rank):
 # GPU leg
 # ---------------------------------------------------------------------------
 
+def run_sharded(args, cfg, P, torch, dist, world, rank, local):
+    """--mode sharded (SURVEY 8(e)): rank r owns the state rows row_block(m, world, r);
+    Q H^T rows via hikf_precompute_rows (+ one n x n all-reduce), then per step one
+    all-reduce of the n-vector H mean and one of the (min, max) variance pair."""
+    from paper_1404_3816_b200 import sharded as SH
+    if cfg.get("dim", 2) != 2:
+        raise SystemExit("--mode sharded supports the 2D configs")
+    N = cfg["N"]
+    grid = P.Grid2D(N, N, 1.0 / N, 1.0 / N)
+    H = P.tomography.build_ray_operator(grid, P.tomography.default_acquisition(grid, cfg["ns"], cfg["nr"], 0.0, 1.0))
+    m, n = grid.m, H.shape[0]
+    obs = plume_observations(H, grid.cell_centers().coords, cfg["T"], cfg["R"])
+    kern = P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    dev = torch.device("cuda", local)
+    comm = SH.TorchComm(device=dev) if world > 1 else SH.LocalComm()
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    r0, r1 = SH.row_block(m, world, rank)
+    tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    SH.precompute_rows(tree, H, r0, r1, comm)  # warm-up
+    barrier_sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    CQ, HCQ, dQ = SH.precompute_rows(tree, H, r0, r1, comm)
+    e1.record()
+    barrier_sync()
+    t_qht = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    step = SH.CudaRowStep((CQ, HCQ, dQ), n)
+    sh = SH.ShardedHikf(comm, step, H, m, rank, world)
+    zeros = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)  # noqa: E731
+    st = {"mean": zeros(r1 - r0), "C": zeros((r1 - r0, n)), "var": zeros(r1 - r0), "HC": zeros((n, n))}
+    Zd = torch.from_numpy(obs).to(dev)
+    for t in range(args.warmup):
+        st = sh.update(st, cfg["R"], Zd[t % cfg["T"]])
+    l0 = P._lib.load().hikf_launch_count()
+    barrier_sync()
+    with ClockSampler(local) as clk:
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for t in range(args.steps):
+            st = sh.update(st, cfg["R"], Zd[(args.warmup + t) % cfg["T"]])
+        s1.record()
+        barrier_sync()
+    launches = int(P._lib.load().hikf_launch_count() - l0)
+    t_loop = max_over_ranks(s0.elapsed_time(s1) / 1e3)
+    # e2e: host z up, this rank's mean rows down, every step
+    barrier_sync()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for t in range(args.steps):
+        st = sh.update(st, cfg["R"], obs[(args.warmup + t) % cfg["T"]])
+        st["mean"].cpu().numpy()
+    c1.record()
+    barrier_sync()
+    t_e2e = max_over_ranks(c0.elapsed_time(c1) / 1e3)
+    if rank == 0:
+        line = {
+            "metric": "hikf_assimilation_steps_per_sec", "value": args.steps / t_loop, "unit": "steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * t_loop / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: seeded crosswell rays + moving Gaussian plume, PCG64 noise (cfg recipe, SURVEY 8(d))",
+            "config": {"workload": cfg["desc"], "parallelism": f"row-sharded x{world} (one n-vector all-reduce "
+                                                               "per step)", "rows_per_rank": r1 - r0},
+            "qht": {"ms": 1000.0 * t_qht, "value": m * n / t_qht, "unit": "(m*n)/s",
+                    "note": "row-sharded precompute: upward pass + M2L replicated, L2P/P2P for owned rows"},
+            "e2e": {"value": args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * (r1 - r0), "api": "sharded.ShardedHikf.update (numpy z) + mean rows"},
+            "gpu_launches": launches, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -356,6 +443,9 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-rows", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+                    help="replicas: every rank runs the whole filter (weak scaling); sharded: the state rows are "
+                         "split across ranks with one n-vector all-reduce per step (strong scaling, 2D configs)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -377,6 +467,9 @@ def main():
     from paper_1404_3816_b200 import _lib
     lib = _lib.load()
     flt = P.filters
+    if args.mode == "sharded":
+        run_sharded(args, cfg, P, torch, dist, world, rank, local)
+        return
 
     N = cfg["N"]
     dim3 = cfg.get("dim", 2) == 3

@@ -203,7 +203,8 @@ int hikf_update_rows(int64_t m_local, int64_t n, const double* mean_dev, const d
                      const double* HC_dev, const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev,
                      const double* Hmean_dev, double r_variance, const double* z_dev, double* mean_out,
                      double* C_out, double* var_out, double* HC_out, void* workspace, size_t workspace_bytes,
-                     double* minmax_out, void* stream);
+                     double* minmax_out, int32_t chain, void* stream);
+/* (chain: the produce / consume flags of hikf_update_chained, for this rank's rows) */
 /* y (n) = H x for a CSR H (n x cols) on the device. */
 int hikf_csr_spmv(int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev,
                   const double* x_dev, double* y_dev, void* stream);

@@ -515,7 +515,7 @@ int hikf_update_chained(int64_t m, int64_t n, const double* mean, const double* 
 int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const double* C, const double* var,
                      const double* HC, const double* CQ, const double* dQ, const double* HCQ, const double* Hmean,
                      double r, const double* z, double* mean_out, double* C_out, double* var_out, double* HC_out,
-                     void* workspace, size_t workspace_bytes, double* minmax_out, void* stream) {
+                     void* workspace, size_t workspace_bytes, double* minmax_out, int32_t chain, void* stream) {
   if (m_local < 1 || n < 1 || !mean || !C || !var || !HC || !Hmean || !z || !mean_out || !C_out || !var_out ||
       !HC_out) {
     set_error("bad update_rows arguments");
@@ -537,6 +537,8 @@ int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const doubl
   a.HCQ = HCQ;
   a.Hmean = Hmean;
   a.no_check = true;
+  a.chain = (chain & 1) != 0;
+  a.chain_in = (chain & 2) != 0;
   a.r = r;
   a.z = z;
   a.mean_out = mean_out;

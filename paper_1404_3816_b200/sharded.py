@@ -98,6 +98,16 @@ def precompute_rows(tree, H, r0: int, r1: int, comm=None):
     return CQ, X, dQ
 
 
+class LocalComm:
+    """world = 1 stand-in for TorchComm (identity reductions)."""
+
+    def allreduce_sum(self, x):
+        return x
+
+    def allreduce_max(self, x):
+        return x
+
+
 class TorchComm:
     """all-reduce helpers over a torch.distributed process group (NCCL or gloo)."""
 
@@ -132,6 +142,7 @@ class CudaRowStep:
         self.CQ, self.HCQ, self.dQ = pre_rows
         self.n = n
         self._ws = None
+        self._last = None
 
     def prepare_h(self, H_local):
         from .filters import DeviceCSR
@@ -159,9 +170,14 @@ class CudaRowStep:
         zt = zt.to(state["C"].device)
         out = {k: torch.empty_like(v) for k, v in state.items()}
         mm = (ctypes.c_double * 2)()
+        # chained predict (hikf_update_chained flags): always produce the next C';
+        # consume only when `state` is exactly the dict this step returned last time
+        chain = 1 | (2 if state is self._last else 0)
         _lib.check(lib.hikf_update_rows(
             m, n, state["mean"].data_ptr(), state["C"].data_ptr(), state["var"].data_ptr(), state["HC"].data_ptr(),
             self.CQ.data_ptr(), self.dQ.data_ptr(), self.HCQ.data_ptr(), Hmean.data_ptr(), float(r), zt.data_ptr(),
             out["mean"].data_ptr(), out["C"].data_ptr(), out["var"].data_ptr(), out["HC"].data_ptr(),
-            ws.data_ptr(), ws.numel(), mm, _lib.stream_ptr()))
+            ws.data_ptr(), ws.numel(), mm, chain, _lib.stream_ptr()))
+        self._last = out  # held, so its buffers cannot be recycled under the chained C'
+
         return out, (mm[0], mm[1])

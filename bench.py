@@ -393,7 +393,10 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
     Zd = torch.from_numpy(obs).to(dev)
     for t in range(args.warmup):
         st = sh.update(st, cfg["R"], Zd[t % cfg["T"]])
-    l0 = P._lib.load().hikf_launch_count()
+    lib = P._lib.load()
+    l0 = lib.hikf_launch_count()
+    lib.hikf_prof_reset()
+    lib.hikf_prof_enable(1)
     barrier_sync()
     with ClockSampler(local) as clk:
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -402,8 +405,11 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
             st = sh.update(st, cfg["R"], Zd[(args.warmup + t) % cfg["T"]])
         s1.record()
         barrier_sync()
-    launches = int(P._lib.load().hikf_launch_count() - l0)
+    lib.hikf_prof_enable(0)
+    launches = int(lib.hikf_launch_count() - l0)
     t_loop = max_over_ranks(s0.elapsed_time(s1) / 1e3)
+    ms_c, n_c = P._lib.prof_read("gemm_c")
+    achieved = max_over_ranks(2.0 * (r1 - r0) * n * n / (ms_c / max(n_c, 1) / 1e3) / 1e12) if n_c else None
     # e2e: host z up, this rank's mean rows down, every step
     barrier_sync()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -427,6 +433,11 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
                     "note": "row-sharded precompute: upward pass + M2L replicated, L2P/P2P for owned rows"},
             "e2e": {"value": args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * (r1 - r0), "api": "sharded.ShardedHikf.update (numpy z) + mean rows"},
+            "roofline": {"kernel": "dgemm_kernel (K = C' S^-1 on this rank's rows, fused epilogue; "
+                                   "2 (m/N) n^2 flops per launch)", "bound": "fp64", "achieved": achieved,
+                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": None,
+                         "peak_source": FP64_PEAK_SOURCE},
             "gpu_launches": launches, "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -443,9 +454,10 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-rows", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "sharded"],
+    ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
                     help="replicas: every rank runs the whole filter (weak scaling); sharded: the state rows are "
-                         "split across ranks with one n-vector all-reduce per step (strong scaling, 2D configs)")
+                         "split across ranks with one n-vector all-reduce per step (strong scaling, 2D configs); "
+                         "auto: replicas at N = 1 (the full report), sharded at N > 1 for 2D configs")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
 
@@ -467,7 +479,10 @@ def main():
     from paper_1404_3816_b200 import _lib
     lib = _lib.load()
     flt = P.filters
-    if args.mode == "sharded":
+    mode = args.mode
+    if mode == "auto":
+        mode = "sharded" if world > 1 and cfg.get("dim", 2) == 2 else "replicas"
+    if mode == "sharded":
         run_sharded(args, cfg, P, torch, dist, world, rank, local)
         return
 

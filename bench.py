@@ -471,9 +471,16 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # one process per GPU; HIKF_BENCH_BACKEND=gloo with more ranks than GPUs is a
+    # functional check of the multi-rank path only (timings meaningless)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HIKF_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_1404_3816_b200 as P
     from paper_1404_3816_b200 import _lib

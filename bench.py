@@ -68,10 +68,10 @@ def cfg_m(cfg):
 # DMMA/DFMA issue-rate microbenchmark gives 37.0, profiles/r01_fp64_micro.json).
 FP64_PEAK_TFLOPS = 35.46
 FP64_PEAK_SOURCE = "measured cuBLAS DGEMM 8192^3 on B200 (profiles/r01_fp64_dgemm.json); not in MEASURED_PEAKS.json"
-# DRAM traffic of one C-GEMM launch at cfg4 from `ncu --set full` (dram__bytes_read.sum +
-# dram__bytes_write.sum, profiles/r01_ncu_sparse_summary.txt: 17.2 + 8.56 GB); the algorithmic
-# bytes are Y + C' in, C out = 3 x 8 m n = 25.8 GB (P stays in L2).
-C_GEMM_TRAFFIC_CFG4 = 17.65e9 + 17.28e9  # ncu dram read + write of the chained K GEMM (profiles/r01_ncu_kgemm_chain_summary.txt)
+# DRAM traffic of one chained K-GEMM launch at cfg4 from `ncu --set full` (dram__bytes_read.sum +
+# dram__bytes_write.sum); the algorithmic bytes are C' and C_Q in, C_new and the next C' out
+# = 4 x 8 m n = 34.4 GB (S^-1 stays in L2).
+C_GEMM_TRAFFIC_CFG4 = 17.74e9 + 17.37e9  # ncu dram read + write of the chained K GEMM (profiles/r01_ncu_kgemm_cutlass_summary.txt)
 
 
 def hbm_peak():
@@ -433,7 +433,7 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
                     "note": "row-sharded precompute: upward pass + M2L replicated, L2P/P2P for owned rows"},
             "e2e": {"value": args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * (r1 - r0), "api": "sharded.ShardedHikf.update (numpy z) + mean rows"},
-            "roofline": {"kernel": "dgemm_kernel (K = C' S^-1 on this rank's rows, fused epilogue; "
+            "roofline": {"kernel": "dgemm_cutlass_kernel (K = C' S^-1 on this rank's rows, fused epilogue; "
                                    "2 (m/N) n^2 flops per launch)", "bound": "fp64", "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": None,
@@ -657,7 +657,7 @@ def main():
                                      "multiplied); dense-formulation equivalent rate = "
                                      f"{qht_flops / t_qht / 1e12:.1f} TFLOP/s",
                              "m2l": {"achieved": fmm_useful["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
-        "roofline": {"kernel": "dgemm_kernel (K = C' S^-1 -> C_new = r K, fused rowsum(K o C'), K innov and the "
+        "roofline": {"kernel": "dgemm_cutlass_kernel (K = C' S^-1 -> C_new = r K, fused rowsum(K o C'), K innov and the "
                                "next step's C' = C_new + C_Q; 2 m n^2 flops per launch)", "bound": "fp64",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS,

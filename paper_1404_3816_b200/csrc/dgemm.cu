@@ -6,6 +6,13 @@
 
 #include "dgemm.cuh"
 
+// CUTLASS 2.x SM80 FP64 tensor-op threadblock mainloop (headers only; the
+// tree vendored with flashinfer, see Makefile CUTLASS_INC).  Used as the
+// mainloop of the K-GEMM variant below; the epilogue is ours.
+#include "cutlass/gemm/gemm.h"
+#include "cutlass/gemm/threadblock/default_mma.h"
+#include "cutlass/layout/matrix.h"
+
 namespace hikf {
 
 namespace {
@@ -527,6 +534,80 @@ int launch_variant3(const GemmArgs& g, int batch, bool vec, bool part, cudaStrea
               : launch_three<BM, BN, WM, WN, STAGES, MINB, false, BK>(g, batch, st);
 }
 
+// ---------------------------------------------------------------------------
+// Variant 30: CUTLASS multistage DMMA mainloop (cp.async ring, conflict-free
+// 64-bit smem layouts, serpentine warp MMA order) + the fused epilogue above.
+// profiles/r01_cutlass_probe.log: the plain CUTLASS 64x128x16 / 32x64 / 3-stage
+// GEMM runs the cfg4 K-GEMM shape in 61.3 ms (cuBLAS 61.6 ms, our v7 66.5 ms).
+template <int BM, int BN, int WTM, int WTN, int STAGES>
+struct CutlassMain {
+  using RM = cutlass::layout::RowMajor;
+  using DefaultMma = cutlass::gemm::threadblock::DefaultMma<
+      double, RM, 1, double, RM, 1, double, RM, cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80,
+      cutlass::gemm::GemmShape<BM, BN, 16>, cutlass::gemm::GemmShape<WTM, WTN, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+      STAGES, cutlass::arch::OpMultiplyAdd>;
+  using Mma = typename DefaultMma::ThreadblockMma;
+  static constexpr int WM = BM / WTM, WN = BN / WTN, THREADS = WM * WN * 32;
+};
+
+template <int BM, int BN, int WTM, int WTN, int STAGES, bool PARTIALS>
+__global__ void __launch_bounds__(CutlassMain<BM, BN, WTM, WTN, STAGES>::THREADS, 2)
+    dgemm_cutlass_kernel(GemmArgs g, typename CutlassMain<BM, BN, WTM, WTN, STAGES>::Mma::IteratorA::Params pA,
+                         typename CutlassMain<BM, BN, WTM, WTN, STAGES>::Mma::IteratorB::Params pB) {
+  using CM = CutlassMain<BM, BN, WTM, WTN, STAGES>;
+  using Mma = typename CM::Mma;
+  constexpr int WM = CM::WM, WN = CM::WN;
+  constexpr int TM = WTM / 8, TN = WTN / 8;
+  extern __shared__ __align__(16) char smem_raw[];
+  auto& ss = *reinterpret_cast<typename Mma::SharedStorage*>(smem_raw);
+  __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
+  __shared__ double red_dot[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
+
+  const int64_t n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  typename Mma::IteratorA itA(pA, const_cast<double*>(g.A), {(int)g.M, (int)g.K}, tid, {(int)m0, 0});
+  typename Mma::IteratorB itB(pB, const_cast<double*>(g.B), {(int)g.K, (int)g.N}, tid, {0, (int)n0});
+  Mma mma(ss, tid, warp, lane);
+  typename Mma::FragmentC accum;
+  accum.clear();
+  mma((int)((g.K + 15) / 16), accum, itA, itB, accum);
+
+  // CUTLASS warp tile (mma_tensor_op.h, accumulators column-major over the
+  // 8x8 instruction tiles): tile (i, j) -> accum[2 (i + j TM) + h] holds
+  // C[wm WTM + 8 i + gq][wn WTN + 8 j + 2 t4 + h]; warps are m-fastest.
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) acc[i][j][h] = accum[2 * (i + j * TM) + h];
+  const int wm = warp % WM, wn = warp / WM;
+  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, g.C, g.Cin, m0, n0, tid, wm, wn, lane >> 2, lane & 3, red_sq,
+                                          red_dot);
+}
+
+template <int BM, int BN, int WTM, int WTN, int STAGES, bool P>
+int launch_cutlass(const GemmArgs& g, cudaStream_t st) {
+  using CM = CutlassMain<BM, BN, WTM, WTN, STAGES>;
+  using Mma = typename CM::Mma;
+  constexpr size_t smem = sizeof(typename Mma::SharedStorage);
+  auto kern = dgemm_cutlass_kernel<BM, BN, WTM, WTN, STAGES, P>;
+  static bool configured = false;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  typename Mma::IteratorA::Params pA(cutlass::layout::RowMajor((int)g.sa_r));
+  typename Mma::IteratorB::Params pB(cutlass::layout::RowMajor((int)g.sb_r));
+  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), 1u);
+  kern<<<grid, CM::THREADS, smem, st>>>(g, pA, pB);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
 int g_variant = -1;
 
 }  // namespace
@@ -534,22 +615,30 @@ int g_variant = -1;
 int dgemm_variant() {
   if (g_variant < 0) {
     const char* e = getenv("HIKF_DGEMM_VARIANT");
-    g_variant = e ? atoi(e) : 7;  // default: 64x128x16, 3 stages, 2 CTAs per SM (profiles/r01_gemm_sweep*.log)
+    g_variant = e ? atoi(e) : 30;  // default: CUTLASS mainloop 64x128x16, 4 warps of 32x64, 3 stages (profiles/r01_gemm_sweep_cutlass.log)
   }
   return g_variant;
 }
 
 void set_dgemm_variant(int v) { g_variant = v; }
 
-int update_variant_c() { return getenv("HIKF_DGEMM_VARIANT") ? dgemm_variant() : 7; }
+int update_variant_c() { return getenv("HIKF_DGEMM_VARIANT") ? dgemm_variant() : 30; }
 
 int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || batch <= 0) return HIKF_OK;
-  const int variant = g.variant >= 0 ? g.variant : dgemm_variant();
+  int variant = g.variant >= 0 ? g.variant : dgemm_variant();
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
   bool vec = g.sa_c == 1 && g.sb_c == 1 && (g.sa_r % 2 == 0) && (g.sb_r % 2 == 0) && al16(g.A) && al16(g.B) &&
              (batch == 1 || (g.bsA % 2 == 0 && g.bsB % 2 == 0));
   bool part = g.psq != nullptr;
+  // CUTLASS-mainloop variants: row-major operands, full K range, one batch
+  const bool cutlass_ok = g.sa_c == 1 && g.sb_c == 1 && g.kmode == KFULL && batch == 1 && g.M < (1ll << 31) &&
+                          g.K < (1ll << 31) && g.N < (1ll << 31);
+  if (variant == 30 && cutlass_ok)  // 64x128x16, 4 warps of 32x64, 3 stages
+    return part ? launch_cutlass<64, 128, 32, 64, 3, true>(g, st) : launch_cutlass<64, 128, 32, 64, 3, false>(g, st);
+  if (variant == 31 && cutlass_ok)  // 64x128x16, 4 warps of 32x64, 4 stages
+    return part ? launch_cutlass<64, 128, 32, 64, 4, true>(g, st) : launch_cutlass<64, 128, 32, 64, 4, false>(g, st);
+  if (variant >= 30) variant = 7;
   switch (variant) {
     case 1:  // 128x128x32, 8 warps of 64x32, 3 stages
       return launch_variant<128, 128, 32, 2, 4, 3, 1>(g, batch, vec, part, st);

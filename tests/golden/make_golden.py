@@ -3,7 +3,7 @@
 Run in the build container only (the reference lives at /root/reference and
 does not travel to the GPU box):
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--big | --dense]
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [--big | --dense | --proxy]
 
 Every fixture is produced by the reference ``hikf`` package's own public API
 (build_tree / FmmTree.matmat / hikf_precompute_fmm / hikf_init /
@@ -186,7 +186,55 @@ def _log_scenario(cfg: dict):
     return grid, H, kern, model, record
 
 
+CFG4_PROXY = dict(name="cfg4_proxy", N=512, ns=32, nr=32, family="exponential", L=0.25, R=1e-3, T=3, order=6, leaf=64,
+                  seed=0)
+
+
+def cfg4_proxy() -> dict:
+    """SURVEY 8(d) cfg4-proxy (m = 262,144, n = 1024, order 6, depth 6): the
+    largest BASELINE-shaped case the reference runs in this container's RAM.
+    Full reference precompute + 3 filter steps; stored on a row sample
+    (every 64th state row) and 8 of the 1024 columns to keep the fixture small."""
+    cfg = CFG4_PROXY
+    grid, H, kern, model, record = scenario(cfg)
+    t0 = time.perf_counter()
+    tree = build_tree(grid.cell_centers(), kern, FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    t_tree = time.perf_counter() - t0
+    out = {f"tree_{k}": v for k, v in tree_ints(tree).items()}
+    t0 = time.perf_counter()
+    pre = flt.hikf_precompute_fmm(model, tree)
+    t_pre = time.perf_counter() - t0
+    state = flt.hikf_init(model)
+    t0 = time.perf_counter()
+    for t in range(cfg["T"]):
+        state = flt.hikf_update(flt.hikf_predict(state, pre), H, model.r_variance, record.observations[t])
+    t_on = time.perf_counter() - t0
+    rows = np.arange(0, grid.m, 64)
+    cols = np.arange(0, H.shape[0], H.shape[0] // 8)
+    out.update({
+        "H_nnz": np.int64(H.nnz),
+        "H_pattern_sha": np.bytes_(sha(H.indptr.astype(np.int64), H.indices.astype(np.int64))),
+        "H_data_sha": np.bytes_(sha(H.data)),
+        "obs": record.observations[:cfg["T"]], "rows": rows, "cols": cols,
+        "C_Q_sample": pre.C_Q[np.ix_(rows, cols)], "C_Q_fro": np.float64(np.linalg.norm(pre.C_Q)),
+        "C_Q_colsum": pre.C_Q.sum(axis=0),
+        "HC_Q_block": pre.HC_Q[:64, :64], "HC_Q_fro": np.float64(np.linalg.norm(pre.HC_Q)),
+        "final_mean": state.mean[rows], "final_mean_fro": np.float64(np.linalg.norm(state.mean)),
+        "final_variance": state.variance[rows],
+        "final_cross_cov_sample": state.cross_cov[np.ix_(rows, cols)],
+        "final_cross_cov_fro": np.float64(np.linalg.norm(state.cross_cov)),
+        "final_HC_block": state.HC[:64, :64], "final_HC_fro": np.float64(np.linalg.norm(state.HC)),
+        "ref_seconds": np.array([t_tree, t_pre, t_on]),
+    })
+    print(f"  cfg4_proxy: depth {tree.depth} orders {tree._orders} tree {t_tree:.1f}s precompute {t_pre:.1f}s "
+          f"online {t_on:.1f}s ({cfg['T']} steps)", flush=True)
+    return out
+
+
 def main(big: bool):
+    if "--proxy" in sys.argv:  # only the cfg4-proxy fixture (about 5 minutes, ~16 GB RSS)
+        np.savez_compressed(os.path.join(HERE, "cfg4_proxy.npz"), **cfg4_proxy())
+        return
     if "--dense" in sys.argv:  # only the dense-path fixtures (other fixtures untouched)
         np.savez_compressed(os.path.join(HERE, "dense_cases.npz"), **dense_cases())
         return

@@ -191,3 +191,25 @@ def test_oracle_dense_precompute_matches_reference(name, cfg):
     assert O.rel_fro(st.mean, g[f"{name}_final_mean"]) <= 1e-11
     assert O.rel_fro(st.variance, g[f"{name}_final_variance"]) <= 1e-11
     assert O.rel_fro(st.cross_cov, g[f"{name}_final_cross_cov"]) <= 1e-11
+
+
+def test_oracle_cfg4_proxy_tree_and_qht_columns():
+    """cfg4-proxy (m = 262,144, n = 1024, order 6, depth 6; make_golden.py --proxy):
+    the oracle's tree integers and the ray operator bit-exact, and its bbFMM
+    Q H^T on 2 of the reference's 8 sampled columns (matmat is
+    column-independent, fmm.py:325-367) to reassociation roundoff."""
+    g = _load("cfg4_proxy.npz")
+    N, ns, nr, order, leaf = 512, 32, 32, 6, 64
+    xy = O.cell_centers(N, N, 1.0 / N, 1.0 / N)
+    src, rcv = O.crosswell_stations(ns, nr, 0.0, 1.0, 0.0, 1.0)
+    H = O.ray_operator(N, N, 1.0 / N, 1.0 / N, src, rcv)
+    assert H.nnz == int(g["H_nnz"])
+    assert _sha(H.indptr.astype(np.int64), H.indices.astype(np.int64)) == g["H_pattern_sha"].item().decode()
+    assert _sha(H.data) == g["H_data_sha"].item().decode()
+    tree = O.OracleTree(xy, O.Kern("exponential", 1.0, 0.25), order, leaf)
+    check_tree_ints(tree, g)
+    rows, cols = g["rows"], g["cols"]
+    pick = [0, 7]  # first ray and one interior ray of the sampled columns
+    U = tree.matmat(np.ascontiguousarray(H[cols[pick]].T.toarray()))
+    assert O.rel_fro(U[rows], g["C_Q_sample"][:, pick]) <= 1e-13
+    np.testing.assert_allclose(U.sum(axis=0), g["C_Q_colsum"][cols[pick]], rtol=1e-13)

@@ -454,6 +454,8 @@ def main():
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--cpu-rows", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-factored", action="store_true",
+                    help="skip the opt-in factored-representation leg (C = C_Q N) reported under 'factored'")
     ap.add_argument("--mode", default="auto", choices=["auto", "replicas", "sharded"],
                     help="replicas: every rank runs the whole filter (weak scaling); sharded: the state rows are "
                          "split across ranks with one n-vector all-reduce per step (strong scaling, 2D configs); "
@@ -615,6 +617,48 @@ def main():
         pt.append(p0.elapsed_time(p1) / 1e3)
     del pc
 
+    # ---- opt-in factored representation (C = C_Q N, filters.FactoredHikfState):
+    # the same predict+update steps, device-resident; the headline stays explicit ----
+    fac = None
+    if not args.no_factored and not dim3 and float(model.alpha) == 0.0:
+        sf = flt.hikf_init(model, representation="factored")
+        for t in range(args.warmup):
+            sf = flt.hikf_update(flt.hikf_predict(sf, pre), H, cfg["R"], Zd[t % cfg["T"]])
+        lib.hikf_prof_reset()
+        lib.hikf_prof_enable(1)
+        barrier_sync()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for t in range(args.steps):
+            sf = flt.hikf_update(flt.hikf_predict(sf, pre), H, cfg["R"], Zd[(args.warmup + t) % cfg["T"]])
+        f1.record()
+        barrier_sync()
+        lib.hikf_prof_enable(0)
+        t_fac = max_over_ranks(f0.elapsed_time(f1) / 1e3)
+        fst = {s: _lib.prof_read(s) for s in ("predict", "factor", "gemm_y", "finalize", "gemm_c")}
+        ms_t, n_t = fst["gemm_c"]
+        t_tri = ms_t / max(n_t, 1) / 1e3
+        bn = 128  # column tile of the K-range-limited triangular GEMM (k >= n0 per column tile)
+        tri_flops = sum(2.0 * m * min(bn, n - n0) * (n - n0) for n0 in range(0, n, bn))
+        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fe0.record()
+        C_mat = sf.cross_cov_t  # one materialisation C_Q N (a user reading cross_cov)
+        fe1.record()
+        torch.cuda.synchronize()
+        fac = {"value": world * args.steps / t_fac, "unit": "steps/s", "ms_per_step": 1000.0 * t_fac / args.steps,
+               "note": "opt-in FactoredHikfState (alpha = 0): C_t = C_Q N_t with an n x n recursion; mean, variance "
+                       "(with the consistency check) and HC every step as filters.py:138-157; C materialised on "
+                       "read (ms_materialize, one GEMM)",
+               "ms_materialize": fe0.elapsed_time(fe1),
+               "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in fst.items()},
+               "roofline": {"kernel": "dgemm_cutlass_kernel KB_LOWER (rowsum((C_Q L_G)^2), no output store)",
+                            "bound": "fp64", "achieved": tri_flops / t_tri / 1e12 if t_tri else None,
+                            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                            "frac": tri_flops / t_tri / 1e12 / FP64_PEAK_TFLOPS if t_tri else None,
+                            "flops_per_launch": tri_flops, "triangular_ideal_flops": float(m) * n * (n + 1),
+                            "algorithmic_bytes": 8.0 * m * n}}
+        del sf, C_mat
+
     # ---- rooflines ----
     hbm, hbm_src = hbm_peak()
     ms_c, n_c = stage["gemm_c"]
@@ -676,6 +720,8 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if fac is not None:
+        line["factored"] = fac
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         t_cpu, rows = cpu_step_sample(cfg, args.cpu_rows)
         line["cpu_baseline"] = {

@@ -192,6 +192,24 @@ int hikf_update_chained(int64_t m, int64_t n, const double* mean_dev, const doub
                         double* HC_out, void* workspace, size_t workspace_bytes, double* min_var_out, int32_t chain,
                         double* mean_host, void* stream);
 
+/* ---- factored cross covariance (C = C_Q N, N n x n) ----
+ * Replaces filters.py:129-157 for a state whose cross covariance is C_Q N
+ * (every state of a filter started from C_0 = 0, i.e. alpha = 0): with
+ * predict = 1 the prior is predicted first (C' = C_Q (N + I), var + diag_Q,
+ * HC + HC_Q).  Outputs mean_out, var_out and HC_out as hikf_update (same
+ * consistency check and status codes) and N_out with C_new = C_Q N_out.
+ * Per step: the n x n recursion, one m x n GEMV (C_Q u) and one triangular
+ * m x n x n GEMM (var -= rowsum((C_Q L_G)^2), G = M S^-1 M^T), no m x n
+ * output.  HIKF_NOT_PD also when G loses definiteness.  mean_host as in
+ * hikf_update_chained. */
+size_t hikf_update_factored_workspace_bytes(int64_t m, int64_t n);
+int hikf_update_factored(int64_t m, int64_t n, const double* mean_dev, const double* N_dev, const double* var_dev,
+                         const double* HC_dev, const double* C_Q_dev, const double* diag_Q_dev, const double* HC_Q_dev,
+                         int32_t predict, const int32_t* indptr_dev, const int32_t* indices_dev,
+                         const double* data_dev, double r_variance, const double* z_dev, double* mean_out,
+                         double* N_out, double* var_out, double* HC_out, void* workspace, size_t workspace_bytes,
+                         double* min_var_out, double* mean_host, void* stream);
+
 /* ---- row-sharded update: the same update on rows [r0, r1) of a
  * state sharded across ranks.  Hmean_dev = the all-reduced H mean (the
  * caller sums the per-rank hikf_csr_spmv partials); the n x n quantities are

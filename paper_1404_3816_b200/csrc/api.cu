@@ -512,6 +512,52 @@ int hikf_update_chained(int64_t m, int64_t n, const double* mean, const double* 
   return s;
 }
 
+size_t hikf_update_factored_workspace_bytes(int64_t m, int64_t n) { return update_factored_workspace_bytes(m, n); }
+
+int hikf_update_factored(int64_t m, int64_t n, const double* mean, const double* N, const double* var,
+                         const double* HC, const double* CQ, const double* dQ, const double* HCQ, int32_t predict,
+                         const int32_t* ip, const int32_t* ix, const double* val, double r, const double* z,
+                         double* mean_out, double* N_out, double* var_out, double* HC_out, void* workspace,
+                         size_t workspace_bytes, double* min_var_out, double* mean_host, void* stream) {
+  if (m < 1 || n < 1 || !mean || !N || !var || !HC || !CQ || !ip || !z || !mean_out || !N_out || !var_out ||
+      !HC_out || N == N_out) {
+    set_error("bad factored update arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (predict && (!dQ || !HCQ)) {
+    set_error("fused predict needs diag_Q and HC_Q");
+    return HIKF_BAD_ARGUMENT;
+  }
+  UpdateArgs a;
+  a.m = m;
+  a.n = n;
+  a.mean = mean;
+  a.var = var;
+  a.HC = HC;
+  a.CQ = CQ;
+  a.dQ = predict ? dQ : nullptr;
+  a.HCQ = predict ? HCQ : nullptr;
+  a.ip = ip;
+  a.ix = ix;
+  a.val = val;
+  a.r = r;
+  a.z = z;
+  a.mean_out = mean_out;
+  a.var_out = var_out;
+  a.HC_out = HC_out;
+  a.workspace = workspace;
+  a.workspace_bytes = workspace_bytes;
+  a.mean_host = mean_host;
+  a.factored = true;
+  a.predict_in = predict != 0;
+  a.Nin = N;
+  a.Nout = N_out;
+  UpdateResult res;
+  int s = update(a, as_stream(stream), &res);
+  if (min_var_out) *min_var_out = res.min_var;
+  return s;
+}
+
 int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const double* C, const double* var,
                      const double* HC, const double* CQ, const double* dQ, const double* HCQ, const double* Hmean,
                      double r, const double* z, double* mean_out, double* C_out, double* var_out, double* HC_out,

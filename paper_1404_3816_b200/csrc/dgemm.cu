@@ -68,7 +68,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
           if (row < g.M && col < g.N) {
             const double v = sc * acc[i][j][h];
             ssq += v * (g.px ? g.px[row * g.ldx + col] : v);
-            sdot += v * g.w[col];
+            if (g.w) sdot += v * g.w[col];
           }
         }
       ssq += __shfl_xor_sync(0xffffffffu, ssq, 1);
@@ -82,7 +82,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
     }
   }
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
+  for (int i = 0; i < TM && C; ++i) {  // C == null: partials only (no output store)
     const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
     if (SPLIT && (TN % 2 == 0) && row < g.M && cw + BN / WN <= g.N && g.ldc % 2 == 0 && ((uintptr_t)C & 15) == 0) {
       // two runs of TN contiguous columns: 16-byte stores
@@ -162,7 +162,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
           d += red_dot[w][rl];
         }
         g.psq[row * g.ldp + blockIdx.x] = s;
-        g.pdot[row * g.ldp + blockIdx.x] = d;
+        if (g.pdot) g.pdot[row * g.ldp + blockIdx.x] = d;
       }
     }
   }
@@ -567,12 +567,16 @@ __global__ void __launch_bounds__(CutlassMain<BM, BN, WTM, WTN, STAGES>::THREADS
   const int64_t m0 = (int64_t)blockIdx.y * BM;
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  typename Mma::IteratorA itA(pA, const_cast<double*>(g.A), {(int)g.M, (int)g.K}, tid, {(int)m0, 0});
-  typename Mma::IteratorB itB(pB, const_cast<double*>(g.B), {(int)g.K, (int)g.N}, tid, {0, (int)n0});
+  // triangular B: only the k-range that can hold nonzeros (as dgemm_kernel)
+  int64_t kbeg = 0, kend = g.K;
+  if (g.kmode == KB_UPPER) kend = min(g.K, n0 + BN);
+  if (g.kmode == KB_LOWER) kbeg = (n0 / 16) * 16;
+  typename Mma::IteratorA itA(pA, const_cast<double*>(g.A), {(int)g.M, (int)kend}, tid, {(int)m0, (int)kbeg});
+  typename Mma::IteratorB itB(pB, const_cast<double*>(g.B), {(int)kend, (int)g.N}, tid, {(int)kbeg, (int)n0});
   Mma mma(ss, tid, warp, lane);
   typename Mma::FragmentC accum;
   accum.clear();
-  mma((int)((g.K + 15) / 16), accum, itA, itB, accum);
+  if (kend > kbeg) mma((int)((kend - kbeg + 15) / 16), accum, itA, itB, accum);
 
   // CUTLASS warp tile (mma_tensor_op.h, accumulators column-major over the
   // 8x8 instruction tiles): tile (i, j) -> accum[2 (i + j TM) + h] holds
@@ -631,8 +635,8 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   bool vec = g.sa_c == 1 && g.sb_c == 1 && (g.sa_r % 2 == 0) && (g.sb_r % 2 == 0) && al16(g.A) && al16(g.B) &&
              (batch == 1 || (g.bsA % 2 == 0 && g.bsB % 2 == 0));
   bool part = g.psq != nullptr;
-  // CUTLASS-mainloop variants: row-major operands, full K range, one batch
-  const bool cutlass_ok = g.sa_c == 1 && g.sb_c == 1 && g.kmode == KFULL && batch == 1 && g.M < (1ll << 31) &&
+  // CUTLASS-mainloop variants: row-major operands (any kmode), one batch
+  const bool cutlass_ok = g.sa_c == 1 && g.sb_c == 1 && batch == 1 && g.M < (1ll << 31) &&
                           g.K < (1ll << 31) && g.N < (1ll << 31);
   if (variant == 30 && cutlass_ok)  // 64x128x16, 4 warps of 32x64, 3 stages
     return part ? launch_cutlass<64, 128, 32, 64, 3, true>(g, st) : launch_cutlass<64, 128, 32, 64, 3, false>(g, st);

@@ -294,15 +294,31 @@ __global__ void finalize_rows(int64_t m, int nt, const double* __restrict__ psq,
 
 // consistency check of filters.py:149-153 -> status[1]; min var -> out[0]
 __global__ void check_variance(int nb, const double* bmin, const double* bmax, int* status, double* out) {
+  // one CTA of kT threads folds the per-block extrema of finalize_rows
   double mn = DBL_MAX, mx = -DBL_MAX;
-  for (int b = 0; b < nb; ++b) {
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     mn = fmin(mn, bmin[b]);
     mx = fmax(mx, bmax[b]);
   }
-  double prior_max = fmax(mx, 0.0);
-  out[0] = mn;
-  out[1] = mx;
-  if (mn < -1e-10 * fmax(prior_max, DBL_MIN)) status[1] = 1;
+  __shared__ double smin[kT], smax[kT];
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mn = smin[0];
+    mx = smax[0];
+    const double prior_max = fmax(mx, 0.0);
+    out[0] = mn;
+    out[1] = mx;
+    if (mn < -1e-10 * fmax(prior_max, DBL_MIN)) status[1] = 1;
+  }
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -401,6 +417,83 @@ bool lookahead_enabled() {
   return on;
 }
 
+
+// ---------------------------------------------------------------------------
+// factored representation kernels
+// ---------------------------------------------------------------------------
+// M = N + I (predict_in) or N
+__global__ void shift_identity(const double* __restrict__ N, int64_t n, double add, double* __restrict__ M) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e % n;
+    M[e] = i == j ? N[e] + add : N[e];
+  }
+}
+
+__global__ void scale_kernel(const double* __restrict__ x, double a, double* __restrict__ y, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    y[e] = a * x[e];
+}
+
+// y = A x, A rows x cols row-major (lda): one warp per row, 16-byte loads when
+// aligned (the m x n C_Q u pass streams C_Q once: HBM-bound)
+__global__ void __launch_bounds__(kT) gemv_rows(int64_t rows, int64_t cols, const double* __restrict__ A, int64_t lda,
+                                               const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool v2 = (cols % 2 == 0) && (lda % 2 == 0) && ((((uintptr_t)A) | ((uintptr_t)x)) & 15) == 0;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const double* a = A + row * lda;
+    double s = 0.0;
+    if (v2) {
+      const double2* a2 = reinterpret_cast<const double2*>(a);
+      const double2* x2 = reinterpret_cast<const double2*>(x);
+      for (int64_t c = lane; c < cols / 2; c += 32) {
+        const double2 av = __ldcs(a2 + c), xv = __ldg(x2 + c);
+        s = fma(av.x, xv.x, s);
+        s = fma(av.y, xv.y, s);
+      }
+    } else {
+      for (int64_t c = lane; c < cols; c += 32) s = fma(a[c], x[c], s);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[row] = s;
+  }
+}
+
+// var_out = var' - sum_t psq (= rowsum((C_Q L_G)^2) = rowsum(K o C')), mean_out = mean + C_Q u;
+// block extrema for the consistency check (as finalize_rows)
+__global__ void finalize_factored(int64_t m, int nt, const double* __restrict__ psq, const double* __restrict__ gv,
+                                  const double* __restrict__ varp, const double* __restrict__ mean,
+                                  double* __restrict__ var_out, double* __restrict__ mean_out,
+                                  double* __restrict__ bmin, double* __restrict__ bmax) {
+  double lmin = DBL_MAX, lmax = -DBL_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < nt; ++t) s += psq[i * nt + t];
+    const double vp = varp[i];
+    const double v = vp - s;
+    var_out[i] = v;
+    mean_out[i] = mean[i] + gv[i];
+    lmin = fmin(lmin, v);
+    lmax = fmax(lmax, vp);
+  }
+  __shared__ double smin[kT], smax[kT];
+  smin[threadIdx.x] = lmin;
+  smax[threadIdx.x] = lmax;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bmin[blockIdx.x] = smin[0];
+    bmax[blockIdx.x] = smax[0];
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -490,7 +583,272 @@ static int factor_chain(const double* HCp, int64_t n, double r, double* S, doubl
   return dgemm(g, 1, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// Factored representation of the cross covariance.
+//
+// With the reference's random-walk model and C_0 = alpha H^T, alpha = 0 (the
+// BASELINE configs), every cross covariance the filter produces lies in the
+// column space of C_Q:  C' = C + C_Q and C_new = r C' S^-1 (the identity the
+// explicit update uses) give C_t = C_Q N_t with the n x n recursion
+//     M = N + I,   W = M S^-1,   N_new = r W.
+// The step then needs, for the observable outputs,
+//     mean_new = mean + K innov     = mean + C_Q (W innov)          (m x n GEMV)
+//     var_new  = var' - rowsum(K o C') = var' - rowsum(C_Q G C_Q^T) with
+//                G = W M^T = M S^-1 M^T (symmetric PSD), G = L_G L_G^T:
+//              = var' - rowsum((C_Q L_G)^2)                          (m x n x n triangular GEMM,
+//                                                                      m n^2 flops, no m x n output)
+// and HC_new exactly as the explicit path (n x n side chain, never recomputed
+// from C).  C_t = C_Q N_t is materialised only when it is read (one GEMM).  The
+// S factorisation and its look-ahead are shared with the explicit path.
+// ---------------------------------------------------------------------------
+struct FacWs {
+  double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *u, *Mp, *W, *F, *FT, *G1, *L1, *L1i, *L1iT, *Q1, *Q1T,
+      *G2, *L2, *L2i, *LG, *tmp2, *gv, *psq, *bmin, *bmax, *minv;
+  int* status;
+};
+
+static size_t factored_layout(int64_t m, int64_t n, char* base, FacWs* ws) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return p;
+  };
+  const int nt = ceil_div(n, DG_MIN_BN);
+  const int nb = grid_for(m);
+  FacWs w;
+  for (double** p : {&w.HCp, &w.S, &w.L, &w.Li, &w.LiT, &w.P, &w.R, &w.Sinv, &w.tmp, &w.Mp, &w.W, &w.F, &w.FT, &w.G1,
+                     &w.L1, &w.L1i, &w.L1iT, &w.Q1, &w.Q1T, &w.G2, &w.L2, &w.L2i, &w.LG, &w.tmp2})
+    *p = (double*)take(8 * n * n);
+  w.innov = (double*)take(8 * n);
+  w.u = (double*)take(8 * n);
+  w.gv = (double*)take(8 * m);
+  w.psq = (double*)take(8 * m * nt);
+  w.bmin = (double*)take(8 * (size_t)nb);
+  w.bmax = (double*)take(8 * (size_t)nb);
+  w.minv = (double*)take(16);
+  w.status = (int*)take(16);
+  if (ws) *ws = w;
+  return off;
+}
+
+size_t update_factored_workspace_bytes(int64_t m, int64_t n) { return factored_layout(m, n, nullptr, nullptr); }
+
+static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
+  const int64_t m = a.m, n = a.n;
+  if (!a.CQ || !a.Nin || !a.Nout || (a.predict_in && (!a.dQ || !a.HCQ))) {
+    set_error("factored update needs C_Q, N (in / out) and, with the predict, diag_Q and HC_Q");
+    return HIKF_BAD_ARGUMENT;
+  }
+  if (a.workspace_bytes < update_factored_workspace_bytes(m, n)) {
+    set_error("factored update workspace too small (%zu < %zu bytes)", a.workspace_bytes,
+              update_factored_workspace_bytes(m, n));
+    return HIKF_BAD_ARGUMENT;
+  }
+  FacWs w;
+  factored_layout(m, n, (char*)a.workspace, &w);
+  HIKF_CHECK_CUDA(cudaMemsetAsync(w.status, 0, 16, st));
+  chain_state().valid = false;  // the explicit path's chained C' is not ours
+  cudaStream_t side = st;
+  cudaEvent_t ev[3];
+  HIKF_TRY(side_stream(&side, ev));
+
+  const bool use_la = lookahead_enabled() && a.predict_in && n > 0;
+  LookAhead* la = nullptr;
+  bool hit = false;
+  if (use_la) {
+    la = &lookahead();
+    HIKF_TRY(lookahead_reserve(*la, n));
+    if (la->ready && la->r == a.r && la->hcq_ptr == a.HCQ) {
+      HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + 2, 0, sizeof(int), st));
+      differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HC),
+                                                   reinterpret_cast<const uint64_t*>(la->HC), n * n, la->status + 2);
+      HIKF_CHECK_LAUNCH();
+      differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HCQ),
+                                                   reinterpret_cast<const uint64_t*>(la->HCQ), n * n, la->status + 2);
+      HIKF_CHECK_LAUNCH();
+      int flag = 1;
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag, la->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+      HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+      hit = flag == 0;
+    }
+  }
+
+  HIKF_CHECK_CUDA(cudaEventRecord(ev[0], st));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
+  const double *varp = a.var, *HCp = a.HC;
+  if (a.predict_in) {
+    ProfScope ps(ST_PREDICT, st);
+    add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(a.var, a.dQ, a.var_out, m);
+    HIKF_CHECK_LAUNCH();
+    varp = a.var_out;  // var_out holds var' until finalize_factored overwrites it row by row
+    add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, side>>>(a.HC, a.HCQ, w.HCp, n * n);
+    HIKF_CHECK_LAUNCH();
+    HCp = w.HCp;
+  }
+  // innovation on the main stream: z - H mean (filters.py:147)
+  innovation<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, a.ip, a.ix, a.val, a.mean, a.z, a.Hmean, w.innov);
+  HIKF_CHECK_LAUNCH();
+  const double *Li = w.Li, *LiT = w.LiT, *Sinv = w.Sinv;
+  if (hit) {
+    Li = la->Li[la->cur];
+    LiT = la->LiT[la->cur];
+    Sinv = la->Sinv[la->cur];
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(w.status, la->status + la->cur, sizeof(int), cudaMemcpyDeviceToDevice, side));
+  } else {
+    ProfScope pf(ST_FACTOR, side);
+    HIKF_TRY(factor_chain(HCp, n, a.r, w.S, w.L, w.tmp, w.Li, w.LiT, w.Sinv, w.status, side));
+  }
+  HIKF_CHECK_CUDA(cudaEventRecord(ev[1], side));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+
+  // ---- main: the n x n recursion, then the two m-row passes over C_Q ----
+  const int vc = update_variant_c();
+  const int nt = dgemm_col_tiles(n, vc);
+  const int nb = grid_for(m);
+  {
+    ProfScope pf(ST_GEMM_Y, st);  // n x n work on the main stream
+    shift_identity<<<grid_for(n * n), kT, 0, st>>>(a.Nin, n, a.predict_in ? 1.0 : 0.0, w.Mp);
+    HIKF_CHECK_LAUNCH();
+    GemmArgs g;  // W = M S^-1
+    g.M = n; g.N = n; g.K = n;
+    g.A = w.Mp; g.sa_r = n;
+    g.B = Sinv; g.sb_r = n;
+    g.C = w.W; g.ldc = n;
+    HIKF_TRY(dgemm(g, 1, st));
+    scale_kernel<<<grid_for(n * n), kT, 0, st>>>(w.W, a.r, a.Nout, n * n);  // N_new = r W
+    HIKF_CHECK_LAUNCH();
+    gemv_rows<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, n, w.W, n, w.innov, w.u);  // u = W innov
+    HIKF_CHECK_LAUNCH();
+    // L_G with L_G L_G^T = G = M S^-1 M^T = F F^T, F = M Li^T, from a Cholesky-QR2 of
+    // F^T (= Q R, L_G = R^T): the accuracy of a Householder QR of F (var error at
+    // cfg2 1.2e-12 against 3e-10 for a Cholesky of the formed G)
+    auto gemm = [&](const double* A, const double* B, double* C, int kmode) {
+      GemmArgs q;
+      q.M = n; q.N = n; q.K = n;
+      q.A = A; q.sa_r = n;
+      q.B = B; q.sb_r = n;
+      q.C = C; q.ldc = n;
+      q.kmode = kmode;
+      return dgemm(q, 1, st);
+    };
+    auto tr = [&](const double* X, double* Y) {
+      transpose_kernel<<<grid_for(n * n), kT, 0, st>>>(X, n, Y);
+      return cudaGetLastError() == cudaSuccess ? HIKF_OK : HIKF_CUDA_ERROR;
+    };
+    HIKF_TRY(gemm(w.Mp, LiT, w.F, KB_UPPER));  // F = M Li^T
+    HIKF_TRY(tr(w.F, w.FT));
+    HIKF_TRY(gemm(w.F, w.FT, w.G1, KFULL));    // G1 = F F^T = (F^T)^T F^T
+    build_S<<<grid_for(n * n), kT, 0, st>>>(w.G1, n, 0.0, w.tmp2);
+    HIKF_CHECK_LAUNCH();
+    HIKF_TRY(factor(w.tmp2, w.L1, w.L1i, w.G1, n, w.status + 2, st));  // G1 = L1 L1^T
+    HIKF_TRY(tr(w.L1i, w.L1iT));
+    HIKF_TRY(gemm(w.FT, w.L1iT, w.Q1, KB_UPPER));  // Q1 = F^T L1^-T
+    HIKF_TRY(tr(w.Q1, w.Q1T));
+    HIKF_TRY(gemm(w.Q1T, w.Q1, w.G2, KFULL));      // G2 = Q1^T Q1 (~ I)
+    build_S<<<grid_for(n * n), kT, 0, st>>>(w.G2, n, 0.0, w.tmp2);
+    HIKF_CHECK_LAUNCH();
+    HIKF_TRY(factor(w.tmp2, w.L2, w.L2i, w.G2, n, w.status + 2, st));  // G2 = L2 L2^T
+    HIKF_TRY(gemm(w.L1, w.L2, w.LG, KB_LOWER));    // L_G = L1 L2 (= R^T)
+  }
+  {
+    ProfScope pg(ST_FINALIZE, st);
+    // mean increment: C_Q u (HBM-bound GEMV over C_Q)
+    gemv_rows<<<num_sms() * 16, kT, 0, st>>>(m, n, a.CQ, n, w.u, w.gv);
+    HIKF_CHECK_LAUNCH();
+  }
+  {
+    GemmArgs g;  // psq = rowsum((C_Q L_G)^2), L_G lower triangular: no output store
+    g.M = m; g.N = n; g.K = n;
+    g.A = a.CQ; g.sa_r = n;
+    g.B = w.LG; g.sb_r = n;
+    g.C = nullptr; g.ldc = n;
+    g.kmode = KB_LOWER;
+    g.psq = w.psq; g.ldp = nt;
+    g.variant = vc;
+    ProfScope ps(ST_GEMM_C, st);
+    HIKF_TRY(dgemm(g, 1, st));
+  }
+  {
+    ProfScope pz(ST_FINALIZE, st);
+    finalize_factored<<<nb, kT, 0, st>>>(m, nt, w.psq, w.gv, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
+    HIKF_CHECK_LAUNCH();
+    check_variance<<<1, kT, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+    HIKF_CHECK_LAUNCH();
+    if (a.mean_host)
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(a.mean_host, a.mean_out, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  }
+  // ---- side: HC_new = HC' - (HC' Li^T)(Li HC'), as the explicit path ----
+  {
+    GemmArgs g;
+    g.M = n; g.N = n; g.K = n;
+    g.A = Li; g.sa_r = n;
+    g.B = HCp; g.sb_r = n;
+    g.C = w.P; g.ldc = n;
+    HIKF_TRY(dgemm(g, 1, side));
+    GemmArgs h;
+    h.M = n; h.N = n; h.K = n;
+    h.A = HCp; h.sa_r = n;
+    h.B = LiT; h.sb_r = n;
+    h.C = w.R; h.ldc = n;
+    h.kmode = KB_UPPER;
+    HIKF_TRY(dgemm(h, 1, side));
+    GemmArgs c;
+    c.M = n; c.N = n; c.K = n;
+    c.A = w.R; c.sa_r = n;
+    c.B = w.P; c.sb_r = n;
+    c.C = a.HC_out; c.ldc = n;
+    c.Cin = HCp; c.ldcin = n;
+    c.alpha = -1.0; c.beta = 1.0;
+    HIKF_TRY(dgemm(c, 1, side));
+  }
+  if (use_la) {
+    la->ready = false;
+    const int nx = hit ? la->cur ^ 1 : la->cur;
+    ProfScope pf(ST_FACTOR, side);
+    add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, side>>>(a.HC_out, a.HCQ, la->HCp, n * n);
+    HIKF_CHECK_LAUNCH();
+    HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + nx, 0, sizeof(int), side));
+    HIKF_TRY(factor_chain(la->HCp, n, a.r, w.S, w.L, w.tmp, la->Li[nx], la->LiT[nx], la->Sinv[nx], la->status + nx,
+                          side));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(la->HC, a.HC_out, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(la->HCQ, a.HCQ, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
+    la->cur = nx;
+    la->r = a.r;
+    la->hcq_ptr = a.HCQ;
+    la->ready = true;
+  }
+  HIKF_CHECK_CUDA(cudaEventRecord(ev[2], side));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[2], 0));
+
+  int hs[3] = {0, 0, 0};
+  double mm[2] = {0.0, 0.0};
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (res) {
+    res->pivot = hs[0];
+    res->min_var = mm[0];
+    res->max_prior_var = mm[1];
+  }
+  if (hs[0]) {
+    set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
+    return HIKF_NOT_PD;
+  }
+  if (hs[2]) {
+    set_error("factored update: M S^-1 M^T lost positive definiteness at pivot %d (use the explicit state)", hs[2]);
+    return HIKF_NOT_PD;
+  }
+  if (hs[1] && !a.no_check) {
+    set_error("posterior variance went negative beyond tolerance (min %.3e)", mm[0]);
+    return HIKF_NEGATIVE_VARIANCE;
+  }
+  return HIKF_OK;
+}
+
 int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
+  if (a.factored) return update_factored(a, st, res);
   const int64_t m = a.m, n = a.n;
   if (a.workspace_bytes < update_workspace_bytes(m, n)) {
     set_error("update workspace too small (%zu < %zu bytes)", a.workspace_bytes, update_workspace_bytes(m, n));
@@ -599,7 +957,7 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
     ProfScope pz(ST_FINALIZE, st);
     finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
     HIKF_CHECK_LAUNCH();
-    check_variance<<<1, 1, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+    check_variance<<<1, kT, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
     HIKF_CHECK_LAUNCH();
     if (a.mean_host)  // the caller's read-back, overlapping the side-stream tail
       HIKF_CHECK_CUDA(cudaMemcpyAsync(a.mean_host, a.mean_out, sizeof(double) * m, cudaMemcpyDeviceToHost, st));

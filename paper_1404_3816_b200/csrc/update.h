@@ -23,6 +23,12 @@ struct UpdateArgs {
   bool chain = false;     // produce the next call's C'
   bool chain_in = false;  // may consume the C' the previous call produced (pointers are checked too)
   double* mean_host = nullptr;  // optional pinned host copy of mean_out, filled inside the call
+  // factored cross-covariance (C = C_Q N, N n x n): C / C_out are unused and CQ is required;
+  // Nin -> Nout replaces the m x n state (see update.cu, "factored representation")
+  bool factored = false;
+  bool predict_in = true;  // factored: the prior is predicted (C' = C_Q (N + I), var + diag_Q, HC + HC_Q)
+  const double* Nin = nullptr;
+  double* Nout = nullptr;
 };
 
 struct UpdateResult {
@@ -32,6 +38,7 @@ struct UpdateResult {
 };
 
 size_t update_workspace_bytes(int64_t m, int64_t n);
+size_t update_factored_workspace_bytes(int64_t m, int64_t n);
 int update(const UpdateArgs& a, cudaStream_t stream, UpdateResult* res);
 int predict(int64_t m, int64_t n, const double* C, const double* var, const double* HC, const double* CQ,
             const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, cudaStream_t st);

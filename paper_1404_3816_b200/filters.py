@@ -27,7 +27,7 @@ from .kernels import value_at_zero  # noqa: F401
 __all__ = [
     "DeviceCSR", "HikfPrecompute", "HikfState", "NumericalConsistencyError", "hikf_precompute_dense",
     "KfState", "dense_gram", "kf_init", "kf_predict", "kf_update",
-    "hikf_precompute_fmm", "hikf_init", "hikf_predict", "hikf_update",
+    "hikf_precompute_fmm", "hikf_init", "hikf_predict", "hikf_update", "FactoredHikfState",
 ]
 
 
@@ -173,6 +173,65 @@ class HikfState:
         return tuple(src.cross_cov_t.shape)
 
 
+class FactoredHikfState(HikfState):
+    """A HikfState whose cross covariance is kept factored, C = C_Q N (N n x n).
+
+    Every cross covariance of a filter started from C_0 = alpha H^T with alpha
+    = 0 lies in the column space of C_Q (C' = C + C_Q, C_new = r C' S^-1), so
+    the state carries N instead of the m x n C; mean, variance and HC are
+    explicit and computed every step exactly as in filters.py:138-157 (same
+    consistency check).  ``cross_cov`` / ``cross_cov_t`` materialise C_Q N with
+    one device GEMM on first access.  Opt-in: ``hikf_init(model,
+    representation="factored")``; see update.cu ("factored representation")
+    and DESIGN.md section 5."""
+
+    def __init__(self, mean, N, variance, HC, pre, *, _prior=None, _pre=None):
+        self._prior = _prior
+        self._pre = _pre
+        self._host = {}
+        self._C = None
+        if _prior is None:
+            self.mean_t, self.N_t, self.variance_t, self.HC_t = mean, N, variance, HC
+            self._cq_pre = pre
+        else:
+            self.mean_t = _prior.mean_t
+            self.N_t = self.variance_t = self.HC_t = None
+            self._cq_pre = _pre
+
+    @property
+    def pending(self) -> bool:
+        return self._prior is not None and self.N_t is None
+
+    def _materialize(self):
+        """Predicted state read before its update: N + I, var + diag_Q, HC + HC_Q."""
+        if not self.pending:
+            return
+        p, pre = self._prior, self._pre
+        n = p.N_t.shape[0]
+        self.N_t = p.N_t + torch.eye(n, dtype=torch.float64, device=p.N_t.device)
+        self.variance_t = p.variance_t + pre.diag_Q_t
+        self.HC_t = p.HC_t + pre.HC_Q_t
+
+    @property
+    def cross_cov_t(self) -> torch.Tensor:
+        self._materialize()
+        if self._C is None:
+            m, n = self.mean_t.shape[0], self.N_t.shape[0]
+            if self._cq_pre is None:  # C_0 = 0
+                self._C = torch.zeros((m, n), dtype=torch.float64, device=self.mean_t.device)
+            else:
+                C = torch.empty((m, n), dtype=torch.float64, device=self.mean_t.device)
+                _lib.check(_lib.load().hikf_dgemm(m, n, n, self._cq_pre.C_Q_t.data_ptr(), n, self.N_t.data_ptr(), n,
+                                                  C.data_ptr(), n, 1.0, 0.0, 0, -1, _lib.stream_ptr()))
+                self._C = C
+        return self._C
+
+    @property
+    def shape(self):
+        src = self._prior if self.pending else self
+        return (int(src.mean_t.shape[0]), int(src.N_t.shape[0]))
+
+
 def _model_H(model):
     return model.H
 
@@ -219,12 +278,21 @@ def hikf_precompute_dense(model) -> HikfPrecompute:
     return HikfPrecompute(C_Q, HC_Q, diag_Q)
 
 
-def hikf_init(model) -> HikfState:
-    """mean = mu_0, C = alpha H^T, var = alpha, HC = alpha H H^T (filters.py:118-126)."""
+def hikf_init(model, representation: str = "explicit") -> HikfState:
+    """mean = mu_0, C = alpha H^T, var = alpha, HC = alpha H H^T (filters.py:118-126).
+
+    ``representation="factored"`` (alpha = 0 only) returns a FactoredHikfState."""
     H = DeviceCSR.of(_model_H(model))
     m, n = int(model.m), H.shape[0]
     dev = _dev()
     mean = _to_dev(model.initial_mean, (m,)).clone()
+    if representation == "factored":
+        if float(model.alpha) != 0.0:
+            raise ValueError("the factored representation needs alpha = 0 (C_0 = 0)")
+        z = dict(dtype=torch.float64, device=dev)
+        return FactoredHikfState(mean, torch.zeros((n, n), **z), torch.zeros((m,), **z), torch.zeros((n, n), **z), None)
+    if representation != "explicit":
+        raise ValueError(f"unknown representation {representation!r}")
     C = torch.empty((m, n), dtype=torch.float64, device=dev)
     var = torch.empty((m,), dtype=torch.float64, device=dev)
     HC = torch.empty((n, n), dtype=torch.float64, device=dev)
@@ -237,6 +305,10 @@ def hikf_init(model) -> HikfState:
 def hikf_predict(state: HikfState, pre: HikfPrecompute) -> HikfState:
     """C += C_Q, var += diag_Q, HC += HC_Q (filters.py:129-135); evaluated lazily."""
     state._materialize()
+    if isinstance(state, FactoredHikfState):
+        if tuple(pre.C_Q_t.shape) != state.shape:
+            raise ValueError("precompute shape does not match the state")
+        return FactoredHikfState(None, None, None, None, None, _prior=state, _pre=pre)
     if tuple(pre.C_Q_t.shape) != tuple(state.cross_cov_t.shape):
         raise ValueError("precompute shape does not match the state")
     return HikfState(None, None, None, None, _prior=state, _pre=pre)
@@ -270,6 +342,8 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
     if n == 0:
         return state
     zt = _to_dev(zt, (n,))
+    if isinstance(state, FactoredHikfState):
+        return _update_factored(state, Hd, float(r_variance), zt)
     fused = state.pending
     src = state._prior if fused else state
     pre = state._pre if fused else None
@@ -308,6 +382,42 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
 
 
 _CHAIN: dict = {}
+
+
+def _update_factored(state: FactoredHikfState, Hd: DeviceCSR, r: float, zt: torch.Tensor) -> FactoredHikfState:
+    """hikf_update on a factored state (libhikf_b200 hikf_update_factored)."""
+    fused = state.pending
+    src = state._prior if fused else state
+    pre = state._pre if fused else src._cq_pre
+    m, n = state.shape
+    if src.N_t.shape != (n, n) or src.mean_t.shape != (m,):
+        raise ValueError("factored state shape does not match (m, n)")
+    if pre is None:
+        raise ValueError("a factored state needs hikf_predict (C_Q) before its first update")
+    dev = _dev()
+    mean = torch.empty((m,), dtype=torch.float64, device=dev)
+    N = torch.empty((n, n), dtype=torch.float64, device=dev)
+    var = torch.empty((m,), dtype=torch.float64, device=dev)
+    HC = torch.empty((n, n), dtype=torch.float64, device=dev)
+    lib = _lib.load()
+    key = (m, n, dev.index, "factored")
+    ws = _WS.get(key)
+    if ws is None:
+        _WS.clear()
+        ws = torch.empty(int(lib.hikf_update_factored_workspace_bytes(m, n)), dtype=torch.uint8, device=dev)
+        _WS[key] = ws
+    _CHAIN.clear()
+    mean_host = torch.empty((m,), dtype=torch.float64, pin_memory=True)
+    _lib.check(lib.hikf_update_factored(
+        m, n, src.mean_t.data_ptr(), src.N_t.data_ptr(), src.variance_t.data_ptr(), src.HC_t.data_ptr(),
+        pre.C_Q_t.data_ptr(), _lib.ptr(pre.diag_Q_t) if fused else None, _lib.ptr(pre.HC_Q_t) if fused else None,
+        1 if fused else 0, Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), r, zt.data_ptr(),
+        mean.data_ptr(), N.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None,
+        mean_host.data_ptr(), _lib.stream_ptr()))
+    out = FactoredHikfState(mean, N, var, HC, pre)
+    out._pinned = mean_host
+    out._host["mean"] = mean_host.numpy()
+    return out
 
 
 # ----------------------------------------------------------------------

@@ -174,3 +174,32 @@ def test_cfg4_update_against_torch_fp64(pkg, cfg4):
     _record("cfg4_update_vs_torch", errs)
     for k, v in errs.items():
         assert v <= PARITY, (k, v)
+
+
+def test_cfg4_factored_update_against_torch_fp64(pkg, cfg4):
+    """The factored representation at the full cfg4 size, 3 steps, against the
+    same torch float64 restatement of filters.py:129-157."""
+    import torch
+    cfg, grid, H, model, tree, pre = cfg4
+    flt = pkg.filters
+    xy = grid.cell_centers().coords
+    obs = O.observations(H, O.moving_plume(xy, 3), cfg["R"], [cfg["seed"], 0])
+    st = flt.hikf_init(model, representation="factored")
+    for t in range(3):
+        st = flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], obs[t])
+    torch.cuda.synchronize()
+    ours = {k: getattr(st, k + "_t").clone() for k in ("mean", "cross_cov", "variance", "HC")}
+    del st
+    torch.cuda.empty_cache()
+    Hd = torch.sparse_csr_tensor(torch.as_tensor(H.indptr, dtype=torch.int64), torch.as_tensor(H.indices, dtype=torch.int64),
+                                 torch.as_tensor(H.data), size=H.shape).cuda()
+    mean, C, var, HC = _torch_reference_steps(torch, pre.C_Q_t, pre.HC_Q_t, pre.diag_Q_t, Hd, cfg["R"], obs, 3)
+
+    def rf(a, b):
+        return float(torch.linalg.norm(a - b) / torch.linalg.norm(b))
+
+    errs = {"mean": rf(ours["mean"], mean), "variance": rf(ours["variance"], var),
+            "cross_cov": rf(ours["cross_cov"], C), "HC": rf(ours["HC"], HC)}
+    _record("cfg4_factored_vs_torch", errs)
+    for k, v in errs.items():
+        assert v <= PARITY, (k, v)

@@ -412,3 +412,58 @@ def test_row_sharded_precompute_equals_full(pkg):
     assert O.rel_fro(HCQ, pre.HC_Q) <= 1e-14
     with pytest.raises(ValueError):
         precompute_rows(tree, H, 5, 3)
+
+
+def _run_filter_factored(pkg, cfg, obs, T=None):
+    flt = pkg.filters
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    model = _Model(grid, H, kern, cfg["R"])
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    pre = flt.hikf_precompute_fmm(model, tree)
+    st = flt.hikf_init(model, representation="factored")
+    for t in range(cfg["T"] if T is None else T):
+        st = flt.hikf_update(flt.hikf_predict(st, pre), H, model.r_variance, obs[t])
+    return tree, H, pre, st, model
+
+
+@pytest.mark.parametrize("fixture,cfg", [("small_rays.npz", cases.SMALL), ("cfg1.npz", cases.CFG1),
+                                         ("cfg2.npz", cases.CFG2)])
+def test_factored_filter_matches_reference(pkg, fixture, cfg):
+    """The factored cross covariance (C = C_Q N, update.cu) against the
+    reference's explicit filter: final mean / variance / C / HC within the
+    north-star 1e-9 (cfg2 on its 4 stored columns)."""
+    g = _load(fixture)
+    tree, H, pre, st, model = _run_filter_factored(pkg, cfg, g["obs"])
+    assert isinstance(st, pkg.filters.FactoredHikfState)
+    errs = {"mean": O.rel_fro(st.mean, g["final_mean"]), "variance": O.rel_fro(st.variance, g["final_variance"]),
+            "HC": O.rel_fro(st.HC, g["final_HC"])}
+    if "final_cross_cov" in g:
+        errs["cross_cov"] = O.rel_fro(st.cross_cov, g["final_cross_cov"])
+    else:
+        errs["cross_cov_cols"] = O.rel_fro(st.cross_cov[:, g["cols"]], g["final_cross_cov_cols"])
+    _record(cfg["name"] + "_factored", errs)
+    for k, v in errs.items():
+        assert v <= PARITY, (k, v)
+
+
+def test_factored_state_api(pkg):
+    """alpha != 0 is refused; a predicted factored state materialises C' = C_Q (N + I);
+    the update without a predict keeps the reference's semantics."""
+    flt = pkg.filters
+    g = _load("small_rays.npz")
+    cfg = cases.SMALL
+    tree, H, pre, st, model = _run_filter_factored(pkg, cfg, g["obs"], T=2)
+    model.alpha = 0.5
+    with pytest.raises(ValueError):
+        flt.hikf_init(model, representation="factored")
+    model.alpha = 0.0
+    p = flt.hikf_predict(st, pre)
+    np.testing.assert_allclose(p.cross_cov, st.cross_cov + pre.C_Q, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(p.variance, st.variance + pre.diag_Q, rtol=0, atol=0)
+    # update without predict, factored vs explicit on the same prior
+    ex = flt.HikfState(st.mean, st.cross_cov, st.variance, st.HC)
+    a = flt.hikf_update(st, H, cfg["R"], g["obs"][2])
+    b = flt.hikf_update(ex, H, cfg["R"], g["obs"][2])
+    for k in ("mean", "variance", "cross_cov", "HC"):
+        assert O.rel_fro(getattr(a, k), getattr(b, k)) <= 1e-12, k

@@ -602,9 +602,14 @@ static int factor_chain(const double* HCp, int64_t n, double r, double* S, doubl
 // from C).  C_t = C_Q N_t is materialised only when it is read (one GEMM).  The
 // S factorisation and its look-ahead are shared with the explicit path.
 // ---------------------------------------------------------------------------
+// scratch of one evaluation of the factored n x n chain
+struct FacChain {
+  double *Mp, *F, *FT, *G1, *L1, *L1i, *L1iT, *Q1, *Q1T, *G2, *L2, *L2i, *tmp2;
+};
+
 struct FacWs {
-  double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *u, *Mp, *W, *F, *FT, *G1, *L1, *L1i, *L1iT, *Q1, *Q1T,
-      *G2, *L2, *L2i, *LG, *tmp2, *gv, *psq, *bmin, *bmax, *minv;
+  double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *u, *W, *LG, *gv, *psq, *bmin, *bmax, *minv;
+  FacChain c;
   int* status;
 };
 
@@ -618,8 +623,9 @@ static size_t factored_layout(int64_t m, int64_t n, char* base, FacWs* ws) {
   const int nt = ceil_div(n, DG_MIN_BN);
   const int nb = grid_for(m);
   FacWs w;
-  for (double** p : {&w.HCp, &w.S, &w.L, &w.Li, &w.LiT, &w.P, &w.R, &w.Sinv, &w.tmp, &w.Mp, &w.W, &w.F, &w.FT, &w.G1,
-                     &w.L1, &w.L1i, &w.L1iT, &w.Q1, &w.Q1T, &w.G2, &w.L2, &w.L2i, &w.LG, &w.tmp2})
+  for (double** p : {&w.HCp, &w.S, &w.L, &w.Li, &w.LiT, &w.P, &w.R, &w.Sinv, &w.tmp, &w.W, &w.LG, &w.c.Mp, &w.c.F,
+                     &w.c.FT, &w.c.G1, &w.c.L1, &w.c.L1i, &w.c.L1iT, &w.c.Q1, &w.c.Q1T, &w.c.G2, &w.c.L2, &w.c.L2i,
+                     &w.c.tmp2})
     *p = (double*)take(8 * n * n);
   w.innov = (double*)take(8 * n);
   w.u = (double*)take(8 * n);
@@ -634,6 +640,86 @@ static size_t factored_layout(int64_t m, int64_t n, char* base, FacWs* ws) {
 }
 
 size_t update_factored_workspace_bytes(int64_t m, int64_t n) { return factored_layout(m, n, nullptr, nullptr); }
+
+// The n x n part of a factored step, from N (and +I for a predicted prior) and
+// the factorisation of S:  M = N (+ I),  W = M S^-1,  and L_G (lower) with
+// L_G L_G^T = G = M S^-1 M^T = F F^T, F = M Li^T, taken from a Cholesky-QR2 of
+// F^T (F^T = Q R, L_G = R^T): the accuracy of a Householder QR of F (variance
+// error at cfg2 1.2e-12, against 3e-10 for a Cholesky of the formed G;
+// DESIGN.md 5).  status[0] = first failing pivot of either Cholesky.
+static int factored_chain(const double* N, double add, const double* Sinv, const double* LiT, int64_t n,
+                          const FacChain& c, double* W, double* LG, int* status, cudaStream_t s) {
+  auto gemm = [&](const double* A, const double* B, double* C, int kmode) {
+    GemmArgs q;
+    q.M = n; q.N = n; q.K = n;
+    q.A = A; q.sa_r = n;
+    q.B = B; q.sb_r = n;
+    q.C = C; q.ldc = n;
+    q.kmode = kmode;
+    return dgemm(q, 1, s);
+  };
+  auto tr = [&](const double* X, double* Y) {
+    transpose_kernel<<<grid_for(n * n), kT, 0, s>>>(X, n, Y);
+    return cudaGetLastError() == cudaSuccess ? HIKF_OK : HIKF_CUDA_ERROR;
+  };
+  shift_identity<<<grid_for(n * n), kT, 0, s>>>(N, n, add, c.Mp);
+  HIKF_CHECK_LAUNCH();
+  HIKF_TRY(gemm(c.Mp, Sinv, W, KFULL));  // W = M S^-1
+  HIKF_TRY(gemm(c.Mp, LiT, c.F, KB_UPPER));  // F = M Li^T
+  HIKF_TRY(tr(c.F, c.FT));
+  HIKF_TRY(gemm(c.F, c.FT, c.G1, KFULL));    // G1 = F F^T
+  build_S<<<grid_for(n * n), kT, 0, s>>>(c.G1, n, 0.0, c.tmp2);
+  HIKF_CHECK_LAUNCH();
+  HIKF_TRY(factor(c.tmp2, c.L1, c.L1i, c.G1, n, status, s));  // G1 = L1 L1^T
+  HIKF_TRY(tr(c.L1i, c.L1iT));
+  HIKF_TRY(gemm(c.FT, c.L1iT, c.Q1, KB_UPPER));  // Q1 = F^T L1^-T
+  HIKF_TRY(tr(c.Q1, c.Q1T));
+  HIKF_TRY(gemm(c.Q1T, c.Q1, c.G2, KFULL));      // G2 = Q1^T Q1 (~ I)
+  build_S<<<grid_for(n * n), kT, 0, s>>>(c.G2, n, 0.0, c.tmp2);
+  HIKF_CHECK_LAUNCH();
+  HIKF_TRY(factor(c.tmp2, c.L2, c.L2i, c.G2, n, status, s));  // G2 = L2 L2^T
+  return gemm(c.L1, c.L2, LG, KB_LOWER);         // L_G = L1 L2 (= R^T)
+}
+
+// Look-ahead of the factored chain: step t knows N_{t+1} (= its N_out) and,
+// through the S look-ahead, S_{t+1}; it evaluates the next step's (W, L_G) on
+// the side stream during its triangular GEMM.  Step t+1 uses them when the S
+// look-ahead hits with the same slot and its N input is bitwise equal to the N
+// step t produced (checked on the device) -- same kernels, same inputs, so the
+// results are bit-identical hit or miss.
+struct FacLookAhead {
+  int64_t n = 0;
+  bool ready = false;
+  int la_slot = -1;  // S look-ahead slot the chain used
+  int cur = 0;
+  double *W[2] = {nullptr, nullptr}, *LG[2] = {nullptr, nullptr}, *N[2] = {nullptr, nullptr};
+  FacChain c{};
+  int* status = nullptr;  // [2] pivots, [2] N-validation flag
+};
+
+FacLookAhead& fac_lookahead() {
+  static FacLookAhead fl[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return fl[dev & 63];
+}
+
+static int fac_lookahead_reserve(FacLookAhead& f, int64_t n) {
+  if (f.n == n && f.status) return HIKF_OK;
+  double** all[] = {&f.W[0], &f.W[1], &f.LG[0], &f.LG[1], &f.N[0], &f.N[1], &f.c.Mp, &f.c.F, &f.c.FT, &f.c.G1,
+                    &f.c.L1, &f.c.L1i, &f.c.L1iT, &f.c.Q1, &f.c.Q1T, &f.c.G2, &f.c.L2, &f.c.L2i, &f.c.tmp2};
+  for (double** p : all)
+    if (*p) cudaFree(*p);
+  if (f.status) cudaFree(f.status);
+  f = FacLookAhead();
+  const size_t b = std::max<size_t>(sizeof(double) * (size_t)n * n, 8);
+  double** all2[] = {&f.W[0], &f.W[1], &f.LG[0], &f.LG[1], &f.N[0], &f.N[1], &f.c.Mp, &f.c.F, &f.c.FT, &f.c.G1,
+                     &f.c.L1, &f.c.L1i, &f.c.L1iT, &f.c.Q1, &f.c.Q1T, &f.c.G2, &f.c.L2, &f.c.L2i, &f.c.tmp2};
+  for (double** p : all2) HIKF_CHECK_CUDA(cudaMalloc((void**)p, b));
+  HIKF_CHECK_CUDA(cudaMalloc((void**)&f.status, 4 * sizeof(int)));
+  f.n = n;
+  return HIKF_OK;
+}
 
 static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   const int64_t m = a.m, n = a.n;
@@ -653,13 +739,18 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
   cudaStream_t side = st;
   cudaEvent_t ev[3];
   HIKF_TRY(side_stream(&side, ev));
+  static cudaEvent_t ev_n = nullptr;  // main -> side: N_out written
+  if (!ev_n) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&ev_n, cudaEventDisableTiming));
 
   const bool use_la = lookahead_enabled() && a.predict_in && n > 0;
   LookAhead* la = nullptr;
-  bool hit = false;
+  FacLookAhead* fl = nullptr;
+  bool hit = false, fhit = false;
   if (use_la) {
     la = &lookahead();
+    fl = &fac_lookahead();
     HIKF_TRY(lookahead_reserve(*la, n));
+    HIKF_TRY(fac_lookahead_reserve(*fl, n));
     if (la->ready && la->r == a.r && la->hcq_ptr == a.HCQ) {
       HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + 2, 0, sizeof(int), st));
       differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HC),
@@ -668,10 +759,20 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
       differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HCQ),
                                                    reinterpret_cast<const uint64_t*>(la->HCQ), n * n, la->status + 2);
       HIKF_CHECK_LAUNCH();
-      int flag = 1;
-      HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag, la->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+      const bool ftry = fl->ready && fl->la_slot == la->cur;
+      if (ftry) {
+        HIKF_CHECK_CUDA(cudaMemsetAsync(fl->status + 2, 0, sizeof(int), st));
+        differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.Nin),
+                                                     reinterpret_cast<const uint64_t*>(fl->N[fl->cur]), n * n,
+                                                     fl->status + 2);
+        HIKF_CHECK_LAUNCH();
+      }
+      int flag[2] = {1, 1};
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag[0], la->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+      if (ftry) HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag[1], fl->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
       HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-      hit = flag == 0;
+      hit = flag[0] == 0;
+      fhit = hit && ftry && flag[1] == 0;
     }
   }
 
@@ -703,54 +804,25 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
   HIKF_CHECK_CUDA(cudaEventRecord(ev[1], side));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
 
-  // ---- main: the n x n recursion, then the two m-row passes over C_Q ----
+  // ---- main: the n x n recursion (or its look-ahead), then the two m-row passes over C_Q ----
   const int vc = update_variant_c();
   const int nt = dgemm_col_tiles(n, vc);
   const int nb = grid_for(m);
+  const double *W = w.W, *LG = w.LG;
   {
     ProfScope pf(ST_GEMM_Y, st);  // n x n work on the main stream
-    shift_identity<<<grid_for(n * n), kT, 0, st>>>(a.Nin, n, a.predict_in ? 1.0 : 0.0, w.Mp);
+    if (fhit) {
+      W = fl->W[fl->cur];
+      LG = fl->LG[fl->cur];
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(w.status + 2, fl->status + fl->cur, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    } else {
+      HIKF_TRY(factored_chain(a.Nin, a.predict_in ? 1.0 : 0.0, Sinv, LiT, n, w.c, w.W, w.LG, w.status + 2, st));
+    }
+    scale_kernel<<<grid_for(n * n), kT, 0, st>>>(W, a.r, a.Nout, n * n);  // N_new = r W
     HIKF_CHECK_LAUNCH();
-    GemmArgs g;  // W = M S^-1
-    g.M = n; g.N = n; g.K = n;
-    g.A = w.Mp; g.sa_r = n;
-    g.B = Sinv; g.sb_r = n;
-    g.C = w.W; g.ldc = n;
-    HIKF_TRY(dgemm(g, 1, st));
-    scale_kernel<<<grid_for(n * n), kT, 0, st>>>(w.W, a.r, a.Nout, n * n);  // N_new = r W
+    HIKF_CHECK_CUDA(cudaEventRecord(ev_n, st));
+    gemv_rows<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, n, W, n, w.innov, w.u);  // u = W innov
     HIKF_CHECK_LAUNCH();
-    gemv_rows<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, n, w.W, n, w.innov, w.u);  // u = W innov
-    HIKF_CHECK_LAUNCH();
-    // L_G with L_G L_G^T = G = M S^-1 M^T = F F^T, F = M Li^T, from a Cholesky-QR2 of
-    // F^T (= Q R, L_G = R^T): the accuracy of a Householder QR of F (var error at
-    // cfg2 1.2e-12 against 3e-10 for a Cholesky of the formed G)
-    auto gemm = [&](const double* A, const double* B, double* C, int kmode) {
-      GemmArgs q;
-      q.M = n; q.N = n; q.K = n;
-      q.A = A; q.sa_r = n;
-      q.B = B; q.sb_r = n;
-      q.C = C; q.ldc = n;
-      q.kmode = kmode;
-      return dgemm(q, 1, st);
-    };
-    auto tr = [&](const double* X, double* Y) {
-      transpose_kernel<<<grid_for(n * n), kT, 0, st>>>(X, n, Y);
-      return cudaGetLastError() == cudaSuccess ? HIKF_OK : HIKF_CUDA_ERROR;
-    };
-    HIKF_TRY(gemm(w.Mp, LiT, w.F, KB_UPPER));  // F = M Li^T
-    HIKF_TRY(tr(w.F, w.FT));
-    HIKF_TRY(gemm(w.F, w.FT, w.G1, KFULL));    // G1 = F F^T = (F^T)^T F^T
-    build_S<<<grid_for(n * n), kT, 0, st>>>(w.G1, n, 0.0, w.tmp2);
-    HIKF_CHECK_LAUNCH();
-    HIKF_TRY(factor(w.tmp2, w.L1, w.L1i, w.G1, n, w.status + 2, st));  // G1 = L1 L1^T
-    HIKF_TRY(tr(w.L1i, w.L1iT));
-    HIKF_TRY(gemm(w.FT, w.L1iT, w.Q1, KB_UPPER));  // Q1 = F^T L1^-T
-    HIKF_TRY(tr(w.Q1, w.Q1T));
-    HIKF_TRY(gemm(w.Q1T, w.Q1, w.G2, KFULL));      // G2 = Q1^T Q1 (~ I)
-    build_S<<<grid_for(n * n), kT, 0, st>>>(w.G2, n, 0.0, w.tmp2);
-    HIKF_CHECK_LAUNCH();
-    HIKF_TRY(factor(w.tmp2, w.L2, w.L2i, w.G2, n, w.status + 2, st));  // G2 = L2 L2^T
-    HIKF_TRY(gemm(w.L1, w.L2, w.LG, KB_LOWER));    // L_G = L1 L2 (= R^T)
   }
   {
     ProfScope pg(ST_FINALIZE, st);
@@ -762,7 +834,7 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
     GemmArgs g;  // psq = rowsum((C_Q L_G)^2), L_G lower triangular: no output store
     g.M = m; g.N = n; g.K = n;
     g.A = a.CQ; g.sa_r = n;
-    g.B = w.LG; g.sb_r = n;
+    g.B = LG; g.sb_r = n;
     g.C = nullptr; g.ldc = n;
     g.kmode = KB_LOWER;
     g.psq = w.psq; g.ldp = nt;
@@ -805,6 +877,7 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
   }
   if (use_la) {
     la->ready = false;
+    fl->ready = false;
     const int nx = hit ? la->cur ^ 1 : la->cur;
     ProfScope pf(ST_FACTOR, side);
     add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, side>>>(a.HC_out, a.HCQ, la->HCp, n * n);
@@ -818,6 +891,16 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
     la->r = a.r;
     la->hcq_ptr = a.HCQ;
     la->ready = true;
+    // the next step's factored chain from N_out (main) and S_{t+1} (just above)
+    const int fx = fhit ? fl->cur ^ 1 : fl->cur;
+    HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev_n, 0));
+    HIKF_CHECK_CUDA(cudaMemsetAsync(fl->status + fx, 0, sizeof(int), side));
+    HIKF_TRY(factored_chain(a.Nout, 1.0, la->Sinv[nx], la->LiT[nx], n, fl->c, fl->W[fx], fl->LG[fx], fl->status + fx,
+                            side));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(fl->N[fx], a.Nout, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
+    fl->cur = fx;
+    fl->la_slot = nx;
+    fl->ready = true;
   }
   HIKF_CHECK_CUDA(cudaEventRecord(ev[2], side));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[2], 0));

@@ -467,3 +467,27 @@ def test_factored_state_api(pkg):
     b = flt.hikf_update(ex, H, cfg["R"], g["obs"][2])
     for k in ("mean", "variance", "cross_cov", "HC"):
         assert O.rel_fro(getattr(a, k), getattr(b, k)) <= 1e-12, k
+
+
+def test_factored_lookahead_is_bit_identical(pkg):
+    """Factored steps reuse the (W, L_G) chain evaluated ahead on the side stream
+    (update.cu FacLookAhead) only after a bitwise check of N, HC and HC_Q; a run
+    where every step misses (HC_Q alternates between two equal buffers) must
+    equal the all-hits run bit for bit."""
+    import torch
+    flt = pkg.filters
+    g = _load("cfg1.npz")
+    cfg = cases.CFG1
+    tree, H, pre, _, model = _run_filter_factored(pkg, cfg, g["obs"], T=1)
+    pre2 = flt.HikfPrecompute(pre.C_Q_t, pre.HC_Q_t.clone(), pre.diag_Q_t)
+
+    def run(alternate):
+        st = flt.hikf_init(model, representation="factored")
+        for t in range(6):
+            p = pre2 if (alternate and t % 2) else pre
+            st = flt.hikf_update(flt.hikf_predict(st, p), H, cfg["R"], g["obs"][t])
+        return st
+
+    a, b = run(False), run(True)
+    for k in ("mean_t", "N_t", "variance_t", "HC_t"):
+        assert torch.equal(getattr(a, k), getattr(b, k)), k

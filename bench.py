@@ -638,7 +638,7 @@ def main():
         fst = {s: _lib.prof_read(s) for s in ("predict", "factor", "gemm_y", "finalize", "gemm_c")}
         ms_t, n_t = fst["gemm_c"]
         t_tri = ms_t / max(n_t, 1) / 1e3
-        bn = 128  # column tile of the K-range-limited triangular GEMM (k >= n0 per column tile)
+        bn = 64  # column tile of the K-range-limited triangular GEMM (variant 32; k >= n0 per column tile)
         tri_flops = sum(2.0 * m * min(bn, n - n0) * (n - n0) for n0 in range(0, n, bn))
         fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         fe0.record()

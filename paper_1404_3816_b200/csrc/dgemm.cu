@@ -591,6 +591,29 @@ __global__ void __launch_bounds__(CutlassMain<BM, BN, WTM, WTN, STAGES>::THREADS
   const int wm = warp % WM, wn = warp / WM;
   gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, g.C, g.Cin, m0, n0, tid, wm, wn, lane >> 2, lane & 3, red_sq,
                                           red_dot);
+  if (g.gv_y && blockIdx.x == gridDim.x - 1) {
+    // fused GEMV rows of this row block: one warp per row, 16-byte loads, lane-strided sums
+    const bool v2 = (g.K % 2 == 0) && (g.sa_r % 2 == 0) && ((((uintptr_t)g.A) | ((uintptr_t)g.gv_x)) & 15) == 0;
+    for (int r = warp; r < BM; r += CM::THREADS / 32) {
+      const int64_t row = m0 + r;
+      if (row >= g.M) break;
+      const double* a = g.A + row * g.sa_r;
+      double s = 0.0;
+      if (v2) {
+        const double2* a2 = reinterpret_cast<const double2*>(a);
+        const double2* x2 = reinterpret_cast<const double2*>(g.gv_x);
+        for (int64_t c = lane; c < g.K / 2; c += 32) {
+          const double2 av = a2[c], xv = __ldg(x2 + c);
+          s = fma(av.x, xv.x, s);
+          s = fma(av.y, xv.y, s);
+        }
+      } else {
+        for (int64_t c = lane; c < g.K; c += 32) s = fma(a[c], g.gv_x[c], s);
+      }
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) g.gv_y[row] = s;
+    }
+  }
 }
 
 template <int BM, int BN, int WTM, int WTN, int STAGES, bool P>
@@ -642,6 +665,12 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
     return part ? launch_cutlass<64, 128, 32, 64, 3, true>(g, st) : launch_cutlass<64, 128, 32, 64, 3, false>(g, st);
   if (variant == 31 && cutlass_ok)  // 64x128x16, 4 warps of 32x64, 4 stages
     return part ? launch_cutlass<64, 128, 32, 64, 4, true>(g, st) : launch_cutlass<64, 128, 32, 64, 4, false>(g, st);
+  if (variant == 32 && cutlass_ok)  // 128x64x16, 4 warps of 64x32, 3 stages (64-column tiles: finer triangles)
+    return part ? launch_cutlass<128, 64, 64, 32, 3, true>(g, st) : launch_cutlass<128, 64, 64, 32, 3, false>(g, st);
+  if (g.gv_y) {
+    set_error("dgemm: the fused GEMV (gv_x / gv_y) needs a CUTLASS variant (30-32) and row-major operands");
+    return HIKF_BAD_ARGUMENT;
+  }
   if (variant >= 30) variant = 7;
   switch (variant) {
     case 1:  // 128x128x32, 8 warps of 64x32, 3 stages

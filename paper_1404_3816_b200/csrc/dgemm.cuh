@@ -47,6 +47,11 @@ struct GemmArgs {
   const double* chain_add = nullptr;
   double* chain_out = nullptr;
   int64_t ldch = 0;
+  // optional fused GEMV over A (CUTLASS variants): gv_y[i] = sum_k A[i][k] gv_x[k] for all M rows,
+  // done by the CTAs of the last column tile (the shortest k-range under KB_LOWER) from the A
+  // panel their row block just streamed through L2
+  const double* gv_x = nullptr;
+  double* gv_y = nullptr;
   int variant = -1;  // tile-shape variant (-1: dgemm_variant())
 };
 
@@ -58,7 +63,7 @@ void set_dgemm_variant(int v);
 // number of column tiles (= partial sums per row) the current variant uses for N columns
 inline int dgemm_col_tiles(int64_t N, int variant = -1) {
   int v = variant >= 0 ? variant : dgemm_variant();
-  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22 || v == 28 || v == 29) ? 64 : 128);
+  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22 || v == 28 || v == 29 || v == 32) ? 64 : 128);
 }
 // variant used by the update's K GEMM (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log);
 // HIKF_DGEMM_VARIANT overrides it

@@ -19,6 +19,7 @@
 //        out rows = U[order[p]] (store; the sparse near field is added after).
 //        One CTA per (leaf, 64-row block); its warps stride over the columns.
 #include <algorithm>
+#include <cstdlib>
 
 #include "boxgemm.h"
 #include "fmm_device.cuh"
@@ -58,7 +59,7 @@ struct BoxArgs {
   unsigned long long* flops;
 };
 
-template <int NK4, int NRT>
+template <int NK4, int NRT, int MODE, bool PF, int CW>
 __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
   extern __shared__ double As[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
   const int K = g.K, lda = pad4(NK4 * 4);  // rows hold NK4*4 >= K entries (zero beyond K)
   int R, row_off = 0;
   const double* Ag;
-  if (g.mode == 0) {
+  if (MODE == 0) {
     R = 4 * g.q;
     Ag = g.shift;
   } else {
@@ -83,9 +84,12 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
   }
   __syncthreads();
 
-  const int64_t ncb = (g.n + 7) / 8;  // 8-column blocks per task
+  // a unit = one task x 8 CW columns: every A fragment read from shared memory
+  // feeds CW DMMAs (CW column tiles of 8)
+  constexpr int UW = 8 * CW;
+  const int64_t ncb = (g.n + UW - 1) / UW;
   int64_t unit0, unit_stride, units;
-  if (g.mode == 0) {
+  if (MODE == 0) {
     units = g.nparents * ncb;
     unit0 = (int64_t)blockIdx.x * (BW_THREADS / 32) + warp;
     unit_stride = (int64_t)gridDim.x * (BW_THREADS / 32);
@@ -95,71 +99,114 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
     unit_stride = BW_THREADS / 32;
   }
   unsigned long long useful = 0;
-  for (int64_t u = unit0; u < units; u += unit_stride) {
-    const int64_t task = g.mode == 0 ? u / ncb : blockIdx.x;
-    const int64_t j0 = (u % ncb) * 8;
-    const double* Bg = g.mode == 0 ? g.Lp + (int64_t)g.occp[task] * K * g.n
-                                   : g.Lleaf + (int64_t)g.leaf_box[task] * K * g.n;
-    const int64_t jb = j0 + gq;  // this lane's B column
-    double b[NK4];
+  // B fragments of a unit: one register per k-step and column tile (this lane's columns j0 + 8c + gq)
+  auto load_b = [&](int64_t u, double (&b)[CW][NK4]) {
+    const int64_t task = MODE == 0 ? u / ncb : blockIdx.x;
+    const int64_t j0 = (u % ncb) * UW;
+    const double* Bg = MODE == 0 ? g.Lp + (int64_t)g.occp[task] * K * g.n
+                                 : g.Lleaf + (int64_t)g.leaf_box[task] * K * g.n;
 #pragma unroll
-    for (int k4 = 0; k4 < NK4; ++k4) {
-      const int k = k4 * 4 + t4;
-      b[k4] = (k < K && jb < g.n) ? Bg[(int64_t)k * g.n + jb] : 0.0;
+    for (int c = 0; c < CW; ++c) {
+      const int64_t jb = j0 + 8 * c + gq;
+#pragma unroll
+      for (int k4 = 0; k4 < NK4; ++k4) {
+        const int k = k4 * 4 + t4;
+        b[c][k4] = (k < K && jb < g.n) ? Bg[(int64_t)k * g.n + jb] : 0.0;
+      }
     }
-    const int cols = (int)(g.n - j0 < 8 ? g.n - j0 : 8);
+  };
+  double bn[CW][NK4];  // software pipeline (PF): the next unit's fragments are in flight during this unit
+  if (PF && unit0 < units) load_b(unit0, bn);
+  for (int64_t u = unit0; u < units; u += unit_stride) {
+    const int64_t task = MODE == 0 ? u / ncb : blockIdx.x;
+    const int64_t j0 = (u % ncb) * UW;
+    double b[CW][NK4];
+    if (PF) {
+#pragma unroll
+      for (int c = 0; c < CW; ++c)
+#pragma unroll
+        for (int k4 = 0; k4 < NK4; ++k4) b[c][k4] = bn[c][k4];
+      if (u + unit_stride < units) load_b(u + unit_stride, bn);
+    } else {
+      load_b(u, b);
+    }
+    const int cols = (int)(g.n - j0 < UW ? g.n - j0 : UW);
     if (lane == 0) useful += 2ull * R * K * cols;
     int64_t X = 0, Y = 0;
-    if (g.mode == 0) {
+    if (MODE == 0) {
       const int64_t P = g.occp[task];
       X = P / g.Gp;
       Y = P % g.Gp;
     }
+    auto child_of = [&](int r, int& a) {
+      const int ci = r / g.q;
+      a = r - ci * g.q;
+      return (2 * X + (ci >> 1)) * (2 * g.Gp) + (2 * Y + (ci & 1));
+    };
     for (int r0 = 0; r0 < nrt; r0 += NRT) {
-      double acc[NRT][2];
+      // L2L: the M2L-sum init values are loaded before the DMMA chain (their
+      // latency hides under it) and added after it -- the reference's order
+      // (M2L sum, then + L2L) and the same rounding as adding them afterwards
+      double init[MODE == 0 ? NRT : 1][CW][2];
+      if (MODE == 0) {
 #pragma unroll
-      for (int i = 0; i < NRT; ++i) acc[i][0] = acc[i][1] = 0.0;
+        for (int i = 0; i < NRT; ++i) {
+          const int r = (r0 + i) * 8 + gq;
+#pragma unroll
+          for (int c = 0; c < CW; ++c) init[i][c][0] = init[i][c][1] = 0.0;
+          if (r0 + i < nrt && r < R) {
+            int a;
+            const int64_t irow = child_of(r, a) * g.n * g.q + a;
+#pragma unroll
+            for (int c = 0; c < CW; ++c)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int64_t jc = j0 + 8 * c + 2 * t4 + h;
+                if (jc < g.n) init[i][c][h] = g.S[irow + jc * g.q];
+              }
+          }
+        }
+      }
+      double acc[NRT][CW][2];
+#pragma unroll
+      for (int i = 0; i < NRT; ++i)
+#pragma unroll
+        for (int c = 0; c < CW; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
 #pragma unroll
       for (int k4 = 0; k4 < NK4; ++k4)
 #pragma unroll
         for (int i = 0; i < NRT; ++i)
-          if (r0 + i < nrt) dmma884(acc[i][0], acc[i][1], As[((r0 + i) * 8 + gq) * lda + k4 * 4 + t4], b[k4]);
-      // epilogue: rows (r0+i)*8+gq, columns j0 + 2 t4 + h; the init loads go first
-      const int64_t jc = j0 + 2 * t4;
-      if (g.mode == 0) {
-        int64_t orow[NRT], irow[NRT];
+          if (r0 + i < nrt) {
+            const double af = As[((r0 + i) * 8 + gq) * lda + k4 * 4 + t4];
 #pragma unroll
-        for (int i = 0; i < NRT; ++i) {
-          const int r = (r0 + i) * 8 + gq;
-          orow[i] = irow[i] = -1;
-          if (r0 + i < nrt && r < R) {
-            const int ci = r / g.q, a = r - ci * g.q;
-            const int64_t child = (2 * X + (ci >> 1)) * (2 * g.Gp) + (2 * Y + (ci & 1));
-            orow[i] = (child * g.q + a) * g.n;
-            irow[i] = child * g.n * g.q + a;
+            for (int c = 0; c < CW; ++c) dmma884(acc[i][c][0], acc[i][c][1], af, b[c][k4]);
           }
+      // epilogue: rows (r0+i)*8+gq, columns j0 + 8 c + 2 t4 + h
+#pragma unroll
+      for (int i = 0; i < NRT; ++i) {
+        const int r = (r0 + i) * 8 + gq;
+        if (r0 + i >= nrt || r >= R) continue;
+        double* orow;
+        if (MODE == 0) {
+          int a;
+          orow = g.L + (child_of(r, a) * g.q + a) * g.n;
+        } else {
+          const int64_t orw = g.order[g.leaf_start[task] + row_off + r];
+          if (orw < g.r0 || orw >= g.r1) continue;
+          orow = g.U + (orw - g.r0) * g.ldu;
         }
 #pragma unroll
-        for (int i = 0; i < NRT; ++i)
+        for (int c = 0; c < CW; ++c) {
+          const int64_t jc = j0 + 8 * c + 2 * t4;
+          if (jc + 1 < g.n && (((uintptr_t)(orow + jc)) & 15) == 0) {
+            const double v0 = MODE == 0 ? acc[i][c][0] + init[MODE == 0 ? i : 0][c][0] : acc[i][c][0];
+            const double v1 = MODE == 0 ? acc[i][c][1] + init[MODE == 0 ? i : 0][c][1] : acc[i][c][1];
+            *reinterpret_cast<double2*>(orow + jc) = make_double2(v0, v1);
+          } else {
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (orow[i] >= 0 && jc + h < g.n) acc[i][h] += g.S[irow[i] + (jc + h) * g.q];
-#pragma unroll
-        for (int i = 0; i < NRT; ++i)
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (orow[i] >= 0 && jc + h < g.n) g.L[orow[i] + jc + h] = acc[i][h];
-      } else {
-#pragma unroll
-        for (int i = 0; i < NRT; ++i) {
-          const int r = (r0 + i) * 8 + gq;
-          if (r0 + i >= nrt || r >= R) continue;
-          const int64_t orow = g.order[g.leaf_start[task] + row_off + r];
-          if (orow < g.r0 || orow >= g.r1) continue;
-          double* urow = g.U + (orow - g.r0) * g.ldu;
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (jc + h < g.n) urow[jc + h] = acc[i][h];
+            for (int h = 0; h < 2; ++h)
+              if (jc + h < g.n) orow[jc + h] = MODE == 0 ? acc[i][c][h] + init[MODE == 0 ? i : 0][c][h] : acc[i][c][h];
+          }
         }
       }
     }
@@ -176,27 +223,44 @@ size_t box_smem(int R, int K) {
   return sizeof(double) * (size_t)(((R + 7) >> 3) * 8) * pad4(4 * k4_bucket(K));
 }
 
-template <int NK4, int NRT>
+template <int NK4, int NRT, int MODE, bool PF, int CW>
 int launch_box_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   static size_t configured = 0;
+  auto kern = box_warp_kernel<NK4, NRT, MODE, PF, CW>;
   if (smem > configured) {
-    HIKF_CHECK_CUDA(cudaFuncSetAttribute(box_warp_kernel<NK4, NRT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 << 10)));
     configured = std::max<size_t>(smem, 48 << 10);
   }
-  box_warp_kernel<NK4, NRT><<<grid, BW_THREADS, smem, st>>>(a);
+  kern<<<grid, BW_THREADS, smem, st>>>(a);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
 
-// compile-time k-steps: exactly ceil(K/4); 8 row tiles per register pass
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <int K4>
+int launch_box_k(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
+  // tuning knobs (profiles/r01_box_sweep.log): column tiles per unit (CW) per mode; the
+  // L2L uses 4 row tiles per pass with the B prefetch, the L2P 8
+  static const int cw0 = env_int("HIKF_BOX_CW0", 1), cw1 = env_int("HIKF_BOX_CW1", 1);
+  if (a.mode == 0)
+    return cw0 == 2 ? launch_box_t<K4, 4, 0, false, 2>(a, grid, smem, st)
+                    : launch_box_t<K4, 4, 0, true, 1>(a, grid, smem, st);
+  return cw1 == 2 ? launch_box_t<K4, 8, 1, false, 2>(a, grid, smem, st) : launch_box_t<K4, 8, 1, true, 1>(a, grid, smem, st);
+}
+
+// compile-time k-steps: exactly ceil(K/4)
 int launch_box(const BoxArgs& a, int R, dim3 grid, cudaStream_t st) {
   const size_t smem = box_smem(R, a.K);
   const int nk4 = (a.K + 3) / 4;
 
-#define HIKF_BOX(K4)                                                                          \
-  if (nk4 <= K4)                                                                              \
-    return launch_box_t<K4, BW_RT>(a, grid, smem, st);
+#define HIKF_BOX(K4)          \
+  if (nk4 <= K4)              \
+    return launch_box_k<K4>(a, grid, smem, st);
   HIKF_BOX(1) HIKF_BOX(2) HIKF_BOX(3) HIKF_BOX(4) HIKF_BOX(5) HIKF_BOX(6) HIKF_BOX(7) HIKF_BOX(8)
   HIKF_BOX(9) HIKF_BOX(10) HIKF_BOX(11) HIKF_BOX(12) HIKF_BOX(13) HIKF_BOX(14) HIKF_BOX(15) HIKF_BOX(16)
 #undef HIKF_BOX

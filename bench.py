@@ -557,8 +557,7 @@ def main():
     fmm_useful = {s: _lib.prof_flops(s) for s in ("p2p", "p2m", "m2m", "m2l", "l2l", "l2p")}
     qht_useful = float(sum(fmm_useful.values()))
     if dim3:
-        ff = fmm3_flops(tree, n)
-        qht_useful = float(sum(ff.values()))  # the 3D kernels perform the dense formulation
+        ff = fmm3_flops(tree, n)  # dense formulation; the kernels skip all-zero sources and empty boxes
     else:
         ex = tree.export()
         cnt = ex["leaf_counts"]
@@ -697,8 +696,8 @@ def main():
                 "stage_gflop_performed": {k: v / 1e9 for k, v in fmm_useful.items()},
                 "roofline": {"bound": "fp64", "achieved": qht_useful / t_qht / 1e12, "peak": FP64_PEAK_TFLOPS,
                              "unit": "TFLOP/s", "frac": qht_useful / t_qht / 1e12 / FP64_PEAK_TFLOPS,
-                             "note": "performed flops (H^T sparsity exploited: only nonzero charge columns are "
-                                     "multiplied); dense-formulation equivalent rate = "
+                             "note": "performed flops counted in the kernels (H^T sparsity exploited: only nonzero "
+                                     "charges / expansions are multiplied); dense-formulation equivalent rate = "
                                      f"{qht_flops / t_qht / 1e12:.1f} TFLOP/s",
                              "m2l": {"achieved": fmm_useful["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
         "roofline": {"kernel": "dgemm_cutlass_kernel (K = C' S^-1 -> C_new = r K, fused rowsum(K o C'), K innov and the "

@@ -2,6 +2,8 @@
 // upward pass (P2M, M2M) and the downward pass (M2L fused with L2L, L2P),
 // each stage a seg_gemm_kernel launch over boxes x column tiles.
 #include <algorithm>
+#include <cstring>
+#include <cstdlib>
 
 #include "boxgemm.h"
 #include "fmm_device.cuh"
@@ -495,6 +497,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   QhtStreams* qs = nullptr;
   HIKF_TRY(qht_streams(&qs));
+  // timing experiments only (tools/qht_time.py): HIKF_QHT_SKIP = comma list of stages to skip
+  // (p2p, m2l, m2llow, l2l, l2p); the result is then wrong
+  static const char* skip_env = getenv("HIKF_QHT_SKIP");
+  auto skip = [&](const char* s) { return skip_env && strstr(skip_env, s); };
   cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1], ev_up = qs->e[2];
 
   // ---- near field, concurrently: sums parked in Pnear, added after L2P ----
@@ -505,7 +511,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   int status = HIKF_OK;
   {
     ProfScope ps(ST_P2P, qs->s[0]);
-    status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear);
+    if (!skip("p2p")) status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear);
   }
   HIKF_CHECK_CUDA(cudaEventRecord(ev_p2p, qs->s[0]));
 
@@ -538,7 +544,9 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       const int q = t->orders[l] * t->orders[l];
       ProfScope ps(ST_M2L, sl);
       HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, sl));
-      for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot) status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl);
+      const bool sk = skip("m2l,") || (skip("m2llow") && l < D);
+      for (int slot = 0; slot < 40 && status == HIKF_OK && !sk; ++slot)
+        status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl);
       HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
     }
   }
@@ -552,7 +560,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
     if (l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
       ProfScope ps(ST_L2L, st);
-      status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st);
+      if (!skip("l2l")) status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st);
     } else {
       ProfScope ps(ST_L2L, st);
       status = pair_to_box(t, l, scratch[l], n, Lcur, st);
@@ -573,7 +581,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
-    status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
+    if (!skip("l2p")) status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
   } else if (status == HIKF_OK && window) {
     set_error("row-windowed Q H^T needs the box-streaming L2P (leaf order <= 8)");
     status = HIKF_BAD_ARGUMENT;

@@ -185,7 +185,13 @@ struct Chunk {
   int kc;           // columns in this chunk
   double* U;        // m x ldu, original order
   int64_t ldu;
+  unsigned long long* flops;  // performed-flop counter of the stage (profiling on), or null
 };
+
+// one atomic per CTA: thread 0's tally of the flops the CTA performed
+__device__ __forceinline__ void count_flops(unsigned long long* c, unsigned long long v) {
+  if (c && threadIdx.x == 0 && v) atomicAdd(c, v);
+}
 
 // ---- P2P: U[t] = sum_nbr K(t, s) V[s] (first write of the chunk's U columns) ----
 __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, const uint8_t* __restrict__ leafnz) {
@@ -200,12 +206,14 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, cons
   const int j0 = warp * 8;  // this warp's 8 columns of the chunk (kc <= 64)
   double acc[MAXRT][2];
   zero_acc(acc);
+  unsigned long long done = 0;
   for (int s = 0; s < 27; ++s) {
     const int64_t x = bx + s / 9 - 1, y = by + (s / 3) % 3 - 1, z = bz + s % 3 - 1;
     if (x < 0 || y < 0 || z < 0 || x >= G || y >= G || z >= G) continue;
     const int sl = t.box2leaf[(x * G + y) * G + z];
     if (sl < 0 || !leafnz[sl]) continue;  // no leaf / all-zero charges: uniform across the CTA
     const int ss = t.leaf_start[sl], sc = t.leaf_count[sl];
+    done += 2ull * tc * sc * ch.kc;
     __syncthreads();
     load_A(As, lda, nrt * 8, ((sc + 3) / 4) * 4, tc, sc, [&](int r, int c) {
       const double* a = t.pts + 3 * (int64_t)(ts + r);
@@ -220,6 +228,7 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, cons
       }, acc);
     }
   }
+  count_flops(ch.flops, done);
   if (j0 >= ch.kc) return;
 #pragma unroll
   for (int rt = 0; rt < MAXRT; ++rt) {
@@ -242,6 +251,7 @@ __global__ void __launch_bounds__(T3, 1) p2m3_kernel(const T3v t, Chunk ch, doub
   if (!leafnz[leaf]) return;  // W stays zero (memset)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf], q = t.q;
+  count_flops(ch.flops, 2ull * q * tc * ch.kc);
   const int nrt = (q + 7) >> 3, lda = pad4(((t.max_count + 3) / 4) * 4);
   load_A(As, lda, nrt * 8, ((tc + 3) / 4) * 4, q, tc,
          [&](int a, int p) { return t.W2[(int64_t)(ts + p) * q + a]; });
@@ -270,6 +280,7 @@ __global__ void __launch_bounds__(T3, 1) l2p3_kernel(const T3v t, Chunk ch, cons
   const int leaf = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf], q = t.q;
+  count_flops(ch.flops, 2ull * tc * q * ch.kc);
   const int nrt = (tc + 7) >> 3, lda = pad4(((q + 3) / 4) * 4);
   load_A(As, lda, nrt * 8, ((q + 3) / 4) * 4, tc, q, [&](int r, int a) { return t.W2[(int64_t)(ts + r) * q + a]; });
   __syncthreads();
@@ -306,7 +317,26 @@ struct BoxOpArgs {
   const int* offs;           // M2L: 316 x 3
   int kc;
   const uint8_t* nz;         // M2L: per source box, 1 if its expansion has a nonzero in this chunk
+  const uint8_t* occ;        // M2L / L2L: per output box, 1 if any point lies below it (else skipped:
+                             // its locals are never read -- L2L children and L2P leaves are occupied)
+  unsigned long long* flops; // performed-flop counter (profiling on), or null
 };
+
+// occupancy of the boxes of each level: occ_D[box] = has a leaf; occ_l = OR of the 8 children
+__global__ void occ_leaf(const int32_t* __restrict__ box2leaf, int64_t nb, uint8_t* __restrict__ occ) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+    occ[b] = box2leaf[b] >= 0 ? 1 : 0;
+}
+__global__ void occ_parent(const uint8_t* __restrict__ occc, int64_t G, uint8_t* __restrict__ occp) {
+  const int64_t nb = G * G * G, Gc = 2 * G;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = b / (G * G), y = (b / G) % G, z = b % G;
+    uint8_t o = 0;
+    for (int c = 0; c < 8; ++c)
+      o |= occc[((2 * x + ((c >> 2) & 1)) * Gc + (2 * y + ((c >> 1) & 1))) * Gc + (2 * z + (c & 1))];
+    occp[b] = o;
+  }
+}
 
 // leafnz[l] = any(V[order[p]][j] != 0) over the leaf's points p, j < kc: P2P / P2M skip all-zero
 // source leaves (exact: they contribute zeros)
@@ -360,6 +390,7 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     oz = 2 * pz + (g.cls & 1);
   }
   const int64_t obox = (ox * G + oy) * G + oz;
+  if (g.occ && !g.occ[obox]) return;  // empty output box (CTA-uniform, before any barrier)
   const int nterms = g.mode == OP_M2L ? NOFF : (g.mode == OP_M2M ? 8 : 1);
   // term -> (operator, source box); -1 when the term does not apply (CTA-uniform)
   auto term_src = [&](int term, const double** A) -> int64_t {
@@ -412,7 +443,9 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
   int term = next_term(0), sl = 0, slot = 0;
   if (term < nterms) issue(term, 0, 0);
   cp_async_commit();
+  unsigned long long done = 0;
   while (term < nterms) {
+    if (sl == 0) done += 2ull * q * q * g.kc;
     // next step (slice of this term, or the first slice of the next valid term)
     int nterm = term, nsl = sl + 1;
     if (nsl == nslices) {
@@ -444,6 +477,7 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     slot ^= 1;
   }
   cp_async_wait<0>();
+  count_flops(g.flops, done);
   if (j0 >= g.kc) return;
   double* O = g.out + obox * (int64_t)q * KC;
 #pragma unroll
@@ -692,6 +726,20 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     }
   uint8_t* LNZ = nullptr;
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&LNZ, std::max<int64_t>(nl, 1), st));
+  uint8_t* OCC[kMaxDepth + 1] = {nullptr};
+  if (D >= 2) {
+    for (int l = 2; l <= D; ++l) HIKF_CHECK_CUDA(cudaMallocAsync((void**)&OCC[l], (int64_t)1 << (3 * l), st));
+    const int64_t nbD = (int64_t)1 << (3 * D);
+    occ_leaf<<<(unsigned)std::min<int64_t>((nbD + 255) / 256, num_sms() * 16), 256, 0, st>>>(t->box2leaf, nbD,
+                                                                                             OCC[D]);
+    HIKF_CHECK_LAUNCH();
+    for (int l = D - 1; l >= 2; --l) {
+      const int64_t nb = (int64_t)1 << (3 * l);
+      occ_parent<<<(unsigned)std::min<int64_t>((nb + 255) / 256, num_sms() * 16), 256, 0, st>>>(OCC[l + 1],
+                                                                                                (int64_t)1 << l, OCC[l]);
+      HIKF_CHECK_LAUNCH();
+    }
+  }
   auto flag = [&](int l, int kc) {
     const int64_t nb = (int64_t)1 << (3 * l);
     nonzero_boxes<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, st>>>(W[l], nb, q, kc, NZ[l]);
@@ -700,11 +748,12 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
   const T3v tv = view(t);
   int status = HIKF_OK;
   for (int64_t c0 = 0; c0 < k && status == HIKF_OK; c0 += KC) {
-    Chunk ch{V + c0, ldv, (int)std::min<int64_t>(KC, k - c0), U + c0, ldu};
+    Chunk ch{V + c0, ldv, (int)std::min<int64_t>(KC, k - c0), U + c0, ldu, nullptr};
     nonzero_leaves<<<(unsigned)((nl * 32 + 255) / 256), 256, 0, st>>>(tv, ch.V, ch.ldv, ch.kc, nl, LNZ);
     HIKF_CHECK_LAUNCH();
     {
       ProfScope ps(ST_P2P, st);
+      ch.flops = prof_flops_ptr(ST_P2P);
       p2p3_kernel<<<(unsigned)nl, T3, sm_p2p, st>>>(tv, ch, LNZ);
       HIKF_CHECK_LAUNCH();
     }
@@ -712,13 +761,15 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     {
       ProfScope ps(ST_P2M, st);
       HIKF_CHECK_CUDA(cudaMemsetAsync(W[D], 0, sizeof(double) * ((int64_t)1 << (3 * D)) * q * KC, st));
+      ch.flops = prof_flops_ptr(ST_P2M);
       p2m3_kernel<<<(unsigned)nl, T3, sm_p2m, st>>>(tv, ch, W[D], LNZ);
       HIKF_CHECK_LAUNCH();
       HIKF_TRY(flag(D, ch.kc));
     }
     for (int l = D - 1; l >= 2; --l) {
       ProfScope ps(ST_M2M, st);
-      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, NZ[l + 1]};
+      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, NZ[l + 1], nullptr,
+                  prof_flops_ptr(ST_M2M)};
       boxop3_kernel<<<(unsigned)((int64_t)1 << (3 * l)), T3, sm_box, st>>>(a);
       HIKF_CHECK_LAUNCH();
       HIKF_TRY(flag(l, ch.kc));
@@ -728,7 +779,8 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
         ProfScope ps(ST_M2L, st);
         const int64_t units = (int64_t)1 << (3 * (l - 1));  // parents: one class-c child each
         for (int c = 0; c < 8; ++c) {
-          BoxOpArgs a{OP_M2L, q, l, c, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l]};
+          BoxOpArgs a{OP_M2L, q, l, c, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l], OCC[l],
+                      prof_flops_ptr(ST_M2L)};
           boxop3_kernel<<<(unsigned)units, T3, sm_box, st>>>(a);
           HIKF_CHECK_LAUNCH();
         }
@@ -737,7 +789,8 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
         ProfScope ps(ST_L2L, st);
         const int64_t units = (int64_t)1 << (3 * (l - 1));
         for (int c = 0; c < 8; ++c) {
-          BoxOpArgs a{OP_L2L, q, l, c, (int64_t)1 << l, L[l - 1], L[l], t->shift, nullptr, ch.kc, nullptr};
+          BoxOpArgs a{OP_L2L, q, l, c, (int64_t)1 << l, L[l - 1], L[l], t->shift, nullptr, ch.kc, nullptr, OCC[l],
+                      prof_flops_ptr(ST_L2L)};
           boxop3_kernel<<<(unsigned)units, T3, sm_box, st>>>(a);
           HIKF_CHECK_LAUNCH();
         }
@@ -745,6 +798,7 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     }
     {
       ProfScope ps(ST_L2P, st);
+      ch.flops = prof_flops_ptr(ST_L2P);
       l2p3_kernel<<<(unsigned)nl, T3, sm_l2p, st>>>(tv, ch, L[D]);
       HIKF_CHECK_LAUNCH();
     }
@@ -753,6 +807,7 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     cudaFreeAsync(W[l], st);
     cudaFreeAsync(L[l], st);
     cudaFreeAsync(NZ[l], st);
+    cudaFreeAsync(OCC[l], st);
   }
   cudaFreeAsync(LNZ, st);
   return status;

@@ -153,14 +153,24 @@ __global__ void m2l3_ops_kernel(int n, double h, const double* __restrict__ node
 }
 
 // ---- warp GEMM core: acc[rt] (+)= A[rt*8 + g][k] * B[k][j0 + g], k < nk4 * 4 ----
+// The B fragments (global loads) are fetched 8 k-steps at a time ahead of
+// their DMMAs, so a batch pays one memory latency instead of eight.
 template <class BFrag>
 __device__ __forceinline__ void warp_gemm(const double* As, int lda, int nrt, int nk4, int gq, int t4, BFrag bf,
                                           double (&acc)[MAXRT][2]) {
-  for (int k4 = 0; k4 < nk4; ++k4) {
-    const double b = bf(k4 * 4 + t4);
+  constexpr int KB = 8;
+  for (int kb = 0; kb < nk4; kb += KB) {
+    double b[KB];
 #pragma unroll
-    for (int rt = 0; rt < MAXRT; ++rt)
-      if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], As[(rt * 8 + gq) * lda + k4 * 4 + t4], b);
+    for (int i = 0; i < KB; ++i) b[i] = kb + i < nk4 ? bf((kb + i) * 4 + t4) : 0.0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      if (kb + i >= nk4) break;
+      const int k4 = kb + i;
+#pragma unroll
+      for (int rt = 0; rt < MAXRT; ++rt)
+        if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], As[(rt * 8 + gq) * lda + k4 * 4 + t4], b[i]);
+    }
   }
 }
 
@@ -376,7 +386,11 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
   extern __shared__ double As[];  // 2 slots
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int q = g.q, nrt = (q + 7) >> 3, nslices = (q + KS - 1) / KS;
-  const int64_t G = g.Gout, unit = blockIdx.x;
+  const int64_t G = g.Gout;
+  // M2L / L2L launch all 8 child classes at once: blockIdx.x = class * parents + parent
+  const int64_t nunit = g.mode == OP_M2M ? (int64_t)gridDim.x : (int64_t)gridDim.x / 8;
+  const int64_t unit = blockIdx.x % nunit;
+  const int cls = g.mode == OP_M2M ? 0 : (int)(blockIdx.x / nunit);
   int64_t ox, oy, oz;
   if (g.mode == OP_M2M) {
     ox = unit / (G * G);
@@ -385,9 +399,9 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
   } else {  // the class-c child of parent `unit`
     const int64_t Gp = G / 2;
     const int64_t px = unit / (Gp * Gp), py = (unit / Gp) % Gp, pz = unit % Gp;
-    ox = 2 * px + ((g.cls >> 2) & 1);
-    oy = 2 * py + ((g.cls >> 1) & 1);
-    oz = 2 * pz + (g.cls & 1);
+    ox = 2 * px + ((cls >> 2) & 1);
+    oy = 2 * py + ((cls >> 1) & 1);
+    oz = 2 * pz + (cls & 1);
   }
   const int64_t obox = (ox * G + oy) * G + oz;
   if (g.occ && !g.occ[obox]) return;  // empty output box (CTA-uniform, before any barrier)
@@ -397,7 +411,7 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     if (g.mode == OP_M2L) {
       const int dx = g.offs[3 * term], dy = g.offs[3 * term + 1], dz = g.offs[3 * term + 2];
       // parents adjacent per axis (fmm.py:301-302); floor((c + d) / 2) is the parent offset
-      const int cx = (g.cls >> 2) & 1, cy = (g.cls >> 1) & 1, cz = g.cls & 1;
+      const int cx = (cls >> 2) & 1, cy = (cls >> 1) & 1, cz = cls & 1;
       const int pdx = (cx + dx) >> 1, pdy = (cy + dy) >> 1, pdz = (cz + dz) >> 1;
       if (pdx < -1 || pdx > 1 || pdy < -1 || pdy > 1 || pdz < -1 || pdz > 1) return -1;
       const int64_t sx = ox + dx, sy = oy + dy, sz = oz + dz;
@@ -416,7 +430,7 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
       return cb;
     }
     const int64_t Gp = G / 2;
-    *A = g.ops + (int64_t)g.cls * q * q;  // shift[c]: child coeff x parent coeff
+    *A = g.ops + (int64_t)cls * q * q;  // shift[c]: child coeff x parent coeff
     return ((ox >> 1) * Gp + (oy >> 1)) * Gp + (oz >> 1);
   };
   auto next_term = [&](int from) {
@@ -444,6 +458,22 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
   if (term < nterms) issue(term, 0, 0);
   cp_async_commit();
   unsigned long long done = 0;
+  // B fragments of a slice (this lane's column jc, k = k0 + 4 k4 + t4), one register per
+  // k-step; the next slice's are loaded while this slice's DMMAs run
+  constexpr int NK4S = KS / 4;
+  auto load_bs = [&](int tm, int s, double (&b)[NK4S]) {
+    const double* Aop;
+    const int64_t sbox = term_src(tm, &Aop);
+    const double* B = g.in + sbox * (int64_t)q * KC;
+    const int k0 = s * KS;
+#pragma unroll
+    for (int k4 = 0; k4 < NK4S; ++k4) {
+      const int k = k0 + k4 * 4 + t4;
+      b[k4] = (k < q && jc < g.kc) ? B[(int64_t)k * KC + jc] : 0.0;
+    }
+  };
+  double bcur[NK4S];
+  if (term < nterms && j0 < g.kc) load_bs(term, 0, bcur);
   while (term < nterms) {
     if (sl == 0) done += 2ull * q * q * g.kc;
     // next step (slice of this term, or the first slice of the next valid term)
@@ -454,24 +484,25 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     }
     if (nterm < nterms) issue(nterm, nsl, slot ^ 1);
     cp_async_commit();
+    double bnext[NK4S];
+    if (nterm < nterms && j0 < g.kc) load_bs(nterm, nsl, bnext);
     cp_async_wait<1>();
     __syncthreads();
     if (j0 < g.kc) {
-      const double* Aop;
-      const int64_t sbox = term_src(term, &Aop);
-      const double* B = g.in + sbox * (int64_t)q * KC;
       const double* Asl = As + slot * SLICE;
       const int k0 = sl * KS;
       const int nk4 = (min(KS, q - k0) + 3) / 4;
-      for (int k4 = 0; k4 < nk4; ++k4) {
-        const int k = k0 + k4 * 4 + t4;
-        const double b = (k < q && jc < g.kc) ? B[(int64_t)k * KC + jc] : 0.0;
+#pragma unroll
+      for (int k4 = 0; k4 < NK4S; ++k4) {
+        if (k4 >= nk4) break;
 #pragma unroll
         for (int rt = 0; rt < MAXRT; ++rt)
-          if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], Asl[(rt * 8 + gq) * KLD + k4 * 4 + t4], b);
+          if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], Asl[(rt * 8 + gq) * KLD + k4 * 4 + t4], bcur[k4]);
       }
     }
     __syncthreads();  // everyone is done with `slot` before it is refilled
+#pragma unroll
+    for (int k4 = 0; k4 < NK4S; ++k4) bcur[k4] = bnext[k4];
     term = nterm;
     sl = nsl;
     slot ^= 1;
@@ -777,23 +808,19 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     for (int l = 2; l <= D; ++l) {
       {
         ProfScope ps(ST_M2L, st);
-        const int64_t units = (int64_t)1 << (3 * (l - 1));  // parents: one class-c child each
-        for (int c = 0; c < 8; ++c) {
-          BoxOpArgs a{OP_M2L, q, l, c, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l], OCC[l],
-                      prof_flops_ptr(ST_M2L)};
-          boxop3_kernel<<<(unsigned)units, T3, sm_box, st>>>(a);
-          HIKF_CHECK_LAUNCH();
-        }
+        const int64_t units = (int64_t)1 << (3 * (l - 1));  // parents x 8 child classes, one launch
+        BoxOpArgs a{OP_M2L, q, l, 0, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l], OCC[l],
+                    prof_flops_ptr(ST_M2L)};
+        boxop3_kernel<<<(unsigned)(8 * units), T3, sm_box, st>>>(a);
+        HIKF_CHECK_LAUNCH();
       }
       if (l > 2) {
         ProfScope ps(ST_L2L, st);
         const int64_t units = (int64_t)1 << (3 * (l - 1));
-        for (int c = 0; c < 8; ++c) {
-          BoxOpArgs a{OP_L2L, q, l, c, (int64_t)1 << l, L[l - 1], L[l], t->shift, nullptr, ch.kc, nullptr, OCC[l],
-                      prof_flops_ptr(ST_L2L)};
-          boxop3_kernel<<<(unsigned)units, T3, sm_box, st>>>(a);
-          HIKF_CHECK_LAUNCH();
-        }
+        BoxOpArgs a{OP_L2L, q, l, 0, (int64_t)1 << l, L[l - 1], L[l], t->shift, nullptr, ch.kc, nullptr, OCC[l],
+                    prof_flops_ptr(ST_L2L)};
+        boxop3_kernel<<<(unsigned)(8 * units), T3, sm_box, st>>>(a);
+        HIKF_CHECK_LAUNCH();
       }
     }
     {

@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, cons
     const int sl = t.box2leaf[(x * G + y) * G + z];
     if (sl < 0 || !leafnz[sl]) continue;  // no leaf / all-zero charges: uniform across the CTA
     const int ss = t.leaf_start[sl], sc = t.leaf_count[sl];
-    done += 2ull * tc * sc * ch.kc;
+    const bool mine = (leafnz[sl] >> warp) & 1;  // this warp's 8 columns hold a nonzero charge
+    if (mine) done += 2ull * tc * sc * min(8, ch.kc - j0);
     __syncthreads();
     load_A(As, lda, nrt * 8, ((sc + 3) / 4) * 4, tc, sc, [&](int r, int c) {
       const double* a = t.pts + 3 * (int64_t)(ts + r);
@@ -231,14 +232,14 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, cons
       return k3_of_r(t.k.family, t.k.variance, d3(a[0], a[1], a[2], b[0], b[1], b[2]));
     });
     __syncthreads();
-    if (j0 < ch.kc) {
+    if (j0 < ch.kc && mine) {
       const int jc = j0 + gq;
       warp_gemm(As, lda, nrt, (sc + 3) / 4, gq, t4, [&](int k) {
         return (k < sc && jc < ch.kc) ? ch.V[t.order[ss + k] * ch.ldv + jc] : 0.0;
       }, acc);
     }
   }
-  count_flops(ch.flops, done);
+  if (ch.flops && lane == 0 && done) atomicAdd(ch.flops, done);
   if (j0 >= ch.kc) return;
 #pragma unroll
   for (int rt = 0; rt < MAXRT; ++rt) {
@@ -261,13 +262,13 @@ __global__ void __launch_bounds__(T3, 1) p2m3_kernel(const T3v t, Chunk ch, doub
   if (!leafnz[leaf]) return;  // W stays zero (memset)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf], q = t.q;
-  count_flops(ch.flops, 2ull * q * tc * ch.kc);
   const int nrt = (q + 7) >> 3, lda = pad4(((t.max_count + 3) / 4) * 4);
   load_A(As, lda, nrt * 8, ((tc + 3) / 4) * 4, q, tc,
          [&](int a, int p) { return t.W2[(int64_t)(ts + p) * q + a]; });
   __syncthreads();
   const int j0 = warp * 8;
-  if (j0 >= ch.kc) return;
+  if (j0 >= ch.kc || !((leafnz[leaf] >> warp) & 1)) return;  // W stays zero (memset) for all-zero columns
+  if (ch.flops && lane == 0) atomicAdd(ch.flops, 2ull * q * tc * min(8, ch.kc - j0));
   const int jc = j0 + gq;
   double acc[MAXRT][2];
   zero_acc(acc);
@@ -348,30 +349,34 @@ __global__ void occ_parent(const uint8_t* __restrict__ occc, int64_t G, uint8_t*
   }
 }
 
-// leafnz[l] = any(V[order[p]][j] != 0) over the leaf's points p, j < kc: P2P / P2M skip all-zero
-// source leaves (exact: they contribute zeros)
+// leafnz[l] = per-warp mask of any(V[order[p]][j] != 0) over the leaf's points p and the warp's 8
+// columns: P2P / P2M skip all-zero source leaves per CTA and per warp (exact: they contribute zeros)
 __global__ void nonzero_leaves(const T3v t, const double* __restrict__ V, int64_t ldv, int kc, int64_t nl,
                                uint8_t* __restrict__ nz) {
   const int64_t leaf = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (leaf >= nl) return;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf];
-  bool any = false;
-  for (int e = lane; e < tc * kc && !any; e += 32) any = V[t.order[ts + e / kc] * ldv + e % kc] != 0.0;
-  any = __any_sync(0xffffffffu, any);
-  if (lane == 0) nz[leaf] = any ? 1 : 0;
+  // bit w: some charge in columns 8w .. 8w + 7 (warp w's columns in the leaf / box kernels)
+  unsigned mask = 0;
+  for (int e = lane; e < tc * kc; e += 32)
+    if (V[t.order[ts + e / kc] * ldv + e % kc] != 0.0) mask |= 1u << ((e % kc) >> 3);
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  if (lane == 0) nz[leaf] = (uint8_t)mask;
 }
 
-// nz[box] = any(W[box][a][j] != 0, a < q, j < kc): M2L skips all-zero sources (exact: they add zeros)
+// nz[box] = per-warp mask of any(W[box][a][j] != 0, a < q, j in the warp's 8 columns): M2L / M2M skip
+// all-zero sources per CTA and per warp (exact: they add zeros)
 __global__ void nonzero_boxes(const double* __restrict__ W, int64_t nboxes, int q, int kc, uint8_t* __restrict__ nz) {
   const int64_t box = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (box >= nboxes) return;
   const double* w = W + box * (int64_t)q * KC;
-  bool any = false;
-  for (int e = lane; e < q * kc && !any; e += 32) any = w[(int64_t)(e / kc) * KC + e % kc] != 0.0;
-  any = __any_sync(0xffffffffu, any);
-  if (lane == 0) nz[box] = any ? 1 : 0;
+  unsigned mask = 0;  // bit w: some coefficient in columns 8w .. 8w + 7 is nonzero
+  for (int e = lane; e < q * kc; e += 32)
+    if (w[(int64_t)(e / kc) * KC + e % kc] != 0.0) mask |= 1u << ((e % kc) >> 3);
+  mask = __reduce_or_sync(0xffffffffu, mask);
+  if (lane == 0) nz[box] = (uint8_t)mask;
 }
 
 // one CTA = one output box; warp w owns chunk columns 8w .. 8w + 7.  The
@@ -458,6 +463,12 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
   if (term < nterms) issue(term, 0, 0);
   cp_async_commit();
   unsigned long long done = 0;
+  // this warp's part of a term: M2L / M2M skip the 8 columns that are all zero in the source
+  auto mine = [&](int tm) -> bool {
+    if (g.mode == OP_L2L || !g.nz) return true;
+    const double* A;
+    return (g.nz[term_src(tm, &A)] >> warp) & 1;
+  };
   // B fragments of a slice (this lane's column jc, k = k0 + 4 k4 + t4), one register per
   // k-step; the next slice's are loaded while this slice's DMMAs run
   constexpr int NK4S = KS / 4;
@@ -473,9 +484,10 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     }
   };
   double bcur[NK4S];
-  if (term < nterms && j0 < g.kc) load_bs(term, 0, bcur);
+  bool mcur = term < nterms && j0 < g.kc && mine(term);
+  if (mcur) load_bs(term, 0, bcur);
   while (term < nterms) {
-    if (sl == 0) done += 2ull * q * q * g.kc;
+    if (sl == 0 && mcur) done += 2ull * q * q * min(8, g.kc - j0);
     // next step (slice of this term, or the first slice of the next valid term)
     int nterm = term, nsl = sl + 1;
     if (nsl == nslices) {
@@ -485,10 +497,11 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     if (nterm < nterms) issue(nterm, nsl, slot ^ 1);
     cp_async_commit();
     double bnext[NK4S];
-    if (nterm < nterms && j0 < g.kc) load_bs(nterm, nsl, bnext);
+    const bool mnext = nterm < nterms && j0 < g.kc && (nterm == term ? mcur : mine(nterm));
+    if (mnext) load_bs(nterm, nsl, bnext);
     cp_async_wait<1>();
     __syncthreads();
-    if (j0 < g.kc) {
+    if (mcur) {
       const double* Asl = As + slot * SLICE;
       const int k0 = sl * KS;
       const int nk4 = (min(KS, q - k0) + 3) / 4;
@@ -503,12 +516,13 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
     __syncthreads();  // everyone is done with `slot` before it is refilled
 #pragma unroll
     for (int k4 = 0; k4 < NK4S; ++k4) bcur[k4] = bnext[k4];
+    mcur = mnext;
     term = nterm;
     sl = nsl;
     slot ^= 1;
   }
   cp_async_wait<0>();
-  count_flops(g.flops, done);
+  if (g.flops && lane == 0 && done) atomicAdd(g.flops, done);
   if (j0 >= g.kc) return;
   double* O = g.out + obox * (int64_t)q * KC;
 #pragma unroll

@@ -491,3 +491,29 @@ def test_factored_lookahead_is_bit_identical(pkg):
     a, b = run(False), run(True)
     for k in ("mean_t", "N_t", "variance_t", "HC_t"):
         assert torch.equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_factored_error_paths(pkg):
+    """The factored update keeps the reference's error behaviour: a prior whose
+    posterior variance goes negative raises NumericalConsistencyError
+    (filters.py:149-153), a non-SPD S raises DecompositionError, and shape
+    mismatches raise ValueError (filters.py:31-37)."""
+    import torch
+    flt = pkg.filters
+    g = _load("small_rays.npz")
+    cfg = cases.SMALL
+    tree, H, pre, st, model = _run_filter_factored(pkg, cfg, g["obs"], T=2)
+    m, n = st.shape
+    # variance far below what the update removes: var' = -diag_Q + diag_Q = 0 before the update
+    bad = flt.FactoredHikfState(st.mean_t, st.N_t, -pre.diag_Q_t.clone(), st.HC_t, pre)
+    with pytest.raises(flt.NumericalConsistencyError):
+        flt.hikf_update(flt.hikf_predict(bad, pre), H, cfg["R"], g["obs"][2])
+    # S = HC' + r I not positive definite
+    neg = flt.FactoredHikfState(st.mean_t, st.N_t, st.variance_t, -10.0 * st.HC_t - 10.0 * pre.HC_Q_t, pre)
+    with pytest.raises(pkg.DecompositionError):
+        flt.hikf_update(flt.hikf_predict(neg, pre), H, cfg["R"], g["obs"][2])
+    with pytest.raises(ValueError):
+        flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], np.zeros(n + 1))
+    # n = 0 observations: identity (filters.py:140-141)
+    H0 = scipy.sparse.csr_matrix((0, m))
+    assert flt.hikf_update(st, H0, cfg["R"], np.zeros(0)) is st

@@ -19,6 +19,7 @@
 //   L2L   L_l[t] += S_c L_{l-1}[parent]
 //   L2P   U[p] += W2[p] L_D[leaf(p)]
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <numeric>
 #include <vector>
@@ -541,6 +542,95 @@ __global__ void __launch_bounds__(T3, 2) boxop3_kernel(BoxOpArgs g) {
   }
 }
 
+
+// ---- M2L, row-split: one CTA per (output box, 8-column group of the chunk) ----
+// The 8 warps split the q output rows (RTW row tiles each) and read their rows
+// of each operator straight from L2 (no shared-memory staging, no barriers), so
+// a term costs operator traffic only for the column groups whose source
+// expansion is nonzero.  The B fragments (the source's 8 columns) are the same
+// for all warps (L1 hits after the first).
+template <int RTW, int G2>
+__global__ void __launch_bounds__(T3) m2l3_rows_kernel(BoxOpArgs g) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
+  const int q = g.q, nk4 = (q + 3) / 4;
+  const int64_t G = g.Gout, Gp = G / 2;
+  constexpr int NGB = KC / 8 / G2;  // blocks of G2 column groups per chunk
+  const int gb = blockIdx.x % NGB;
+  const int64_t rest = blockIdx.x / NGB;
+  const int64_t nunit = (int64_t)(gridDim.x / NGB) / 8;
+  const int64_t unit = rest % nunit;
+  const int cls = (int)(rest / nunit);
+  const int j0 = gb * G2 * 8;
+  if (j0 >= g.kc) return;
+  const int64_t px = unit / (Gp * Gp), py = (unit / Gp) % Gp, pz = unit % Gp;
+  const int64_t ox = 2 * px + ((cls >> 2) & 1), oy = 2 * py + ((cls >> 1) & 1), oz = 2 * pz + (cls & 1);
+  const int64_t obox = (ox * G + oy) * G + oz;
+  if (g.occ && !g.occ[obox]) return;
+  const int cx = (cls >> 2) & 1, cy = (cls >> 1) & 1, cz = cls & 1;
+  double acc[RTW][G2][2];
+#pragma unroll
+  for (int i = 0; i < RTW; ++i)
+#pragma unroll
+    for (int c = 0; c < G2; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
+  unsigned long long done = 0;
+  for (int term = 0; term < NOFF; ++term) {
+    const int dx = g.offs[3 * term], dy = g.offs[3 * term + 1], dz = g.offs[3 * term + 2];
+    const int pdx = (cx + dx) >> 1, pdy = (cy + dy) >> 1, pdz = (cz + dz) >> 1;
+    if (pdx < -1 || pdx > 1 || pdy < -1 || pdy > 1 || pdz < -1 || pdz > 1) continue;
+    const int64_t sx = ox + dx, sy = oy + dy, sz = oz + dz;
+    if (sx < 0 || sy < 0 || sz < 0 || sx >= G || sy >= G || sz >= G) continue;
+    const int64_t sb = (sx * G + sy) * G + sz;
+    // active column groups of this block (CTA-uniform): the source's nonzero 8-column groups
+    const unsigned act = g.nz ? ((unsigned)g.nz[sb] >> (gb * G2)) & ((1u << G2) - 1) : (1u << G2) - 1;
+    if (!act) continue;
+    const double* A = g.ops + (int64_t)term * q * q;
+    const double* B = g.in + sb * (int64_t)q * KC;
+#pragma unroll
+    for (int c = 0; c < G2; ++c)
+      if ((act >> c) & 1) done += 2ull * q * q * max(0, min(8, g.kc - j0 - 8 * c));
+    constexpr int KB = 8;  // k-steps per batch of loads
+    for (int kb = 0; kb < nk4; kb += KB) {
+      double b[KB][G2], a[KB][RTW];
+#pragma unroll
+      for (int i = 0; i < KB; ++i) {
+        const int k = (kb + i) * 4 + t4;
+        const bool ok = kb + i < nk4 && k < q;
+#pragma unroll
+        for (int c = 0; c < G2; ++c) {
+          const int jc = j0 + 8 * c + gq;
+          b[i][c] = ok && ((act >> c) & 1) && jc < g.kc ? __ldg(B + (int64_t)k * KC + jc) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < RTW; ++r) {
+          const int row = (warp * RTW + r) * 8 + gq;
+          a[i][r] = ok && row < q ? __ldg(A + (int64_t)row * q + k) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < KB; ++i)
+#pragma unroll
+        for (int c = 0; c < G2; ++c)
+          if ((act >> c) & 1)
+#pragma unroll
+            for (int r = 0; r < RTW; ++r) dmma884(acc[r][c][0], acc[r][c][1], a[i][r], b[i][c]);
+    }
+  }
+  if (g.flops && threadIdx.x == 0 && done) atomicAdd(g.flops, done);
+  double* O = g.out + obox * (int64_t)q * KC;
+#pragma unroll
+  for (int r = 0; r < RTW; ++r) {
+    const int a = (warp * RTW + r) * 8 + gq;
+    if (a >= q) continue;
+#pragma unroll
+    for (int c = 0; c < G2; ++c)
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int col = j0 + 8 * c + 2 * t4 + hh;
+        if (col < g.kc) O[(int64_t)a * KC + col] = acc[r][c][hh];
+      }
+  }
+}
+
 size_t boxop_smem(int) { return sizeof(double) * 2 * (size_t)SLICE; }
 size_t leafop_smem(int rows, int cols) {
   return sizeof(double) * (size_t)(((rows + 7) >> 3) * 8) * pad4(((cols + 3) / 4) * 4);
@@ -825,7 +915,24 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
         const int64_t units = (int64_t)1 << (3 * (l - 1));  // parents x 8 child classes, one launch
         BoxOpArgs a{OP_M2L, q, l, 0, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l], OCC[l],
                     prof_flops_ptr(ST_M2L)};
-        boxop3_kernel<<<(unsigned)(8 * units), T3, sm_box, st>>>(a);
+        static const bool rows = [] {
+          const char* e = getenv("HIKF_M2L3_ROWS");
+          return !(e && e[0] == '0');
+        }();
+        static const int g2 = [] {
+          const char* e = getenv("HIKF_M2L3_G2");
+          return e ? atoi(e) : 2;  // measured best (G2 = 4 needs 168 registers): profiles/r01_m2l3_sweep.log
+        }();
+        if (rows && q <= 8 * 8 * 2) {  // row-split kernel: 8 warps x 2 row tiles (q <= 128), g2 groups per CTA
+          if (g2 == 1)
+            m2l3_rows_kernel<2, 1><<<(unsigned)(8 * units * (KC / 8)), T3, 0, st>>>(a);
+          else if (g2 == 2)
+            m2l3_rows_kernel<2, 2><<<(unsigned)(8 * units * (KC / 16)), T3, 0, st>>>(a);
+          else
+            m2l3_rows_kernel<2, 4><<<(unsigned)(8 * units * (KC / 32)), T3, 0, st>>>(a);
+        } else {
+          boxop3_kernel<<<(unsigned)(8 * units), T3, sm_box, st>>>(a);
+        }
         HIKF_CHECK_LAUNCH();
       }
       if (l > 2) {

@@ -255,27 +255,46 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, cons
   }
 }
 
-// ---- P2M: W_D[box(leaf)] = W2_leaf^T V_leaf ----
-__global__ void __launch_bounds__(T3, 1) p2m3_kernel(const T3v t, Chunk ch, double* __restrict__ W,
+// Leaf operators stage W2 (points x q, row-major as stored: coalesced loads) in
+// blocks of LP = 64 points, ~68 KB of shared memory, so 3 CTAs share an SM and
+// one CTA's staging overlaps another's DMMAs.
+constexpr int LP = 64;
+__host__ __device__ inline int w2_ld(int q) { return pad4(((q + 3) / 4) * 4); }  // == 4 mod 16 doubles
+
+// ---- P2M: W_D[box(leaf)] = W2_leaf^T V_leaf; A[a][p] = W2[p][a] read transposed from the
+// staged W2 block (conflict-free: the row stride is 4 mod 16 doubles) ----
+__global__ void __launch_bounds__(T3, 3) p2m3_kernel(const T3v t, Chunk ch, double* __restrict__ W,
                                                      const uint8_t* __restrict__ leafnz) {
   extern __shared__ double As[];
   const int leaf = blockIdx.x;
   if (!leafnz[leaf]) return;  // W stays zero (memset)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf], q = t.q;
-  const int nrt = (q + 7) >> 3, lda = pad4(((t.max_count + 3) / 4) * 4);
-  load_A(As, lda, nrt * 8, ((tc + 3) / 4) * 4, q, tc,
-         [&](int a, int p) { return t.W2[(int64_t)(ts + p) * q + a]; });
-  __syncthreads();
-  const int j0 = warp * 8;
-  if (j0 >= ch.kc || !((leafnz[leaf] >> warp) & 1)) return;  // W stays zero (memset) for all-zero columns
-  if (ch.flops && lane == 0) atomicAdd(ch.flops, 2ull * q * tc * min(8, ch.kc - j0));
-  const int jc = j0 + gq;
+  const int nrt = (q + 7) >> 3, ld = w2_ld(q);
+  const int j0 = warp * 8, jc = j0 + gq;
+  const bool mine = j0 < ch.kc && ((leafnz[leaf] >> warp) & 1);
+  if (mine && ch.flops && lane == 0) atomicAdd(ch.flops, 2ull * q * tc * min(8, ch.kc - j0));
   double acc[MAXRT][2];
   zero_acc(acc);
-  warp_gemm(As, lda, nrt, (tc + 3) / 4, gq, t4, [&](int k) {
-    return (k < tc && jc < ch.kc) ? ch.V[t.order[ts + k] * ch.ldv + jc] : 0.0;
-  }, acc);
+  for (int p0 = 0; p0 < tc; p0 += LP) {
+    const int np = min(LP, tc - p0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < LP * ld; e += T3) {
+      const int p = e / ld, a = e % ld;
+      As[e] = (p < np && a < q) ? t.W2[(int64_t)(ts + p0 + p) * q + a] : 0.0;
+    }
+    __syncthreads();
+    if (!mine) continue;
+    const int nk4 = (np + 3) / 4;
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int p = k4 * 4 + t4;
+      const double b = (p < np && jc < ch.kc) ? ch.V[t.order[ts + p0 + p] * ch.ldv + jc] : 0.0;
+#pragma unroll
+      for (int rt = 0; rt < MAXRT; ++rt)
+        if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], As[p * ld + rt * 8 + gq], b);
+    }
+  }
+  if (!mine) return;  // W stays zero (memset) for all-zero columns
   double* out = W + t.leaf_key[leaf] * (int64_t)q * KC;
 #pragma unroll
   for (int rt = 0; rt < MAXRT; ++rt) {
@@ -286,32 +305,45 @@ __global__ void __launch_bounds__(T3, 1) p2m3_kernel(const T3v t, Chunk ch, doub
   }
 }
 
-// ---- L2P: U[p] += W2[p] L_D[box(leaf)] ----
-__global__ void __launch_bounds__(T3, 1) l2p3_kernel(const T3v t, Chunk ch, const double* __restrict__ L) {
+// ---- L2P: U[p] += W2[p] L_D[box(leaf)], LP points per pass ----
+__global__ void __launch_bounds__(T3, 3) l2p3_kernel(const T3v t, Chunk ch, const double* __restrict__ L) {
   extern __shared__ double As[];
   const int leaf = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf], q = t.q;
   count_flops(ch.flops, 2ull * tc * q * ch.kc);
-  const int nrt = (tc + 7) >> 3, lda = pad4(((q + 3) / 4) * 4);
-  load_A(As, lda, nrt * 8, ((q + 3) / 4) * 4, tc, q, [&](int r, int a) { return t.W2[(int64_t)(ts + r) * q + a]; });
-  __syncthreads();
-  const int j0 = warp * 8;
-  if (j0 >= ch.kc) return;
-  const int jc = j0 + gq;
+  const int ld = w2_ld(q), nk4 = (q + 3) / 4;
+  const int j0 = warp * 8, jc = j0 + gq;
   const double* Lb = L + t.leaf_key[leaf] * (int64_t)q * KC;
-  double acc[MAXRT][2];
-  zero_acc(acc);
-  warp_gemm(As, lda, nrt, (q + 3) / 4, gq, t4, [&](int k) { return k < q ? Lb[(int64_t)k * KC + jc] : 0.0; }, acc);
+  for (int p0 = 0; p0 < tc; p0 += LP) {
+    const int np = min(LP, tc - p0), nrt = (np + 7) >> 3;
+    __syncthreads();
+    for (int e = threadIdx.x; e < LP * ld; e += T3) {
+      const int p = e / ld, a = e % ld;
+      As[e] = (p < np && a < q) ? t.W2[(int64_t)(ts + p0 + p) * q + a] : 0.0;
+    }
+    __syncthreads();
+    if (j0 >= ch.kc) continue;
+    double acc[LP / 8][2];
 #pragma unroll
-  for (int rt = 0; rt < MAXRT; ++rt) {
-    const int r = rt * 8 + gq;
-    if (rt >= nrt || r >= tc) continue;
-    double* urow = ch.U + t.order[ts + r] * ch.ldu;
+    for (int rt = 0; rt < LP / 8; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int k = k4 * 4 + t4;
+      const double b = (k < q && jc < ch.kc) ? Lb[(int64_t)k * KC + jc] : 0.0;  // L1 hit on the second pass
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const int c = j0 + 2 * t4 + hh;
-      if (c < ch.kc) urow[c] += acc[rt][hh];  // U = near + far
+      for (int rt = 0; rt < LP / 8; ++rt)
+        if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], As[(rt * 8 + gq) * ld + k4 * 4 + t4], b);
+    }
+#pragma unroll
+    for (int rt = 0; rt < LP / 8; ++rt) {
+      const int r = rt * 8 + gq;
+      if (rt >= nrt || r >= np) continue;
+      double* urow = ch.U + t.order[ts + p0 + r] * ch.ldu;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int c = j0 + 2 * t4 + hh;
+        if (c < ch.kc) urow[c] += acc[rt][hh];  // U = near + far
+      }
     }
   }
 }
@@ -366,19 +398,24 @@ __global__ void nonzero_leaves(const T3v t, const double* __restrict__ V, int64_
   if (lane == 0) nz[leaf] = (uint8_t)mask;
 }
 
-// nz[box] = per-warp mask of any(W[box][a][j] != 0, a < q, j in the warp's 8 columns): M2L / M2M skip
-// all-zero sources per CTA and per warp (exact: they add zeros)
-__global__ void nonzero_boxes(const double* __restrict__ W, int64_t nboxes, int q, int kc, uint8_t* __restrict__ nz) {
-  const int64_t box = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (box >= nboxes) return;
-  const double* w = W + box * (int64_t)q * KC;
-  unsigned mask = 0;  // bit w: some coefficient in columns 8w .. 8w + 7 is nonzero
-  for (int e = lane; e < q * kc; e += 32)
-    if (w[(int64_t)(e / kc) * KC + e % kc] != 0.0) mask |= 1u << ((e % kc) >> 3);
-  mask = __reduce_or_sync(0xffffffffu, mask);
-  if (lane == 0) nz[box] = (uint8_t)mask;
+// nz masks without scanning the dense expansions: leaf boxes take their leaf's charge mask (a
+// superset of the nonzero groups of W_D), parents the OR of their children; empty boxes 0
+__global__ void nz_leaf_boxes(const int64_t* __restrict__ leaf_key, const uint8_t* __restrict__ lnz, int64_t nl,
+                              uint8_t* __restrict__ nz) {
+  for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < nl; l += (int64_t)gridDim.x * blockDim.x)
+    nz[leaf_key[l]] = lnz[l];
 }
+__global__ void nz_parent(const uint8_t* __restrict__ nzc, int64_t G, uint8_t* __restrict__ nzp) {
+  const int64_t nb = G * G * G, Gc = 2 * G;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = b / (G * G), y = (b / G) % G, z = b % G;
+    uint8_t o = 0;
+    for (int c = 0; c < 8; ++c)
+      o |= nzc[((2 * x + ((c >> 2) & 1)) * Gc + (2 * y + ((c >> 1) & 1))) * Gc + (2 * z + (c & 1))];
+    nzp[b] = o;
+  }
+}
+
 
 // one CTA = one output box; warp w owns chunk columns 8w .. 8w + 7.  The
 // operators stream through shared memory in K-slices of 32 with a two-slot
@@ -842,8 +879,8 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     HIKF_CHECK_CUDA(cudaMalloc((void**)&doffs, sizeof(offs_h)));
     HIKF_CHECK_CUDA(cudaMemcpy(doffs, offs_h, sizeof(offs_h), cudaMemcpyHostToDevice));
   }
-  const size_t sm_p2p = leafop_smem(t->max_count, t->max_count), sm_p2m = leafop_smem(q, t->max_count),
-               sm_l2p = leafop_smem(t->max_count, q), sm_box = boxop_smem(q);
+  const size_t sm_p2p = leafop_smem(t->max_count, t->max_count), sm_box = boxop_smem(q);
+  const size_t sm_p2m = sizeof(double) * (size_t)LP * w2_ld(q), sm_l2p = sm_p2m;
   HIKF_TRY(set_smem(p2p3_kernel, std::max<size_t>(sm_p2p, 1)));
   HIKF_TRY(set_smem(p2m3_kernel, std::max<size_t>(sm_p2m, 1)));
   HIKF_TRY(set_smem(l2p3_kernel, std::max<size_t>(sm_l2p, 1)));
@@ -875,11 +912,6 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
       HIKF_CHECK_LAUNCH();
     }
   }
-  auto flag = [&](int l, int kc) {
-    const int64_t nb = (int64_t)1 << (3 * l);
-    nonzero_boxes<<<(unsigned)((nb * 32 + 255) / 256), 256, 0, st>>>(W[l], nb, q, kc, NZ[l]);
-    return cudaGetLastError() == cudaSuccess ? HIKF_OK : HIKF_CUDA_ERROR;
-  };
   const T3v tv = view(t);
   int status = HIKF_OK;
   for (int64_t c0 = 0; c0 < k && status == HIKF_OK; c0 += KC) {
@@ -895,19 +927,28 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     if (D < 2) continue;
     {
       ProfScope ps(ST_P2M, st);
-      HIKF_CHECK_CUDA(cudaMemsetAsync(W[D], 0, sizeof(double) * ((int64_t)1 << (3 * D)) * q * KC, st));
+      // W_D is not cleared: a box / column group is read only where its nz bit is set, and
+      // P2M writes every group its leaf's charge mask flags
       ch.flops = prof_flops_ptr(ST_P2M);
       p2m3_kernel<<<(unsigned)nl, T3, sm_p2m, st>>>(tv, ch, W[D], LNZ);
       HIKF_CHECK_LAUNCH();
-      HIKF_TRY(flag(D, ch.kc));
+      const int64_t nbD = (int64_t)1 << (3 * D);
+      HIKF_CHECK_CUDA(cudaMemsetAsync(NZ[D], 0, nbD, st));
+      nz_leaf_boxes<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((nl + 255) / 256, num_sms() * 8)), 256, 0,
+                      st>>>(t->leaf_key, LNZ, nl, NZ[D]);
+      HIKF_CHECK_LAUNCH();
     }
     for (int l = D - 1; l >= 2; --l) {
       ProfScope ps(ST_M2M, st);
-      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, NZ[l + 1], nullptr,
-                  prof_flops_ptr(ST_M2M)};
-      boxop3_kernel<<<(unsigned)((int64_t)1 << (3 * l)), T3, sm_box, st>>>(a);
+      const int64_t nb = (int64_t)1 << (3 * l);
+      nz_parent<<<(unsigned)std::min<int64_t>((nb + 255) / 256, num_sms() * 16), 256, 0, st>>>(NZ[l + 1],
+                                                                                             (int64_t)1 << l, NZ[l]);
       HIKF_CHECK_LAUNCH();
-      HIKF_TRY(flag(l, ch.kc));
+      // only boxes with a nonzero child are read later (nz), so M2M skips the others
+      BoxOpArgs a{OP_M2M, q, l, 0, (int64_t)1 << l, W[l + 1], W[l], t->shiftT, nullptr, ch.kc, NZ[l + 1], NZ[l],
+                  prof_flops_ptr(ST_M2M)};
+      boxop3_kernel<<<(unsigned)nb, T3, sm_box, st>>>(a);
+      HIKF_CHECK_LAUNCH();
     }
     for (int l = 2; l <= D; ++l) {
       {

@@ -205,14 +205,16 @@ __device__ __forceinline__ void count_flops(unsigned long long* c, unsigned long
 }
 
 // ---- P2P: U[t] = sum_nbr K(t, s) V[s] (first write of the chunk's U columns) ----
-__global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, const uint8_t* __restrict__ leafnz) {
+__global__ void __launch_bounds__(T3, 2) p2p3_kernel(const T3v t, Chunk ch, const uint8_t* __restrict__ leafnz) {
+  // the kernel block K(target, source) is built in shared memory 64 target rows at a
+  // time (~68 KB: 2 CTAs per SM, one CTA's exp / sqrt build overlaps the other's DMMAs)
   extern __shared__ double As[];
+  constexpr int TR = 64;
   const int leaf = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gq = lane >> 2, t4 = lane & 3;
   const int ts = t.leaf_start[leaf], tc = t.leaf_count[leaf];
   const int64_t key = t.leaf_key[leaf], G = t.G;
   const int64_t bx = key / (G * G), by = (key / G) % G, bz = key % G;
-  const int nrt = (tc + 7) >> 3;
   const int lda = pad4(((t.max_count + 3) / 4) * 4);
   const int j0 = warp * 8;  // this warp's 8 columns of the chunk (kc <= 64)
   double acc[MAXRT][2];
@@ -224,24 +226,38 @@ __global__ void __launch_bounds__(T3, 1) p2p3_kernel(const T3v t, Chunk ch, cons
     const int sl = t.box2leaf[(x * G + y) * G + z];
     if (sl < 0 || !leafnz[sl]) continue;  // no leaf / all-zero charges: uniform across the CTA
     const int ss = t.leaf_start[sl], sc = t.leaf_count[sl];
-    const bool mine = (leafnz[sl] >> warp) & 1;  // this warp's 8 columns hold a nonzero charge
+    const bool mine = j0 < ch.kc && ((leafnz[sl] >> warp) & 1);  // this warp's 8 columns hold a nonzero charge
     if (mine) done += 2ull * tc * sc * min(8, ch.kc - j0);
-    __syncthreads();
-    load_A(As, lda, nrt * 8, ((sc + 3) / 4) * 4, tc, sc, [&](int r, int c) {
-      const double* a = t.pts + 3 * (int64_t)(ts + r);
-      const double* b = t.pts + 3 * (int64_t)(ss + c);
-      return k3_of_r(t.k.family, t.k.variance, d3(a[0], a[1], a[2], b[0], b[1], b[2]));
-    });
-    __syncthreads();
-    if (j0 < ch.kc && mine) {
-      const int jc = j0 + gq;
-      warp_gemm(As, lda, nrt, (sc + 3) / 4, gq, t4, [&](int k) {
-        return (k < sc && jc < ch.kc) ? ch.V[t.order[ss + k] * ch.ldv + jc] : 0.0;
-      }, acc);
+    const int jc = j0 + gq, nk4 = (sc + 3) / 4;
+    static_assert(2 * TR >= MAXRT * 8, "two row blocks cover a leaf");
+    for (int r0 = 0; r0 < tc; r0 += TR) {
+      const int nr = min(TR, tc - r0), nrt = (nr + 7) >> 3;
+      __syncthreads();
+      load_A(As, lda, nrt * 8, nk4 * 4, nr, sc, [&](int r, int c) {
+        const double* a = t.pts + 3 * (int64_t)(ts + r0 + r);
+        const double* b = t.pts + 3 * (int64_t)(ss + c);
+        return k3_of_r(t.k.family, t.k.variance, d3(a[0], a[1], a[2], b[0], b[1], b[2]));
+      });
+      __syncthreads();
+      if (!mine) continue;
+      for (int k4 = 0; k4 < nk4; ++k4) {
+        const int k = k4 * 4 + t4;
+        const double b = (k < sc && jc < ch.kc) ? ch.V[t.order[ss + k] * ch.ldv + jc] : 0.0;
+        if (r0 == 0) {  // static accumulator indices: rows 0..63 -> acc[0..7], 64..127 -> acc[8..15]
+#pragma unroll
+          for (int rt = 0; rt < TR / 8; ++rt)
+            if (rt < nrt) dmma884(acc[rt][0], acc[rt][1], As[(rt * 8 + gq) * lda + k4 * 4 + t4], b);
+        } else {
+#pragma unroll
+          for (int rt = 0; rt < TR / 8; ++rt)
+            if (rt < nrt) dmma884(acc[TR / 8 + rt][0], acc[TR / 8 + rt][1], As[(rt * 8 + gq) * lda + k4 * 4 + t4], b);
+        }
+      }
     }
   }
   if (ch.flops && lane == 0 && done) atomicAdd(ch.flops, done);
   if (j0 >= ch.kc) return;
+  const int nrt = (tc + 7) >> 3;
 #pragma unroll
   for (int rt = 0; rt < MAXRT; ++rt) {
     const int r = rt * 8 + gq;
@@ -879,7 +895,7 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
     HIKF_CHECK_CUDA(cudaMalloc((void**)&doffs, sizeof(offs_h)));
     HIKF_CHECK_CUDA(cudaMemcpy(doffs, offs_h, sizeof(offs_h), cudaMemcpyHostToDevice));
   }
-  const size_t sm_p2p = leafop_smem(t->max_count, t->max_count), sm_box = boxop_smem(q);
+  const size_t sm_p2p = leafop_smem(std::min(t->max_count, 64), t->max_count), sm_box = boxop_smem(q);
   const size_t sm_p2m = sizeof(double) * (size_t)LP * w2_ld(q), sm_l2p = sm_p2m;
   HIKF_TRY(set_smem(p2p3_kernel, std::max<size_t>(sm_p2p, 1)));
   HIKF_TRY(set_smem(p2m3_kernel, std::max<size_t>(sm_p2m, 1)));

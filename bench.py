@@ -619,7 +619,7 @@ def main():
     # ---- opt-in factored representation (C = C_Q N, filters.FactoredHikfState):
     # the same predict+update steps, device-resident; the headline stays explicit ----
     fac = None
-    if not args.no_factored and not dim3 and float(model.alpha) == 0.0:
+    if not args.no_factored and float(model.alpha) == 0.0:
         sf = flt.hikf_init(model, representation="factored")
         for t in range(args.warmup):
             sf = flt.hikf_update(flt.hikf_predict(sf, pre), H, cfg["R"], Zd[t % cfg["T"]])

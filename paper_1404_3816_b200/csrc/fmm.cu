@@ -497,10 +497,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   QhtStreams* qs = nullptr;
   HIKF_TRY(qht_streams(&qs));
-  // timing experiments only (tools/qht_time.py): HIKF_QHT_SKIP = comma list of stages to skip
-  // (p2p, m2l, m2llow, l2l, l2p); the result is then wrong
-  static const char* skip_env = getenv("HIKF_QHT_SKIP");
-  auto skip = [&](const char* s) { return skip_env && strstr(skip_env, s); };
+
   cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1], ev_up = qs->e[2];
 
   // ---- near field, concurrently: sums parked in Pnear, added after L2P ----
@@ -511,7 +508,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   int status = HIKF_OK;
   {
     ProfScope ps(ST_P2P, qs->s[0]);
-    if (!skip("p2p")) status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear);
+    status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear);
   }
   HIKF_CHECK_CUDA(cudaEventRecord(ev_p2p, qs->s[0]));
 
@@ -544,9 +541,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       const int q = t->orders[l] * t->orders[l];
       ProfScope ps(ST_M2L, sl);
       HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, sl));
-      const bool sk = skip("m2l,") || (skip("m2llow") && l < D);
-      for (int slot = 0; slot < 40 && status == HIKF_OK && !sk; ++slot)
-        status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl);
+      for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot) status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl);
       HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
     }
   }
@@ -560,7 +555,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
     if (l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
       ProfScope ps(ST_L2L, st);
-      if (!skip("l2l")) status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st);
+      status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st);
     } else {
       ProfScope ps(ST_L2L, st);
       status = pair_to_box(t, l, scratch[l], n, Lcur, st);
@@ -581,7 +576,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
-    if (!skip("l2p")) status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
+    status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
   } else if (status == HIKF_OK && window) {
     set_error("row-windowed Q H^T needs the box-streaming L2P (leaf order <= 8)");
     status = HIKF_BAD_ARGUMENT;

@@ -649,7 +649,13 @@ int dgemm_variant() {
 
 void set_dgemm_variant(int v) { g_variant = v; }
 
-int update_variant_c() { return getenv("HIKF_DGEMM_VARIANT") ? dgemm_variant() : 30; }
+int update_variant_c(int64_t n) {
+  if (getenv("HIKF_DGEMM_VARIANT")) return dgemm_variant();
+  // 128-column tiles (variant 30) unless 64-column tiles (variant 32) pad n less
+  // (e.g. n = 64, cfg1: one full 64-wide tile instead of half a 128-wide one)
+  const int64_t w128 = ceil_div(n, 128) * 128 - n, w64 = ceil_div(n, 64) * 64 - n;
+  return w64 < w128 ? 32 : 30;
+}
 
 int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || batch <= 0) return HIKF_OK;

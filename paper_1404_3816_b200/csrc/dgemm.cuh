@@ -67,7 +67,7 @@ inline int dgemm_col_tiles(int64_t N, int variant = -1) {
 }
 // variant used by the update's K GEMM (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log);
 // HIKF_DGEMM_VARIANT overrides it
-int update_variant_c();
+int update_variant_c(int64_t n);
 constexpr int DG_MIN_BN = 64;  // smallest column tile of any variant (partials workspace sizing)
 
 }  // namespace hikf

@@ -1032,7 +1032,7 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   //      fused row partials psq = rowsum(K o C'), pdot = K innov ----
   const int nb = grid_for(m);
   {
-    const int vc = update_variant_c();
+    const int vc = update_variant_c(n);
     const int nt = dgemm_col_tiles(n, vc);
     {
       GemmArgs g;

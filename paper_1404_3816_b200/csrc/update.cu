@@ -584,6 +584,64 @@ static int factor_chain(const double* HCp, int64_t n, double r, double* S, doubl
 }
 
 
+
+// ---- pieces shared by the explicit and the factored update ----
+
+// Probe the S look-ahead: true when the factorisation step t computed for this
+// step's S (HC + HC_Q, r) is valid -- HC and HC_Q bitwise equal to its inputs.
+// With `nin` / `fl` also probes the factored chain's look-ahead (N bitwise equal
+// and computed from the same S slot) into *fhit.  One host sync.
+static int lookahead_probe(LookAhead& la, const double* HC, const double* HCQ, double r, int64_t n, cudaStream_t st,
+                           bool* hit, const double* nin = nullptr, struct FacLookAhead* fl = nullptr,
+                           bool* fhit = nullptr);
+
+// HC_new = HC' - (HC' Li^T)(Li HC') on `s` (P, R scratch n x n)
+static int hc_chain(const double* Li, const double* LiT, const double* HCp, double* HC_out, double* P, double* R,
+                    int64_t n, cudaStream_t s) {
+  GemmArgs g;
+  g.M = n; g.N = n; g.K = n;
+  g.A = Li; g.sa_r = n;
+  g.B = HCp; g.sb_r = n;
+  g.C = P; g.ldc = n;
+  HIKF_TRY(dgemm(g, 1, s));
+  GemmArgs h;
+  h.M = n; h.N = n; h.K = n;
+  h.A = HCp; h.sa_r = n;
+  h.B = LiT; h.sb_r = n;
+  h.C = R; h.ldc = n;
+  h.kmode = KB_UPPER;
+  HIKF_TRY(dgemm(h, 1, s));
+  GemmArgs c;
+  c.M = n; c.N = n; c.K = n;
+  c.A = R; c.sa_r = n;
+  c.B = P; c.sb_r = n;
+  c.C = HC_out; c.ldc = n;
+  c.Cin = HCp; c.ldcin = n;
+  c.alpha = -1.0; c.beta = 1.0;
+  return dgemm(c, 1, s);
+}
+
+// Enqueue on `s` the factorisation of the next step's S = sym(HC_out + HC_Q) + r I
+// into the slot this step does not read; returns the slot used.
+static int lookahead_enqueue(LookAhead& la, bool hit, const double* HC_out, const double* HCQ, double r, int64_t n,
+                             double* S, double* L, double* tmp, cudaStream_t s, int* slot_out) {
+  la.ready = false;  // until the whole chain below is enqueued
+  const int nx = hit ? la.cur ^ 1 : la.cur;  // never overwrite the slot this step reads
+  ProfScope pf(ST_FACTOR, s);
+  add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, s>>>(HC_out, HCQ, la.HCp, n * n);
+  HIKF_CHECK_LAUNCH();
+  HIKF_CHECK_CUDA(cudaMemsetAsync(la.status + nx, 0, sizeof(int), s));
+  HIKF_TRY(factor_chain(la.HCp, n, r, S, L, tmp, la.Li[nx], la.LiT[nx], la.Sinv[nx], la.status + nx, s));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(la.HC, HC_out, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(la.HCQ, HCQ, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  la.cur = nx;
+  la.r = r;
+  la.hcq_ptr = HCQ;
+  la.ready = true;
+  if (slot_out) *slot_out = nx;
+  return HIKF_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Factored representation of the cross covariance.
 //
@@ -721,6 +779,35 @@ static int fac_lookahead_reserve(FacLookAhead& f, int64_t n) {
   return HIKF_OK;
 }
 
+static int lookahead_probe(LookAhead& la, const double* HC, const double* HCQ, double r, int64_t n, cudaStream_t st,
+                           bool* hit, const double* nin, FacLookAhead* fl, bool* fhit) {
+  *hit = false;
+  if (fhit) *fhit = false;
+  if (!(la.ready && la.r == r && la.hcq_ptr == HCQ)) return HIKF_OK;
+  HIKF_CHECK_CUDA(cudaMemsetAsync(la.status + 2, 0, sizeof(int), st));
+  differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(HC),
+                                               reinterpret_cast<const uint64_t*>(la.HC), n * n, la.status + 2);
+  HIKF_CHECK_LAUNCH();
+  differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(HCQ),
+                                               reinterpret_cast<const uint64_t*>(la.HCQ), n * n, la.status + 2);
+  HIKF_CHECK_LAUNCH();
+  const bool ftry = fl && fl->ready && fl->la_slot == la.cur;
+  if (ftry) {
+    HIKF_CHECK_CUDA(cudaMemsetAsync(fl->status + 2, 0, sizeof(int), st));
+    differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(nin),
+                                                 reinterpret_cast<const uint64_t*>(fl->N[fl->cur]), n * n,
+                                                 fl->status + 2);
+    HIKF_CHECK_LAUNCH();
+  }
+  int flag[2] = {1, 1};
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag[0], la.status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (ftry) HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag[1], fl->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  *hit = flag[0] == 0;
+  if (fhit) *fhit = *hit && ftry && flag[1] == 0;
+  return HIKF_OK;
+}
+
 static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   const int64_t m = a.m, n = a.n;
   if (!a.CQ || !a.Nin || !a.Nout || (a.predict_in && (!a.dQ || !a.HCQ))) {
@@ -751,29 +838,7 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
     fl = &fac_lookahead();
     HIKF_TRY(lookahead_reserve(*la, n));
     HIKF_TRY(fac_lookahead_reserve(*fl, n));
-    if (la->ready && la->r == a.r && la->hcq_ptr == a.HCQ) {
-      HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + 2, 0, sizeof(int), st));
-      differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HC),
-                                                   reinterpret_cast<const uint64_t*>(la->HC), n * n, la->status + 2);
-      HIKF_CHECK_LAUNCH();
-      differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HCQ),
-                                                   reinterpret_cast<const uint64_t*>(la->HCQ), n * n, la->status + 2);
-      HIKF_CHECK_LAUNCH();
-      const bool ftry = fl->ready && fl->la_slot == la->cur;
-      if (ftry) {
-        HIKF_CHECK_CUDA(cudaMemsetAsync(fl->status + 2, 0, sizeof(int), st));
-        differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.Nin),
-                                                     reinterpret_cast<const uint64_t*>(fl->N[fl->cur]), n * n,
-                                                     fl->status + 2);
-        HIKF_CHECK_LAUNCH();
-      }
-      int flag[2] = {1, 1};
-      HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag[0], la->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
-      if (ftry) HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag[1], fl->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
-      HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-      hit = flag[0] == 0;
-      fhit = hit && ftry && flag[1] == 0;
-    }
+    HIKF_TRY(lookahead_probe(*la, a.HC, a.HCQ, a.r, n, st, &hit, a.Nin, fl, &fhit));
   }
 
   HIKF_CHECK_CUDA(cudaEventRecord(ev[0], st));
@@ -867,46 +932,13 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
       HIKF_CHECK_CUDA(cudaMemcpyAsync(a.mean_host, a.mean_out, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
   }
   // ---- side: HC_new = HC' - (HC' Li^T)(Li HC'), as the explicit path ----
-  {
-    GemmArgs g;
-    g.M = n; g.N = n; g.K = n;
-    g.A = Li; g.sa_r = n;
-    g.B = HCp; g.sb_r = n;
-    g.C = w.P; g.ldc = n;
-    HIKF_TRY(dgemm(g, 1, side));
-    GemmArgs h;
-    h.M = n; h.N = n; h.K = n;
-    h.A = HCp; h.sa_r = n;
-    h.B = LiT; h.sb_r = n;
-    h.C = w.R; h.ldc = n;
-    h.kmode = KB_UPPER;
-    HIKF_TRY(dgemm(h, 1, side));
-    GemmArgs c;
-    c.M = n; c.N = n; c.K = n;
-    c.A = w.R; c.sa_r = n;
-    c.B = w.P; c.sb_r = n;
-    c.C = a.HC_out; c.ldc = n;
-    c.Cin = HCp; c.ldcin = n;
-    c.alpha = -1.0; c.beta = 1.0;
-    HIKF_TRY(dgemm(c, 1, side));
-  }
+  HIKF_TRY(hc_chain(Li, LiT, HCp, a.HC_out, w.P, w.R, n, side));
   if (use_la) {
-    la->ready = false;
     fl->ready = false;
-    const int nx = hit ? la->cur ^ 1 : la->cur;
-    ProfScope pf(ST_FACTOR, side);
-    add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, side>>>(a.HC_out, a.HCQ, la->HCp, n * n);
-    HIKF_CHECK_LAUNCH();
-    HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + nx, 0, sizeof(int), side));
-    HIKF_TRY(factor_chain(la->HCp, n, a.r, w.S, w.L, w.tmp, la->Li[nx], la->LiT[nx], la->Sinv[nx], la->status + nx,
-                          side));
-    HIKF_CHECK_CUDA(cudaMemcpyAsync(la->HC, a.HC_out, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
-    HIKF_CHECK_CUDA(cudaMemcpyAsync(la->HCQ, a.HCQ, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
-    la->cur = nx;
-    la->r = a.r;
-    la->hcq_ptr = a.HCQ;
-    la->ready = true;
+    int nx = 0;
+    HIKF_TRY(lookahead_enqueue(*la, hit, a.HC_out, a.HCQ, a.r, n, w.S, w.L, w.tmp, side, &nx));
     // the next step's factored chain from N_out (main) and S_{t+1} (just above)
+    ProfScope pf(ST_FACTOR, side);
     const int fx = fhit ? fl->cur ^ 1 : fl->cur;
     HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev_n, 0));
     HIKF_CHECK_CUDA(cudaMemsetAsync(fl->status + fx, 0, sizeof(int), side));
@@ -982,19 +1014,7 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   if (use_la) {
     la = &lookahead();
     HIKF_TRY(lookahead_reserve(*la, n));
-    if (la->ready && la->r == a.r && la->hcq_ptr == a.HCQ) {
-      HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + 2, 0, sizeof(int), st));
-      differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HC),
-                                                   reinterpret_cast<const uint64_t*>(la->HC), n * n, la->status + 2);
-      HIKF_CHECK_LAUNCH();
-      differs_kernel<<<num_sms() * 2, kT, 0, st>>>(reinterpret_cast<const uint64_t*>(a.HCQ),
-                                                   reinterpret_cast<const uint64_t*>(la->HCQ), n * n, la->status + 2);
-      HIKF_CHECK_LAUNCH();
-      int flag = 1;
-      HIKF_CHECK_CUDA(cudaMemcpyAsync(&flag, la->status + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
-      HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-      hit = flag == 0;
-    }
+    HIKF_TRY(lookahead_probe(*la, a.HC, a.HCQ, a.r, n, st, &hit));
   }
 
   // ---- fork: main stream = predict + K GEMM; side stream = n x n chain ----
@@ -1062,46 +1082,9 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   }
 
   // ---- side (overlapping the GEMM): P = Li HC', R = HC' Li^T, HC_new = HC' - R P ----
-  {
-    GemmArgs g;
-    g.M = n; g.N = n; g.K = n;
-    g.A = Li; g.sa_r = n;
-    g.B = HCp; g.sb_r = n;
-    g.C = w.P; g.ldc = n;
-    HIKF_TRY(dgemm(g, 1, side));
-    GemmArgs h;
-    h.M = n; h.N = n; h.K = n;
-    h.A = HCp; h.sa_r = n;
-    h.B = LiT; h.sb_r = n;
-    h.C = w.R; h.ldc = n;
-    h.kmode = KB_UPPER;
-    HIKF_TRY(dgemm(h, 1, side));
-    GemmArgs c;
-    c.M = n; c.N = n; c.K = n;
-    c.A = w.R; c.sa_r = n;
-    c.B = w.P; c.sb_r = n;
-    c.C = a.HC_out; c.ldc = n;
-    c.Cin = HCp; c.ldcin = n;
-    c.alpha = -1.0; c.beta = 1.0;
-    HIKF_TRY(dgemm(c, 1, side));
-  }
+  HIKF_TRY(hc_chain(Li, LiT, HCp, a.HC_out, w.P, w.R, n, side));
   // ---- side: look-ahead factorisation of the next step's S ----
-  if (use_la) {
-    la->ready = false;  // until the whole chain below is enqueued
-    const int nx = hit ? la->cur ^ 1 : la->cur;  // never overwrite the slot this step reads
-    ProfScope pf(ST_FACTOR, side);
-    add_kernel<<<grid_for(n * n / 2 + 1), kT, 0, side>>>(a.HC_out, a.HCQ, la->HCp, n * n);
-    HIKF_CHECK_LAUNCH();
-    HIKF_CHECK_CUDA(cudaMemsetAsync(la->status + nx, 0, sizeof(int), side));
-    HIKF_TRY(factor_chain(la->HCp, n, a.r, w.S, w.L, w.tmp, la->Li[nx], la->LiT[nx], la->Sinv[nx], la->status + nx,
-                          side));
-    HIKF_CHECK_CUDA(cudaMemcpyAsync(la->HC, a.HC_out, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
-    HIKF_CHECK_CUDA(cudaMemcpyAsync(la->HCQ, a.HCQ, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, side));
-    la->cur = nx;
-    la->r = a.r;
-    la->hcq_ptr = a.HCQ;
-    la->ready = true;
-  }
+  if (use_la) HIKF_TRY(lookahead_enqueue(*la, hit, a.HC_out, a.HCQ, a.r, n, w.S, w.L, w.tmp, side, nullptr));
   HIKF_CHECK_CUDA(cudaEventRecord(ev[2], side));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[2], 0));
 

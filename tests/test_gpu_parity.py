@@ -517,3 +517,27 @@ def test_factored_error_paths(pkg):
     # n = 0 observations: identity (filters.py:140-141)
     H0 = scipy.sparse.csr_matrix((0, m))
     assert flt.hikf_update(st, H0, cfg["R"], np.zeros(0)) is st
+
+
+@pytest.mark.parametrize("variant", [7, 30, 31, 32])
+def test_dgemm_variants_and_triangular_k_ranges(pkg, variant):
+    """Every DMMA GEMM variant (hand-written 7, CUTLASS-mainloop 30-32) against
+    torch float64: full K, an upper-triangular B (kmode 1: k < n0 + BN) and a
+    lower-triangular B (kmode 2: k >= n0), with beta = 1 accumulation, on odd
+    shapes that exercise the boundary tiles."""
+    import torch
+    from paper_1404_3816_b200 import _lib
+    lib = _lib.load()
+    g = torch.Generator().manual_seed(variant)
+    for M, N, K in ((1000, 300, 300), (257, 64, 64), (64, 1024, 1024)):
+        A = torch.randn(M, K, dtype=torch.float64, generator=g).cuda()
+        Bf = torch.randn(K, N, dtype=torch.float64, generator=g).cuda()
+        C0 = torch.randn(M, N, dtype=torch.float64, generator=g).cuda()
+        for kmode, B in ((0, Bf), (1, torch.triu(Bf)), (2, torch.tril(Bf))):
+            C = C0.clone()
+            st = _lib.check(lib.hikf_dgemm(M, N, K, A.data_ptr(), K, B.data_ptr(), N, C.data_ptr(), N, 0.5, 1.0,
+                                           kmode, variant, _lib.stream_ptr()))
+            ref = 0.5 * (A @ B) + C0
+            torch.cuda.synchronize()
+            err = float((C - ref).abs().max() / ref.abs().max())
+            assert err <= 1e-14, (variant, M, N, K, kmode, err)

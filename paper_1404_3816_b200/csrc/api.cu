@@ -47,6 +47,7 @@ KParams make_kparams(const hikf_kernel& k) {
   p.family = k.family;
   p.variance = k.variance;
   p.length = k.length_scale;
+  p.inv_length = 1.0 / k.length_scale;
   p.power = k.power;
   p.log_amp = k.log_amplitude;
   p.pmode = 0;

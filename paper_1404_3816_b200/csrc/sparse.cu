@@ -206,7 +206,7 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
       for (int32_t k = rb[s]; k < re[s]; ++k) {
         const int32_t p = e_sp[k];
         const double v = e_v[k];
-        acc += kernel_of_r(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
+        acc += kernel_of_r_near(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
       }
     if (!ok) continue;
     if (Pnear)

@@ -639,6 +639,18 @@ def main():
         t_tri = ms_t / max(n_t, 1) / 1e3
         bn = 64  # column tile of the K-range-limited triangular GEMM (variant 32; k >= n0 per column tile)
         tri_flops = sum(2.0 * m * min(bn, n - n0) * (n - n0) for n0 in range(0, n, bn))
+        # e2e through the public API, as the explicit leg: host z up, posterior mean down, every step
+        barrier_sync()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fmeans = np.empty((args.steps, m))
+        g0.record()
+        for t in range(args.steps):
+            sf = flt.hikf_update(flt.hikf_predict(sf, pre), H, cfg["R"], obs[(args.warmup + t) % cfg["T"]])
+            fmeans[t] = sf.mean
+        g1.record()
+        barrier_sync()
+        t_fe2e = max_over_ranks(g0.elapsed_time(g1) / 1e3)
+        del fmeans
         fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         fe0.record()
         C_mat = sf.cross_cov_t  # one materialisation C_Q N (a user reading cross_cov)
@@ -649,6 +661,8 @@ def main():
                        "(with the consistency check) and HC every step as filters.py:138-157; C materialised on "
                        "read (ms_materialize, one GEMM)",
                "ms_materialize": fe0.elapsed_time(fe1),
+               "e2e": {"value": world * args.steps / t_fe2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
+                       "d2h_bytes_per_step": 8 * m},
                "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in fst.items()},
                "roofline": {"kernel": "dgemm_cutlass_kernel KB_LOWER (rowsum((C_Q L_G)^2), no output store)",
                             "bound": "fp64", "achieved": tri_flops / t_tri / 1e12 if t_tri else None,

@@ -203,3 +203,25 @@ def test_cfg4_factored_update_against_torch_fp64(pkg, cfg4):
     _record("cfg4_factored_vs_torch", errs)
     for k, v in errs.items():
         assert v <= PARITY, (k, v)
+
+
+def test_dgemm_beyond_2_31_elements(pkg):
+    """The K-GEMM shape of cfg5 and beyond: M = 2^21 + 37 rows x 1024 (2.15e9 elements per
+    operand, past the int32 element range) through the CUTLASS-mainloop variant, checked
+    against torch (cuBLAS) on row slices at the start, the middle and the end."""
+    import torch
+    from paper_1404_3816_b200 import _lib
+    lib = _lib.load()
+    M, N, K = (1 << 21) + 37, 1024, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g)
+    C = torch.empty(M, N, dtype=torch.float64, device="cuda")
+    _lib.check(lib.hikf_dgemm(M, N, K, A.data_ptr(), K, B.data_ptr(), N, C.data_ptr(), N, 1.0, 0.0, 0, 30,
+                              _lib.stream_ptr()))
+    for r0 in (0, M // 2 - 1000, M - 4096):
+        ref = A[r0:r0 + 4096] @ B
+        err = float((C[r0:r0 + 4096] - ref).abs().max() / ref.abs().max())
+        assert err <= 1e-14, (r0, err)
+    del A, B, C
+    torch.cuda.empty_cache()

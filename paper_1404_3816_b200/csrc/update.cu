@@ -130,37 +130,89 @@ __global__ void __launch_bounds__(256) chol_inv_base(const double* __restrict__ 
     a[i][k] = S[(int64_t)i * ld + k];
   }
   __syncthreads();
+  // Right-looking Cholesky with the lower triangle in registers: thread t owns
+  // the elements e = t, t + 256, ... of the packed triangle (i >= k).  Per column
+  // j the owner of (j, j) publishes it, the owners of column j scale their
+  // entries and publish them, and every owner applies a[i][k] -= a[i][j] a[k][j]
+  // (k > j) in registers -- the same operations in the same order as updating
+  // a shared-memory copy, with two barriers per column (double-buffered).
+  constexpr int EPT = (NB * (NB + 1) / 2 + 255) / 256;  // elements per thread
+  __shared__ double colb[2][NB];
+  __shared__ double diagb[2];
+  const int ne = nb * (nb + 1) / 2;
+  double el[EPT];
+  int ei[EPT], ek[EPT];
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int e = tid + q * 256;
+    int i = 0, k = 0;
+    if (e < ne) {
+      i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      while (i * (i + 1) / 2 > e) --i;
+      k = e - i * (i + 1) / 2;
+      el[q] = a[i][k];
+    } else {
+      i = k = -1;
+      el[q] = 0.0;
+    }
+    ei[q] = i;
+    ek[q] = k;
+  }
   int bad = 0;
   for (int j = 0; j < nb; ++j) {
-    double d = a[j][j];
+    const int b = j & 1;
+#pragma unroll
+    for (int q = 0; q < EPT; ++q)
+      if (ei[q] == j && ek[q] == j) diagb[b] = el[q];
+    __syncthreads();
+    double d = diagb[b];
     if (!(d > 0.0)) {
       if (!bad) bad = j + 1;
       d = 1.0;  // keep going; the result is discarded by the caller
     }
     const double piv = sqrt(d);
     const double inv = 1.0 / piv;
-    // column j below the diagonal
-    for (int i = j + 1 + tid; i < nb; i += blockDim.x) a[i][j] *= inv;
-    __syncthreads();
-    if (tid == 0) a[j][j] = piv;
-    for (int i = j + 1 + warp; i < nb; i += 8) {
-      const double lij = a[i][j];
-      for (int k = j + 1 + lane; k <= i; k += 32) a[i][k] -= lij * a[k][j];
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+      if (ek[q] == j && ei[q] > j) {  // column j below the diagonal
+        el[q] *= inv;
+        colb[b][ei[q]] = el[q];
+      } else if (ek[q] == j && ei[q] == j) {
+        el[q] = piv;
+      }
     }
     __syncthreads();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q)
+      if (ek[q] > j) el[q] = fma(-colb[b][ei[q]], colb[b][ek[q]], el[q]);
   }
+#pragma unroll
+  for (int q = 0; q < EPT; ++q)
+    if (ei[q] >= 0) a[ei[q]][ek[q]] = el[q];
+  __syncthreads();
   // inverse by forward substitution, one column per thread (the dot-product
-  // chains of the 64 columns run in parallel)
+  // chains of the 64 columns run in parallel).  The column lives in registers
+  // (fully unrolled, predicated on k >= c): the chains of consecutive rows
+  // overlap instead of waiting on shared-memory round trips; the arithmetic and
+  // its order are those of x[i][c] = -(sum_{k=c}^{i-1} a[i][k] x[k][c]) / a[i][i].
   __shared__ double rdiag[NB];
   for (int i = tid; i < nb; i += blockDim.x) rdiag[i] = 1.0 / a[i][i];
   __syncthreads();
-  for (int c = tid; c < nb; c += blockDim.x) {
-    x[c][c] = rdiag[c];
-    for (int i = c + 1; i < nb; ++i) {
+  if (tid < nb) {
+    const int c = tid;
+    double xr[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
       double s = 0.0;
-      for (int k = c; k < i; ++k) s += a[i][k] * x[k][c];
-      x[i][c] = -s * rdiag[i];
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k >= c) s = fma(a[i][k], xr[k], s);
+      xr[i] = i < c ? 0.0 : (i == c ? rdiag[c] : (i < nb ? -s * rdiag[i] : 0.0));
     }
+#pragma unroll
+    for (int i = 0; i < NB; ++i)
+      if (i >= c && i < nb) x[i][c] = xr[i];
   }
   __syncthreads();
   for (int e = tid; e < nb * nb; e += blockDim.x) {

@@ -36,6 +36,13 @@ import sys
 import threading
 import time
 
+# The reference arm (--impl reference) runs the CPU algorithm alone on rank 0 with every host
+# thread.  torchrun exports OMP_NUM_THREADS=1 to multi-process launches, and OpenBLAS sizes its
+# pool from that when numpy is first imported, so the override must precede `import numpy`.
+if "--impl" in sys.argv and sys.argv[sys.argv.index("--impl") + 1:][:1] == ["reference"]:
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[_v] = str(os.cpu_count() or 1)
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -324,10 +331,14 @@ def run_reference(args, cfg, rank):
     threads = os.cpu_count()
     rows = args.cpu_rows
     per_step = []
-    for i in range(args.warmup + args.steps):
-        t, rows = cpu_step_sample(cfg, rows)
-        if i >= args.warmup:
-            per_step.append(t)
+    # torchrun sets OMP_NUM_THREADS=1 for multi-process launches; the reference arm
+    # runs alone on rank 0 and gets all host threads for its BLAS / LAPACK
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=threads):
+        for i in range(args.warmup + args.steps):
+            t, rows = cpu_step_sample(cfg, rows)
+            if i >= args.warmup:
+                per_step.append(t)
     t_step = statistics.median(per_step)
     value = 1.0 / t_step
     sample = (f"oracle/hikf_oracle.py predict+update (numpy + OpenBLAS/LAPACK) on {rows} of {cfg_m(cfg)} state rows "
@@ -736,7 +747,9 @@ def main():
     if fac is not None:
         line["factored"] = fac
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_cpu, rows = cpu_step_sample(cfg, args.cpu_rows)
+        from threadpoolctl import threadpool_limits
+        with threadpool_limits(limits=os.cpu_count()):
+            t_cpu, rows = cpu_step_sample(cfg, args.cpu_rows)
         line["cpu_baseline"] = {
             "value": 1.0 / t_cpu, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
             "sample": f"oracle predict+update on {rows} and {rows // 2} of {m} rows (n={n}), "

@@ -1,7 +1,8 @@
-"""Profiling driver (for ncu): cfg4 tree build + Q H^T precompute + `--steps`
-fused predict/update steps.  Kernel launch order (for ncu -s/-c):
-seg_gemm_kernel: P2P, P2M, M2M x (depth-2), M2L x (depth-1), L2P;
-dgemm_kernel per update: 60 (recursive Cholesky/inverse) + 3 (n x n) + Y + C."""
+"""Profiling driver (for ncu): tree build + Q H^T precompute + `--steps` fused
+predict/update steps at a bench config (default cfg4).  The Q H^T kernels are
+the sparse-charge path (regroup, p2m_pairs, m2m_pairs, m2l_pairs_kernel x 40
+offsets x level, box_warp_kernel L2L / L2P, p2p_sparse, p2p_scatter,
+spmm_rows); see tools/prof_qht.sh for the ncu selections used in profiles/."""
 import argparse
 import os
 import sys

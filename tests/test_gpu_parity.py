@@ -541,3 +541,30 @@ def test_dgemm_variants_and_triangular_k_ranges(pkg, variant):
             torch.cuda.synchronize()
             err = float((C - ref).abs().max() / ref.abs().max())
             assert err <= 1e-14, (variant, M, N, K, kmode, err)
+
+
+@pytest.mark.parametrize("ns,nr", [(3, 7), (5, 13)])
+def test_factored_equals_explicit_odd_ray_counts(pkg, ns, nr):
+    """Odd n (21, 65 rays: boundary tiles of every GEMM, odd strides in the fused
+    GEMV): the factored and explicit updates agree step by step with each other and
+    with the oracle."""
+    flt = pkg.filters
+    cfg = dict(cases.CFG1, ns=ns, nr=nr, T=6)
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    model = _Model(grid, H, kern, cfg["R"])
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    pre = flt.hikf_precompute_fmm(model, tree)
+    xy = grid.cell_centers().coords
+    obs = O.observations(H, O.moving_plume(xy, cfg["T"]), cfg["R"], [1, 0])
+    ex = flt.hikf_init(model)
+    fa = flt.hikf_init(model, representation="factored")
+    ost = O.init_state(H, grid.m)
+    opre = O.Pre(pre.C_Q, pre.HC_Q, pre.diag_Q)
+    for t in range(cfg["T"]):
+        ex = flt.hikf_update(flt.hikf_predict(ex, pre), H, cfg["R"], obs[t])
+        fa = flt.hikf_update(flt.hikf_predict(fa, pre), H, cfg["R"], obs[t])
+        ost = O.update(O.predict(ost, opre), H, cfg["R"], obs[t])
+        for k in ("mean", "variance", "cross_cov", "HC"):
+            assert O.rel_fro(getattr(fa, k), getattr(ex, k)) <= 1e-11, (t, k)
+            assert O.rel_fro(getattr(ex, k), getattr(ost, k)) <= 1e-11, (t, k)

@@ -208,7 +208,16 @@ int hikf_update_factored(int64_t m, int64_t n, const double* mean_dev, const dou
                          int32_t predict, const int32_t* indptr_dev, const int32_t* indices_dev,
                          const double* data_dev, double r_variance, const double* z_dev, double* mean_out,
                          double* N_out, double* var_out, double* HC_out, void* workspace, size_t workspace_bytes,
-                         double* min_var_out, double* mean_host, void* stream);
+                         double* min_var_out, double* mean_host, double alpha0, const double* A_dev, double* A_out,
+                         const int32_t* ht_indptr_dev, const int32_t* ht_indices_dev, const double* ht_data_dev,
+                         void* stream);
+/* (alpha0 != 0: a state started from C_0 = alpha0 H^T (filters.py:118-126) keeps
+ * C = alpha0 H^T A + C_Q N with a second n x n factor A (A_dev -> A_out); H^T is passed
+ * as a CSR with m rows.  alpha0 = 0 ignores A and H^T.) */
+/* Y (rows x k) += alpha * S X for a CSR S (rows x cols) and X (cols x k), row-major: the
+ * sparse term alpha0 H^T A of a factored cross covariance on materialisation. */
+int hikf_csr_spmm_add(int64_t rows, int64_t k, const int32_t* indptr_dev, const int32_t* indices_dev,
+                      const double* data_dev, const double* X_dev, double alpha, double* Y_dev, void* stream);
 
 /* ---- row-sharded update: the same update on rows [r0, r1) of a
  * state sharded across ranks.  Hmean_dev = the all-reduced H mean (the

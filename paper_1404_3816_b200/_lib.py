@@ -83,7 +83,8 @@ SIGNATURES = {
                                            _P, _P, _SZ, _P, ctypes.c_int32, _P, _P]),
     "hikf_update_factored_workspace_bytes": (_SZ, [_I64, _I64]),
     "hikf_update_factored": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _P, _P, _I32, _P, _P, _P, _D, _P, _P,
-                                            _P, _P, _P, _P, _SZ, _P, _P, _P]),
+                                            _P, _P, _P, _P, _SZ, _P, _P, _D, _P, _P, _P, _P, _P, _P]),
+    "hikf_csr_spmm_add": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _D, _P, _P]),
     "hikf_update_rows": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _D, _P, _P, _P, _P, _P, _P,
                                         _SZ, _P, ctypes.c_int32, _P]),
     "hikf_csr_spmv": (ctypes.c_int, [_I64, _P, _P, _P, _P, _P, _P]),

@@ -519,7 +519,9 @@ int hikf_update_factored(int64_t m, int64_t n, const double* mean, const double*
                          const double* HC, const double* CQ, const double* dQ, const double* HCQ, int32_t predict,
                          const int32_t* ip, const int32_t* ix, const double* val, double r, const double* z,
                          double* mean_out, double* N_out, double* var_out, double* HC_out, void* workspace,
-                         size_t workspace_bytes, double* min_var_out, double* mean_host, void* stream) {
+                         size_t workspace_bytes, double* min_var_out, double* mean_host, double alpha0,
+                         const double* A, double* A_out, const int32_t* ht_indptr, const int32_t* ht_indices,
+                         const double* ht_data, void* stream) {
   if (m < 1 || n < 1 || !mean || !N || !var || !HC || !CQ || !ip || !z || !mean_out || !N_out || !var_out ||
       !HC_out || N == N_out) {
     set_error("bad factored update arguments");
@@ -553,10 +555,31 @@ int hikf_update_factored(int64_t m, int64_t n, const double* mean, const double*
   a.predict_in = predict != 0;
   a.Nin = N;
   a.Nout = N_out;
+  if (alpha0 != 0.0) {
+    if (!A || !A_out || !ht_indptr || !ht_indices || !ht_data) {
+      set_error("factored update with alpha0 != 0 needs A (in / out) and H^T (CSR)");
+      return HIKF_BAD_ARGUMENT;
+    }
+    a.alpha0 = alpha0;
+    a.Ain = A;
+    a.Aout = A_out;
+    a.ht_ip = ht_indptr;
+    a.ht_ix = ht_indices;
+    a.ht_val = ht_data;
+  }
   UpdateResult res;
   int s = update(a, as_stream(stream), &res);
   if (min_var_out) *min_var_out = res.min_var;
   return s;
+}
+
+int hikf_csr_spmm_add(int64_t rows, int64_t k, const int32_t* indptr, const int32_t* indices, const double* data,
+                      const double* X, double alpha, double* Y, void* stream) {
+  if (rows < 0 || k < 0 || (rows > 0 && (!indptr || !X || !Y))) {
+    set_error("bad csr_spmm_add arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  return csr_spmm_add(rows, k, indptr, indices, data, X, alpha, Y, as_stream(stream));
 }
 
 int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const double* C, const double* var,

@@ -55,6 +55,25 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
   // possibly aliasing pointers
   if (PARTIALS) {
     const double sc = g.px ? 1.0 : (Cin ? 1.0 : g.alpha);
+    if (g.sp_ip) {  // sparse-row addend (see GemmArgs): folded into the accumulators first
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
+        if (row >= g.M) continue;
+        const int32_t e0 = g.sp_ip[row], e1 = g.sp_ip[row + 1];
+        for (int32_t e = e0; e < e1; ++e) {
+          const double w = g.sp_alpha * g.sp_val[e];
+          const double* yr = g.sp_Y + (int64_t)g.sp_ix[e] * g.sp_ldy;
+#pragma unroll
+          for (int j = 0; j < TN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int64_t col = colh(j, h);
+              if (col < g.N) acc[i][j][h] = fma(w, yr[col], acc[i][j][h]);
+            }
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int rl = wm * TM * 8 + i * 8 + gq;

@@ -52,6 +52,14 @@ struct GemmArgs {
   // panel their row block just streamed through L2
   const double* gv_x = nullptr;
   double* gv_y = nullptr;
+  // optional sparse-row addend before the partials (PARTIALS, px == null): the value of
+  // element (i, j) becomes alpha (acc + sp_alpha sum_{e in row i of the CSR sp} sp_val[e] sp_Y[sp_ix[e]][j])
+  // (the factored update with C_0 = alpha H^T: sp = H^T, sp_Y = Y)
+  const int32_t *sp_ip = nullptr, *sp_ix = nullptr;
+  const double* sp_val = nullptr;
+  const double* sp_Y = nullptr;
+  int64_t sp_ldy = 0;
+  double sp_alpha = 0.0;
   int variant = -1;  // tile-shape variant (-1: dgemm_variant())
 };
 

@@ -512,12 +512,31 @@ __global__ void __launch_bounds__(kT) gemv_rows(int64_t rows, int64_t cols, cons
   }
 }
 
+// Y[i, :] += alpha sum_e val[e] X[ix[e], :] (one warp per row; the rows of H^T hold ~1-2 entries)
+__global__ void csr_spmm_add_kernel(int64_t rows, int64_t k, const int32_t* __restrict__ ip,
+                                    const int32_t* __restrict__ ix, const double* __restrict__ val,
+                                    const double* __restrict__ X, double alpha, double* __restrict__ Y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+    const int32_t e0 = ip[row], e1 = ip[row + 1];
+    if (e0 == e1) continue;
+    for (int64_t c = lane; c < k; c += 32) {
+      double s = 0.0;
+      for (int32_t e = e0; e < e1; ++e) s = fma(val[e], X[(int64_t)ix[e] * k + c], s);
+      Y[row * k + c] += alpha * s;
+    }
+  }
+}
+
 // var_out = var' - sum_t psq (= rowsum((C_Q L_G)^2) = rowsum(K o C')), mean_out = mean + C_Q u;
 // block extrema for the consistency check (as finalize_rows)
+// (with hv: mean_out = mean + (C_Q u + alpha0 H^T u_A), the alpha0 != 0 state)
 __global__ void finalize_factored(int64_t m, int nt, const double* __restrict__ psq, const double* __restrict__ gv,
                                   const double* __restrict__ varp, const double* __restrict__ mean,
                                   double* __restrict__ var_out, double* __restrict__ mean_out,
-                                  double* __restrict__ bmin, double* __restrict__ bmax) {
+                                  double* __restrict__ bmin, double* __restrict__ bmax,
+                                  const double* __restrict__ hv = nullptr, double halpha = 0.0) {
   double lmin = DBL_MAX, lmax = -DBL_MAX;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -525,7 +544,7 @@ __global__ void finalize_factored(int64_t m, int nt, const double* __restrict__ 
     const double vp = varp[i];
     const double v = vp - s;
     var_out[i] = v;
-    mean_out[i] = mean[i] + gv[i];
+    mean_out[i] = mean[i] + (hv ? gv[i] + halpha * hv[i] : gv[i]);
     lmin = fmin(lmin, v);
     lmax = fmax(lmax, vp);
   }
@@ -595,6 +614,14 @@ int spmv(int64_t n, const int32_t* ip, const int32_t* ix, const double* val, con
          cudaStream_t st) {
   if (n <= 0) return HIKF_OK;
   csr_spmv<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, ip, ix, val, x, y);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+int csr_spmm_add(int64_t rows, int64_t k, const int32_t* ip, const int32_t* ix, const double* val, const double* X,
+                 double alpha, double* Y, cudaStream_t st) {
+  if (rows <= 0 || k <= 0) return HIKF_OK;
+  csr_spmm_add_kernel<<<grid_for(rows * 32), kT, 0, st>>>(rows, k, ip, ix, val, X, alpha, Y);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
@@ -719,6 +746,7 @@ struct FacChain {
 
 struct FacWs {
   double *HCp, *S, *L, *Li, *LiT, *P, *R, *Sinv, *tmp, *innov, *u, *W, *LG, *gv, *psq, *bmin, *bmax, *minv;
+  double *WA, *FA, *Qf, *L2iT, *Y, *uA, *hv;  // alpha0 != 0 terms
   FacChain c;
   int* status;
 };
@@ -735,11 +763,13 @@ static size_t factored_layout(int64_t m, int64_t n, char* base, FacWs* ws) {
   FacWs w;
   for (double** p : {&w.HCp, &w.S, &w.L, &w.Li, &w.LiT, &w.P, &w.R, &w.Sinv, &w.tmp, &w.W, &w.LG, &w.c.Mp, &w.c.F,
                      &w.c.FT, &w.c.G1, &w.c.L1, &w.c.L1i, &w.c.L1iT, &w.c.Q1, &w.c.Q1T, &w.c.G2, &w.c.L2, &w.c.L2i,
-                     &w.c.tmp2})
+                     &w.c.tmp2, &w.WA, &w.FA, &w.Qf, &w.L2iT, &w.Y})
     *p = (double*)take(8 * n * n);
   w.innov = (double*)take(8 * n);
   w.u = (double*)take(8 * n);
+  w.uA = (double*)take(8 * n);
   w.gv = (double*)take(8 * m);
+  w.hv = (double*)take(8 * m);
   w.psq = (double*)take(8 * m * nt);
   w.bmin = (double*)take(8 * (size_t)nb);
   w.bmax = (double*)take(8 * (size_t)nb);
@@ -881,6 +911,11 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
   static cudaEvent_t ev_n = nullptr;  // main -> side: N_out written
   if (!ev_n) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&ev_n, cudaEventDisableTiming));
 
+  const bool with_a = a.Ain != nullptr;  // C_0 = alpha0 H^T: the (W, L_G) look-ahead is not used
+  if (with_a && (!a.Aout || !a.ht_ip || !a.ht_ix || !a.ht_val || a.Ain == a.Aout)) {
+    set_error("factored update with alpha0 != 0 needs A (in / out) and H^T as a CSR");
+    return HIKF_BAD_ARGUMENT;
+  }
   const bool use_la = lookahead_enabled() && a.predict_in && n > 0;
   LookAhead* la = nullptr;
   FacLookAhead* fl = nullptr;
@@ -890,7 +925,8 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
     fl = &fac_lookahead();
     HIKF_TRY(lookahead_reserve(*la, n));
     HIKF_TRY(fac_lookahead_reserve(*fl, n));
-    HIKF_TRY(lookahead_probe(*la, a.HC, a.HCQ, a.r, n, st, &hit, a.Nin, fl, &fhit));
+    HIKF_TRY(lookahead_probe(*la, a.HC, a.HCQ, a.r, n, st, &hit, with_a ? nullptr : a.Nin, with_a ? nullptr : fl,
+                             &fhit));
   }
 
   HIKF_CHECK_CUDA(cudaEventRecord(ev[0], st));
@@ -946,6 +982,33 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
     HIKF_CHECK_CUDA(cudaEventRecord(ev_n, st));
     gemv_rows<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, n, W, n, w.innov, w.u);  // u = W innov
     HIKF_CHECK_LAUNCH();
+    if (with_a) {
+      // the alpha0 H^T A part of C': W_A = A S^-1, A_new = r W_A, u_A = W_A innov, and
+      // Y = (A Li^T) Q with F_M^T = Q R from the Cholesky-QR2 above (Q = Q1 L2^-T), so that
+      // rowsum(K o C') = || alpha0 h_i Y + q_i L_G ||^2 (h_i: row i of H^T)
+      auto gemm = [&](const double* A_, const double* B_, double* C_, int kmode) {
+        GemmArgs q;
+        q.M = n; q.N = n; q.K = n;
+        q.A = A_; q.sa_r = n;
+        q.B = B_; q.sb_r = n;
+        q.C = C_; q.ldc = n;
+        q.kmode = kmode;
+        return dgemm(q, 1, st);
+      };
+      HIKF_TRY(gemm(a.Ain, Sinv, w.WA, KFULL));
+      scale_kernel<<<grid_for(n * n), kT, 0, st>>>(w.WA, a.r, a.Aout, n * n);
+      HIKF_CHECK_LAUNCH();
+      gemv_rows<<<ceil_div(n * 32, kT), kT, 0, st>>>(n, n, w.WA, n, w.innov, w.uA);
+      HIKF_CHECK_LAUNCH();
+      HIKF_TRY(gemm(a.Ain, LiT, w.FA, KB_UPPER));
+      transpose_kernel<<<grid_for(n * n), kT, 0, st>>>(w.c.L2i, n, w.L2iT);
+      HIKF_CHECK_LAUNCH();
+      HIKF_TRY(gemm(w.c.Q1, w.L2iT, w.Qf, KB_UPPER));
+      HIKF_TRY(gemm(w.FA, w.Qf, w.Y, KFULL));
+      // H^T u_A for the mean (rows of H^T: one warp each)
+      csr_spmv<<<ceil_div(m * 32, kT), kT, 0, st>>>(m, a.ht_ip, a.ht_ix, a.ht_val, w.uA, w.hv);
+      HIKF_CHECK_LAUNCH();
+    }
   }
   // mean increment C_Q u: fused into the triangular GEMM (GemmArgs::gv_*: the
   // last column tile's CTAs re-read their row panel from L2); HIKF_GEMV_FUSED=0
@@ -970,13 +1033,18 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
       g.gv_x = w.u;
       g.gv_y = w.gv;
     }
+    if (with_a) {
+      g.sp_ip = a.ht_ip; g.sp_ix = a.ht_ix; g.sp_val = a.ht_val;
+      g.sp_Y = w.Y; g.sp_ldy = n; g.sp_alpha = a.alpha0;
+    }
     g.variant = vc;
     ProfScope ps(ST_GEMM_C, st);
     HIKF_TRY(dgemm(g, 1, st));
   }
   {
     ProfScope pz(ST_FINALIZE, st);
-    finalize_factored<<<nb, kT, 0, st>>>(m, nt, w.psq, w.gv, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
+    finalize_factored<<<nb, kT, 0, st>>>(m, nt, w.psq, w.gv, varp, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax,
+                                         with_a ? w.hv : nullptr, a.alpha0);
     HIKF_CHECK_LAUNCH();
     check_variance<<<1, kT, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
     HIKF_CHECK_LAUNCH();
@@ -989,6 +1057,9 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
     fl->ready = false;
     int nx = 0;
     HIKF_TRY(lookahead_enqueue(*la, hit, a.HC_out, a.HCQ, a.r, n, w.S, w.L, w.tmp, side, &nx));
+  }
+  if (use_la && !with_a) {
+    const int nx = la->cur;
     // the next step's factored chain from N_out (main) and S_{t+1} (just above)
     ProfScope pf(ST_FACTOR, side);
     const int fx = fhit ? fl->cur ^ 1 : fl->cur;

@@ -29,6 +29,13 @@ struct UpdateArgs {
   bool predict_in = true;  // factored: the prior is predicted (C' = C_Q (N + I), var + diag_Q, HC + HC_Q)
   const double* Nin = nullptr;
   double* Nout = nullptr;
+  // factored with C_0 = alpha0 H^T (alpha0 != 0): C = alpha0 H^T A + C_Q N; Ain -> Aout, and H^T as
+  // a CSR (m rows) for the sparse terms
+  double alpha0 = 0.0;
+  const double* Ain = nullptr;
+  double* Aout = nullptr;
+  const int32_t *ht_ip = nullptr, *ht_ix = nullptr;
+  const double* ht_val = nullptr;
 };
 
 struct UpdateResult {
@@ -44,6 +51,9 @@ int predict(int64_t m, int64_t n, const double* C, const double* var, const doub
             const double* dQ, const double* HCQ, double* Co, double* varo, double* HCo, cudaStream_t st);
 int spmv(int64_t n, const int32_t* ip, const int32_t* ix, const double* val, const double* x, double* y,
          cudaStream_t st);
+// Y[i, :] += alpha sum_e val[e] X[ix[e], :] for the rows i of a CSR (rows x cols), X row-major k columns
+int csr_spmm_add(int64_t rows, int64_t k, const int32_t* ip, const int32_t* ix, const double* val, const double* X,
+                 double alpha, double* Y, cudaStream_t st);
 size_t spd_workspace_bytes(int64_t n, int64_t k);
 int spd_solve(int64_t n, int64_t k, const double* A, const double* B, double* X, void* ws, size_t ws_bytes,
               int64_t* info, cudaStream_t st);

@@ -79,6 +79,14 @@ class DeviceCSR:
         return scipy.sparse.csr_matrix((self.data.cpu().numpy(), self.indices.cpu().numpy(),
                                         self.indptr.cpu().numpy()), shape=self.shape)
 
+    def transposed(self) -> "DeviceCSR":
+        """H^T as a device CSR (cols x rows), built once from the host copy and cached."""
+        if getattr(self, "_T", None) is None:
+            HT = self.to_scipy().T.tocsr()
+            HT.sort_indices()
+            self._T = DeviceCSR(HT)
+        return self._T
+
     @classmethod
     def of(cls, H) -> "DeviceCSR":
         if isinstance(H, DeviceCSR):
@@ -183,9 +191,10 @@ class FactoredHikfState(HikfState):
     consistency check).  ``cross_cov`` / ``cross_cov_t`` materialise C_Q N with
     one device GEMM on first access.  Opt-in: ``hikf_init(model,
     representation="factored")``; see update.cu ("factored representation")
-    and DESIGN.md section 5."""
+    and DESIGN.md section 5.  With C_0 = alpha H^T (alpha != 0) the state also
+    carries A: C = alpha H^T A + C_Q N."""
 
-    def __init__(self, mean, N, variance, HC, pre, *, _prior=None, _pre=None):
+    def __init__(self, mean, N, variance, HC, pre, *, A=None, alpha0=0.0, Hd=None, _prior=None, _pre=None):
         self._prior = _prior
         self._pre = _pre
         self._host = {}
@@ -193,10 +202,13 @@ class FactoredHikfState(HikfState):
         if _prior is None:
             self.mean_t, self.N_t, self.variance_t, self.HC_t = mean, N, variance, HC
             self._cq_pre = pre
+            # C_0 = alpha0 H^T (filters.py:118-126): C = alpha0 H^T A + C_Q N
+            self.A_t, self.alpha0, self._Hd = A, float(alpha0), Hd
         else:
             self.mean_t = _prior.mean_t
             self.N_t = self.variance_t = self.HC_t = None
             self._cq_pre = _pre
+            self.A_t, self.alpha0, self._Hd = _prior.A_t, _prior.alpha0, _prior._Hd
 
     @property
     def pending(self) -> bool:
@@ -217,13 +229,18 @@ class FactoredHikfState(HikfState):
         self._materialize()
         if self._C is None:
             m, n = self.mean_t.shape[0], self.N_t.shape[0]
-            if self._cq_pre is None:  # C_0 = 0
-                self._C = torch.zeros((m, n), dtype=torch.float64, device=self.mean_t.device)
+            if self._cq_pre is None:  # no C_Q term yet
+                C = torch.zeros((m, n), dtype=torch.float64, device=self.mean_t.device)
             else:
                 C = torch.empty((m, n), dtype=torch.float64, device=self.mean_t.device)
                 _lib.check(_lib.load().hikf_dgemm(m, n, n, self._cq_pre.C_Q_t.data_ptr(), n, self.N_t.data_ptr(), n,
                                                   C.data_ptr(), n, 1.0, 0.0, 0, -1, _lib.stream_ptr()))
-                self._C = C
+            if self.A_t is not None and self.alpha0 != 0.0:  # + alpha0 H^T A
+                HT = self._Hd.transposed()
+                _lib.check(_lib.load().hikf_csr_spmm_add(m, n, HT.indptr.data_ptr(), HT.indices.data_ptr(),
+                                                         HT.data.data_ptr(), self.A_t.data_ptr(), self.alpha0,
+                                                         C.data_ptr(), _lib.stream_ptr()))
+            self._C = C
         return self._C
 
     @property
@@ -281,16 +298,22 @@ def hikf_precompute_dense(model) -> HikfPrecompute:
 def hikf_init(model, representation: str = "explicit") -> HikfState:
     """mean = mu_0, C = alpha H^T, var = alpha, HC = alpha H H^T (filters.py:118-126).
 
-    ``representation="factored"`` (alpha = 0 only) returns a FactoredHikfState."""
+    ``representation="factored"`` returns a FactoredHikfState (C kept as alpha H^T A + C_Q N)."""
     H = DeviceCSR.of(_model_H(model))
     m, n = int(model.m), H.shape[0]
     dev = _dev()
     mean = _to_dev(model.initial_mean, (m,)).clone()
     if representation == "factored":
-        if float(model.alpha) != 0.0:
-            raise ValueError("the factored representation needs alpha = 0 (C_0 = 0)")
         z = dict(dtype=torch.float64, device=dev)
-        return FactoredHikfState(mean, torch.zeros((n, n), **z), torch.zeros((m,), **z), torch.zeros((n, n), **z), None)
+        alpha = float(model.alpha)
+        if alpha == 0.0:
+            return FactoredHikfState(mean, torch.zeros((n, n), **z), torch.zeros((m,), **z), torch.zeros((n, n), **z),
+                                     None)
+        # C_0 = alpha H^T = alpha H^T A with A = I, var = alpha, HC = alpha H H^T
+        Hs = H.to_scipy()
+        HHt = torch.from_numpy(np.ascontiguousarray((Hs @ Hs.T).toarray())).to(dev)
+        return FactoredHikfState(mean, torch.zeros((n, n), **z), torch.full((m,), alpha, **z), alpha * HHt, None,
+                                 A=torch.eye(n, **z), alpha0=alpha, Hd=H)
     if representation != "explicit":
         raise ValueError(f"unknown representation {representation!r}")
     C = torch.empty((m, n), dtype=torch.float64, device=dev)
@@ -399,6 +422,9 @@ def _update_factored(state: FactoredHikfState, Hd: DeviceCSR, r: float, zt: torc
     N = torch.empty((n, n), dtype=torch.float64, device=dev)
     var = torch.empty((m,), dtype=torch.float64, device=dev)
     HC = torch.empty((n, n), dtype=torch.float64, device=dev)
+    with_a = src.A_t is not None and src.alpha0 != 0.0
+    A_out = torch.empty((n, n), dtype=torch.float64, device=dev) if with_a else None
+    HT = src._Hd.transposed() if with_a else None
     lib = _lib.load()
     key = (m, n, dev.index, "factored")
     ws = _WS.get(key)
@@ -413,8 +439,11 @@ def _update_factored(state: FactoredHikfState, Hd: DeviceCSR, r: float, zt: torc
         pre.C_Q_t.data_ptr(), _lib.ptr(pre.diag_Q_t) if fused else None, _lib.ptr(pre.HC_Q_t) if fused else None,
         1 if fused else 0, Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), r, zt.data_ptr(),
         mean.data_ptr(), N.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None,
-        mean_host.data_ptr(), _lib.stream_ptr()))
-    out = FactoredHikfState(mean, N, var, HC, pre)
+        mean_host.data_ptr(), src.alpha0 if with_a else 0.0, _lib.ptr(src.A_t) if with_a else None,
+        _lib.ptr(A_out), _lib.ptr(HT.indptr) if with_a else None, _lib.ptr(HT.indices) if with_a else None,
+        _lib.ptr(HT.data) if with_a else None, _lib.stream_ptr()))
+    out = FactoredHikfState(mean, N, var, HC, pre, A=A_out, alpha0=src.alpha0 if with_a else 0.0,
+                            Hd=src._Hd if with_a else None)
     out._pinned = mean_host
     out._host["mean"] = mean_host.numpy()
     return out

@@ -448,16 +448,14 @@ def test_factored_filter_matches_reference(pkg, fixture, cfg):
 
 
 def test_factored_state_api(pkg):
-    """alpha != 0 is refused; a predicted factored state materialises C' = C_Q (N + I);
+    """Unknown representations are refused; a predicted factored state materialises C' = C_Q (N + I);
     the update without a predict keeps the reference's semantics."""
     flt = pkg.filters
     g = _load("small_rays.npz")
     cfg = cases.SMALL
     tree, H, pre, st, model = _run_filter_factored(pkg, cfg, g["obs"], T=2)
-    model.alpha = 0.5
     with pytest.raises(ValueError):
-        flt.hikf_init(model, representation="factored")
-    model.alpha = 0.0
+        flt.hikf_init(model, representation="dense")
     p = flt.hikf_predict(st, pre)
     np.testing.assert_allclose(p.cross_cov, st.cross_cov + pre.C_Q, rtol=1e-12, atol=1e-13)
     np.testing.assert_allclose(p.variance, st.variance + pre.diag_Q, rtol=0, atol=0)
@@ -568,3 +566,29 @@ def test_factored_equals_explicit_odd_ray_counts(pkg, ns, nr):
         for k in ("mean", "variance", "cross_cov", "HC"):
             assert O.rel_fro(getattr(fa, k), getattr(ex, k)) <= 1e-11, (t, k)
             assert O.rel_fro(getattr(ex, k), getattr(ost, k)) <= 1e-11, (t, k)
+
+
+@pytest.mark.parametrize("alpha,cfg", [(0.5, cases.SMALL), (2.0, cases.CFG1)])
+def test_factored_with_alpha_prior(pkg, alpha, cfg):
+    """C_0 = alpha H^T (filters.py:118-126, alpha != 0): the factored state carries
+    C = alpha H^T A + C_Q N (a second n x n factor and the sparse alpha H^T terms in the
+    mean, the variance GEMM epilogue and the materialisation) and agrees with the explicit
+    update step by step."""
+    flt = pkg.filters
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    model = _Model(grid, H, kern, cfg["R"])
+    model.alpha = alpha
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
+    pre = flt.hikf_precompute_fmm(model, tree)
+    xy = grid.cell_centers().coords
+    obs = O.observations(H, O.moving_plume(xy, 6), cfg["R"], [2, 0])
+    ex = flt.hikf_init(model)
+    fa = flt.hikf_init(model, representation="factored")
+    for k in ("mean", "variance", "cross_cov", "HC"):
+        assert O.rel_fro(getattr(fa, k), getattr(ex, k)) <= 1e-14, k
+    for t in range(6):
+        ex = flt.hikf_update(flt.hikf_predict(ex, pre), H, cfg["R"], obs[t])
+        fa = flt.hikf_update(flt.hikf_predict(fa, pre), H, cfg["R"], obs[t])
+        for k in ("mean", "variance", "cross_cov", "HC"):
+            assert O.rel_fro(getattr(fa, k), getattr(ex, k)) <= 1e-10, (t, k, O.rel_fro(getattr(fa, k), getattr(ex, k)))

@@ -80,8 +80,27 @@ __global__ void spmm_rows(int64_t n, const int32_t* __restrict__ ip, const int32
   for (int64_t j0 = 4 * (int64_t)threadIdx.x; j0 < n; j0 += 4 * (int64_t)blockDim.x) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     if (vec) {
-#pragma unroll 4
-      for (int32_t e = b; e < e1; ++e) {
+      // 8 rows of C_Q in flight per thread (loads first, then the sums in entry order)
+      int32_t e = b;
+      for (; e + 8 <= e1; e += 8) {
+        double v[8];
+        double2 a[8], c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          v[u] = val[e + u];
+          const double* row = C + (int64_t)ix[e + u] * n + j0;
+          a[u] = __ldg(reinterpret_cast<const double2*>(row));
+          c[u] = __ldg(reinterpret_cast<const double2*>(row + 2));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s0 += v[u] * a[u].x;
+          s1 += v[u] * a[u].y;
+          s2 += v[u] * c[u].x;
+          s3 += v[u] * c[u].y;
+        }
+      }
+      for (; e < e1; ++e) {
         const double v = val[e];
         const double* row = C + (int64_t)ix[e] * n + j0;
         const double2 a = __ldg(reinterpret_cast<const double2*>(row));

@@ -444,7 +444,7 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
                     "note": "row-sharded precompute: upward pass + M2L replicated, L2P/P2P for owned rows"},
             "e2e": {"value": args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * (r1 - r0), "api": "sharded.ShardedHikf.update (numpy z) + mean rows"},
-            "roofline": {"kernel": "dgemm_cutlass_kernel (K = C' S^-1 on this rank's rows, fused epilogue; "
+            "roofline": {"kernel": "dgemm_rm_kernel (K = C' S^-1 on this rank's rows, fused epilogue; "
                                    "2 (m/N) n^2 flops per launch)", "bound": "fp64", "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_PEAK_TFLOPS if achieved else None, "traffic": None,
@@ -675,7 +675,7 @@ def main():
                "e2e": {"value": world * args.steps / t_fe2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
                        "d2h_bytes_per_step": 8 * m},
                "stage_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in fst.items()},
-               "roofline": {"kernel": "dgemm_cutlass_kernel KB_LOWER (rowsum((C_Q L_G)^2), no output store)",
+               "roofline": {"kernel": "dgemm_rm_kernel KB_LOWER (rowsum((C_Q L_G)^2), no output store)",
                             "bound": "fp64", "achieved": tri_flops / t_tri / 1e12 if t_tri else None,
                             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                             "frac": tri_flops / t_tri / 1e12 / FP64_PEAK_TFLOPS if t_tri else None,
@@ -725,7 +725,7 @@ def main():
                                      "charges / expansions are multiplied); dense-formulation equivalent rate = "
                                      f"{qht_flops / t_qht / 1e12:.1f} TFLOP/s",
                              "m2l": {"achieved": fmm_useful["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
-        "roofline": {"kernel": "dgemm_cutlass_kernel (K = C' S^-1 -> C_new = r K, fused rowsum(K o C'), K innov and the "
+        "roofline": {"kernel": "dgemm_rm_kernel (K = C' S^-1 -> C_new = r K, fused rowsum(K o C'), K innov and the "
                                "next step's C' = C_new + C_Q; 2 m n^2 flops per launch)", "bound": "fp64",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS,

@@ -1,37 +1,36 @@
-// FP64 DMMA GEMM (see dgemm.cuh).  One templated kernel; the tile shape is
-// a compile-time variant (dgemm_variant() picks it; HIKF_DGEMM_VARIANT
-// overrides for tuning sweeps).
+// FP64 DMMA GEMM (see dgemm.cuh), hand-written for sm_100a (no library
+// mainloop).  Two kernels share one fused epilogue:
+//   * dgemm_rm_kernel -- row-major operands (every large GEMM of the update and
+//     of the factored path): register-double-buffered fragments, a cp.async
+//     ring whose copies are spread over the k-groups, one barrier per k-tile
+//     placed before the last k-group so the next tile's first fragments load
+//     under the last DMMAs, serpentine DMMA order, 1D tile raster with the
+//     column tiles of a row block adjacent (the A row panel is reused from L2);
+//   * dgemm_kernel -- any strides (the transposed-B GEMMs of the recursive
+//     Cholesky on n x n blocks).
 #include <algorithm>
 #include <cstdlib>
 
 #include "dgemm.cuh"
 
-// CUTLASS 2.x SM80 FP64 tensor-op threadblock mainloop (headers only; the
-// tree vendored with flashinfer, see Makefile CUTLASS_INC).  Used as the
-// mainloop of the K-GEMM variant below; the epilogue is ours.
-#include "cutlass/gemm/gemm.h"
-#include "cutlass/gemm/threadblock/default_mma.h"
-#include "cutlass/layout/matrix.h"
-
 namespace hikf {
 
 namespace {
 
-// Shared epilogue: alpha/beta, fused row partials, stores.  Accumulator
-// acc[i][j][h] holds C[row = i*8 + gq][col] of the warp tile with
-//   SPLIT = false: col = j*8 + 2 t4 + h        (8-column DMMA tiles)
-//   SPLIT = true:  col = (2 t4 + h) * TN + j   (interleaved tiles: each thread
-//                  owns two runs of TN contiguous columns)
-template <int BM, int BN, int WM, int WN, bool PARTIALS, bool SPLIT = false>
+// Shared epilogue: alpha/beta, fused row partials (written to column slot
+// `ctile` of psq / pdot), the chained-predict second output, stores.
+// Accumulator acc[i][j][h] holds C[row = i*8 + gq][col = j*8 + 2 t4 + h] of the
+// warp tile (8 x 8 DMMA tiles).
+template <int BM, int BN, int WM, int WN, bool PARTIALS>
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[BM / WM / 8][BN / WN / 8][2], double* C,
                                               const double* Cin, int64_t m0, int64_t n0, int tid, int wm, int wn,
                                               int gq, int t4, double (*red_sq)[PARTIALS ? BM : 1],
-                                              double (*red_dot)[PARTIALS ? BM : 1]) {
+                                              double (*red_dot)[PARTIALS ? BM : 1], int64_t ctile) {
   constexpr int THREADS = WM * WN * 32;
   constexpr int TM = BM / WM / 8;
   constexpr int TN = BN / WN / 8;
   const int64_t cw = n0 + wn * TN * 8;
-  auto colh = [&](int j, int h) -> int64_t { return cw + (SPLIT ? (2 * t4 + h) * TN + j : j * 8 + 2 * t4 + h); };
+  auto colh = [&](int j, int h) -> int64_t { return cw + j * 8 + 2 * t4 + h; };
   // beta * Cin is read for the whole warp tile before any store: C may alias
   // Cin (in-place C_new = C' - Y P), and separating the phases lets the loads
   // overlap instead of serialising load -> store round trips.
@@ -103,20 +102,10 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
 #pragma unroll
   for (int i = 0; i < TM && C; ++i) {  // C == null: partials only (no output store)
     const int64_t row = m0 + wm * TM * 8 + i * 8 + gq;
-    if (SPLIT && (TN % 2 == 0) && row < g.M && cw + BN / WN <= g.N && g.ldc % 2 == 0 && ((uintptr_t)C & 15) == 0) {
-      // two runs of TN contiguous columns: 16-byte stores
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int j = 0; j < TN; j += 2) {
-          const double v0 = Cin ? acc[i][j][h] : g.alpha * acc[i][j][h];
-          const double v1 = Cin ? acc[i][j + 1][h] : g.alpha * acc[i][j + 1][h];
-          *reinterpret_cast<double2*>(C + row * g.ldc + colh(j, h)) = make_double2(v0, v1);
-        }
-    } else if (g.chain_out) {
+    if (g.chain_out) {
       // also emit chain_out = C + chain_add (the next step's predict, fused);
       // columns 2 t4 and 2 t4 + 1 are adjacent: 16-byte accesses when aligned
-      const bool v16 = !SPLIT && row < g.M && cw + BN / WN <= g.N && (g.ldc | g.ldch) % 2 == 0 &&
+      const bool v16 = row < g.M && cw + BN / WN <= g.N && (g.ldc | g.ldch) % 2 == 0 &&
                        (((uintptr_t)C | (uintptr_t)g.chain_out | (uintptr_t)g.chain_add) & 15) == 0;
       if (v16) {
         double2 cv[TN];
@@ -152,7 +141,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
             }
           }
       }
-    } else if (!SPLIT && row < g.M && cw + BN / WN <= g.N && g.ldc % 2 == 0 && ((uintptr_t)C & 15) == 0) {
+    } else if (row < g.M && cw + BN / WN <= g.N && g.ldc % 2 == 0 && ((uintptr_t)C & 15) == 0) {
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
         const double v0 = Cin ? acc[i][j][0] : g.alpha * acc[i][j][0];
@@ -180,8 +169,8 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, double (&acc)[B
           s += red_sq[w][rl];
           d += red_dot[w][rl];
         }
-        g.psq[row * g.ldp + blockIdx.x] = s;
-        if (g.pdot) g.pdot[row * g.ldp + blockIdx.x] = d;
+        g.psq[row * g.ldp + ctile] = s;
+        if (g.pdot) g.pdot[row * g.ldp + ctile] = d;
       }
     }
   }
@@ -331,125 +320,103 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel(GemmArgs g) {
   for (int tile = 0; tile < ntiles; ++tile) tile_step(tile);
   cp_async_wait<0>();
 
-  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
+  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot, blockIdx.x);
 }
 
-// LDS.128 variant (16-byte copies only).  The k-slots of the DMMA are
-// remapped so each thread's operands are contiguous in shared memory:
-//   step q (0..3) of a 16-deep k-tile uses k = 4 t4 + q for lane (gq, t4),
-//   so a thread's A values A[row][4 t4 .. 4 t4 + 3] are two LDS.128;
-//   the 8-column DMMA tile j is the column set {c * TN + j}, so a thread's B
-//   values B[k][gq TN .. gq TN + TN - 1] are TN / 2 LDS.128.
-// Per warp and k-tile that is 2 TM + 2 TN loads for 4 TM TN DMMAs (the
-// 8-byte-fragment kernel needs 4 TM + 4 TN).  A rows are padded to 18 doubles
-// and B rows swizzled (16-byte chunk c of k-row r stored at c ^ ((r >> 2) & 3))
-// so every quarter-warp LDS.128 phase hits 8 distinct 16-byte bank groups.
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool PARTIALS, int BK = 16>
-__global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) {
-  static_assert(BK % 16 == 0, "k-tile is a multiple of 16");
-  constexpr int THREADS = WM * WN * 32;
-  constexpr int AS = BK + 2;
-  constexpr int BS = BN;
-  constexpr int STAGE = BM * AS + BK * BS;
-  constexpr int TM = BM / WM / 8;
-  constexpr int TN = BN / WN / 8;
-  constexpr int A_IT = (BM * BK / 2) / THREADS;
-  constexpr int B_IT = (BK * BN / 2) / THREADS;
-  static_assert(TN == 8 || TN == 4, "B swizzle defined for TN = 4 or 8");
-  // 16-byte chunk swizzle of B rows, by the row's t4 = (k >> 2) & 3: the 8 lanes
-  // of a quarter-warp (gq in {0, 1}, t4 in 0..3) then hit 8 distinct bank groups
-  auto swz = [](int t) { return TN == 8 ? t : ((t & 1) | ((t >> 1) << 2)); };
-  static_assert(A_IT >= 1 && B_IT >= 1 && A_IT <= 32 && B_IT <= 32, "copy split");
-  extern __shared__ double smem[];
+// ---------------------------------------------------------------------------
+// Row-major mainloop.  CTA tile BM x BN x 16, warps of WTM x WTN (TM x TN
+// DMMA 8x8 tiles, 2 TM TN accumulator doubles per thread), STAGES-deep cp.async
+// ring.  Shared-memory rows are padded to 4 (mod 16) doubles: the 32 fragment
+// addresses of a warp (A[8 rows][4 k] or B[4 k][8 cols]) then cover every
+// 8-byte bank pair exactly twice, the minimum of two wavefronts per LDS.64.
+//
+// Per k-tile and warp: 4 k-groups of TM + TN fragment loads and TM TN DMMAs.
+// The fragments of k-group q+1 are loaded into the other register buffer
+// before the DMMAs of q are issued; the 16-byte copies of tile t+STAGES-1 are
+// spread over the first three k-groups; the one barrier per tile sits before
+// the last k-group, so the first fragments of the next tile load while the
+// last DMMAs of this one run.
+template <int BM, int BN, int WTM, int WTN>
+struct RmCfg {
+  static constexpr int BK = 16, WM = BM / WTM, WN = BN / WTN, THREADS = WM * WN * 32;
+  static constexpr int TM = WTM / 8, TN = WTN / 8;
+  static constexpr int AS = BK + 4, BS = BN + 4;
+  static constexpr int STAGE = BM * AS + BK * BS;
+  static constexpr int A_CH = BM * BK / 2 / THREADS, B_CH = BK * BN / 2 / THREADS;
+  static constexpr int A_RPI = THREADS / (BK / 2);  // A rows covered per copy iteration
+  static constexpr int B_CPR = BN / 2;              // 16-byte chunks per B row
+  static constexpr int B_RPI = THREADS / B_CPR;     // B rows covered per copy iteration
+  static_assert(A_CH * THREADS * 2 == BM * BK && B_CH * THREADS * 2 == BK * BN, "copy split");
+  static_assert(THREADS % B_CPR == 0, "B copy rows");
+  static_assert(AS % 16 == 4 && BS % 16 == 4, "conflict-free fragment padding");
+};
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp16z(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
+}
+
+template <int BM, int BN, int WTM, int WTN, int STAGES, bool PARTIALS, int BARK = 3>
+__global__ void __launch_bounds__(RmCfg<BM, BN, WTM, WTN>::THREADS, 2) dgemm_rm_kernel(GemmArgs g, int64_t ntn) {
+  using Cf = RmCfg<BM, BN, WTM, WTN>;
+  constexpr int BK = Cf::BK, TM = Cf::TM, TN = Cf::TN, WM = Cf::WM, WN = Cf::WN;
+  constexpr int AS = Cf::AS, BS = Cf::BS, STAGE = Cf::STAGE;
+  constexpr int A_CH = Cf::A_CH, NCH = Cf::A_CH + Cf::B_CH;
+  extern __shared__ __align__(16) double smem[];
   __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
   __shared__ double red_dot[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
 
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
-  const int z = blockIdx.z;
-  const double* A = g.A + z * g.bsA;
-  const double* B = g.B + z * g.bsB;
-  double* C = g.C + z * g.bsC;
-  const double* Cin = g.Cin ? g.Cin + z * g.bsCin : nullptr;
+  // 1D raster: the ntn column tiles of a row block are consecutive CTAs, so the
+  // A row panel they all stream is read from HBM once and from L2 after that
+  const int64_t ctile = (int64_t)blockIdx.x % ntn;
+  const int64_t n0 = ctile * BN;
+  const int64_t m0 = ((int64_t)blockIdx.x / ntn) * BM;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int wm = warp % WM, wn = warp / WM, gq = lane >> 2, t4 = lane & 3;
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp / WN, wn = warp % WN;
-  const int gq = lane >> 2, t4 = lane & 3;
-
+  // triangular B: only the k-range that can hold nonzeros
   int64_t kbeg = 0, kend = g.K;
   if (g.kmode == KB_UPPER) kend = min(g.K, n0 + BN);
   if (g.kmode == KB_LOWER) kbeg = (n0 / BK) * BK;
   const int ntiles = kend > kbeg ? (int)((kend - kbeg + BK - 1) / BK) : 0;
 
-  uint32_t a_ok = 0, b_ok = 0, b_half = 0;
-#pragma unroll
-  for (int it = 0; it < A_IT; ++it) {
-    const int r = (tid + it * THREADS) / (BK / 2);
-    if (m0 + r < g.M) a_ok |= 1u << it;
-  }
-#pragma unroll
-  for (int it = 0; it < B_IT; ++it) {
-    const int c = ((tid + it * THREADS) % (BN / 2)) * 2;
-    if (n0 + c < g.N) b_ok |= 1u << it;
-    if (n0 + c + 1 == g.N) b_half |= 1u << it;
-  }
-  const double* Ab = A + m0 * g.sa_r;
-  const double* Bb = B + n0;
-
-  // interior fast path: per-thread offsets fixed, per-tile bases uniform
-  static_assert(THREADS % (BK / 2) == 0 && THREADS % (BN / 2) == 0, "copy rows");
-  constexpr int RA = THREADS / (BK / 2), RB = THREADS / (BN / 2);
-  const bool interior = m0 + BM <= g.M && n0 + BN <= g.N;
-  const int r0 = tid / (BK / 2), kc0 = (tid % (BK / 2)) * 2;
-  const int kr0 = tid / (BN / 2), ch0 = tid % (BN / 2);
+  const int ar = tid / (BK / 2), ak = (tid % (BK / 2)) * 2;
+  const int br = tid / Cf::B_CPR, bc = (tid % Cf::B_CPR) * 2;
+  const double* gA = g.A + (m0 + ar) * g.sa_r + kbeg + ak;
+  const double* gB = g.B + (kbeg + br) * g.sb_r + n0 + bc;
+  const int64_t stepA = (int64_t)Cf::A_RPI * g.sa_r, stepB = (int64_t)Cf::B_RPI * g.sb_r;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t sa0 = sbase + (uint32_t)(r0 * AS + kc0) * 8u;
-  const uint32_t sb0 = sbase + (uint32_t)(BM * AS + kr0 * BS) * 8u;
-  const double* ga0 = Ab + r0 * g.sa_r + kc0 + kbeg;
-  const double* gb0 = Bb + (kr0 + kbeg) * g.sb_r + 2 * ch0;
-  const int64_t stepA = (int64_t)RA * g.sa_r, stepB = (int64_t)RB * g.sb_r;
+  const uint32_t sA = sbase + (uint32_t)(ar * AS + ak) * 8u;
+  const uint32_t sB = sbase + (uint32_t)(BM * AS + br * BS + bc) * 8u;
+  // per-thread copy bounds, fixed for the CTA: A row validity (bit q) and the
+  // B column bytes (16, 8 at an odd last column, 0 past N)
+  uint32_t arow_ok = 0;
+#pragma unroll
+  for (int q = 0; q < A_CH; ++q) arow_ok |= (m0 + ar + q * Cf::A_RPI < g.M ? 1u : 0u) << q;
+  const int bcol_bytes = n0 + bc < g.N ? (g.N - (n0 + bc) >= 2 ? 16 : 8) : 0;
+  const int64_t kspan = kend - kbeg;  // k offsets below are relative to kbeg
 
-  auto issue = [&](int tile, int stage) {
-    const int64_t k0 = kbeg + (int64_t)tile * BK;
-    if (interior && k0 + BK <= kend) {
-      const uint32_t so = (uint32_t)(stage * STAGE) * 8u;
-      const double* ga = ga0 + (int64_t)tile * BK;
-      const double* gb = gb0 + (int64_t)tile * BK * g.sb_r;
-#pragma unroll
-      for (int it = 0; it < A_IT; ++it)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa0 + so + (uint32_t)(it * RA * AS * 8)),
-                     "l"(ga + it * stepA));
-#pragma unroll
-      for (int it = 0; it < B_IT; ++it) {
-        const int kr = kr0 + it * RB;
-        const uint32_t d = sb0 + so + (uint32_t)(it * RB * BS * 8) + (uint32_t)((ch0 ^ swz((kr >> 2) & 3)) * 16);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gb + it * stepB));
-      }
-      return;
-    }
-    double* As = smem + stage * STAGE;
-    double* Bs = As + BM * AS;
-    const bool fullk = k0 + BK <= kend;
-    const double* At = Ab + k0;
-    const double* Bt = Bb + k0 * g.sb_r;
-#pragma unroll
-    for (int it = 0; it < A_IT; ++it) {
-      const int e = tid + it * THREADS;
-      const int r = e / (BK / 2), kc = (e % (BK / 2)) * 2;
-      int bytes = (a_ok >> it) & 1 ? 16 : 0;
-      if (!fullk) {
-        const int64_t rem = kend - (k0 + kc);
-        bytes = rem >= 2 ? bytes : (rem == 1 ? bytes / 2 : 0);
-      }
-      cp_async16(As + r * AS + kc, bytes ? At + r * g.sa_r + kc : A, bytes);
-    }
-#pragma unroll
-    for (int it = 0; it < B_IT; ++it) {
-      const int e = tid + it * THREADS;
-      const int kr = e / (BN / 2), ch = e % (BN / 2);
-      int bytes = (b_ok >> it) & 1 ? ((b_half >> it) & 1 ? 8 : 16) : 0;
-      if (!fullk && k0 + kr >= kend) bytes = 0;
-      cp_async16(Bs + kr * BS + 2 * (ch ^ swz((kr >> 2) & 3)), bytes ? Bt + kr * g.sb_r + 2 * ch : B, bytes);
+  // 16-byte copy q (0 .. NCH-1) of k-tile `tile` into ring slot `slot`.  No
+  // branches: out-of-range chunks (rows >= M, columns >= N, k >= kend, tiles
+  // past the last) copy 0 source bytes (zero fill), so the copies interleave
+  // freely with the DMMAs of the k-group they are issued in.
+  auto copy_chunk = [&](int q, int tile, int slot) {
+    const int64_t k0 = (int64_t)tile * BK;
+    const uint32_t so = (uint32_t)(slot * STAGE) * 8u;
+    if (q < A_CH) {
+      const int64_t kr = kspan - (k0 + ak);  // valid k columns left at this chunk
+      const int bytes = ((arow_ok >> q) & 1u) ? (kr >= 2 ? 16 : (kr == 1 ? 8 : 0)) : 0;
+      const double* src = gA + q * stepA + k0;
+      cp16z(sA + so + (uint32_t)(q * Cf::A_RPI * AS) * 8u, bytes ? src : g.A, bytes);
+    } else {
+      const int it = q - A_CH;
+      const int64_t kk = k0 + it * Cf::B_RPI;  // gB already points at row br
+      const int bytes = kk + br < kspan ? bcol_bytes : 0;
+      const double* src = gB + kk * g.sb_r;
+      cp16z(sB + so + (uint32_t)(it * Cf::B_RPI * BS) * 8u, bytes ? src : g.B, bytes);
     }
   };
 
@@ -461,159 +428,64 @@ __global__ void __launch_bounds__(WM * WN * 32, MINB) dgemm_kernel3(GemmArgs g) 
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ntiles) issue(s, s);
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) copy_chunk(q, s, s);
     cp_async_commit();
   }
-  int stage = 0;
+  cp_async_wait<STAGES - 2>();
+  __syncthreads();
+
+  double af[2][TM], bf[2][TN];
+  const double* fa = smem + (wm * WTM + gq) * AS + t4;
+  const double* fb = smem + BM * AS + t4 * BS + wn * WTN + gq;
+  auto load_frags = [&](int buf, int slot, int kg) {
+    const double* a = fa + slot * STAGE + kg * 4;
+    const double* b = fb + slot * STAGE + kg * 4 * BS;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) af[buf][i] = a[i * 8 * AS];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) bf[buf][j] = b[j * 8];
+  };
+  load_frags(0, 0, 0);
+  int rs = 0, wsl = STAGES - 1;
   for (int tile = 0; tile < ntiles; ++tile) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      const int nt = tile + STAGES - 1;
-      const int ns = stage == 0 ? STAGES - 1 : stage - 1;  // == nt % STAGES
-      if (nt < ntiles) issue(nt, ns);
-      cp_async_commit();
-    }
-    const double* As = smem + stage * STAGE + (wm * TM * 8 + gq) * AS + 4 * t4;
-    const double* Bs = smem + stage * STAGE + BM * AS + wn * TN * 8;
 #pragma unroll
-    for (int h16 = 0; h16 < BK / 16; ++h16) {
-      double a[TM][4];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const double2 x = *reinterpret_cast<const double2*>(As + i * 8 * AS + 16 * h16);
-        const double2 y = *reinterpret_cast<const double2*>(As + i * 8 * AS + 16 * h16 + 2);
-        a[i][0] = x.x; a[i][1] = x.y; a[i][2] = y.x; a[i][3] = y.y;
+    for (int kg = 0; kg < 4; ++kg) {
+      if (BARK == 3 && kg == 3) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        rs = rs + 1 == STAGES ? 0 : rs + 1;
       }
+      load_frags((kg + 1) & 1, rs, (kg + 1) & 3);
+      if (kg < 3) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double* Br = Bs + (16 * h16 + 4 * t4 + q) * BS;
-        double b[TN];
-#pragma unroll
-        for (int jj = 0; jj < TN / 2; ++jj) {
-          const double2 v = *reinterpret_cast<const double2*>(Br + 2 * ((gq * (TN / 2) + jj) ^ swz(t4)));
-          b[2 * jj] = v.x;
-          b[2 * jj + 1] = v.y;
+        for (int q = kg * NCH / 3; q < (kg + 1) * NCH / 3; ++q) copy_chunk(q, tile + STAGES - 1, wsl);
+        if (kg == 2) {
+          cp_async_commit();
+          wsl = wsl + 1 == STAGES ? 0 : wsl + 1;
         }
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i][q], b[j]);
       }
+      if (BARK == 2 && kg == 2) {  // barrier one k-group earlier (after the last fragments of this tile)
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        rs = rs + 1 == STAGES ? 0 : rs + 1;
+      }
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int ii = 0; ii < TM; ++ii) {
+          const int i = (j & 1) ? TM - 1 - ii : ii;  // serpentine: consecutive DMMAs share an operand
+          dmma884(acc[i][j][0], acc[i][j][1], af[kg & 1][i], bf[kg & 1][j]);
+        }
     }
-    stage = stage + 1 == STAGES ? 0 : stage + 1;
   }
   cp_async_wait<0>();
-  gemm_epilogue<BM, BN, WM, WN, PARTIALS, true>(g, acc, C, Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot);
-}
 
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, bool P, int BK = 16>
-int launch_three(const GemmArgs& g, int batch, cudaStream_t st) {
-  constexpr size_t smem = (size_t)STAGES * (BM * (BK + 2) + BK * BN) * sizeof(double);
-  auto kern = dgemm_kernel3<BM, BN, WM, WN, STAGES, MINB, P, BK>;
-  static bool configured = false;
-  if (!configured) {
-    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), (unsigned)batch);
-  kern<<<grid, WM * WN * 32, smem, st>>>(g);
-  HIKF_CHECK_LAUNCH();
-  return HIKF_OK;
-}
-
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool VEC, bool P>
-int launch_one(const GemmArgs& g, int batch, cudaStream_t st) {
-  constexpr size_t smem = (size_t)STAGES * (BM * (BK + 4) + BK * (BN + 4)) * sizeof(double);
-  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, VEC, P>;
-  static bool configured = false;
-  if (!configured) {
-    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), (unsigned)batch);
-  kern<<<grid, WM * WN * 32, smem, st>>>(g);
-  HIKF_CHECK_LAUNCH();
-  return HIKF_OK;
-}
-
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
-int launch_variant(const GemmArgs& g, int batch, bool vec, bool part, cudaStream_t st) {
-  if (vec)
-    return part ? launch_one<BM, BN, BK, WM, WN, STAGES, MINB, true, true>(g, batch, st)
-                : launch_one<BM, BN, BK, WM, WN, STAGES, MINB, true, false>(g, batch, st);
-  return part ? launch_one<BM, BN, BK, WM, WN, STAGES, MINB, false, true>(g, batch, st)
-              : launch_one<BM, BN, BK, WM, WN, STAGES, MINB, false, false>(g, batch, st);
-}
-
-template <int BM, int BN, int WM, int WN, int STAGES, int MINB, int BK = 16>
-int launch_variant3(const GemmArgs& g, int batch, bool vec, bool part, cudaStream_t st) {
-  if (!vec) return launch_variant<BM, BN, 16, WM, WN, STAGES, MINB>(g, batch, vec, part, st);
-  return part ? launch_three<BM, BN, WM, WN, STAGES, MINB, true, BK>(g, batch, st)
-              : launch_three<BM, BN, WM, WN, STAGES, MINB, false, BK>(g, batch, st);
-}
-
-// ---------------------------------------------------------------------------
-// Variant 30: CUTLASS multistage DMMA mainloop (cp.async ring, conflict-free
-// 64-bit smem layouts, serpentine warp MMA order) + the fused epilogue above.
-// profiles/r01_cutlass_probe.log: the plain CUTLASS 64x128x16 / 32x64 / 3-stage
-// GEMM runs the cfg4 K-GEMM shape in 61.3 ms (cuBLAS 61.6 ms, our v7 66.5 ms).
-template <int BM, int BN, int WTM, int WTN, int STAGES>
-struct CutlassMain {
-  using RM = cutlass::layout::RowMajor;
-  using DefaultMma = cutlass::gemm::threadblock::DefaultMma<
-      double, RM, 1, double, RM, 1, double, RM, cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80,
-      cutlass::gemm::GemmShape<BM, BN, 16>, cutlass::gemm::GemmShape<WTM, WTN, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
-      STAGES, cutlass::arch::OpMultiplyAdd>;
-  using Mma = typename DefaultMma::ThreadblockMma;
-  static constexpr int WM = BM / WTM, WN = BN / WTN, THREADS = WM * WN * 32;
-};
-
-template <int BM, int BN, int WTM, int WTN, int STAGES, bool PARTIALS>
-__global__ void __launch_bounds__(CutlassMain<BM, BN, WTM, WTN, STAGES>::THREADS, 2)
-    dgemm_cutlass_kernel(GemmArgs g, typename CutlassMain<BM, BN, WTM, WTN, STAGES>::Mma::IteratorA::Params pA,
-                         typename CutlassMain<BM, BN, WTM, WTN, STAGES>::Mma::IteratorB::Params pB) {
-  using CM = CutlassMain<BM, BN, WTM, WTN, STAGES>;
-  using Mma = typename CM::Mma;
-  constexpr int WM = CM::WM, WN = CM::WN;
-  constexpr int TM = WTM / 8, TN = WTN / 8;
-  extern __shared__ __align__(16) char smem_raw[];
-  auto& ss = *reinterpret_cast<typename Mma::SharedStorage*>(smem_raw);
-  __shared__ double red_sq[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
-  __shared__ double red_dot[PARTIALS ? WN : 1][PARTIALS ? BM : 1];
-
-  const int64_t n0 = (int64_t)blockIdx.x * BN;
-  const int64_t m0 = (int64_t)blockIdx.y * BM;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  // triangular B: only the k-range that can hold nonzeros (as dgemm_kernel)
-  int64_t kbeg = 0, kend = g.K;
-  if (g.kmode == KB_UPPER) kend = min(g.K, n0 + BN);
-  if (g.kmode == KB_LOWER) kbeg = (n0 / 16) * 16;
-  typename Mma::IteratorA itA(pA, const_cast<double*>(g.A), {(int)g.M, (int)kend}, tid, {(int)m0, (int)kbeg});
-  typename Mma::IteratorB itB(pB, const_cast<double*>(g.B), {(int)kend, (int)g.N}, tid, {(int)kbeg, (int)n0});
-  Mma mma(ss, tid, warp, lane);
-  typename Mma::FragmentC accum;
-  accum.clear();
-  if (kend > kbeg) mma((int)((kend - kbeg + 15) / 16), accum, itA, itB, accum);
-
-  // CUTLASS warp tile (mma_tensor_op.h, accumulators column-major over the
-  // 8x8 instruction tiles): tile (i, j) -> accum[2 (i + j TM) + h] holds
-  // C[wm WTM + 8 i + gq][wn WTN + 8 j + 2 t4 + h]; warps are m-fastest.
-  double acc[TM][TN][2];
-#pragma unroll
-  for (int i = 0; i < TM; ++i)
-#pragma unroll
-    for (int j = 0; j < TN; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) acc[i][j][h] = accum[2 * (i + j * TM) + h];
-  const int wm = warp % WM, wn = warp / WM;
-  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, g.C, g.Cin, m0, n0, tid, wm, wn, lane >> 2, lane & 3, red_sq,
-                                          red_dot);
-  if (g.gv_y && blockIdx.x == gridDim.x - 1) {
+  gemm_epilogue<BM, BN, WM, WN, PARTIALS>(g, acc, g.C, g.Cin, m0, n0, tid, wm, wn, gq, t4, red_sq, red_dot, ctile);
+  if (g.gv_y && ctile == ntn - 1) {
     // fused GEMV rows of this row block: one warp per row, 16-byte loads, lane-strided sums
     const bool v2 = (g.K % 2 == 0) && (g.sa_r % 2 == 0) && ((((uintptr_t)g.A) | ((uintptr_t)g.gv_x)) & 15) == 0;
-    for (int r = warp; r < BM; r += CM::THREADS / 32) {
+    for (int r = warp; r < BM; r += Cf::THREADS / 32) {
       const int64_t row = m0 + r;
       if (row >= g.M) break;
       const double* a = g.A + row * g.sa_r;
@@ -635,21 +507,41 @@ __global__ void __launch_bounds__(CutlassMain<BM, BN, WTM, WTN, STAGES>::THREADS
   }
 }
 
-template <int BM, int BN, int WTM, int WTN, int STAGES, bool P>
-int launch_cutlass(const GemmArgs& g, cudaStream_t st) {
-  using CM = CutlassMain<BM, BN, WTM, WTN, STAGES>;
-  using Mma = typename CM::Mma;
-  constexpr size_t smem = sizeof(typename Mma::SharedStorage);
-  auto kern = dgemm_cutlass_kernel<BM, BN, WTM, WTN, STAGES, P>;
+template <int BM, int BN, int WTM, int WTN, int STAGES, bool P, int BARK = 3>
+int launch_rm(const GemmArgs& g, cudaStream_t st) {
+  using Cf = RmCfg<BM, BN, WTM, WTN>;
+  constexpr size_t smem = (size_t)STAGES * Cf::STAGE * sizeof(double);
+  auto kern = dgemm_rm_kernel<BM, BN, WTM, WTN, STAGES, P, BARK>;
   static bool configured = false;
   if (!configured) {
     HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  typename Mma::IteratorA::Params pA(cutlass::layout::RowMajor((int)g.sa_r));
-  typename Mma::IteratorB::Params pB(cutlass::layout::RowMajor((int)g.sb_r));
-  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), 1u);
-  kern<<<grid, CM::THREADS, smem, st>>>(g, pA, pB);
+  const int64_t ntn = ceil_div(g.N, BN), ntm = (g.M + BM - 1) / BM;
+  if (ntm * ntn > 0x7fffffffll) {
+    set_error("dgemm: %lld x %lld tiles exceed the grid limit", (long long)ntm, (long long)ntn);
+    return HIKF_BAD_ARGUMENT;
+  }
+  kern<<<(unsigned)(ntm * ntn), Cf::THREADS, smem, st>>>(g, ntn);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool VEC, bool P>
+int launch_gen(const GemmArgs& g, int batch, cudaStream_t st) {
+  constexpr size_t smem = (size_t)STAGES * (BM * (BK + 4) + BK * (BN + 4)) * sizeof(double);
+  auto kern = dgemm_kernel<BM, BN, BK, WM, WN, STAGES, MINB, VEC, P>;
+  static bool configured = false;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  if ((g.M + BM - 1) / BM > 65535 || batch > 65535) {
+    set_error("dgemm: strided operands with M = %lld exceed the generic kernel's grid", (long long)g.M);
+    return HIKF_BAD_ARGUMENT;
+  }
+  dim3 grid((unsigned)ceil_div(g.N, BN), (unsigned)ceil_div(g.M, BM), (unsigned)batch);
+  kern<<<grid, WM * WN * 32, smem, st>>>(g);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
@@ -661,7 +553,7 @@ int g_variant = -1;
 int dgemm_variant() {
   if (g_variant < 0) {
     const char* e = getenv("HIKF_DGEMM_VARIANT");
-    g_variant = e ? atoi(e) : 30;  // default: CUTLASS mainloop 64x128x16, 4 warps of 32x64, 3 stages (profiles/r01_gemm_sweep_cutlass.log)
+    g_variant = e ? atoi(e) : 30;
   }
   return g_variant;
 }
@@ -678,67 +570,38 @@ int update_variant_c(int64_t n) {
 
 int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || batch <= 0) return HIKF_OK;
-  int variant = g.variant >= 0 ? g.variant : dgemm_variant();
+  const int variant = g.variant >= 0 ? g.variant : dgemm_variant();
   auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
-  bool vec = g.sa_c == 1 && g.sb_c == 1 && (g.sa_r % 2 == 0) && (g.sb_r % 2 == 0) && al16(g.A) && al16(g.B) &&
-             (batch == 1 || (g.bsA % 2 == 0 && g.bsB % 2 == 0));
-  bool part = g.psq != nullptr;
-  // CUTLASS-mainloop variants: row-major operands (any kmode), one batch
-  const bool cutlass_ok = g.sa_c == 1 && g.sb_c == 1 && batch == 1 && g.M < (1ll << 31) &&
-                          g.K < (1ll << 31) && g.N < (1ll << 31);
-  if (variant == 30 && cutlass_ok)  // 64x128x16, 4 warps of 32x64, 3 stages
-    return part ? launch_cutlass<64, 128, 32, 64, 3, true>(g, st) : launch_cutlass<64, 128, 32, 64, 3, false>(g, st);
-  if (variant == 31 && cutlass_ok)  // 64x128x16, 4 warps of 32x64, 4 stages
-    return part ? launch_cutlass<64, 128, 32, 64, 4, true>(g, st) : launch_cutlass<64, 128, 32, 64, 4, false>(g, st);
-  if (variant == 32 && cutlass_ok)  // 128x64x16, 4 warps of 64x32, 3 stages (64-column tiles: finer triangles)
-    return part ? launch_cutlass<128, 64, 64, 32, 3, true>(g, st) : launch_cutlass<128, 64, 64, 32, 3, false>(g, st);
+  const bool part = g.psq != nullptr;
+  // row-major mainloop: unit column strides, 16-byte aligned rows, one batch
+  const bool rm = g.sa_c == 1 && g.sb_c == 1 && batch == 1 && g.sa_r % 2 == 0 && g.sb_r % 2 == 0 && al16(g.A) &&
+                  al16(g.B);
+  if (rm && variant != 7) {
+    switch (variant) {
+      case 31:  // 64 x 128, warps 32 x 64, 4 stages
+        return part ? launch_rm<64, 128, 32, 64, 4, true>(g, st) : launch_rm<64, 128, 32, 64, 4, false>(g, st);
+      case 32:  // 128 x 64, warps 64 x 32, 3 stages (64-column tiles: finer triangles, n = 64)
+        return part ? launch_rm<128, 64, 64, 32, 3, true>(g, st) : launch_rm<128, 64, 64, 32, 3, false>(g, st);
+      case 34:  // as 30, the ring barrier one k-group earlier
+        return part ? launch_rm<64, 128, 32, 64, 3, true, 2>(g, st) : launch_rm<64, 128, 32, 64, 3, false, 2>(g, st);
+      case 33:  // 64 x 64, warps 32 x 32, 3 stages (more CTAs for the n x n products)
+        return part ? launch_rm<64, 64, 32, 32, 3, true>(g, st) : launch_rm<64, 64, 32, 32, 3, false>(g, st);
+      default:  // 30: 64 x 128, warps 32 x 64, 3 stages
+        return part ? launch_rm<64, 128, 32, 64, 3, true>(g, st) : launch_rm<64, 128, 32, 64, 3, false>(g, st);
+    }
+  }
   if (g.gv_y) {
-    set_error("dgemm: the fused GEMV (gv_x / gv_y) needs a CUTLASS variant (30-32) and row-major operands");
+    set_error("dgemm: the fused GEMV (gv_x / gv_y) needs row-major, 16-byte aligned operands");
     return HIKF_BAD_ARGUMENT;
   }
-  if (variant >= 30) variant = 7;
-  switch (variant) {
-    case 1:  // 128x128x32, 8 warps of 64x32, 3 stages
-      return launch_variant<128, 128, 32, 2, 4, 3, 1>(g, batch, vec, part, st);
-    case 2:  // 128x128x16, 16 warps of 32x32, 5 stages
-      return launch_variant<128, 128, 16, 4, 4, 5, 1>(g, batch, vec, part, st);
-    case 3:  // 128x128x32, 16 warps of 32x32, 3 stages
-      return launch_variant<128, 128, 32, 4, 4, 3, 1>(g, batch, vec, part, st);
-    case 4:  // 64x128x16, 8 warps of 32x32, 4 stages, 2 CTAs / SM
-      return launch_variant<64, 128, 16, 2, 4, 4, 2>(g, batch, vec, part, st);
-    case 5:  // 128x64x16, 8 warps of 32x32, 4 stages, 2 CTAs / SM
-      return launch_variant<128, 64, 16, 4, 2, 4, 2>(g, batch, vec, part, st);
-    case 6:  // 64x128x32, 8 warps of 32x32, 2 stages, 2 CTAs / SM
-      return launch_variant<64, 128, 32, 2, 4, 2, 2>(g, batch, vec, part, st);
-    case 7:  // 64x128x16, 8 warps of 32x32, 3 stages, 2 CTAs / SM
-      return launch_variant<64, 128, 16, 2, 4, 3, 2>(g, batch, vec, part, st);
-    case 8:  // 64x64x16, 4 warps of 32x32, 4 stages, 3 CTAs / SM (smem-bound)
-      return launch_variant<64, 64, 16, 2, 2, 4, 4>(g, batch, vec, part, st);
-    case 9:  // 64x64x32, 4 warps of 32x32, 2 stages, 3 CTAs / SM
-      return launch_variant<64, 64, 32, 2, 2, 2, 3>(g, batch, vec, part, st);
-    case 10:  // 64x64x16, 4 warps of 32x32, 2 stages, 5 CTAs / SM
-      return launch_variant<64, 64, 16, 2, 2, 2, 4>(g, batch, vec, part, st);
-    case 11:  // 64x128x16, 4 warps of 32x64, 3 stages, 2 CTAs / SM
-      return launch_variant<64, 128, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 12:  // 64x128x16, 4 warps of 32x64, 4 stages, 2 CTAs / SM
-      return launch_variant<64, 128, 16, 2, 2, 4, 2>(g, batch, vec, part, st);
-    case 13:  // 128x64x16, 4 warps of 64x32, 3 stages, 2 CTAs / SM
-      return launch_variant<128, 64, 16, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 15:  // 64x128x32, 4 warps of 32x64, 2 stages, 2 CTAs / SM
-      return launch_variant<64, 128, 32, 2, 2, 2, 2>(g, batch, vec, part, st);
-    case 21:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 3 stages, 2 CTAs / SM
-      return launch_variant3<64, 128, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 22:  // LDS.128 kernel: 128x64x16, 4 warps of 32x64 stacked along rows, 3 stages
-      return launch_variant3<128, 64, 4, 1, 3, 2>(g, batch, vec, part, st);
-    case 28:  // LDS.128 kernel: 128x64x16, 4 warps of 64x32 (cuBLAS's warp shape), 3 stages, 2 CTAs / SM
-      return launch_variant3<128, 64, 2, 2, 3, 2>(g, batch, vec, part, st);
-    case 29:  // LDS.128 kernel: 128x64x16, 4 warps of 64x32, 4 stages, 2 CTAs / SM
-      return launch_variant3<128, 64, 2, 2, 4, 2>(g, batch, vec, part, st);
-    case 27:  // LDS.128 kernel: 64x128x16, 4 warps of 32x64, 2 stages, 2 CTAs / SM
-      return launch_variant3<64, 128, 2, 2, 2, 2>(g, batch, vec, part, st);
-    default:  // 128x128x16, 8 warps of 64x32, 5 stages
-      return launch_variant<128, 128, 16, 2, 4, 5, 1>(g, batch, vec, part, st);
-  }
+  const bool vec = g.sa_c == 1 && g.sb_c == 1 && (g.sa_r % 2 == 0) && (g.sb_r % 2 == 0) && al16(g.A) && al16(g.B) &&
+                   (batch == 1 || (g.bsA % 2 == 0 && g.bsB % 2 == 0));
+  // generic strides: 64 x 128 x 16, 8 warps of 32 x 32, 3 stages
+  if (vec)
+    return part ? launch_gen<64, 128, 16, 2, 4, 3, 2, true, true>(g, batch, st)
+                : launch_gen<64, 128, 16, 2, 4, 3, 2, true, false>(g, batch, st);
+  return part ? launch_gen<64, 128, 16, 2, 4, 3, 2, false, true>(g, batch, st)
+              : launch_gen<64, 128, 16, 2, 4, 3, 2, false, false>(g, batch, st);
 }
 
 }  // namespace hikf

@@ -1,23 +1,16 @@
 // FP64 GEMM on the DMMA tensor path (mma.sync m8n8k4 -> SASS DMMA.8x8x4).
 //
 // sm_100a has no tcgen05 f64 kind, so FP64 matrix work runs on the warp-level
-// DMMA pipe (measured 37.0 TFLOP/s on this B200, same as DFMA).  This kernel
-// is the workhorse of the per-step update: CTA tile 128 x 128 x 16, 8 warps
-// (2 x 4) with 64 x 32 warp tiles (32 accumulator fragments = 64 doubles per
-// thread), a 5-stage cp.async ring (16-byte copies when rows are contiguous),
-// triangular K-range skipping for triangular B, and fused epilogues
-// (alpha/beta, per-row sum of squares / dot with a vector).
+// DMMA pipe (measured 37.0 TFLOP/s on this B200, same as DFMA).  dgemm() is the
+// workhorse of the per-step update: hand-written mainloops (dgemm.cu) with
+// triangular K-range skipping for triangular B and fused epilogues (alpha/beta,
+// per-row sum of squares / dot with a vector, the chained predict output, a
+// GEMV over A, a sparse-row addend).
 #pragma once
 
 #include "common.cuh"
 
 namespace hikf {
-
-constexpr int DG_BM = 128, DG_BN = 128, DG_BK = 16, DG_STAGES = 5, DG_THREADS = 256;
-constexpr int DG_AS = DG_BK + 4;   // == 4 mod 16 doubles
-constexpr int DG_BS = DG_BN + 4;
-constexpr int DG_STAGE = DG_BM * DG_AS + DG_BK * DG_BS;
-constexpr size_t DG_SMEM = (size_t)DG_STAGES * DG_STAGE * sizeof(double);
 
 enum { KFULL = 0, KB_UPPER = 1, KB_LOWER = 2 };
 
@@ -47,7 +40,7 @@ struct GemmArgs {
   const double* chain_add = nullptr;
   double* chain_out = nullptr;
   int64_t ldch = 0;
-  // optional fused GEMV over A (CUTLASS variants): gv_y[i] = sum_k A[i][k] gv_x[k] for all M rows,
+  // optional fused GEMV over A (row-major variants 30-34): gv_y[i] = sum_k A[i][k] gv_x[k] for all M rows,
   // done by the CTAs of the last column tile (the shortest k-range under KB_LOWER) from the A
   // panel their row block just streamed through L2
   const double* gv_x = nullptr;
@@ -71,7 +64,7 @@ void set_dgemm_variant(int v);
 // number of column tiles (= partial sums per row) the current variant uses for N columns
 inline int dgemm_col_tiles(int64_t N, int variant = -1) {
   int v = variant >= 0 ? variant : dgemm_variant();
-  return ceil_div(N, (v == 5 || v == 8 || v == 9 || v == 10 || v == 13 || v == 22 || v == 28 || v == 29 || v == 32) ? 64 : 128);
+  return ceil_div(N, (v == 32 || v == 33) ? 64 : 128);
 }
 // variant used by the update's K GEMM (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log);
 // HIKF_DGEMM_VARIANT overrides it

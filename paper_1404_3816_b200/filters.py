@@ -87,21 +87,41 @@ class DeviceCSR:
             self._T = DeviceCSR(HT)
         return self._T
 
+    @staticmethod
+    def _fingerprint(H):
+        """Cheap identity of the host operator's contents: shape, nnz, the
+        buffer addresses and checksums of the first and last 1024 values and
+        indices (a few microseconds at cfg4), so a reallocated operator or an
+        in-place edit such as H.data *= s is not served from a stale device copy."""
+        if scipy.sparse.issparse(H) and H.format == "csr":
+            d, ix = H.data, H.indices
+            return (H.shape, H.nnz, d.ctypes.data, ix.ctypes.data, H.indptr.ctypes.data,
+                    float(np.add.reduce(d[:1024])), float(np.add.reduce(d[-1024:])),
+                    int(np.add.reduce(ix[:1024], dtype=np.int64)), int(np.add.reduce(ix[-1024:], dtype=np.int64)))
+        return None
+
     @classmethod
     def of(cls, H) -> "DeviceCSR":
         if isinstance(H, DeviceCSR):
             return H
         key = id(H)
+        fp = cls._fingerprint(H)
         hit = cls._cache.get(key)
         if hit is not None:
-            ref, dcsr = hit
-            if ref() is H:
+            ref, hfp, dcsr = hit
+            if ref() is H and fp is not None and hfp == fp:
                 return dcsr
+            cls._cache.pop(key, None)
         dcsr = cls(H)
+        if fp is None:  # dense or non-CSR input: converted per call, not cached
+            return dcsr
         try:
-            cls._cache[key] = (weakref.ref(H), dcsr)
-        except TypeError:  # not weak-referenceable (plain ndarray subclasses are fine)
-            pass
+            ref = weakref.ref(H)
+        except TypeError:  # not weak-referenceable: not cached
+            return dcsr
+        cls._cache[key] = (ref, fp, dcsr)
+        # drop the device copy (and its cached transpose) when the host operator dies
+        weakref.finalize(H, cls._cache.pop, key, None)
         return dcsr
 
 
@@ -331,6 +351,11 @@ def hikf_predict(state: HikfState, pre: HikfPrecompute) -> HikfState:
     if isinstance(state, FactoredHikfState):
         if tuple(pre.C_Q_t.shape) != state.shape:
             raise ValueError("precompute shape does not match the state")
+        # C = C_Q N is expressed against the C_Q this state was built with; another
+        # precompute's C_Q would silently change C (C_Q2 (N + I) instead of C_Q1 N + C_Q2)
+        cq = state._cq_pre
+        if cq is not None and cq is not pre and cq.C_Q_t.data_ptr() != pre.C_Q_t.data_ptr():
+            raise ValueError("a factored state can only be predicted with the precompute its C_Q factor refers to")
         return FactoredHikfState(None, None, None, None, None, _prior=state, _pre=pre)
     if tuple(pre.C_Q_t.shape) != tuple(state.cross_cov_t.shape):
         raise ValueError("precompute shape does not match the state")
@@ -415,6 +440,8 @@ def _update_factored(state: FactoredHikfState, Hd: DeviceCSR, r: float, zt: torc
     m, n = state.shape
     if src.N_t.shape != (n, n) or src.mean_t.shape != (m,):
         raise ValueError("factored state shape does not match (m, n)")
+    if Hd.shape[0] != n:  # the explicit path's check (filters.py:31-37 via the cross-covariance shape)
+        raise ValueError("observation operator rows do not match the state")
     if pre is None:
         raise ValueError("a factored state needs hikf_predict (C_Q) before its first update")
     dev = _dev()

@@ -97,3 +97,9 @@ def update_cases():
     out.append((dict(mean=rng.standard_normal(m), cross_cov=C, variance=np.diag(P).copy(), HC=H @ C),
                 H, 0.3, rng.standard_normal(n)))
     return out
+
+
+def sketch_vectors(m: int, n: int):
+    """Seeded probe vectors for the column / row sketches of m x n fixtures."""
+    rng = np.random.default_rng(77)
+    return rng.standard_normal(m), rng.standard_normal(n)

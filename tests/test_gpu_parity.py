@@ -204,23 +204,50 @@ class _Model:
         self.initial_mean = np.zeros(grid.m)
 
 
-def _run_filter(pkg, cfg, obs):
+def _run_filter(pkg, cfg, obs, representation="explicit", alpha=0.0, step_rows=None):
+    """The scenario through the CUDA path in run_hikf's loop order; with
+    step_rows also returns the mean after every step on those rows."""
     flt = pkg.filters
     grid, H = _gpu_scenario(pkg, cfg)
     kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
     model = _Model(grid, H, kern, cfg["R"])
+    model.alpha = alpha
     tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
     pre = flt.hikf_precompute_fmm(model, tree)
-    st = flt.hikf_init(model)
+    st = flt.hikf_init(model, representation=representation)
+    means = []
     for t in range(cfg["T"]):
         st = flt.hikf_update(flt.hikf_predict(st, pre), H, model.r_variance, obs[t])
+        if step_rows is not None:
+            means.append(st.mean[step_rows])
+    if step_rows is not None:
+        return tree, H, pre, st, np.array(means)
     return tree, H, pre, st
 
 
+def _sketch_errs(A, g, prefix):
+    """Fingerprints of an m x n array vs the reference's (make_golden.sketches):
+    worst per-column norm, column sketch A^T g_m, row sketch A g_n, Frobenius."""
+    gm, gn = cases.sketch_vectors(A.shape[0], A.shape[1])
+    cn = np.linalg.norm(A, axis=0)
+    ref = g[prefix + "col_norms"]
+    # the vector of column norms in relative Frobenius (<= the array's relative Frobenius error, the
+    # north-star metric) and, reported separately, the worst single column's relative norm error
+    return {prefix + "col_norms": O.rel_fro(cn, ref),
+            prefix + "col_norms_worst_column": float(np.max(np.abs(cn - ref) / np.maximum(ref, 1e-300))),
+            prefix + "col_sketch": O.rel_fro(A.T @ gm, g[prefix + "col_sketch"]),
+            prefix + "row_sketch": O.rel_fro(A @ gn, g[prefix + "row_sketch"]),
+            prefix + "fro": abs(np.linalg.norm(A) - float(g[prefix + "fro"])) / float(g[prefix + "fro"])}
+
+
+@pytest.mark.parametrize("representation", ["explicit", "factored"])
 @pytest.mark.parametrize("fixture,cfg", [("small_rays.npz", cases.SMALL), ("cfg1.npz", cases.CFG1)])
-def test_filter_matches_reference(pkg, fixture, cfg):
+def test_filter_matches_reference(pkg, fixture, cfg, representation):
+    """Whole filter runs vs the reference: C_Q, HC_Q, the final state, and the
+    mean after EVERY step (what run_hikf stores in run.means and the metrics /
+    report consume, experiment.py:232-237, 298-378)."""
     g = _load(fixture)
-    tree, H, pre, st = _run_filter(pkg, cfg, g["obs"])
+    tree, H, pre, st, means = _run_filter(pkg, cfg, g["obs"], representation, step_rows=g["step_rows"])
     assert np.array_equal(H.indptr.astype(np.int64), g["H_indptr"])
     assert np.array_equal(H.indices.astype(np.int64), g["H_indices"])
     np.testing.assert_array_equal(H.data, g["H_data"])
@@ -229,31 +256,66 @@ def test_filter_matches_reference(pkg, fixture, cfg):
     for k, ref in (("mean", "final_mean"), ("variance", "final_variance"), ("cross_cov", "final_cross_cov"),
                    ("HC", "final_HC")):
         errs[k] = O.rel_fro(getattr(st, k), g[ref])
-    _record(cfg["name"], errs)
+    errs["step_means"] = O.rel_fro(means, g["step_means"])
+    errs["step_means_worst_step"] = max(O.rel_fro(a, b) for a, b in zip(means, g["step_means"]) if np.any(b))
+    _record(f"{cfg['name']}_{representation}", errs)
     assert errs["C_Q"] <= 1e-13 and errs["HC_Q"] <= 1e-13, errs
     np.testing.assert_array_equal(pre.diag_Q, np.ones(tree.m))
-    for k in ("mean", "variance", "cross_cov", "HC"):
+    for k in ("mean", "variance", "cross_cov", "HC", "step_means", "step_means_worst_step"):
         assert errs[k] <= PARITY, (k, errs[k])
 
 
+@pytest.mark.parametrize("representation", ["explicit", "factored"])
+@pytest.mark.parametrize("cfg", [cases.SMALL, cases.CFG1])
+def test_alpha_prior_matches_reference(pkg, cfg, representation):
+    """hikf_init with alpha = 0.5 (filters.py:118-126: C_0 = alpha H^T, var_0 =
+    alpha, HC_0 = alpha H H^T) through the whole filter, against the real
+    reference run with StateSpaceModel(alpha=0.5) (alpha_cases.npz)."""
+    g = _load("alpha_cases.npz")
+    name = cfg["name"]
+    rows = np.arange(cfg["N"] ** 2)
+    tree, H, pre, st, means = _run_filter(pkg, cfg, g[f"{name}_obs"], representation, alpha=0.5, step_rows=rows)
+    errs = {"C_Q": O.rel_fro(pre.C_Q, g[f"{name}_C_Q"]), "mean": O.rel_fro(st.mean, g[f"{name}_final_mean"]),
+            "variance": O.rel_fro(st.variance, g[f"{name}_final_variance"]),
+            "cross_cov": O.rel_fro(st.cross_cov, g[f"{name}_final_cross_cov"]),
+            "HC": O.rel_fro(st.HC, g[f"{name}_final_HC"]), "step_means": O.rel_fro(means, g[f"{name}_step_means"])}
+    _record(f"{name}_alpha0.5_{representation}", errs)
+    for k, v in errs.items():
+        assert v <= PARITY, (k, v)
+
+
 @pytest.mark.slow
-def test_filter_cfg2_matches_reference(pkg):
-    """cfg2 (m = 65,536, n = 256, 100 steps): the thin-budget case."""
+@pytest.mark.parametrize("representation", ["explicit", "factored"])
+def test_filter_cfg2_matches_reference(pkg, representation):
+    """cfg2 (m = 65,536, n = 256, 100 steps): the thin-budget case.
+    C_Q and the final cross covariance on all 256 columns (every column's norm,
+    seeded column / row sketches, the Frobenius norm) plus 32 full columns of
+    each; the full final mean, variance and HC; the mean after every step on
+    every 16th row."""
     g = _load("cfg2.npz")
-    tree, H, pre, st = _run_filter(pkg, cases.CFG2, g["obs"])
+    tree, H, pre, st, means = _run_filter(pkg, cases.CFG2, g["obs"], representation, step_rows=g["step_rows"])
     assert np.array_equal(H.indptr.astype(np.int64), g["H_indptr"])
     assert np.array_equal(H.indices.astype(np.int64), g["H_indices"])
     check_tree_ints(tree, g)
     cols = g["cols"]
-    errs = {"C_Q_cols": O.rel_fro(pre.C_Q[:, cols], g["C_Q_cols"]),
-            "C_Q_fro": abs(np.linalg.norm(pre.C_Q) - float(g["C_Q_fro"])) / float(g["C_Q_fro"]),
-            "mean": O.rel_fro(st.mean, g["final_mean"]), "variance": O.rel_fro(st.variance, g["final_variance"]),
-            "cross_cov_cols": O.rel_fro(st.cross_cov[:, cols], g["final_cross_cov_cols"]),
-            "HC": O.rel_fro(st.HC, g["final_HC"])}
-    _record("cfg2", errs)
-    assert errs["C_Q_cols"] <= 1e-13 and errs["C_Q_fro"] <= 1e-13, errs
-    for k in ("mean", "variance", "cross_cov_cols", "HC"):
-        assert errs[k] <= PARITY, (k, errs[k])
+    C_Q, C = pre.C_Q, st.cross_cov
+    errs = {"C_Q_cols": O.rel_fro(C_Q[:, cols], g["C_Q_cols"])}
+    errs.update(_sketch_errs(C_Q, g, "C_Q_"))
+    qht = dict(errs)
+    errs.update({"mean": O.rel_fro(st.mean, g["final_mean"]), "variance": O.rel_fro(st.variance, g["final_variance"]),
+                 "cross_cov_cols": O.rel_fro(C[:, cols], g["final_cross_cov_cols"]),
+                 "cross_cov_fro_vs_ref": abs(np.linalg.norm(C) - float(g["cross_cov_fro"])) / float(g["cross_cov_fro"]),
+                 "HC": O.rel_fro(st.HC, g["final_HC"]), "step_means": O.rel_fro(means, g["step_means"])})
+    errs.update(_sketch_errs(C, g, "final_cross_cov_"))
+    _record(f"cfg2_{representation}", errs)
+    worst = max(v for k, v in errs.items() if k not in qht)
+    print(f"cfg2 ({representation}) worst {worst:.3g}: margin {PARITY / worst:.2f}x", errs)
+    for k, v in qht.items():
+        assert v <= (1e-13 if "worst_column" not in k else 1e-12), (k, v)
+    for k, v in errs.items():
+        # one column's own relative error is not the north-star metric (relative Frobenius over the
+        # array); the smallest columns are 12x below the largest, so it gets a 10x looser gate
+        assert v <= (PARITY if "worst_column" not in k else 10 * PARITY), (k, v)
 
 
 def test_dgemm_against_torch(pkg):
@@ -517,9 +579,9 @@ def test_factored_error_paths(pkg):
     assert flt.hikf_update(st, H0, cfg["R"], np.zeros(0)) is st
 
 
-@pytest.mark.parametrize("variant", [7, 30, 31, 32])
+@pytest.mark.parametrize("variant", [7, 30, 31, 32, 33])
 def test_dgemm_variants_and_triangular_k_ranges(pkg, variant):
-    """Every DMMA GEMM variant (hand-written 7, CUTLASS-mainloop 30-32) against
+    """Every DMMA GEMM variant (generic-stride 7, row-major mainloop 30-33) against
     torch float64: full K, an upper-triangular B (kmode 1: k < n0 + BN) and a
     lower-triangular B (kmode 2: k >= n0), with beta = 1 accumulation, on odd
     shapes that exercise the boundary tiles."""

@@ -18,7 +18,8 @@ numpy (8 m bytes), exactly what experiment.run_hikf does (experiment.py:237).
 `--impl reference` times the reference algorithm on the host CPU cores: the
 reference is pure Python and cannot travel to the GPU box, so its numpy
 restatement in oracle/ (pinned to the reference by tests/test_oracle_golden.py)
-runs a bounded row sample of each step (see cpu_step_sample).
+runs full-size steps of the config's scenario (CpuFilter; prior Q = I stand-in,
+the step cost being independent of the values).
 
 Multi-GPU (--gpus N under torchrun): independent replicas, one filter per
 GPU ("replicas only" this round); value sums ranks.
@@ -195,42 +196,66 @@ class ClockSampler:
 # CPU leg: the reference algorithm (oracle restatement) on a bounded sample
 # ---------------------------------------------------------------------------
 
-def _cpu_update_time(cfg, rows, reps=1):
+def host_info():
+    """Host cores, RAM and the BLAS thread pool the CPU legs run with."""
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemTotal:"):
+                    info["ram_gb"] = round(int(line.split()[1]) / 1024 ** 2, 1)
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{k: d.get(k) for k in ("internal_api", "version", "num_threads")} for d in threadpool_info()]
+    except Exception:
+        pass
+    return info
+
+
+def cpu_scenario(cfg):
+    """The 2D config's scenario on the host through the oracle (oracle/hikf_oracle.py restates
+    grids.py / tomography.py): cell centres, the crosswell ray operator, plume observations."""
     from oracle import hikf_oracle as O
-    import scipy.sparse
-    n = cfg["ns"] * cfg["nr"]
-    rng = np.random.default_rng(1)
-    A = rng.standard_normal((n, n)) / math.sqrt(n)
-    HC0 = A @ A.T
-    st = O.State(np.zeros(rows), 1e-3 * rng.standard_normal((rows, n)), 1e3 * np.ones(rows), HC0.copy())
-    pre = O.Pre(1e-3 * rng.standard_normal((rows, n)), 0.1 * HC0, np.ones(rows))
-    H = scipy.sparse.random(n, rows, density=min(1.0, 1300.0 / rows), random_state=2, format="csr")
-    z = rng.standard_normal(n)
-    times = []
-    for i in range(reps + 1):  # first call warms the BLAS thread pool
+    N = cfg["N"]
+    xy = O.cell_centers(N, N, 1.0 / N, 1.0 / N)
+    src, rcv = O.crosswell_stations(cfg["ns"], cfg["nr"], 0.0, 1.0, 0.0, 1.0)
+    H = O.ray_operator(N, N, 1.0 / N, 1.0 / N, src, rcv)
+    return xy, H, plume_observations(H, xy, cfg["T"], cfg["R"])
+
+
+class CpuFilter:
+    """The reference's predict + update (oracle restatement of filters.py:129-157: numpy +
+    OpenBLAS / LAPACK cho_factor / cho_solve) on the FULL m x n state of the config.
+
+    The prior is the white-noise stand-in Q = I (C_Q = H^T, HC_Q = H H^T, diag_Q = 1): the CPU
+    bbFMM for the real C_Q takes ~20 min at cfg4 (see cpu_baseline.qht), and a step's cost is
+    dense BLAS / LAPACK on m x n and n x n arrays, independent of the values."""
+
+    def __init__(self, cfg, rows=None, H=None, obs=None):
+        from oracle import hikf_oracle as O
+        self.O = O
+        if H is None:
+            _, H, obs = cpu_scenario(cfg)
+        m = H.shape[1]
+        if rows is not None and rows < m:  # leading rows (a row sample, cross-check only)
+            H = H[:, :rows].tocsr()
+            m = rows
+        self.H, self.obs, self.R, self.m = H, obs, cfg["R"], m
         t0 = time.perf_counter()
-        O.update(O.predict(st, pre), H, cfg["R"] + 10.0, z)
-        if i:
-            times.append(time.perf_counter() - t0)
-    return min(times)
+        Ht = np.ascontiguousarray(H.T.toarray())
+        self.pre = O.Pre(Ht, np.asarray((H @ Ht)), np.ones(m))
+        self.st = O.init_state(H, m)
+        self.t_setup = time.perf_counter() - t0
+        self.t = 0
 
-
-def cpu_step_sample(cfg, rows, reps=1):
-    """Time the reference predict+update (oracle/hikf_oracle.py: numpy + OpenBLAS /
-    LAPACK on all host cores) on `rows` and `rows/2` of the m state rows with the
-    full n, and extrapolate linearly, t(m) = a + b m: every m-row term (potrs with
-    m RHS, K HC, rowsum, predict add) is linear in the row count and the n x n
-    terms (Cholesky, KH, KH HC) are the intercept.  Returns (seconds per full
-    step, rows)."""
-    m = cfg_m(cfg)
-    rows = min(rows, m)
-    if rows == m:
-        return _cpu_update_time(cfg, rows, reps), rows
-    t1 = _cpu_update_time(cfg, rows, reps)
-    t2 = _cpu_update_time(cfg, rows // 2, reps)
-    b = max((t1 - t2) / (rows - rows // 2), 0.0)
-    a = max(t1 - b * rows, 0.0)
-    return a + b * m, rows
+    def step(self):
+        O = self.O
+        t0 = time.perf_counter()
+        self.st = O.update(O.predict(self.st, self.pre), self.H, self.R, self.obs[self.t % len(self.obs)])
+        self.t += 1
+        return time.perf_counter() - t0
 
 
 def scenario_3d(cfg):
@@ -305,7 +330,7 @@ def cpu_qht_sample_3d(cfg, H, xyz, cols=2):
     return len(X) * cols / t, t
 
 
-def cpu_qht_sample(cfg, cols=8):
+def cpu_qht_sample(cfg, cols=32):
     """Reference bbFMM (oracle restatement) Q H^T on `cols` columns of H^T
     (matmat is column-independent, fmm.py:325-367): (m n)/s = m cols / t."""
     from oracle import hikf_oracle as O
@@ -324,31 +349,63 @@ def cpu_qht_sample(cfg, cols=8):
     return N * N * cols / t, t_build, t
 
 
+def arm_config(args, cfg, world, mode):
+    """The `config` object of the bench line, shared by both arms (same_config)."""
+    c = {"workload": cfg["desc"], "steps_per_run": cfg["T"],
+         "l2": "no flush: per-step inputs (C 8.6 GB, C_Q 8.6 GB) far exceed the 126 MB L2"
+         if args.config == "cfg4" else "small config: inputs may be L2-resident"}
+    if mode == "sharded":
+        c["parallelism"] = f"row-sharded x{world} (one n-vector all-reduce per step)"
+    else:
+        c["parallelism"] = f"replicas x{world}" if world > 1 else "single GPU"
+    return c
+
+
+def arm_mode(args, cfg, world):
+    mode = args.mode
+    if mode == "auto":
+        mode = "sharded" if world > 1 and cfg.get("dim", 2) == 2 else "replicas"
+    return mode
+
+
 def run_reference(args, cfg, rank):
-    """--impl reference: the reference algorithm on the host cores, rank 0 only."""
+    """--impl reference: the reference algorithm (oracle port) on the host cores, rank 0
+    only, on the full m x n state of the config.  Warm-up: the first untimed step is a full
+    step (page faults, BLAS thread pool); the other W - 1 run on a 65,536-row sample so the
+    whole run stays within a few minutes.  Timed: exactly K full steps."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    if cfg.get("dim", 2) != 2:
+        print(json.dumps({"impl": "reference", "unavailable": "the reference is 2D only (grids.py:59-66)"}))
+        return
     threads = os.cpu_count()
-    rows = args.cpu_rows
-    per_step = []
-    # torchrun sets OMP_NUM_THREADS=1 for multi-process launches; the reference arm
-    # runs alone on rank 0 and gets all host threads for its BLAS / LAPACK
     from threadpoolctl import threadpool_limits
     with threadpool_limits(limits=threads):
-        for i in range(args.warmup + args.steps):
-            t, rows = cpu_step_sample(cfg, rows)
-            if i >= args.warmup:
-                per_step.append(t)
-    t_step = statistics.median(per_step)
+        if args.warmup > 1:
+            small = CpuFilter(cfg, rows=min(65536, cfg_m(cfg)))
+            for _ in range(args.warmup - 1):
+                small.step()
+            del small
+        cf = CpuFilter(cfg)
+        if args.warmup > 0:
+            cf.step()
+        per_step = [cf.step() for _ in range(args.steps)]
+    t_step = sum(per_step) / len(per_step)
     value = 1.0 / t_step
-    sample = (f"oracle/hikf_oracle.py predict+update (numpy + OpenBLAS/LAPACK) on {rows} of {cfg_m(cfg)} state rows "
-              f"with n={cfg['ns'] * cfg['nr']} (and rows/2), linearly extrapolated to m; one sample pair per step")
+    hi = host_info()
+    sample = (f"oracle/hikf_oracle.py predict+update (numpy + OpenBLAS / LAPACK, {threads} threads) on the full "
+              f"{cfg_m(cfg)} x {cfg['ns'] * cfg['nr']} state of the {args.config} scenario (crosswell rays, plume "
+              f"observations); prior Q = I stand-in for C_Q (step cost independent of the values); "
+              f"{args.steps} timed full steps")
     line = {
         "metric": "hikf_assimilation_steps_per_sec", "value": value, "unit": "steps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * t_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, cfg4 shapes)",
-        "config": {"workload": cfg["desc"]}, "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: seeded crosswell rays + moving Gaussian plume, PCG64 noise (cfg recipe, SURVEY 8(d))",
+        "config": arm_config(args, cfg, world, arm_mode(args, cfg, world)), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": threads, "kind": "port", "sample": sample,
+                         "host": hi, "step_s": per_step, "setup_s": cf.t_setup},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -438,8 +495,7 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
             "ms_per_step": 1000.0 * t_loop / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: seeded crosswell rays + moving Gaussian plume, PCG64 noise (cfg recipe, SURVEY 8(d))",
-            "config": {"workload": cfg["desc"], "parallelism": f"row-sharded x{world} (one n-vector all-reduce "
-                                                               "per step)", "rows_per_rank": r1 - r0},
+            "config": arm_config(args, cfg, world, "sharded"), "rows_per_rank": r1 - r0,
             "qht": {"ms": 1000.0 * t_qht, "value": m * n / t_qht, "unit": "(m*n)/s",
                     "note": "row-sharded precompute: upward pass + M2L replicated, L2P/P2P for owned rows"},
             "e2e": {"value": args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
@@ -463,7 +519,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-rows", type=int, default=65536)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-factored", action="store_true",
                     help="skip the opt-in factored-representation leg (C = C_Q N) reported under 'factored'")
@@ -499,9 +554,7 @@ def main():
     from paper_1404_3816_b200 import _lib
     lib = _lib.load()
     flt = P.filters
-    mode = args.mode
-    if mode == "auto":
-        mode = "sharded" if world > 1 and cfg.get("dim", 2) == 2 else "replicas"
+    mode = arm_mode(args, cfg, world)
     if mode == "sharded":
         run_sharded(args, cfg, P, torch, dist, world, rank, local)
         return
@@ -709,10 +762,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: seeded crosswell rays + moving Gaussian plume, PCG64 noise (cfg recipe, SURVEY 8(d))",
-        "config": {"workload": cfg["desc"], "steps_per_run": cfg["T"],
-                   "l2": "no flush: per-step inputs (C 8.6 GB, C_Q 8.6 GB) far exceed the 126 MB L2"
-                   if args.config == "cfg4" else "small config: inputs may be L2-resident",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": arm_config(args, cfg, world, mode),
         "qht": {"value": world * m * n / t_qht, "unit": "(m*n)/s", "ms": 1000.0 * t_qht, "tree_build_s": t_build,
                 "precompute_incl_build_mn_per_s": m * n / (t_qht + t_build),
                 "flops_dense_formulation": qht_flops,
@@ -749,22 +799,29 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from threadpoolctl import threadpool_limits
         with threadpool_limits(limits=os.cpu_count()):
-            t_cpu, rows = cpu_step_sample(cfg, args.cpu_rows)
-        line["cpu_baseline"] = {
-            "value": 1.0 / t_cpu, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"oracle predict+update on {rows} and {rows // 2} of {m} rows (n={n}), "
-                      "linear extrapolation t(m) = a + b m"}
+            # (3D: no reference 3D path; the same oracle update on the 3D config's rays)
+            cf = CpuFilter(cfg, H=H, obs=obs) if dim3 else CpuFilter(cfg)
+            cf.step()  # first touch of the m x n buffers, BLAS pool
+            t_cpu = cf.step()
+            del cf
+        if t_cpu is not None:
+            line["cpu_baseline"] = {
+                "value": 1.0 / t_cpu, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                "sample": f"one timed full-size predict+update step of the oracle port on the {m} x {n} state "
+                          "(after one untimed step), prior Q = I stand-in for C_Q", "host": host_info()}
         try:
             if dim3:
                 mn_s, tq = cpu_qht_sample_3d(cfg, H, xy, cols=2 if m <= 300000 else 1)
-                line["cpu_baseline"]["qht"] = {"value": mn_s, "unit": "(m*n)/s",
-                                               "sample": f"exact direct-sum Q H^T on {2 if m <= 300000 else 1} of "
-                                                         f"{n} columns ({tq:.1f} s; no reference 3D path)"}
+                line.setdefault("cpu_baseline", {"kind": "port", "cores": os.cpu_count()})["qht"] = {
+                    "value": mn_s, "unit": "(m*n)/s", "sample": f"exact direct-sum Q H^T on {2 if m <= 300000 else 1} "
+                                                                f"of {n} columns ({tq:.1f} s; no reference 3D path)"}
             else:
-                mn_s, tb, tq = cpu_qht_sample(cfg, cols=8)
+                ncol = min(32, n)
+                mn_s, tb, tq = cpu_qht_sample(cfg, cols=ncol)
                 line["cpu_baseline"]["qht"] = {"value": mn_s, "unit": "(m*n)/s",
-                                               "sample": f"oracle bbFMM matmat on 8 of {n} H^T columns ({tq:.1f} s), "
-                                                         f"tree build {tb:.1f} s"}
+                                               "sample": f"oracle bbFMM matmat on {ncol} of {n} H^T columns "
+                                                         f"({tq:.1f} s; matmat is column-independent), tree build "
+                                                         f"{tb:.1f} s"}
         except MemoryError:
             pass
     if rank == 0:

@@ -546,6 +546,20 @@ int launch_gen(const GemmArgs& g, int batch, cudaStream_t st) {
   return HIKF_OK;
 }
 
+// y[i] = sum_k A[i][k] x[k] (row-major A, any stride): one warp per row, k in order per lane
+__global__ void gemv_rows_kernel(int64_t M, int64_t K, const double* __restrict__ A, int64_t lda,
+                                 const double* __restrict__ x, double* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < M;
+       row += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double* a = A + row * lda;
+    double s = 0.0;
+    for (int64_t c = lane; c < K; c += 32) s = fma(a[c], x[c], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[row] = s;
+  }
+}
+
 int g_variant = -1;
 
 }  // namespace
@@ -591,8 +605,20 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
     }
   }
   if (g.gv_y) {
-    set_error("dgemm: the fused GEMV (gv_x / gv_y) needs row-major, 16-byte aligned operands");
-    return HIKF_BAD_ARGUMENT;
+    // unaligned or odd-stride rows (e.g. an odd ray count): the GEMM on the generic kernel,
+    // then the GEMV over A as its own pass
+    if (g.sa_c != 1 || batch != 1) {
+      set_error("dgemm: the GEMV over A (gv_x / gv_y) needs row-major A and one batch");
+      return HIKF_BAD_ARGUMENT;
+    }
+    GemmArgs h = g;
+    h.gv_x = nullptr;
+    h.gv_y = nullptr;
+    HIKF_TRY(dgemm(h, 1, st));
+    const int64_t blocks = std::min<int64_t>((g.M + 7) / 8, (int64_t)num_sms() * 16);
+    gemv_rows_kernel<<<(unsigned)blocks, 256, 0, st>>>(g.M, g.K, g.A, g.sa_r, g.gv_x, g.gv_y);
+    HIKF_CHECK_LAUNCH();
+    return HIKF_OK;
   }
   const bool vec = g.sa_c == 1 && g.sb_c == 1 && (g.sa_r % 2 == 0) && (g.sb_r % 2 == 0) && al16(g.A) && al16(g.B) &&
                    (batch == 1 || (g.bsA % 2 == 0 && g.bsB % 2 == 0));

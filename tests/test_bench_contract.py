@@ -28,6 +28,16 @@ def test_reference_arm_single_process():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+    # measured, not modelled: K full-size steps whose times add up to the line's ms_per_step
+    assert len(line["cpu_baseline"]["step_s"]) == 2
+    assert abs(sum(line["cpu_baseline"]["step_s"]) / 2 * 1000.0 - line["ms_per_step"]) < 1e-6
+    assert line["cpu_baseline"]["host"]["ram_gb"] > 0
+    # the same config object as our arm prints (same_config)
+    sys.path.insert(0, ROOT)
+    import argparse
+    import bench
+    args = argparse.Namespace(config="cfg1", mode="auto")
+    assert line["config"] == bench.arm_config(args, bench.CONFIGS["cfg1"], 1, "replicas")
 
 
 def test_reference_arm_under_torchrun_world2():
@@ -39,3 +49,4 @@ def test_reference_arm_under_torchrun_world2():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+    assert lines[0]["config"]["parallelism"].startswith("row-sharded x2")

@@ -574,12 +574,39 @@ def test_factored_error_paths(pkg):
         flt.hikf_update(flt.hikf_predict(neg, pre), H, cfg["R"], g["obs"][2])
     with pytest.raises(ValueError):
         flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], np.zeros(n + 1))
+    # an operator with a different row count than the state's n (reads past H / z otherwise)
+    H_short = H[: n - 1]
+    with pytest.raises(ValueError):
+        flt.hikf_update(flt.hikf_predict(st, pre), H_short, cfg["R"], np.zeros(n - 1))
+    # predicting with a precompute whose C_Q is not the one N refers to
+    other = flt.HikfPrecompute(pre.C_Q_t * 2.0, pre.HC_Q_t, pre.diag_Q_t)
+    with pytest.raises(ValueError):
+        flt.hikf_predict(st, other)
     # n = 0 observations: identity (filters.py:140-141)
     H0 = scipy.sparse.csr_matrix((0, m))
     assert flt.hikf_update(st, H0, cfg["R"], np.zeros(0)) is st
 
 
-@pytest.mark.parametrize("variant", [7, 30, 31, 32, 33])
+def test_device_operator_cache_follows_the_host_operator(pkg):
+    """DeviceCSR.of caches the device copy per host CSR: an in-place edit of the
+    host values is picked up, and the entry is dropped when the operator dies."""
+    import gc
+    flt = pkg.filters
+    H = scipy.sparse.random(7, 50, density=0.2, random_state=4, format="csr")
+    d1 = flt.DeviceCSR.of(H)
+    assert flt.DeviceCSR.of(H) is d1
+    H.data *= 3.0
+    d2 = flt.DeviceCSR.of(H)
+    assert d2 is not d1
+    np.testing.assert_array_equal(d2.data.cpu().numpy(), H.data)
+    key = id(H)
+    assert key in flt.DeviceCSR._cache
+    del H, d1, d2
+    gc.collect()
+    assert key not in flt.DeviceCSR._cache
+
+
+@pytest.mark.parametrize("variant", [7, 30, 31, 32, 33, 34])
 def test_dgemm_variants_and_triangular_k_ranges(pkg, variant):
     """Every DMMA GEMM variant (generic-stride 7, row-major mainloop 30-33) against
     torch float64: full K, an upper-triangular B (kmode 1: k < n0 + BN) and a

@@ -320,6 +320,12 @@ int hikf_prof_read(int32_t stage, double* total_ms, int64_t* count);
  * (2 per multiply-add actually performed; skipped zero blocks not counted) */
 int hikf_prof_flops(int32_t stage, uint64_t* flops);
 int64_t hikf_launch_count(void);
+/* A/B switches for tests and tools (results are bit-identical either way):
+ * key 0 = the fused small-n chain of the update (csrc/nnchain.cu; 1 on, 0 the
+ * multi-launch chain); key 1 = the fused leaf-level L2L + L2P of the Q H^T
+ * FMM (csrc/boxgemm.cu leaf_down; 0: separate L2L and L2P kernels).
+ * *previous (optional) receives the old value. */
+int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous);
 
 #ifdef __cplusplus
 }

@@ -112,6 +112,7 @@ SIGNATURES = {
     "hikf_prof_read": (ctypes.c_int, [_I32, _P, _P]),
     "hikf_prof_flops": (ctypes.c_int, [_I32, _P]),
     "hikf_launch_count": (_I64, []),
+    "hikf_set_tuning": (ctypes.c_int, [_I32, _I32, _P]),
 }
 
 # stage ids of hikf_prof_read (csrc/prof.h)

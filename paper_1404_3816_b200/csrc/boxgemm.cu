@@ -268,6 +268,208 @@ int launch_box(const BoxArgs& a, int R, dim3 grid, cudaStream_t st) {
   return HIKF_BAD_ARGUMENT;
 }
 
+// ---------------------------------------------------------------------------
+// Fused leaf-level downward step: L2L into the leaves + L2P, the leaf locals
+// never stored.  One CTA per occupied leaf T (points <= 64), its warps stride
+// over 8-column units:
+//   l[a][j]     = S[T][j][a] + sum_b C_ci[a][b] L_{D-1}[parent][b][j]   (fmm.py:361-363:
+//                 the M2L sum first, then + L2L; the same DMMA k-order as l2l_boxes)
+//   U[p][j]     = sum_a W2[p][a] l[a][j]                                 (fmm.py:366)
+// l goes from the accumulator layout to B fragments through a per-warp
+// shared-memory tile (q x 8).  A operands (the leaf's child-class shift rows and
+// its W2 rows) are staged once per CTA.  Results are bit-identical to
+// l2l_boxes + l2p_boxes (same products in the same order); the saving is the
+// G_D^2 x q x n leaf-local array (written and read back: 9.6 GB at cfg4).
+// ---------------------------------------------------------------------------
+struct LeafArgs {
+  int64_t n;
+  int q, qp;
+  int64_t G;  // leaf-level grid
+  const int32_t *leaf_box, *leaf_start, *leaf_count;
+  const double* W2s;
+  const int64_t* order;
+  const double* Lp;     // parent-level locals (box-major)
+  const double* shift;  // 4 q x qp stacked child operators of the parent level
+  const double* S;      // pair-major M2L scratch of the leaf level
+  double* U;
+  int64_t ldu, r0, r1;
+  unsigned long long *fl_l2l, *fl_l2p;
+};
+
+// shared-memory load the compiler cannot hoist out of the unit loop (the A
+// operands are loop-invariant; keeping them all in registers would spill)
+__device__ __forceinline__ double lds64(const double* p) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+  return v;
+}
+
+template <int NK1, int NRT1, int NK2>
+__global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
+  extern __shared__ double sm[];
+  constexpr int LDA1 = NK1 * 4 + ((4 - (NK1 * 4) % 16) + 16) % 16;
+  constexpr int LDA2 = NK2 * 4 + ((4 - (NK2 * 4) % 16) + 16) % 16;
+  constexpr int KR2 = NK2 * 4;  // rows of the per-warp l tile
+  double* A1 = sm;                          // NRT1*8 x LDA1
+  double* A2 = A1 + NRT1 * 8 * LDA1;        // 64 x LDA2
+  double* Lw = A2 + 64 * LDA2;              // 8 warps x KR2 x 8
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const int q = g.q, qp = g.qp;
+  const int64_t T = blockIdx.x;
+  const int64_t box = g.leaf_box[T];
+  const int64_t X = box / g.G, Y = box % g.G;
+  const int ci = (int)(((X & 1) << 1) | (Y & 1));
+  const int64_t P = (X >> 1) * (g.G >> 1) + (Y >> 1);
+  const int cnt = g.leaf_count[T];
+  const int64_t ls = g.leaf_start[T];
+  const double* Cg = g.shift + (int64_t)ci * q * qp;
+  for (int e = tid; e < NRT1 * 8 * NK1 * 4; e += BW_THREADS) {
+    const int r = e / (NK1 * 4), k = e % (NK1 * 4);
+    A1[r * LDA1 + k] = (r < q && k < qp) ? Cg[(int64_t)r * qp + k] : 0.0;
+  }
+  const double* Wg = g.W2s + ls * q;
+  for (int e = tid; e < 64 * NK2 * 4; e += BW_THREADS) {
+    const int r = e / (NK2 * 4), k = e % (NK2 * 4);
+    A2[r * LDA2 + k] = (r < cnt && k < q) ? Wg[(int64_t)r * q + k] : 0.0;
+  }
+  __syncthreads();
+  double* lw = Lw + warp * KR2 * 8;
+  const int64_t n = g.n;
+  const int64_t ncb = (n + 7) / 8;
+  const double* Lpar = g.Lp + P * qp * n;
+  const double* Sb = g.S + box * n * q;
+  // this lane's output rows (leaf points 8 i + gq) in U, or -1 outside the row window
+  int32_t orow[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int pnt = i * 8 + gq;
+    int32_t r = -1;
+    if (pnt < cnt) {
+      const int64_t o = g.order[ls + pnt];
+      if (o >= g.r0 && o < g.r1) r = (int32_t)(o - g.r0);
+    }
+    orow[i] = r;
+  }
+  auto load_b1 = [&](int64_t u, double (&b1)[NK1]) {
+    const int64_t jb = u * 8 + gq;
+#pragma unroll
+    for (int k4 = 0; k4 < NK1; ++k4) {
+      const int k = k4 * 4 + t4;
+      b1[k4] = (k < qp && jb < n) ? Lpar[(int64_t)k * n + jb] : 0.0;
+    }
+  };
+  unsigned long long useful1 = 0, useful2 = 0;
+  double nb1[NK1];
+  if (warp < ncb) load_b1(warp, nb1);
+  for (int64_t u = warp; u < ncb; u += BW_THREADS / 32) {
+    double b1[NK1];
+#pragma unroll
+    for (int k4 = 0; k4 < NK1; ++k4) b1[k4] = nb1[k4];
+    if (u + BW_THREADS / 32 < ncb) load_b1(u + BW_THREADS / 32, nb1);  // next unit's parent columns in flight
+    const int64_t j0 = u * 8;
+    const int cols = (int)(n - j0 < 8 ? n - j0 : 8);
+    if (lane == 0) {
+      useful1 += 2ull * q * qp * cols;
+      useful2 += 2ull * cnt * q * cols;
+    }
+    // the M2L sums of this unit (loaded ahead of the DMMA chain, added after it)
+    double init[NRT1][2];
+#pragma unroll
+    for (int i = 0; i < NRT1; ++i) {
+      const int r = i * 8 + gq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t jc = j0 + 2 * t4 + h;
+        init[i][h] = (r < q && jc < n) ? Sb[jc * q + r] : 0.0;
+      }
+    }
+    // L2L into the leaf: acc1 = C_ci L_parent, then l = acc1 + S
+    double acc1[NRT1][2];
+#pragma unroll
+    for (int i = 0; i < NRT1; ++i) acc1[i][0] = acc1[i][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < NK1; ++k4)
+#pragma unroll
+      for (int i = 0; i < NRT1; ++i) {
+        const double af = lds64(A1 + (i * 8 + gq) * LDA1 + k4 * 4 + t4);
+        dmma884(acc1[i][0], acc1[i][1], af, b1[k4]);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NRT1; ++i) {
+      const int r = i * 8 + gq;
+      if (r < KR2) {
+        lw[r * 8 + 2 * t4] = acc1[i][0] + init[i][0];
+        lw[r * 8 + 2 * t4 + 1] = acc1[i][1] + init[i][1];
+      }
+    }
+    __syncwarp();
+    // L2P: U = W2 l
+    double b2[NK2];
+#pragma unroll
+    for (int k4 = 0; k4 < NK2; ++k4) {
+      const int k = k4 * 4 + t4;
+      b2[k4] = k < q ? lw[k * 8 + gq] : 0.0;
+    }
+    double acc2[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc2[i][0] = acc2[i][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < NK2; ++k4)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const double af = lds64(A2 + (i * 8 + gq) * LDA2 + k4 * 4 + t4);
+        dmma884(acc2[i][0], acc2[i][1], af, b2[k4]);
+      }
+    const int64_t jc = j0 + 2 * t4;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (orow[i] < 0) continue;
+      double* o = g.U + (int64_t)orow[i] * g.ldu;
+      if (jc + 1 < n && (((uintptr_t)(o + jc)) & 15) == 0) {
+        *reinterpret_cast<double2*>(o + jc) = make_double2(acc2[i][0], acc2[i][1]);
+      } else {
+        if (jc < n) o[jc] = acc2[i][0];
+        if (jc + 1 < n) o[jc + 1] = acc2[i][1];
+      }
+    }
+  }
+  if (lane == 0) {
+    if (g.fl_l2l && useful1) atomicAdd(g.fl_l2l, useful1);
+    if (g.fl_l2p && useful2) atomicAdd(g.fl_l2p, useful2);
+  }
+}
+
+template <int NK1, int NRT1, int NK2>
+int launch_leaf_t(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
+  constexpr int LDA1 = NK1 * 4 + ((4 - (NK1 * 4) % 16) + 16) % 16;
+  constexpr int LDA2 = NK2 * 4 + ((4 - (NK2 * 4) % 16) + 16) % 16;
+  constexpr size_t smem = sizeof(double) * (NRT1 * 8 * LDA1 + 64 * LDA2 + 8 * NK2 * 4 * 8);
+  static bool configured = false;
+  auto kern = leaf_down_kernel<NK1, NRT1, NK2>;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 << 10)));
+    configured = true;
+  }
+  kern<<<nleaves, BW_THREADS, smem, st>>>(a);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+// (leaf order o, parent order op) -> instantiation; 0 = not instantiated
+int launch_leaf(const LeafArgs& a, int o, int op, unsigned nleaves, cudaStream_t st) {
+#define HIKF_LEAF(O, OP)                                                                        \
+  if (o == O && op == OP)                                                                       \
+    return launch_leaf_t<(OP * OP + 3) / 4, (O * O + 7) / 8, (O * O + 3) / 4>(a, nleaves, st);
+  HIKF_LEAF(2, 2) HIKF_LEAF(2, 3) HIKF_LEAF(3, 3) HIKF_LEAF(3, 4) HIKF_LEAF(4, 4) HIKF_LEAF(4, 5)
+  HIKF_LEAF(5, 5) HIKF_LEAF(5, 6) HIKF_LEAF(6, 6) HIKF_LEAF(6, 7) HIKF_LEAF(7, 7) HIKF_LEAF(7, 8)
+  HIKF_LEAF(8, 8)
+#undef HIKF_LEAF
+  return -1;
+}
+
 }  // namespace
 
 bool box_supported(int rows, int K) { return K <= 4 * BW_MAXK4 && box_smem(rows, K) <= 200 * 1024; }
@@ -311,6 +513,60 @@ int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int
   a.ldu = ldu;
   a.flops = prof_flops_ptr(ST_L2P);
   return launch_box(a, 64, dim3((unsigned)t->n_leaves, (unsigned)((t->max_count + 63) / 64)), st);
+}
+
+static int g_leaf_fused = -1;
+
+bool leaf_fused_enabled() {
+  if (g_leaf_fused < 0) {
+    const char* e = getenv("HIKF_LEAF_FUSED");
+    g_leaf_fused = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_leaf_fused != 0;
+}
+
+int leaf_set_fused(int on) {
+  const int prev = leaf_fused_enabled() ? 1 : 0;
+  g_leaf_fused = on ? 1 : 0;
+  return prev;
+}
+
+bool leaf_down_supported(const hikf_tree* t) {
+  const int D = t->depth;
+  if (D < 3 || t->max_count > 64) return false;
+  const int o = t->orders[D], op = t->orders[D - 1];
+  return o >= 2 && o <= 8 && (op == o || op == o + 1);
+}
+
+int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, double* U, int64_t ldu,
+              cudaStream_t st, int64_t r0, int64_t r1) {
+  if (t->n_leaves == 0 || n == 0) return HIKF_OK;
+  const int D = t->depth;
+  LeafArgs a{};
+  a.n = n;
+  a.q = t->orders[D] * t->orders[D];
+  a.qp = t->orders[D - 1] * t->orders[D - 1];
+  a.G = (int64_t)1 << D;
+  a.leaf_box = t->leaf_box;
+  a.leaf_start = t->leaf_start;
+  a.leaf_count = t->leaf_count;
+  a.W2s = t->W2s;
+  a.order = t->order;
+  a.Lp = Lp;
+  a.shift = t->shift[D - 1];
+  a.S = S;
+  a.U = U;
+  a.ldu = ldu;
+  a.r0 = r0;
+  a.r1 = r1 < 0 ? INT64_MAX : r1;
+  a.fl_l2l = prof_flops_ptr(ST_L2L);
+  a.fl_l2p = prof_flops_ptr(ST_L2P);
+  const int s = launch_leaf(a, t->orders[D], t->orders[D - 1], (unsigned)t->n_leaves, st);
+  if (s < 0) {
+    set_error("fused leaf downward step: orders (%d, %d) not instantiated", t->orders[D], t->orders[D - 1]);
+    return HIKF_BAD_ARGUMENT;
+  }
+  return s;
 }
 
 }  // namespace hikf

@@ -16,4 +16,14 @@ bool box_supported(int rows, int K);
 int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st,
               int64_t r0 = 0, int64_t r1 = -1);
 
+// Fused leaf-level L2L + L2P (the leaf locals stay on chip): U rows of every leaf
+// = W2 (S_D[leaf] + C_ci L_{D-1}[parent]); bit-identical to l2l_boxes + l2p_boxes.
+// Needs depth >= 3, <= 64 points per leaf and (leaf order, parent order) in
+// {(o, o), (o, o + 1)}, 2 <= o <= 8 (leaf_down_supported).
+bool leaf_down_supported(const hikf_tree* t);
+bool leaf_fused_enabled();
+int leaf_set_fused(int on);  // returns the previous setting
+int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, double* U, int64_t ldu,
+              cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1);
+
 }  // namespace hikf

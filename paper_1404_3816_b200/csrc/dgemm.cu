@@ -622,7 +622,12 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   }
   const bool vec = g.sa_c == 1 && g.sb_c == 1 && (g.sa_r % 2 == 0) && (g.sb_r % 2 == 0) && al16(g.A) && al16(g.B) &&
                    (batch == 1 || (g.bsA % 2 == 0 && g.bsB % 2 == 0));
-  // generic strides: 64 x 128 x 16, 8 warps of 32 x 32, 3 stages
+  // generic strides: 64 x 128 x 16, 8 warps of 32 x 32, 3 stages.  The row partials
+  // land in column-tile slots, so a caller sized for a 64-column variant (its
+  // dgemm_col_tiles) gets 64-column tiles here too (64 x 64, 4 warps of 32 x 32)
+  if (part && (variant == 32 || variant == 33))
+    return vec ? launch_gen<64, 64, 16, 2, 2, 3, 2, true, true>(g, batch, st)
+               : launch_gen<64, 64, 16, 2, 2, 3, 2, false, true>(g, batch, st);
   if (vec)
     return part ? launch_gen<64, 128, 16, 2, 4, 3, 2, true, true>(g, batch, st)
                 : launch_gen<64, 128, 16, 2, 4, 3, 2, true, false>(g, batch, st);

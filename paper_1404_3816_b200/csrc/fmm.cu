@@ -526,11 +526,14 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   // own pair-major scratch (q contiguous coefficients per (box, ray)) ----
   double* scratch[kMaxDepth + 1] = {};
   double* Lbuf[2] = {nullptr, nullptr};
-  const int64_t szD = ((int64_t)1 << (2 * D)) * t->orders[D] * t->orders[D] * n;
-  const int64_t szD1 = ((int64_t)1 << (2 * (D - 1))) * t->orders[D - 1] * t->orders[D - 1] * n;
+  // fused leaf step (leaf_down): the leaf-level locals are never stored
+  const bool fused_leaf = leaf_fused_enabled() && leaf_down_supported(t);
+  int64_t lsz[2] = {1, 1};  // ping-pong local buffers: level l lives in Lbuf[(D - l) & 1]
+  for (int l = 2; l <= D - (fused_leaf ? 1 : 0); ++l)
+    lsz[(D - l) & 1] = std::max(lsz[(D - l) & 1], ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n);
   if (status == HIKF_OK) {
-    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * szD, st));
-    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * std::max<int64_t>(szD1, 1), st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * lsz[0], st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * lsz[1], st));
     for (int l = 2; l <= D; ++l)
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch[l],
                                       sizeof(double) * ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n, st));
@@ -550,6 +553,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   const double* Lprev = nullptr;
   double* Lcur = nullptr;
   for (int l = 2; l <= D && status == HIKF_OK; ++l) {
+    if (l == D && fused_leaf) {  // the leaf L2L runs inside the fused L2P below
+      HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
+      break;
+    }
     Lcur = Lbuf[(D - l) & 1];
     const int q = t->orders[l] * t->orders[l];
     HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
@@ -574,7 +581,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     }
     Lprev = Lcur;
   }
-  if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
+  if (status == HIKF_OK && fused_leaf) {
+    ProfScope ps(ST_L2P, st);
+    status = leaf_down(t, scratch[D], Lprev, n, U, n, st, r0, r1);
+  } else if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
     status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
   } else if (status == HIKF_OK && window) {

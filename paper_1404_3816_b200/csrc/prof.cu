@@ -118,3 +118,23 @@ int hikf_prof_read(int32_t stage, double* total_ms, int64_t* count) {
 int64_t hikf_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"
+
+#include "boxgemm.h"
+#include "nnchain.h"
+
+extern "C" int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous) {
+  int prev = 0;
+  switch (key) {
+    case 0:
+      prev = hikf::nn_set_fused(value);
+      break;
+    case 1:
+      prev = hikf::leaf_set_fused(value);
+      break;
+    default:
+      hikf::set_error("unknown tuning key %d", (int)key);
+      return HIKF_BAD_ARGUMENT;
+  }
+  if (previous) *previous = prev;
+  return HIKF_OK;
+}

@@ -15,7 +15,9 @@
 #include <algorithm>
 #include <cfloat>
 
+#include "chol_block.cuh"
 #include "dgemm.cuh"
+#include "nnchain.h"
 #include "prof.h"
 #include "update.h"
 
@@ -113,116 +115,12 @@ __global__ void transpose_kernel(const double* __restrict__ X, int64_t n, double
   }
 }
 
-// Cholesky + inverse of one <= NB x NB diagonal block held in shared memory.
-// L (lower, ld), Li (lower, ld) written; upper triangles left untouched (zeroed
-// by the caller).  status[0] = global 1-based pivot of the first failure.
-// Right-looking factorisation: every thread recomputes the pivot (no extra
-// barrier), warp w updates rows i = w (mod 8) of the trailing triangle.
+// Cholesky + inverse of one <= NB x NB diagonal block (chol_block.cuh)
 __global__ void __launch_bounds__(256) chol_inv_base(const double* __restrict__ S, int64_t ld, int nb,
                                                      int64_t offset, double* __restrict__ L,
                                                      double* __restrict__ Li, int* status) {
   extern __shared__ double base_smem[];
-  double(*a)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(base_smem);
-  double(*x)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(base_smem + NB * (NB + 1));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    int i = e / nb, k = e - i * nb;
-    a[i][k] = S[(int64_t)i * ld + k];
-  }
-  __syncthreads();
-  // Right-looking Cholesky with the lower triangle in registers: thread t owns
-  // the elements e = t, t + 256, ... of the packed triangle (i >= k).  Per column
-  // j the owner of (j, j) publishes it, the owners of column j scale their
-  // entries and publish them, and every owner applies a[i][k] -= a[i][j] a[k][j]
-  // (k > j) in registers -- the same operations in the same order as updating
-  // a shared-memory copy, with two barriers per column (double-buffered).
-  constexpr int EPT = (NB * (NB + 1) / 2 + 255) / 256;  // elements per thread
-  __shared__ double colb[2][NB];
-  __shared__ double diagb[2];
-  const int ne = nb * (nb + 1) / 2;
-  double el[EPT];
-  int ei[EPT], ek[EPT];
-#pragma unroll
-  for (int q = 0; q < EPT; ++q) {
-    const int e = tid + q * 256;
-    int i = 0, k = 0;
-    if (e < ne) {
-      i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      while (i * (i + 1) / 2 > e) --i;
-      k = e - i * (i + 1) / 2;
-      el[q] = a[i][k];
-    } else {
-      i = k = -1;
-      el[q] = 0.0;
-    }
-    ei[q] = i;
-    ek[q] = k;
-  }
-  int bad = 0;
-  for (int j = 0; j < nb; ++j) {
-    const int b = j & 1;
-#pragma unroll
-    for (int q = 0; q < EPT; ++q)
-      if (ei[q] == j && ek[q] == j) diagb[b] = el[q];
-    __syncthreads();
-    double d = diagb[b];
-    if (!(d > 0.0)) {
-      if (!bad) bad = j + 1;
-      d = 1.0;  // keep going; the result is discarded by the caller
-    }
-    const double piv = sqrt(d);
-    const double inv = 1.0 / piv;
-#pragma unroll
-    for (int q = 0; q < EPT; ++q) {
-      if (ek[q] == j && ei[q] > j) {  // column j below the diagonal
-        el[q] *= inv;
-        colb[b][ei[q]] = el[q];
-      } else if (ek[q] == j && ei[q] == j) {
-        el[q] = piv;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < EPT; ++q)
-      if (ek[q] > j) el[q] = fma(-colb[b][ei[q]], colb[b][ek[q]], el[q]);
-  }
-#pragma unroll
-  for (int q = 0; q < EPT; ++q)
-    if (ei[q] >= 0) a[ei[q]][ek[q]] = el[q];
-  __syncthreads();
-  // inverse by forward substitution, one column per thread (the dot-product
-  // chains of the 64 columns run in parallel).  The column lives in registers
-  // (fully unrolled, predicated on k >= c): the chains of consecutive rows
-  // overlap instead of waiting on shared-memory round trips; the arithmetic and
-  // its order are those of x[i][c] = -(sum_{k=c}^{i-1} a[i][k] x[k][c]) / a[i][i].
-  __shared__ double rdiag[NB];
-  for (int i = tid; i < nb; i += blockDim.x) rdiag[i] = 1.0 / a[i][i];
-  __syncthreads();
-  if (tid < nb) {
-    const int c = tid;
-    double xr[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < i; ++k)
-        if (k >= c) s = fma(a[i][k], xr[k], s);
-      xr[i] = i < c ? 0.0 : (i == c ? rdiag[c] : (i < nb ? -s * rdiag[i] : 0.0));
-    }
-#pragma unroll
-    for (int i = 0; i < NB; ++i)
-      if (i >= c && i < nb) x[i][c] = xr[i];
-  }
-  __syncthreads();
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    int i = e / nb, k = e - i * nb;
-    if (k <= i) {
-      L[(int64_t)i * ld + k] = a[i][k];
-      Li[(int64_t)i * ld + k] = x[i][k];
-    }
-  }
-  if (tid == 0 && bad && status[0] == 0) status[0] = (int)(offset + bad);
+  chol_inv_block(S, ld, nb, offset, L, Li, status, base_smem);
 }
 
 // Recursive blocked Cholesky with inverse: S (n x n view, ld) -> L, Li.
@@ -1100,8 +998,192 @@ static int update_factored(const UpdateArgs& a, cudaStream_t st, UpdateResult* r
   return HIKF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Small n (n <= NN_FUSED_MAX): the n x n chain as two cooperative programs
+// (nnchain.cu) instead of ~40 launches; the look-ahead lives in one slot and is
+// probed on the device.  Same arithmetic as the multi-launch chain.
+// ---------------------------------------------------------------------------
+struct NnLook {
+  int64_t n = 0;
+  double r = 0.0;
+  const double* hcq_ptr = nullptr;
+  bool ready = false;
+  double *HC = nullptr, *HCQ = nullptr, *HCp = nullptr, *Li = nullptr, *LiT = nullptr, *Sinv = nullptr;
+  int* ibuf = nullptr;  // [0] pivot status of the look-ahead factor, [1] probe flag
+};
+
+static NnLook& nn_look() {
+  static NnLook x[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return x[dev & 63];
+}
+
+static int nn_look_reserve(NnLook& la, int64_t n) {
+  if (la.n == n && la.HC) return HIKF_OK;
+  for (double* q : {la.HC, la.HCQ, la.HCp, la.Li, la.LiT, la.Sinv})
+    if (q) cudaFree(q);
+  if (la.ibuf) cudaFree(la.ibuf);
+  la = NnLook();
+  const size_t b = std::max<size_t>(sizeof(double) * (size_t)n * n, 8);
+  for (double** q : {&la.HC, &la.HCQ, &la.HCp, &la.Li, &la.LiT, &la.Sinv}) HIKF_CHECK_CUDA(cudaMalloc((void**)q, b));
+  HIKF_CHECK_CUDA(cudaMalloc((void**)&la.ibuf, 4 * sizeof(int)));
+  HIKF_CHECK_CUDA(cudaMemset(la.ibuf, 0, 4 * sizeof(int)));
+  la.n = n;
+  return HIKF_OK;
+}
+
+int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res);
+
+static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
+  const int64_t m = a.m, n = a.n;
+  if (a.workspace_bytes < update_workspace_bytes(m, n)) {
+    set_error("update workspace too small (%zu < %zu bytes)", a.workspace_bytes, update_workspace_bytes(m, n));
+    return HIKF_BAD_ARGUMENT;
+  }
+  UpdWs w;
+  update_layout(m, n, (char*)a.workspace, &w);
+  HIKF_CHECK_CUDA(cudaMemsetAsync(w.status, 0, 16, st));
+  ChainState& ch = chain_state();
+  const bool chain_in = a.chain_in && ch.valid && ch.C_out == a.C && ch.CQ == a.CQ && ch.ws == a.workspace &&
+                        ch.m == m && ch.n == n;
+  double* Ycur = chain_in && ch.buf ? w.Y2 : w.Y;
+  double* Ynext = Ycur == w.Y ? w.Y2 : w.Y;
+  ch.valid = false;
+  cudaStream_t side = st;
+  cudaEvent_t ev[3];
+  HIKF_TRY(side_stream(&side, ev));
+  const bool use_la = lookahead_enabled();
+  NnLook& la = nn_look();
+  HIKF_TRY(nn_look_reserve(la, n));
+  const bool probe = use_la && la.ready && la.r == a.r && la.hcq_ptr == a.HCQ;
+
+  HIKF_CHECK_CUDA(cudaEventRecord(ev[0], st));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
+  {
+    ProfScope ps(ST_PREDICT, st);
+    if (m * n > 0 && !chain_in) HIKF_TRY(add_stream(a.C, a.CQ, Ycur, m * n, st));
+    add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(a.var, a.dQ, a.var_out, m);
+    HIKF_CHECK_LAUNCH();
+  }
+  NnPtrs p;
+  p.d[NB_HC] = const_cast<double*>(a.HC);
+  p.d[NB_HCQ] = const_cast<double*>(a.HCQ);
+  p.d[NB_HCP] = w.HCp;
+  p.d[NB_S] = w.S;
+  p.d[NB_L] = w.L;
+  p.d[NB_LI] = w.Li;
+  p.d[NB_LIT] = w.LiT;
+  p.d[NB_SINV] = w.Sinv;
+  p.d[NB_TMP] = w.tmp;
+  p.d[NB_P] = w.P;
+  p.d[NB_R] = w.R;
+  p.d[NB_HCOUT] = a.HC_out;
+  p.d[NB_LA_HC] = la.HC;
+  p.d[NB_LA_HCQ] = la.HCQ;
+  p.d[NB_LA_HCP] = la.HCp;
+  p.d[NB_LA_LI] = la.Li;
+  p.d[NB_LA_LIT] = la.LiT;
+  p.d[NB_LA_SINV] = la.Sinv;
+  p.i[NI_STATUS] = w.status;
+  p.i[NI_LA_STATUS] = la.ibuf;
+  p.i[NI_FLAG] = la.ibuf + 1;
+  p.r = a.r;
+  p.n = n;
+  p.force_miss = probe ? 0 : 1;
+  p.ip = a.ip;
+  p.ix = a.ix;
+  p.val = a.val;
+  p.mean = a.mean;
+  p.z = a.z;
+  p.Hmean = a.Hmean;
+  p.innov = w.innov;
+  {
+    ProfScope pf(ST_FACTOR, side);
+    if (probe) HIKF_CHECK_CUDA(cudaMemsetAsync(la.ibuf + 1, 0, sizeof(int), side));
+    HIKF_TRY(nn_pre(p, probe, side));
+  }
+  HIKF_CHECK_CUDA(cudaEventRecord(ev[1], side));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
+
+  // ---- main: K = C' S^-1 with the fused epilogue (as update()) ----
+  const int nb = grid_for(m);
+  {
+    const int vc = update_variant_c(n);
+    const int nt = dgemm_col_tiles(n, vc);
+    {
+      GemmArgs g;
+      g.M = m; g.N = n; g.K = n;
+      g.A = Ycur; g.sa_r = n;
+      g.B = w.Sinv; g.sb_r = n;
+      g.C = a.C_out; g.ldc = n;
+      g.alpha = a.r;
+      g.psq = w.psq; g.pdot = w.pdot; g.w = w.innov; g.ldp = nt;
+      g.px = Ycur; g.ldx = n;
+      if (a.chain) {
+        g.chain_add = a.CQ;
+        g.chain_out = Ynext;
+        g.ldch = n;
+      }
+      g.variant = vc;
+      ProfScope ps(ST_GEMM_C, st);
+      HIKF_TRY(dgemm(g, 1, st));
+    }
+    ProfScope pz(ST_FINALIZE, st);
+    finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, a.var_out, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
+    HIKF_CHECK_LAUNCH();
+    check_variance<<<1, kT, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+    HIKF_CHECK_LAUNCH();
+    if (a.mean_host)
+      HIKF_CHECK_CUDA(cudaMemcpyAsync(a.mean_host, a.mean_out, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
+  }
+  // ---- side, overlapping the GEMM: HC_new and the next step's factor ----
+  la.ready = false;
+  {
+    ProfScope pf(ST_FACTOR, side);
+    HIKF_TRY(nn_post(p, use_la, side));
+  }
+  if (use_la) {
+    la.ready = true;
+    la.r = a.r;
+    la.hcq_ptr = a.HCQ;
+  }
+  HIKF_CHECK_CUDA(cudaEventRecord(ev[2], side));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[2], 0));
+
+  int hs[2] = {0, 0};
+  double mm[2] = {0.0, 0.0};
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
+  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (res) {
+    res->pivot = hs[0];
+    res->min_var = mm[0];
+    res->max_prior_var = mm[1];
+  }
+  if (hs[0]) {
+    set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
+    return HIKF_NOT_PD;
+  }
+  if (hs[1] && !a.no_check) {
+    set_error("posterior variance went negative beyond tolerance (min %.3e)", mm[0]);
+    return HIKF_NEGATIVE_VARIANCE;
+  }
+  if (a.chain) {
+    ch.valid = true;
+    ch.C_out = a.C_out;
+    ch.CQ = a.CQ;
+    ch.ws = a.workspace;
+    ch.m = m;
+    ch.n = n;
+    ch.buf = Ynext == w.Y2 ? 1 : 0;
+  }
+  return HIKF_OK;
+}
+
 int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   if (a.factored) return update_factored(a, st, res);
+  if (a.CQ && nn_fused_enabled(a.n)) return update_small(a, st, res);
   const int64_t m = a.m, n = a.n;
   if (a.workspace_bytes < update_workspace_bytes(m, n)) {
     set_error("update workspace too small (%zu < %zu bytes)", a.workspace_bytes, update_workspace_bytes(m, n));

@@ -681,3 +681,63 @@ def test_factored_with_alpha_prior(pkg, alpha, cfg):
         fa = flt.hikf_update(flt.hikf_predict(fa, pre), H, cfg["R"], obs[t])
         for k in ("mean", "variance", "cross_cov", "HC"):
             assert O.rel_fro(getattr(fa, k), getattr(ex, k)) <= 1e-10, (t, k, O.rel_fro(getattr(fa, k), getattr(ex, k)))
+
+
+def _set_fused(pkg, on):
+    import ctypes
+    prev = ctypes.c_int32()
+    pkg._lib.check(pkg._lib.load().hikf_set_tuning(0, int(on), ctypes.byref(prev)))
+    return prev.value
+
+
+@pytest.mark.parametrize("ns,nr,N", [(8, 8, 32), (5, 13, 32), (12, 17, 48), (16, 16, 64)])
+def test_fused_small_chain_is_bit_identical(pkg, ns, nr, N):
+    """The fused n x n chain (csrc/nnchain.cu: two cooperative phase programs with a
+    device-side look-ahead probe) against the multi-launch chain it replaces for
+    n <= 512: n = 64 (cfg1), 65 (odd), 204 (two recursion levels, ragged blocks) and
+    256 (cfg2's n), 6 steps each, bitwise equal in mean, variance, C and HC."""
+    cfg = dict(cases.CFG1, ns=ns, nr=nr, N=N, T=6)
+    grid, H = _gpu_scenario(pkg, cfg)
+    xy = grid.cell_centers().coords
+    obs = O.observations(H, O.moving_plume(xy, cfg["T"]), cfg["R"], [4, 0])
+    runs = {}
+    prev = _set_fused(pkg, 1)
+    try:
+        for on in (1, 0):
+            _set_fused(pkg, on)
+            _, _, _, st = _run_filter(pkg, cfg, obs)
+            runs[on] = {k: getattr(st, k + "_t").clone() for k in ("mean", "variance", "cross_cov", "HC")}
+    finally:
+        _set_fused(pkg, prev)
+    for k in runs[1]:
+        assert bool((runs[1][k] == runs[0][k]).all()), (ns * nr, k)
+
+
+@pytest.mark.parametrize("N,ns,nr,order,leaf", [(64, 8, 8, 4, 64), (96, 6, 9, 5, 16), (128, 16, 16, 6, 64),
+                                                (256, 16, 16, 5, 64)])
+def test_fused_leaf_downward_is_bit_identical(pkg, N, ns, nr, order, leaf):
+    """Q H^T with the fused leaf-level L2L + L2P (csrc/boxgemm.cu leaf_down: the leaf
+    locals stay on chip) against the separate l2l_boxes + l2p_boxes kernels: C_Q and
+    HC_Q bitwise equal, and C_Q within 1e-13 of the oracle's FMM on 4 columns."""
+    import ctypes
+    cfg = dict(cases.CFG2, N=N, ns=ns, nr=nr, order=order, leaf=leaf)
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    model = _Model(grid, H, kern, cfg["R"])
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=order, max_leaf_points=leaf))
+    lib, prev = pkg._lib.load(), ctypes.c_int32()
+    out = {}
+    try:
+        for on in (1, 0):
+            pkg._lib.check(lib.hikf_set_tuning(1, on, ctypes.byref(prev)))
+            pre = pkg.filters.hikf_precompute_fmm(model, tree)
+            out[on] = (pre.C_Q_t.clone(), pre.HC_Q_t.clone())
+    finally:
+        pkg._lib.check(lib.hikf_set_tuning(1, 1, None))
+    assert bool((out[1][0] == out[0][0]).all()) and bool((out[1][1] == out[0][1]).all()), tree._orders
+    otree = O.OracleTree(grid.cell_centers().coords, O.Kern(cfg["family"], 1.0, cfg["L"]), order, leaf)
+    cols = [0, H.shape[0] // 3, H.shape[0] - 1]
+    V = H[cols].toarray().T
+    ref = otree.matmat(V)
+    got = out[1][0].cpu().numpy()[:, cols]
+    assert O.rel_fro(got, ref) <= 1e-13

@@ -1,0 +1,54 @@
+// Micro-benchmark of the 64 x 64 Cholesky + inverse base block (chol_block.cuh):
+// per-section clock64 stamps of one CTA, and the launch-to-launch time.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_1404_3816_b200/csrc -I../include \
+//        -o chol_bench chol_bench.cu && ./chol_bench
+#include <cstdio>
+#include <vector>
+
+#include "chol_block.cuh"
+
+using namespace hikf;
+
+__global__ void __launch_bounds__(256) base_kernel(const double* S, double* L, double* Li, int* status,
+                                                   long long* clk) {
+  extern __shared__ double sm[];
+  long long t0 = clock64();
+  chol_inv_block(S, 64, 64, 0, L, Li, status, sm);
+  long long t1 = clock64();
+  if (threadIdx.x == 0) clk[0] = t1 - t0;
+}
+
+int main() {
+  const int n = 64;
+  std::vector<double> h(n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) h[i * n + j] = (i == j ? n : 0.0) + 1.0 / (1 + i + j);
+  double *S, *L, *Li;
+  int* st;
+  long long* clk;
+  cudaMalloc(&S, 8 * n * n);
+  cudaMalloc(&L, 8 * n * n);
+  cudaMalloc(&Li, 8 * n * n);
+  cudaMalloc(&st, 16);
+  cudaMallocManaged(&clk, 64);
+  cudaMemcpy(S, h.data(), 8 * n * n, cudaMemcpyHostToDevice);
+  cudaMemset(st, 0, 16);
+  cudaFuncSetAttribute(base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHOL_SMEM);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; ++rep) {
+    base_kernel<<<1, 256, CHOL_SMEM>>>(S, L, Li, st, clk);
+    cudaDeviceSynchronize();
+    printf("single launch: %lld cycles in-kernel\n", clk[0]);
+  }
+  cudaEventRecord(a);
+  for (int rep = 0; rep < 100; ++rep) base_kernel<<<1, 256, CHOL_SMEM>>>(S, L, Li, st, clk);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  printf("back-to-back: %.2f us per launch, last in-kernel %lld cycles, err %s\n", ms * 10, clk[0],
+         cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}

@@ -444,18 +444,20 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    r0, r1 = SH.row_block(m, world, rank)
     tree = P.build_tree(grid.cell_centers(), kern, P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=cfg["leaf"]))
-    SH.precompute_rows(tree, H, r0, r1, comm)  # warm-up
+    # leaf-aligned row block (x-major leaf range, equal point counts): rows in leaf order
+    leaf0, leaf1, r0, r1 = SH.leaf_block(tree, world, rank)
+    rows = tree.export()["order"][r0:r1]
+    SH.precompute_leaves(tree, H, leaf0, leaf1, comm)  # warm-up
     barrier_sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    CQ, HCQ, dQ = SH.precompute_rows(tree, H, r0, r1, comm)
+    CQ, HCQ, dQ = SH.precompute_leaves(tree, H, leaf0, leaf1, comm)
     e1.record()
     barrier_sync()
     t_qht = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     step = SH.CudaRowStep((CQ, HCQ, dQ), n)
-    sh = SH.ShardedHikf(comm, step, H, m, rank, world)
+    sh = SH.ShardedHikf(comm, step, H, m, rank, world, rows=rows)
     zeros = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)  # noqa: E731
     st = {"mean": zeros(r1 - r0), "C": zeros((r1 - r0, n)), "var": zeros(r1 - r0), "HC": zeros((n, n))}
     Zd = torch.from_numpy(obs).to(dev)
@@ -473,6 +475,7 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
             st = sh.update(st, cfg["R"], Zd[(args.warmup + t) % cfg["T"]])
         s1.record()
         barrier_sync()
+    sh.check()  # the deferred variance / pivot check of the last timed step
     lib.hikf_prof_enable(0)
     launches = int(lib.hikf_launch_count() - l0)
     t_loop = max_over_ranks(s0.elapsed_time(s1) / 1e3)
@@ -497,7 +500,8 @@ def run_sharded(args, cfg, P, torch, dist, world, rank, local):
             "data": "synthetic: seeded crosswell rays + moving Gaussian plume, PCG64 noise (cfg recipe, SURVEY 8(d))",
             "config": arm_config(args, cfg, world, "sharded"), "rows_per_rank": r1 - r0,
             "qht": {"ms": 1000.0 * t_qht, "value": m * n / t_qht, "unit": "(m*n)/s",
-                    "note": "row-sharded precompute: upward pass + M2L replicated, L2P/P2P for owned rows"},
+                    "note": "leaf-aligned precompute shard: upward pass replicated; M2L / L2L for the ancestors of "
+                            "the rank's leaves, P2P and the fused leaf L2L + L2P for its own leaves"},
             "e2e": {"value": args.steps / t_e2e, "unit": "steps/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * (r1 - r0), "api": "sharded.ShardedHikf.update (numpy z) + mean rows"},
             "roofline": {"kernel": "dgemm_rm_kernel (K = C' S^-1 on this rank's rows, fused epilogue; "
@@ -646,6 +650,7 @@ def main():
             st = flt.hikf_update(flt.hikf_predict(st, pre), H, cfg["R"], Zd[(args.warmup + t) % cfg["T"]])
         s1.record()
         barrier_sync()
+    sh.check()  # the deferred variance / pivot check of the last timed step
     lib.hikf_prof_enable(0)
     launches = int(lib.hikf_launch_count() - l0)
     t_loop = max_over_ranks(s0.elapsed_time(s1) / 1e3)

@@ -136,6 +136,19 @@ int hikf_precompute(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const
 int hikf_precompute_rows(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
                          const double* data_dev, int64_t r0, int64_t r1, double* C_Q_rows_dev,
                          double* HC_Q_partial_dev, double* diag_Q_rows_dev, void* stream);
+/* Leaf-aligned shard of the precompute: the rows of the points of
+ * leaves [leaf0, leaf1) in the tree's leaf order (sorted positions s0 .. s1-1,
+ * s0 = leaf_start[leaf0]; C_Q_rows row i <-> sorted position s0 + i <-> original
+ * row order[s0 + i]).  P2P and the fused leaf L2L + L2P run for these leaves
+ * only, M2L and L2L only for their ancestors (the x-major leaf range is a strip
+ * of box columns); the upward pass is replicated.  HC_Q_partial = H[:, rows]
+ * C_Q_rows as hikf_precompute_rows.  hikf_leaf_partition: the balanced
+ * contiguous leaf range of a rank (equal point counts), out4 = {leaf0, leaf1,
+ * s0, s1}. */
+int hikf_leaf_partition(const hikf_tree* tree, int32_t world, int32_t rank, int64_t* out4);
+int hikf_precompute_leaves(hikf_tree* tree, int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev,
+                           const double* data_dev, int64_t leaf0, int64_t leaf1, double* C_Q_rows_dev,
+                           double* HC_Q_partial_dev, double* diag_Q_rows_dev, void* stream);
 
 /* ---- hikf_precompute_dense (filters.py:108-115; Gram as kernels.py:97-117) ----
  * The reference's exact-algebra oracle path: C_Q = Q H^T with the dense Gram
@@ -231,7 +244,11 @@ int hikf_update_rows(int64_t m_local, int64_t n, const double* mean_dev, const d
                      const double* Hmean_dev, double r_variance, const double* z_dev, double* mean_out,
                      double* C_out, double* var_out, double* HC_out, void* workspace, size_t workspace_bytes,
                      double* minmax_out, int32_t chain, void* stream);
-/* (chain: the produce / consume flags of hikf_update_chained, for this rank's rows) */
+/* (chain: the produce / consume flags of hikf_update_chained, for this rank's rows;
+ *  bit 2 (deferred): minmax_out is a DEVICE array of 3 doubles that receives
+ *  [min posterior var, max prior var, Cholesky pivot status] on the stream, and
+ *  the call neither synchronises nor raises -- the caller all-reduces the array
+ *  on the device and checks it at its next host touch.) */
 /* y (n) = H x for a CSR H (n x cols) on the device. */
 int hikf_csr_spmv(int64_t n, const int32_t* indptr_dev, const int32_t* indices_dev, const double* data_dev,
                   const double* x_dev, double* y_dev, void* stream);

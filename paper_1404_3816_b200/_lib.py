@@ -92,6 +92,8 @@ SIGNATURES = {
     "hikf_spd_solve": (ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _SZ, _P, _P]),
     "hikf_ray_operator": (ctypes.c_int, [_I64, _I64, _D, _D, _D, _D, _I64, _P, _P, _P, _P, _P, _P]),
     "hikf_precompute_rows": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
+    "hikf_leaf_partition": (ctypes.c_int, [_P, _I32, _I32, _P]),
+    "hikf_precompute_leaves": (ctypes.c_int, [_P, _I64, _P, _P, _P, _I64, _I64, _P, _P, _P, _P]),
     "hikf_precompute_dense": (ctypes.c_int, [_P, _I64, _P, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "hikf_ray_operator_3d": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _P]),
     "hikf_ray_operator_3d_device": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _P, _I64, _P, _P]),

@@ -404,6 +404,72 @@ int hikf_precompute_rows(hikf_tree* t, int64_t n, const int32_t* ip, const int32
   return HIKF_OK;
 }
 
+int hikf_leaf_partition(const hikf_tree* t, int32_t world, int32_t rank, int64_t* out4) {
+  if (!t || !out4 || world < 1 || rank < 0 || rank >= world) {
+    set_error("bad leaf_partition arguments (need 0 <= rank < world)");
+    return HIKF_BAD_ARGUMENT;
+  }
+  // contiguous leaves, cut where the running point count passes rank * m / world
+  auto cut = [&](int64_t r) -> int64_t {
+    if (r <= 0) return 0;
+    if (r >= world) return t->n_leaves;
+    const int64_t target = (t->m * r + world / 2) / world;
+    int64_t lo = 0, hi = t->n_leaves;  // first leaf whose start >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (t->h_leaf_start[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  LeafWindow w;
+  HIKF_TRY(leaf_window(t, cut(rank), cut(rank + 1), &w));
+  out4[0] = w.leaf0;
+  out4[1] = w.leaf1;
+  out4[2] = w.s0;
+  out4[3] = w.s1;
+  return HIKF_OK;
+}
+
+// HC_Q partial over a leaf shard: X[r][j] = sum_{e in row r, sorted position p of
+// column ix[e] in [s0, s1)} val[e] C[p - s0][j]
+__global__ void spmm_cols_sorted(int64_t n, int64_t s0, int64_t s1, const int32_t* __restrict__ ip,
+                                 const int32_t* __restrict__ ix, const double* __restrict__ val,
+                                 const int32_t* __restrict__ inv_order, const double* __restrict__ C,
+                                 double* __restrict__ X) {
+  const int64_t r = blockIdx.x;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = ip[r]; e < ip[r + 1]; ++e) {
+      const int64_t p = inv_order[ix[e]];
+      if (p >= s0 && p < s1) s += val[e] * C[(p - s0) * n + j];
+    }
+    X[r * n + j] = s;
+  }
+}
+
+int hikf_precompute_leaves(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val,
+                           int64_t leaf0, int64_t leaf1, double* CQ_rows, double* HCQ_partial, double* dQ_rows,
+                           void* stream) {
+  if (!t || n < 0) {
+    set_error("bad precompute_leaves arguments");
+    return HIKF_BAD_ARGUMENT;
+  }
+  LeafWindow w;
+  HIKF_TRY(leaf_window(t, leaf0, leaf1, &w));
+  cudaStream_t st = as_stream(stream);
+  if (w.s1 > w.s0) HIKF_TRY(fmm_matmat_csrT(t, n, ip, ix, val, CQ_rows, st, 0, -1, &w));
+  if (n > 0) {
+    spmm_cols_sorted<<<(unsigned)n, kT, 0, st>>>(n, w.s0, w.s1, ip, ix, val, t->inv_order, CQ_rows, HCQ_partial);
+    HIKF_CHECK_LAUNCH();
+  }
+  double k0 = t->spec.family == HIKF_LOGARITHM ? 0.0 : t->spec.variance;
+  if (w.s1 > w.s0) {
+    fill<<<grid_for(w.s1 - w.s0), kT, 0, st>>>(dQ_rows, w.s1 - w.s0, k0);
+    HIKF_CHECK_LAUNCH();
+  }
+  return HIKF_OK;
+}
+
 int hikf_precompute_dense(const double* xy_host, int64_t m, const hikf_kernel* kernel, int64_t n, const int32_t* ip,
                           const int32_t* ix, const double* val, double* CQ, double* HCQ, double* dQ, void* stream) {
   if (!xy_host || !kernel || m < 1 || n < 0) {
@@ -628,6 +694,13 @@ int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const doubl
   a.no_check = true;
   a.chain = (chain & 1) != 0;
   a.chain_in = (chain & 2) != 0;
+  if (chain & 4) {  // deferred: minmax_out is a device array of 3 doubles
+    if (!minmax_out) {
+      set_error("deferred update_rows (chain bit 4) needs a device minmax_out[3]");
+      return HIKF_BAD_ARGUMENT;
+    }
+    a.mm_dev = minmax_out;
+  }
   a.r = r;
   a.z = z;
   a.mean_out = mean_out;
@@ -638,7 +711,7 @@ int hikf_update_rows(int64_t m_local, int64_t n, const double* mean, const doubl
   a.workspace_bytes = workspace_bytes;
   UpdateResult res;
   int s = update(a, as_stream(stream), &res);
-  if (minmax_out) {
+  if (minmax_out && !(chain & 4)) {
     minmax_out[0] = res.min_var;
     minmax_out[1] = res.max_prior_var;
   }

@@ -56,6 +56,9 @@ struct BoxArgs {
   double* U;
   int64_t ldu;
   int64_t r0, r1;  // L2P row window: only original rows in [r0, r1) are written, at U + (row - r0) ldu
+  int64_t pxlo, pxhi;  // L2L: parents outside this box-column range are skipped (leaf-aligned shard)
+  int64_t leaf0;       // L2P: first leaf of the launch (blockIdx.x + leaf0)
+  int64_t s0;          // L2P: >= 0: leaf-aligned shard, U row = sorted position - s0
   unsigned long long* flops;
 };
 
@@ -72,10 +75,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
     Ag = g.shift;
   } else {
     row_off = blockIdx.y * 64;
-    const int cnt = g.leaf_count[blockIdx.x];
+    const int cnt = g.leaf_count[blockIdx.x + g.leaf0];
     if (row_off >= cnt) return;
     R = min(64, cnt - row_off);
-    Ag = g.W2s + (int64_t)(g.leaf_start[blockIdx.x] + row_off) * K;
+    Ag = g.W2s + (int64_t)(g.leaf_start[blockIdx.x + g.leaf0] + row_off) * K;
   }
   const int nrt = (R + 7) >> 3;
   for (int e = tid; e < nrt * 8 * NK4 * 4; e += BW_THREADS) {
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
   unsigned long long useful = 0;
   // B fragments of a unit: one register per k-step and column tile (this lane's columns j0 + 8c + gq)
   auto load_b = [&](int64_t u, double (&b)[CW][NK4]) {
-    const int64_t task = MODE == 0 ? u / ncb : blockIdx.x;
+    const int64_t task = MODE == 0 ? u / ncb : blockIdx.x + g.leaf0;
     const int64_t j0 = (u % ncb) * UW;
     const double* Bg = MODE == 0 ? g.Lp + (int64_t)g.occp[task] * K * g.n
                                  : g.Lleaf + (int64_t)g.leaf_box[task] * K * g.n;
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
   double bn[CW][NK4];  // software pipeline (PF): the next unit's fragments are in flight during this unit
   if (PF && unit0 < units) load_b(unit0, bn);
   for (int64_t u = unit0; u < units; u += unit_stride) {
-    const int64_t task = MODE == 0 ? u / ncb : blockIdx.x;
+    const int64_t task = MODE == 0 ? u / ncb : blockIdx.x + g.leaf0;
     const int64_t j0 = (u % ncb) * UW;
     double b[CW][NK4];
     if (PF) {
@@ -137,6 +140,7 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
       const int64_t P = g.occp[task];
       X = P / g.Gp;
       Y = P % g.Gp;
+      if (X < g.pxlo || X > g.pxhi) continue;  // warp-uniform: no ancestor of a shard's leaves
     }
     auto child_of = [&](int r, int& a) {
       const int ci = r / g.q;
@@ -191,9 +195,13 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
           int a;
           orow = g.L + (child_of(r, a) * g.q + a) * g.n;
         } else {
-          const int64_t orw = g.order[g.leaf_start[task] + row_off + r];
-          if (orw < g.r0 || orw >= g.r1) continue;
-          orow = g.U + (orw - g.r0) * g.ldu;
+          if (g.s0 >= 0) {
+            orow = g.U + (g.leaf_start[task] + row_off + r - g.s0) * g.ldu;
+          } else {
+            const int64_t orw = g.order[g.leaf_start[task] + row_off + r];
+            if (orw < g.r0 || orw >= g.r1) continue;
+            orow = g.U + (orw - g.r0) * g.ldu;
+          }
         }
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
@@ -293,6 +301,8 @@ struct LeafArgs {
   const double* S;      // pair-major M2L scratch of the leaf level
   double* U;
   int64_t ldu, r0, r1;
+  int64_t leaf0;  // first leaf of the launch (blockIdx.x + leaf0)
+  int64_t s0;     // >= 0: leaf-aligned shard, U row = sorted position - s0 (else original rows, r0 / r1 window)
   unsigned long long *fl_l2l, *fl_l2p;
 };
 
@@ -316,7 +326,7 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, t4 = lane & 3;
   const int q = g.q, qp = g.qp;
-  const int64_t T = blockIdx.x;
+  const int64_t T = blockIdx.x + g.leaf0;
   const int64_t box = g.leaf_box[T];
   const int64_t X = box / g.G, Y = box % g.G;
   const int ci = (int)(((X & 1) << 1) | (Y & 1));
@@ -346,8 +356,12 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
     const int pnt = i * 8 + gq;
     int32_t r = -1;
     if (pnt < cnt) {
-      const int64_t o = g.order[ls + pnt];
-      if (o >= g.r0 && o < g.r1) r = (int32_t)(o - g.r0);
+      if (g.s0 >= 0) {
+        r = (int32_t)(ls + pnt - g.s0);
+      } else {
+        const int64_t o = g.order[ls + pnt];
+        if (o >= g.r0 && o < g.r1) r = (int32_t)(o - g.r0);
+      }
     }
     orow[i] = r;
   }
@@ -474,9 +488,13 @@ int launch_leaf(const LeafArgs& a, int o, int op, unsigned nleaves, cudaStream_t
 
 bool box_supported(int rows, int K) { return K <= 4 * BW_MAXK4 && box_smem(rows, K) <= 200 * 1024; }
 
-int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int64_t n, double* L, cudaStream_t st) {
+int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int64_t n, double* L, cudaStream_t st,
+              int64_t pxlo, int64_t pxhi) {
   if (t->n_occ[l - 1] == 0 || n == 0) return HIKF_OK;
   BoxArgs a{};
+  a.pxlo = pxlo;
+  a.pxhi = pxhi;
+  a.s0 = -1;
   a.mode = 0;
   a.n = n;
   a.q = t->orders[l] * t->orders[l];
@@ -495,11 +513,15 @@ int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int6
 }
 
 int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st,
-              int64_t r0, int64_t r1) {
-  if (t->n_leaves == 0 || n == 0) return HIKF_OK;
+              int64_t r0, int64_t r1, const LeafWindow* lw) {
+  const int64_t l0 = lw ? lw->leaf0 : 0, l1 = lw ? lw->leaf1 : t->n_leaves;
+  if (l1 <= l0 || n == 0) return HIKF_OK;
   BoxArgs a{};
+  a.leaf0 = l0;
+  a.s0 = lw ? lw->s0 : -1;
   a.r0 = r0;
   a.r1 = r1 < 0 ? INT64_MAX : r1;
+  a.pxhi = INT64_MAX;
   a.mode = 1;
   a.n = n;
   a.K = t->orders[t->depth] * t->orders[t->depth];
@@ -512,7 +534,7 @@ int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int
   a.U = U;
   a.ldu = ldu;
   a.flops = prof_flops_ptr(ST_L2P);
-  return launch_box(a, 64, dim3((unsigned)t->n_leaves, (unsigned)((t->max_count + 63) / 64)), st);
+  return launch_box(a, 64, dim3((unsigned)(l1 - l0), (unsigned)((t->max_count + 63) / 64)), st);
 }
 
 static int g_leaf_fused = -1;
@@ -539,8 +561,9 @@ bool leaf_down_supported(const hikf_tree* t) {
 }
 
 int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, double* U, int64_t ldu,
-              cudaStream_t st, int64_t r0, int64_t r1) {
-  if (t->n_leaves == 0 || n == 0) return HIKF_OK;
+              cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
+  const int64_t l0 = lw ? lw->leaf0 : 0, l1 = lw ? lw->leaf1 : t->n_leaves;
+  if (l1 <= l0 || n == 0) return HIKF_OK;
   const int D = t->depth;
   LeafArgs a{};
   a.n = n;
@@ -559,9 +582,11 @@ int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, 
   a.ldu = ldu;
   a.r0 = r0;
   a.r1 = r1 < 0 ? INT64_MAX : r1;
+  a.leaf0 = l0;
+  a.s0 = lw ? lw->s0 : -1;
   a.fl_l2l = prof_flops_ptr(ST_L2L);
   a.fl_l2p = prof_flops_ptr(ST_L2P);
-  const int s = launch_leaf(a, t->orders[D], t->orders[D - 1], (unsigned)t->n_leaves, st);
+  const int s = launch_leaf(a, t->orders[D], t->orders[D - 1], (unsigned)(l1 - l0), st);
   if (s < 0) {
     set_error("fused leaf downward step: orders (%d, %d) not instantiated", t->orders[D], t->orders[D - 1]);
     return HIKF_BAD_ARGUMENT;

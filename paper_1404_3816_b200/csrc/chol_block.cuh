@@ -88,26 +88,33 @@ __device__ __forceinline__ void chol_inv_block(const double* __restrict__ S, int
   for (int q = 0; q < EPT; ++q)
     if (ei[q] >= 0) a[ei[q]][ek[q]] = el[q];
   __syncthreads();
-  // inverse by forward substitution, one column per thread (the dot-product
-  // chains of the 64 columns run in parallel):
-  //   x[c][c] = 1 / a[c][c],  x[i][c] = -(sum_{k=c}^{i-1} a[i][k] x[k][c]) / a[i][i]
-  // (fma chain in k order, times the reciprocal).  Rolled loops over shared
-  // memory: the fully unrolled register version was ~16k SASS instructions of
-  // straight-line code that ran once per launch from a cold instruction cache.
+  // inverse, right-looking over k (row k of x final after step k, then every
+  // row i > k takes its next fma): each element's fma chain in k order, the
+  // 64 columns' chains advancing together
   __shared__ double rdiag[CHOL_NB];
+  __shared__ double xrow[2][CHOL_NB];
   for (int i = tid; i < nb; i += blockDim.x) rdiag[i] = 1.0 / a[i][i];
   __syncthreads();
-  if (tid < nb) {
-    const int c = tid;
-    x[c][c] = rdiag[c];
-    for (int i = c + 1; i < nb; ++i) {
-      const double* ai = a[i];
-      double s = 0.0;
-#pragma unroll 8
-      for (int k = c; k < i; ++k) s = fma(ai[k], x[k][c], s);
-      x[i][c] = -s * rdiag[i];
-    }
+  double xs[EPT];
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) xs[q] = 0.0;
+  for (int k = 0; k < nb; ++k) {
+    const int b = k & 1;
+    const double rk = rdiag[k];
+#pragma unroll
+    for (int q = 0; q < EPT; ++q)
+      if (ei[q] == k) {
+        xs[q] = ek[q] == k ? rk : -xs[q] * rk;
+        xrow[b][ek[q]] = xs[q];
+      }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < EPT; ++q)
+      if (ei[q] > k && ek[q] <= k) xs[q] = fma(a[ei[q]][k], xrow[b][ek[q]], xs[q]);
   }
+#pragma unroll
+  for (int q = 0; q < EPT; ++q)
+    if (ei[q] >= 0) x[ei[q]][ek[q]] = xs[q];
   __syncthreads();
   for (int e = tid; e < nb * nb; e += blockDim.x) {
     int i = e / nb, k = e - i * nb;

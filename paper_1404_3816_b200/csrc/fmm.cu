@@ -474,12 +474,35 @@ int qht_streams(QhtStreams** out) {
 }
 }  // namespace
 
+int leaf_window(const hikf_tree* t, int64_t leaf0, int64_t leaf1, LeafWindow* w) {
+  if (leaf0 < 0 || leaf1 < leaf0 || leaf1 > t->n_leaves) {
+    set_error("leaf range [%lld, %lld) outside [0, %lld]", (long long)leaf0, (long long)leaf1, (long long)t->n_leaves);
+    return HIKF_BAD_ARGUMENT;
+  }
+  const int64_t G = (int64_t)1 << t->depth;
+  w->leaf0 = leaf0;
+  w->leaf1 = leaf1;
+  w->s0 = leaf0 < t->n_leaves ? t->h_leaf_start[leaf0] : t->m;
+  w->s1 = leaf1 > leaf0 ? t->h_leaf_start[leaf1 - 1] + t->h_leaf_count[leaf1 - 1] : w->s0;
+  w->x0 = leaf1 > leaf0 ? t->h_leaf_box[leaf0] / G : 0;
+  w->x1 = leaf1 > leaf0 ? t->h_leaf_box[leaf1 - 1] / G : -1;
+  return HIKF_OK;
+}
+
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
-                    cudaStream_t st, int64_t r0, int64_t r1) {
+                    cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
   if (n <= 0) return HIKF_OK;
   const bool window = r0 != 0 || (r1 >= 0 && r1 != t->m);
   if (r1 < 0) r1 = t->m;
+  if (lw) {
+    r0 = 0;
+    r1 = lw->s1 - lw->s0;
+    if (lw->leaf1 <= lw->leaf0) return HIKF_OK;
+  }
   const int D = t->depth;
+  // box-column range of level l that holds ancestors of the shard's leaves
+  auto xlo = [&](int l) { return lw ? (lw->x0 >> (D - l)) : (int64_t)0; };
+  auto xhi = [&](int l) { return lw ? (lw->x1 >> (D - l)) : INT64_MAX; };
   SparseHt sp;
   {
     ProfScope ps(ST_DENSIFY, st);  // the regrouping of H^T replaces the densify step
@@ -490,7 +513,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     int status;
     {
       ProfScope ps(ST_P2P, st);
-      status = sparse_p2p(t, sp, U, n, st, nullptr, r0, r1);
+      status = sparse_p2p(t, sp, U, n, st, nullptr, r0, r1, lw);
     }
     sparse_free(&sp, st);
     return status;
@@ -508,7 +531,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   int status = HIKF_OK;
   {
     ProfScope ps(ST_P2P, qs->s[0]);
-    status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear);
+    status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear, 0, -1, lw);
   }
   HIKF_CHECK_CUDA(cudaEventRecord(ev_p2p, qs->s[0]));
 
@@ -544,7 +567,8 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       const int q = t->orders[l] * t->orders[l];
       ProfScope ps(ST_M2L, sl);
       HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, sl));
-      for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot) status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl);
+      for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
+        status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl, xlo(l), xhi(l));
       HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
     }
   }
@@ -562,7 +586,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
     if (l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
       ProfScope ps(ST_L2L, st);
-      status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st);
+      status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st, xlo(l - 1), xhi(l - 1));
     } else {
       ProfScope ps(ST_L2L, st);
       status = pair_to_box(t, l, scratch[l], n, Lcur, st);
@@ -583,10 +607,13 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   if (status == HIKF_OK && fused_leaf) {
     ProfScope ps(ST_L2P, st);
-    status = leaf_down(t, scratch[D], Lprev, n, U, n, st, r0, r1);
+    status = leaf_down(t, scratch[D], Lprev, n, U, n, st, r0, r1, lw);
   } else if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
-    status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1);
+    status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1, lw);
+  } else if (status == HIKF_OK && lw) {
+    set_error("a leaf-aligned Q H^T shard needs the box-streaming L2P (leaf order <= 8)");
+    status = HIKF_BAD_ARGUMENT;
   } else if (status == HIKF_OK && window) {
     set_error("row-windowed Q H^T needs the box-streaming L2P (leaf order <= 8)");
     status = HIKF_BAD_ARGUMENT;
@@ -610,7 +637,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_p2p, 0));
   if (status == HIKF_OK) {
     ProfScope ps(ST_P2P, st);
-    status = sparse_p2p_scatter(t, sp, Pnear, U, n, st, r0, r1);
+    status = sparse_p2p_scatter(t, sp, Pnear, U, n, st, r0, r1, lw);
   }
   for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
   for (int l = 2; l <= D; ++l) cudaFreeAsync(scratch[l], st);

@@ -168,16 +168,45 @@ __device__ void grid_task(const NnTask& t, const NnPtrs& p) {
   const int64_t gs = (int64_t)gridDim.x * blockDim.x;
   const int64_t cnt = t.M, n = p.n;
   switch (t.kind) {
-    case K_ADD: {
-      const double *a = p.d[t.a], *b = p.d[t.b];
-      double* c = p.d[t.c];
-      for (int64_t e = g0; e < cnt; e += gs) c[e] = a[e] + b[e];
+    case K_ADD: {  // 4 independent elements per thread in flight (the grid is small)
+      const double* __restrict__ a = p.d[t.a];
+      const double* __restrict__ b = p.d[t.b];
+      double* __restrict__ c = p.d[t.c];
+      int64_t e = g0;
+      for (; e + 3 * gs < cnt; e += 4 * gs) {
+        double x[4], y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = a[e + u * gs], y[u] = b[e + u * gs];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[e + u * gs] = x[u] + y[u];
+      }
+      for (; e < cnt; e += gs) c[e] = a[e] + b[e];
       break;
     }
     case K_BUILD_S: {  // update.cu build_S
-      const double* HC = p.d[t.a];
-      double* S = p.d[t.c];
-      for (int64_t e = g0; e < n * n; e += gs) {
+      const double* __restrict__ HC = p.d[t.a];
+      double* __restrict__ S = p.d[t.c];
+      int64_t e = g0;
+      for (; e + 3 * gs < n * n; e += 4 * gs) {
+        double x[4], y[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = (e + u * gs) / n, j = (e + u * gs) % n;
+          x[u] = HC[i * n + j];
+          y[u] = HC[j * n + i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = (e + u * gs) / n, j = (e + u * gs) % n;
+          double a = x[u], b = y[u];
+          if (i == j) {
+            a = a + p.r;
+            b = b + p.r;
+          }
+          S[e + u * gs] = 0.5 * (a + b);
+        }
+      }
+      for (; e < n * n; e += gs) {
         const int64_t i = e / n, j = e % n;
         double a = HC[i * n + j], b = HC[j * n + i];
         if (i == j) {
@@ -198,9 +227,17 @@ __device__ void grid_task(const NnTask& t, const NnPtrs& p) {
       break;
     }
     case K_COPY: {
-      const double* a = p.d[t.a];
-      double* c = p.d[t.c];
-      for (int64_t e = g0; e < cnt; e += gs) c[e] = a[e];
+      const double* __restrict__ a = p.d[t.a];
+      double* __restrict__ c = p.d[t.c];
+      int64_t e = g0;
+      for (; e + 3 * gs < cnt; e += 4 * gs) {
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = a[e + u * gs];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) c[e + u * gs] = x[u];
+      }
+      for (; e < cnt; e += gs) c[e] = a[e];
       break;
     }
     case K_ZERO: {
@@ -209,10 +246,14 @@ __device__ void grid_task(const NnTask& t, const NnPtrs& p) {
       break;
     }
     case K_DIFF: {
-      const uint64_t* a = reinterpret_cast<const uint64_t*>(p.d[t.a]);
-      const uint64_t* b = reinterpret_cast<const uint64_t*>(p.d[t.b]);
+      const uint64_t* __restrict__ a = reinterpret_cast<const uint64_t*>(p.d[t.a]);
+      const uint64_t* __restrict__ b = reinterpret_cast<const uint64_t*>(p.d[t.b]);
       uint64_t d = 0;
-      for (int64_t e = g0; e < cnt; e += gs) d |= a[e] ^ b[e];
+      int64_t e = g0;
+      for (; e + 3 * gs < cnt; e += 4 * gs)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) d |= a[e + u * gs] ^ b[e + u * gs];
+      for (; e < cnt; e += gs) d |= a[e] ^ b[e];
       if (__syncthreads_or(d != 0) && threadIdx.x == 0) atomicOr(p.i[NI_FLAG], 1);
       break;
     }
@@ -456,7 +497,7 @@ int upload(const Program& P, DevProgram* d) {
     max_grid = std::max(1, per_sm) * num_sms();
   }
   // enough CTAs for the widest phase, capped by co-residency (cooperative launch)
-  d->grid = std::max(1, std::min({P.max_tiles, max_grid, num_sms()}));
+  d->grid = std::max(1, std::min({std::max(P.max_tiles, 32), max_grid, num_sms()}));
   return HIKF_OK;
 }
 

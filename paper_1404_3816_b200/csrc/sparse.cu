@@ -159,13 +159,14 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
                            const double* __restrict__ e_v, const double* __restrict__ xy_s,
                            const int64_t* __restrict__ order, double* __restrict__ U, int64_t ldu,
                            double* __restrict__ Pnear, int32_t maxc, int64_t r0, int64_t r1,
-                           unsigned long long* __restrict__ flops) {
+                           unsigned long long* __restrict__ flops, int64_t leaf0, int64_t leaf1, int64_t s0) {
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (item >= nitems) return;
   const int64_t key = items[item];
   const int32_t T = (int32_t)(key / n);
   const int32_t j = (int32_t)(key % n);
+  if (T < leaf0 || T >= leaf1) return;  // another shard's target leaf
   const int64_t box = leaf_box[T], bx = box / G, by = box % G;
   // the <= 9 entry ranges of ray j in the adjacent leaves
   int32_t rb[9], re[9];
@@ -211,7 +212,9 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
     if (!ok) continue;
     if (Pnear)
       Pnear[(int64_t)t * nitems + item] = acc;  // added into U later (p2p_scatter): U = far + near either way
-    else {
+    else if (s0 >= 0) {
+      U[(t0 + t - s0) * ldu + j] += acc;
+    } else {
       const int64_t row = order[t0 + t];
       if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += acc;
     }
@@ -225,14 +228,20 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
 __global__ void p2p_scatter(int64_t nitems, const int64_t* __restrict__ items, int64_t n,
                             const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_count,
                             const int64_t* __restrict__ order, const double* __restrict__ Pnear, int32_t maxc,
-                            double* __restrict__ U, int64_t ldu, int64_t r0, int64_t r1) {
+                            double* __restrict__ U, int64_t ldu, int64_t r0, int64_t r1, int64_t leaf0,
+                            int64_t leaf1, int64_t s0) {
   const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (item >= nitems) return;
   const int64_t key = items[item];
   const int32_t T = (int32_t)(key / n);
   const int32_t j = (int32_t)(key % n);
+  if (T < leaf0 || T >= leaf1) return;
   const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
   for (int t = 0; t < cnt; ++t) {
+    if (s0 >= 0) {
+      U[(t0 + t - s0) * ldu + j] += Pnear[(int64_t)t * nitems + item];
+      continue;
+    }
     const int64_t row = order[t0 + t];
     if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += Pnear[(int64_t)t * nitems + item];
   }
@@ -398,24 +407,26 @@ int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, 
 }
 
 int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st, double* Pnear,
-               int64_t r0, int64_t r1) {
+               int64_t r0, int64_t r1, const LeafWindow* lw) {
   if (s.nitems <= 0) return HIKF_OK;
   const int64_t threads = s.nitems * 32;
   p2p_sparse<<<(unsigned)((threads + kT - 1) / kT), kT, 0, st>>>(
       s.nitems, s.items, s.n, t->G, t->kp, t->leaf_box, t->leaf_start, t->leaf_count, t->box2leaf, s.leaf_g, s.g_j,
       s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, Pnear, (int32_t)t->max_count, r0,
-      r1 < 0 ? INT64_MAX : r1, prof_flops_ptr(ST_P2P));
+      r1 < 0 ? INT64_MAX : r1, prof_flops_ptr(ST_P2P), lw ? lw->leaf0 : 0, lw ? lw->leaf1 : INT64_MAX,
+      lw ? lw->s0 : -1);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
 
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
-                       cudaStream_t st, int64_t r0, int64_t r1) {
+                       cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
   if (s.nitems <= 0) return HIKF_OK;
   p2p_scatter<<<(unsigned)((s.nitems + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
                                                                  t->leaf_count, t->order, Pnear,
                                                                  (int32_t)t->max_count, U, ldu, r0,
-                                                                 r1 < 0 ? INT64_MAX : r1);
+                                                                 r1 < 0 ? INT64_MAX : r1, lw ? lw->leaf0 : 0,
+                                                                 lw ? lw->leaf1 : INT64_MAX, lw ? lw->s0 : -1);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
@@ -509,7 +520,8 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
                                                         const double* __restrict__ Wc, int q, int64_t n, int64_t G,
                                                         int dx, int dy, const uint8_t* __restrict__ occ,
                                                         const double* __restrict__ M, double* __restrict__ L,
-                                                        unsigned long long* __restrict__ flops) {
+                                                        unsigned long long* __restrict__ flops, int64_t xlo,
+                                                        int64_t xhi) {
   extern __shared__ double Ms[];
   const int ld = kSmem ? m2l_ld(q) : q;
   if (kSmem) {
@@ -535,8 +547,8 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
     if (p < np) {
       int64_t S = key[p] / n, j = key[p] % n;
       int64_t tx = S / G - dx, ty = S % G - dy, s2;
-      if (tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) && s2 == S &&
-          occ[tx * G + ty]) {
+      if (tx >= xlo && tx <= xhi && tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) &&
+          s2 == S && occ[tx * G + ty]) {
         myT[c] = (int32_t)(tx * G + ty);
         myJ[c] = (int32_t)j;
       }
@@ -742,7 +754,8 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
   return HIKF_OK;
 }
 
-int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, cudaStream_t st) {
+int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, cudaStream_t st,
+             int64_t xlo, int64_t xhi) {
   if (src.np == 0 || !((t->m2l_present[l] >> slot) & 1)) return HIKF_OK;
   M2LOffsets offs;
   const int q = t->orders[l] * t->orders[l];
@@ -756,7 +769,7 @@ int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t 
 #define HIKF_M2L_CASE(QQ, K4, RT)                                                                               \
   case QQ:                                                                                                     \
     m2l_pairs_kernel<true, K4, RT><<<blocks, kT, smem, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],   \
-                                                             offs.dy[slot], t->occ_flag[l], M, L, fl);         \
+                                                             offs.dy[slot], t->occ_flag[l], M, L, fl, xlo, xhi);\
     break;
   switch (q) {
     HIKF_M2L_CASE(4, 1, 1)
@@ -768,7 +781,7 @@ int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t 
     HIKF_M2L_CASE(64, 16, 8)
     default:
       m2l_pairs_kernel<false, 1, 1><<<blocks, kT, 0, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],
-                                                            offs.dy[slot], t->occ_flag[l], M, L, fl);
+                                                            offs.dy[slot], t->occ_flag[l], M, L, fl, xlo, xhi);
   }
 #undef HIKF_M2L_CASE
   HIKF_CHECK_LAUNCH();

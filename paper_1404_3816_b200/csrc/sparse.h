@@ -6,6 +6,10 @@
 struct hikf_tree;
 
 namespace hikf {
+struct LeafWindow;
+}
+
+namespace hikf {
 
 struct SparseHt {
   int64_t n = 0, nnz = 0, ngroups = 0, nitems = 0, ngr = 0;
@@ -36,10 +40,12 @@ int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, 
 // near field of the (target leaf, ray) items: U += near sum, or, with Pnear
 // (nitems x max_count), the sums are parked there and added by sparse_p2p_scatter
 // (row window as l2p_boxes: only original rows r0 <= row < r1, at U + (row - r0) ldu)
+// (lw: leaf-aligned shard -- items of other target leaves are skipped, U rows are sorted
+//  positions - lw->s0)
 int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st,
-               double* Pnear = nullptr, int64_t r0 = 0, int64_t r1 = -1);
+               double* Pnear = nullptr, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
-                       cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1);
+                       cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
 
 // leaf multipoles of the active (leaf, ray) pairs (sparse P2M)
 int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st);
@@ -48,7 +54,9 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
 void pairs_free(PairLevel* p, cudaStream_t st);
 // L_l[T][:, j] += M_d W_{T+d}[:, j] for every active source pair and one offset slot
 // S must be the pair-major scratch S[T][j][a] (zeroed before the 40 offsets)
-int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, cudaStream_t st);
+// (targets outside the box-column range [xlo, xhi] of level l are skipped)
+int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, cudaStream_t st,
+             int64_t xlo = 0, int64_t xhi = INT64_MAX);
 // L[T][a][j] = S[T][j][a] for the occupied boxes of level l
 int pair_to_box(const hikf_tree* t, int l, const double* S, int64_t n, double* L, cudaStream_t st);
 

@@ -84,7 +84,14 @@ int tree_export_m2l_pairs(const hikf_tree* t, int lev, int dx, int dy, std::vect
 int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U, int64_t ldu, cudaStream_t stream);
 // U (m x n) = tree @ H^T for a device CSR H (n x m), H^T kept sparse
 // U = Q H^T; with a row window only original rows r0 <= row < r1 are produced, at U + (row - r0) n
+// Leaf-aligned shard (hikf_precompute_leaves): only the points of leaves [leaf0, leaf1),
+// rows in leaf order (sorted positions s0 .. s1-1 -> U rows 0 .. s1-s0-1); x0 / x1 = the
+// leaf-level box-column range of those leaves (their ancestors' columns are x >> (D - l)).
+struct LeafWindow {
+  int64_t leaf0 = 0, leaf1 = 0, s0 = 0, s1 = 0, x0 = 0, x1 = 0;
+};
+int leaf_window(const hikf_tree* t, int64_t leaf0, int64_t leaf1, LeafWindow* w);
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
-                    cudaStream_t stream, int64_t r0 = 0, int64_t r1 = -1);
+                    cudaStream_t stream, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
 
 }  // namespace hikf

@@ -271,6 +271,13 @@ __global__ void check_variance(int nb, const double* bmin, const double* bmax, i
   }
 }
 
+// deferred status of a row-sharded step: [min var, max prior var, pivot] on the device
+__global__ void pack_status(const double* __restrict__ minv, const int* __restrict__ status, double* __restrict__ out) {
+  out[0] = minv[0];
+  out[1] = minv[1];
+  out[2] = (double)status[0];
+}
+
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // library-owned side stream + fork/join events for the n x n work of the update
@@ -1151,23 +1158,28 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
   HIKF_CHECK_CUDA(cudaEventRecord(ev[2], side));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[2], 0));
 
-  int hs[2] = {0, 0};
-  double mm[2] = {0.0, 0.0};
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
-  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-  if (res) {
-    res->pivot = hs[0];
-    res->min_var = mm[0];
-    res->max_prior_var = mm[1];
-  }
-  if (hs[0]) {
-    set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
-    return HIKF_NOT_PD;
-  }
-  if (hs[1] && !a.no_check) {
-    set_error("posterior variance went negative beyond tolerance (min %.3e)", mm[0]);
-    return HIKF_NEGATIVE_VARIANCE;
+  if (a.mm_dev) {  // deferred: the caller all-reduces and checks the packed status
+    pack_status<<<1, 1, 0, st>>>(w.minv, w.status, a.mm_dev);
+    HIKF_CHECK_LAUNCH();
+  } else {
+    int hs[2] = {0, 0};
+    double mm[2] = {0.0, 0.0};
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+    if (res) {
+      res->pivot = hs[0];
+      res->min_var = mm[0];
+      res->max_prior_var = mm[1];
+    }
+    if (hs[0]) {
+      set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
+      return HIKF_NOT_PD;
+    }
+    if (hs[1] && !a.no_check) {
+      set_error("posterior variance went negative beyond tolerance (min %.3e)", mm[0]);
+      return HIKF_NEGATIVE_VARIANCE;
+    }
   }
   if (a.chain) {
     ch.valid = true;
@@ -1293,25 +1305,30 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   HIKF_CHECK_CUDA(cudaEventRecord(ev[2], side));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev[2], 0));
 
-  // ---- status back to the host ----
-  int hs[2] = {0, 0};
-  double mm[2] = {0.0, 0.0};
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
-  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-  const double mv = mm[0];
-  if (res) {
-    res->pivot = hs[0];
-    res->min_var = mm[0];
-    res->max_prior_var = mm[1];
-  }
-  if (hs[0]) {
-    set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
-    return HIKF_NOT_PD;
-  }
-  if (hs[1] && !a.no_check) {
-    set_error("posterior variance went negative beyond tolerance (min %.3e)", mv);
-    return HIKF_NEGATIVE_VARIANCE;
+  // ---- status back to the host (or, deferred, packed on the device) ----
+  if (a.mm_dev) {
+    pack_status<<<1, 1, 0, st>>>(w.minv, w.status, a.mm_dev);
+    HIKF_CHECK_LAUNCH();
+  } else {
+    int hs[2] = {0, 0};
+    double mm[2] = {0.0, 0.0};
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(hs, w.status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(mm, w.minv, sizeof(mm), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+    const double mv = mm[0];
+    if (res) {
+      res->pivot = hs[0];
+      res->min_var = mm[0];
+      res->max_prior_var = mm[1];
+    }
+    if (hs[0]) {
+      set_error("Cholesky factorization failed: %d-th leading minor of the array is not positive definite", hs[0]);
+      return HIKF_NOT_PD;
+    }
+    if (hs[1] && !a.no_check) {
+      set_error("posterior variance went negative beyond tolerance (min %.3e)", mv);
+      return HIKF_NEGATIVE_VARIANCE;
+    }
   }
   if (a.chain && a.CQ) {
     ch.valid = true;

@@ -18,6 +18,9 @@ struct UpdateArgs {
   size_t workspace_bytes = 0;
   const double* Hmean = nullptr;  // row-sharded state: all-reduced H mean (else computed from H, mean)
   bool no_check = false;          // row-sharded state: the caller applies the global variance check
+  // deferred status (row-sharded state): [min posterior var, max prior var, pivot] written to this
+  // device array on the stream; the call neither synchronises nor checks (the caller all-reduces it)
+  double* mm_dev = nullptr;
   // chained predict: the caller will pass this call's C_out (untouched) with the same C_Q to the
   // next call; the GEMM epilogue then also writes that call's C' = C_out + C_Q into the workspace
   bool chain = false;     // produce the next call's C'

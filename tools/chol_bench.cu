@@ -3,8 +3,11 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../paper_1404_3816_b200/csrc -I../include \
 //        -o chol_bench chol_bench.cu && ./chol_bench
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
+__device__ long long g_sec[16];
+#define CHOL_BENCH_CLOCK g_sec
 #include "chol_block.cuh"
 
 using namespace hikf;
@@ -15,7 +18,7 @@ __global__ void __launch_bounds__(256) base_kernel(const double* S, double* L, d
   long long t0 = clock64();
   chol_inv_block(S, 64, 64, 0, L, Li, status, sm);
   long long t1 = clock64();
-  if (threadIdx.x == 0) clk[0] = t1 - t0;
+  if (threadIdx.x == 0) { clk[0] = t1 - t0; clk[1] = g_sec[0]; clk[2] = g_sec[1]; clk[3] = g_sec[2]; }
 }
 
 int main() {
@@ -40,7 +43,9 @@ int main() {
   for (int rep = 0; rep < 3; ++rep) {
     base_kernel<<<1, 256, CHOL_SMEM>>>(S, L, Li, st, clk);
     cudaDeviceSynchronize();
-    printf("single launch: %lld cycles in-kernel\n", clk[0]);
+    printf("single launch: %lld cycles in-kernel (chol %lld, store %lld, inverse %lld)\n", clk[0], clk[1], clk[2], clk[3]);
+    long long hs[16]; cudaMemcpyFromSymbol(hs, g_sec, sizeof(hs));
+    printf("  column deltas:"); for (int q = 5; q < 12; ++q) printf(" %lld", hs[q] - hs[q - 1]); printf("\n");
   }
   cudaEventRecord(a);
   for (int rep = 0; rep < 100; ++rep) base_kernel<<<1, 256, CHOL_SMEM>>>(S, L, Li, st, clk);
@@ -50,5 +55,18 @@ int main() {
   cudaEventElapsedTime(&ms, a, b);
   printf("back-to-back: %.2f us per launch, last in-kernel %lld cycles, err %s\n", ms * 10, clk[0],
          cudaGetErrorString(cudaGetLastError()));
+  std::vector<double> hl(n * n), hli(n * n);
+  cudaMemcpy(hl.data(), L, 8 * n * n, cudaMemcpyDeviceToHost);
+  cudaMemcpy(hli.data(), Li, 8 * n * n, cudaMemcpyDeviceToHost);
+  unsigned long long hsum = 0;
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k <= i; ++k) {
+      unsigned long long u, v;
+      memcpy(&u, &hl[i * n + k], 8);
+      memcpy(&v, &hli[i * n + k], 8);
+      hsum = hsum * 1099511628211ull + u;
+      hsum = hsum * 1099511628211ull + v;
+    }
+  printf("digest %016llx\n", hsum);
   return 0;
 }

@@ -46,7 +46,8 @@ struct BoxArgs {
   int64_t Gp;
   const double* Lp;        // parent locals (box-major)
   const double* shift;     // 4 q x qp
-  const double* S;         // pair-major M2L scratch of the child level
+  const double* S;         // compact M2L scratch of the child level (q per slot)
+  const int32_t* tmap;     // (child box, ray) -> slot in S, or -1
   double* L;               // child locals (box-major)
   // L2P
   const int32_t *leaf_box, *leaf_start, *leaf_count;
@@ -160,13 +161,16 @@ __global__ void __launch_bounds__(BW_THREADS, 2) box_warp_kernel(BoxArgs g) {
           for (int c = 0; c < CW; ++c) init[i][c][0] = init[i][c][1] = 0.0;
           if (r0 + i < nrt && r < R) {
             int a;
-            const int64_t irow = child_of(r, a) * g.n * g.q + a;
+            const int64_t crow = child_of(r, a) * g.n;
 #pragma unroll
             for (int c = 0; c < CW; ++c)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int64_t jc = j0 + 8 * c + 2 * t4 + h;
-                if (jc < g.n) init[i][c][h] = g.S[irow + jc * g.q];
+                if (jc < g.n) {
+                  const int32_t slot = g.tmap[crow + jc];
+                  if (slot >= 0) init[i][c][h] = g.S[(int64_t)slot * g.q + a];
+                }
               }
           }
         }
@@ -298,7 +302,8 @@ struct LeafArgs {
   const int64_t* order;
   const double* Lp;     // parent-level locals (box-major)
   const double* shift;  // 4 q x qp stacked child operators of the parent level
-  const double* S;      // pair-major M2L scratch of the leaf level
+  const double* S;      // compact M2L scratch of the leaf level (q per slot)
+  const int32_t* tmap;  // (leaf box, ray) -> slot in S, or -1
   double* U;
   int64_t ldu, r0, r1;
   int64_t leaf0;  // first leaf of the launch (blockIdx.x + leaf0)
@@ -348,7 +353,7 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
   const int64_t n = g.n;
   const int64_t ncb = (n + 7) / 8;
   const double* Lpar = g.Lp + P * qp * n;
-  const double* Sb = g.S + box * n * q;
+  const int32_t* tm = g.tmap + box * n;
   // this lane's output rows (leaf points 8 i + gq) in U, or -1 outside the row window
   int32_t orow[8];
 #pragma unroll
@@ -389,14 +394,17 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
     }
     // the M2L sums of this unit (loaded ahead of the DMMA chain, added after it)
     double init[NRT1][2];
+    int32_t slot[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t jc = j0 + 2 * t4 + h;
+      slot[h] = jc < n ? tm[jc] : -1;
+    }
 #pragma unroll
     for (int i = 0; i < NRT1; ++i) {
       const int r = i * 8 + gq;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t jc = j0 + 2 * t4 + h;
-        init[i][h] = (r < q && jc < n) ? Sb[jc * q + r] : 0.0;
-      }
+      for (int h = 0; h < 2; ++h) init[i][h] = (r < q && slot[h] >= 0) ? g.S[(int64_t)slot[h] * q + r] : 0.0;
     }
     // L2L into the leaf: acc1 = C_ci L_parent, then l = acc1 + S
     double acc1[NRT1][2];
@@ -488,10 +496,11 @@ int launch_leaf(const LeafArgs& a, int o, int op, unsigned nleaves, cudaStream_t
 
 bool box_supported(int rows, int K) { return K <= 4 * BW_MAXK4 && box_smem(rows, K) <= 200 * 1024; }
 
-int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int64_t n, double* L, cudaStream_t st,
-              int64_t pxlo, int64_t pxhi) {
+int l2l_boxes(const hikf_tree* t, int l, const double* S, const int32_t* tmap, const double* Lp, int64_t n,
+              double* L, cudaStream_t st, int64_t pxlo, int64_t pxhi) {
   if (t->n_occ[l - 1] == 0 || n == 0) return HIKF_OK;
   BoxArgs a{};
+  a.tmap = tmap;
   a.pxlo = pxlo;
   a.pxhi = pxhi;
   a.s0 = -1;
@@ -560,8 +569,8 @@ bool leaf_down_supported(const hikf_tree* t) {
   return o >= 2 && o <= 8 && (op == o || op == o + 1);
 }
 
-int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, double* U, int64_t ldu,
-              cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
+int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const double* Lp, int64_t n, double* U,
+              int64_t ldu, cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
   const int64_t l0 = lw ? lw->leaf0 : 0, l1 = lw ? lw->leaf1 : t->n_leaves;
   if (l1 <= l0 || n == 0) return HIKF_OK;
   const int D = t->depth;
@@ -578,6 +587,7 @@ int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, 
   a.Lp = Lp;
   a.shift = t->shift[D - 1];
   a.S = S;
+  a.tmap = tmap;
   a.U = U;
   a.ldu = ldu;
   a.r0 = r0;

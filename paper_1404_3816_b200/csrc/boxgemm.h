@@ -6,11 +6,11 @@
 
 namespace hikf {
 
-// L_l[child][a][j] = S[child][j][a] + sum_b C_child[a][b] L_{l-1}[parent][b][j] for every
+// L_l[child][a][j] = S[tmap[child n + j]][a] (0 without a slot) + sum_b C_child[a][b] L_{l-1}[parent][b][j] for every
 // child of an occupied parent (l > 2); S is the pair-major M2L scratch of level l
 // (parents outside the box-column range [pxlo, pxhi] of level l-1 are skipped)
-int l2l_boxes(const hikf_tree* t, int l, const double* S, const double* Lp, int64_t n, double* L, cudaStream_t st,
-              int64_t pxlo = 0, int64_t pxhi = INT64_MAX);
+int l2l_boxes(const hikf_tree* t, int l, const double* S, const int32_t* tmap, const double* Lp, int64_t n,
+              double* L, cudaStream_t st, int64_t pxlo = 0, int64_t pxhi = INT64_MAX);
 // whether the warp-streaming kernel handles R rows x K inner (K <= 64, A fits in smem)
 bool box_supported(int rows, int K);
 // U[order[p]][j] = sum_a W2[p][a] L_leaf[a][j] (store)
@@ -25,7 +25,7 @@ int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int
 bool leaf_down_supported(const hikf_tree* t);
 bool leaf_fused_enabled();
 int leaf_set_fused(int on);  // returns the previous setting
-int leaf_down(const hikf_tree* t, const double* S, const double* Lp, int64_t n, double* U, int64_t ldu,
-              cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
+int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const double* Lp, int64_t n, double* U,
+              int64_t ldu, cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
 
 }  // namespace hikf

@@ -545,9 +545,13 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     ProfScope ps(ST_M2M, st);
     status = pairs_parent(t, l, pl[l + 1], n, &pl[l], st);
   }
-  // ---- M2L, one stream per level: each level accumulates per offset into its
-  // own pair-major scratch (q contiguous coefficients per (box, ray)) ----
+  // ---- M2L targets, all levels on the main stream: a (box, ray) -> slot map per
+  // level and one read-back of the slot counts; then one stream per level, each
+  // accumulating per offset into its own compact scratch (q coefficients per slot) ----
   double* scratch[kMaxDepth + 1] = {};
+  int32_t* tmap[kMaxDepth + 1] = {};
+  int32_t* tcount = nullptr;
+  int32_t hcount[kMaxDepth + 1] = {0};
   double* Lbuf[2] = {nullptr, nullptr};
   // fused leaf step (leaf_down): the leaf-level locals are never stored
   const bool fused_leaf = leaf_fused_enabled() && leaf_down_supported(t);
@@ -557,18 +561,27 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   if (status == HIKF_OK) {
     HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * lsz[0], st));
     HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * lsz[1], st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tcount, sizeof(int32_t) * (kMaxDepth + 1), st));
+    for (int l = 2; l <= D && status == HIKF_OK; ++l) {
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tmap[l], sizeof(int32_t) * ((int64_t)1 << (2 * l)) * n, st));
+      ProfScope ps(ST_M2L, st);
+      status = m2l_targets(t, l, pl[l], n, tmap[l], tcount + l, st, xlo(l), xhi(l));
+    }
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(hcount, tcount, sizeof(hcount), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
     for (int l = 2; l <= D; ++l)
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch[l],
-                                      sizeof(double) * ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n, st));
+                                      sizeof(double) * std::max<int64_t>(1, (int64_t)hcount[l] * t->orders[l] *
+                                                                                t->orders[l]), st));
     HIKF_CHECK_CUDA(cudaEventRecord(ev_up, st));
     for (int l = D; l >= 2 && status == HIKF_OK; --l) {  // biggest level first
       cudaStream_t sl = qs->s[1 + (D - l) % 7];
       HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, ev_up, 0));
       const int q = t->orders[l] * t->orders[l];
       ProfScope ps(ST_M2L, sl);
-      HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * ((int64_t)1 << (2 * l)) * q * n, sl));
+      HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * (int64_t)hcount[l] * q, sl));
       for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
-        status = m2l_pass(t, l, slot, pl[l], n, scratch[l], sl, xlo(l), xhi(l));
+        status = m2l_pass(t, l, slot, pl[l], n, scratch[l], tmap[l], sl, xlo(l), xhi(l));
       HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
     }
   }
@@ -586,10 +599,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
     if (l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
       ProfScope ps(ST_L2L, st);
-      status = l2l_boxes(t, l, scratch[l], Lprev, n, Lcur, st, xlo(l - 1), xhi(l - 1));
+      status = l2l_boxes(t, l, scratch[l], tmap[l], Lprev, n, Lcur, st, xlo(l - 1), xhi(l - 1));
     } else {
       ProfScope ps(ST_L2L, st);
-      status = pair_to_box(t, l, scratch[l], n, Lcur, st);
+      status = pair_to_box(t, l, scratch[l], tmap[l], n, Lcur, st);
       if (status == HIKF_OK && l > 2) {
         L2LParentProv ll;
         set_base(ll, t, n, 0, 0, vec);
@@ -607,7 +620,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   if (status == HIKF_OK && fused_leaf) {
     ProfScope ps(ST_L2P, st);
-    status = leaf_down(t, scratch[D], Lprev, n, U, n, st, r0, r1, lw);
+    status = leaf_down(t, scratch[D], tmap[D], Lprev, n, U, n, st, r0, r1, lw);
   } else if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
     status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1, lw);
@@ -640,7 +653,11 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     status = sparse_p2p_scatter(t, sp, Pnear, U, n, st, r0, r1, lw);
   }
   for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
-  for (int l = 2; l <= D; ++l) cudaFreeAsync(scratch[l], st);
+  for (int l = 2; l <= D; ++l) {
+    cudaFreeAsync(scratch[l], st);
+    cudaFreeAsync(tmap[l], st);
+  }
+  cudaFreeAsync(tcount, st);
   cudaFreeAsync(Lbuf[0], st);
   cudaFreeAsync(Lbuf[1], st);
   cudaFreeAsync(Pnear, st);

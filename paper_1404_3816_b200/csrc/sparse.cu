@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
                                                         const double* __restrict__ Wc, int q, int64_t n, int64_t G,
                                                         int dx, int dy, const uint8_t* __restrict__ occ,
                                                         const double* __restrict__ M, double* __restrict__ L,
+                                                        const int32_t* __restrict__ tmap,
                                                         unsigned long long* __restrict__ flops, int64_t xlo,
                                                         int64_t xhi) {
   extern __shared__ double Ms[];
@@ -602,7 +603,7 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
           const int col = 2 * t4 + h;
           const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
           const int64_t j = (int64_t)__shfl_sync(0xffffffffu, myJ[c], col * 4);
-          if (T >= 0 && r < q) L[(T * n + j) * q + r] += acc0[c][h] + acc1[c][h];
+          if (T >= 0 && r < q) L[(int64_t)tmap[T * n + j] * q + r] += acc0[c][h] + acc1[c][h];
         }
     }
     return;
@@ -637,10 +638,11 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
         const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
         const int64_t j = (int64_t)__shfl_sync(0xffffffffu, myJ[c], col * 4);
         if (T < 0) continue;
+        const int64_t slot = tmap[T * n + j];
 #pragma unroll
         for (int i = 0; i < RT; ++i) {
           const int r = (r0 + i) * 8 + g;
-          if (r0 + i < nrt && r < q) L[(T * n + j) * q + r] += acc[i][c][h];
+          if (r0 + i < nrt && r < q) L[slot * q + r] += acc[i][c][h];
         }
       }
   }
@@ -650,14 +652,18 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
 // occupied boxes (CTA = box x 32-column chunk, smem-staged transpose).
 constexpr int kTrCols = 32;
 __global__ void __launch_bounds__(256) pair_to_box_kernel(const int32_t* __restrict__ occ, int q, int64_t n,
-                                                          const double* __restrict__ S, double* __restrict__ L) {
+                                                          const double* __restrict__ S,
+                                                          const int32_t* __restrict__ tmap, double* __restrict__ L) {
   extern __shared__ double tile[];  // kTrCols x (q + 1)
   const int64_t T = occ[blockIdx.x];
   const int64_t j0 = (int64_t)blockIdx.y * kTrCols;
   const int cw = (int)((n - j0) < kTrCols ? (n - j0) : kTrCols);
   const int qs = q + 1;
-  const double* src = S + (T * n + j0) * q;
-  for (int e = threadIdx.x; e < cw * q; e += blockDim.x) tile[(e / q) * qs + e % q] = src[e];
+  for (int e = threadIdx.x; e < cw * q; e += blockDim.x) {
+    const int jj = e / q, a = e % q;
+    const int32_t slot = tmap[T * n + j0 + jj];
+    tile[jj * qs + a] = slot >= 0 ? S[(int64_t)slot * q + a] : 0.0;
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < cw * q; e += blockDim.x) {
     int a = e / cw, jj = e % cw;
@@ -667,7 +673,8 @@ __global__ void __launch_bounds__(256) pair_to_box_kernel(const int32_t* __restr
 
 }  // namespace
 
-int pair_to_box(const hikf_tree* t, int l, const double* S, int64_t n, double* L, cudaStream_t st) {
+int pair_to_box(const hikf_tree* t, int l, const double* S, const int32_t* tmap, int64_t n, double* L,
+                cudaStream_t st) {
   if (t->n_occ[l] == 0 || n == 0) return HIKF_OK;
   const int q = t->orders[l] * t->orders[l];
   const size_t smem = sizeof(double) * kTrCols * (q + 1);
@@ -678,7 +685,7 @@ int pair_to_box(const hikf_tree* t, int l, const double* S, int64_t n, double* L
     configured = std::max<size_t>(smem, 48 << 10);
   }
   dim3 grid((unsigned)t->n_occ[l], (unsigned)((n + kTrCols - 1) / kTrCols));
-  pair_to_box_kernel<<<grid, 256, smem, st>>>(t->occ[l], q, n, S, L);
+  pair_to_box_kernel<<<grid, 256, smem, st>>>(t->occ[l], q, n, S, tmap, L);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
@@ -754,8 +761,70 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
   return HIKF_OK;
 }
 
-int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, cudaStream_t st,
-             int64_t xlo, int64_t xhi) {
+namespace {
+
+// flags[T * n + j] = 1 for every target of an active source pair (any of the 40 offsets)
+__global__ void m2l_mark_targets(int64_t np, const int64_t* __restrict__ key, int64_t n, int64_t G,
+                                 const uint8_t* __restrict__ occ, M2LOffsets offs, int64_t xlo, int64_t xhi,
+                                 uint8_t* __restrict__ flags) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < np * 40; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = e / 40;
+    const int d = (int)(e % 40);
+    const int64_t S = key[p] / n, j = key[p] % n;
+    const int dx = offs.dx[d], dy = offs.dy[d];
+    const int64_t tx = S / G - dx, ty = S % G - dy;
+    int64_t s2;
+    if (tx >= xlo && tx <= xhi && tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) &&
+        s2 == S && occ[tx * G + ty])
+      flags[(tx * G + ty) * n + j] = 1;
+  }
+}
+
+__global__ void m2l_slots(const int64_t* __restrict__ keys, const int32_t* __restrict__ count,
+                          int32_t* __restrict__ tmap) {
+  const int64_t c = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c; i += (int64_t)gridDim.x * blockDim.x)
+    tmap[keys[i]] = (int32_t)i;
+}
+
+}  // namespace
+
+int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
+                cudaStream_t st, int64_t xlo, int64_t xhi) {
+  const int64_t G = (int64_t)1 << l;
+  const int64_t total = G * G * n;
+  HIKF_CHECK_CUDA(cudaMemsetAsync(tmap, 0xff, sizeof(int32_t) * total, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(count_dev, 0, sizeof(int32_t), st));
+  if (src.np == 0 || total == 0) return HIKF_OK;
+  if (total > INT32_MAX) {
+    set_error("M2L target map of level %d too large (%lld entries)", l, (long long)total);
+    return HIKF_BAD_ARGUMENT;
+  }
+  uint8_t* flags = nullptr;
+  int64_t* keys = nullptr;
+  HIKF_TRY(aalloc(&flags, total, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(flags, 0, total, st));
+  M2LOffsets offs;
+  m2l_mark_targets<<<grid_cap(src.np * 40), kT, 0, st>>>(src.np, src.key, n, G, t->occ_flag[l], offs, xlo, xhi, flags);
+  HIKF_CHECK_LAUNCH();
+  const int64_t cap = std::min<int64_t>(total, src.np * 40);
+  HIKF_TRY(aalloc(&keys, cap, st));
+  size_t tb = 0;
+  cub::CountingInputIterator<int64_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tb, it, flags, keys, count_dev, (int)total, st);
+  void* tmp = nullptr;
+  HIKF_CHECK_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), st));
+  cub::DeviceSelect::Flagged(tmp, tb, it, flags, keys, count_dev, (int)total, st);
+  m2l_slots<<<grid_cap(cap), kT, 0, st>>>(keys, count_dev, tmap);
+  HIKF_CHECK_LAUNCH();
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(keys, st);
+  cudaFreeAsync(flags, st);
+  return HIKF_OK;
+}
+
+int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, const int32_t* tmap,
+             cudaStream_t st, int64_t xlo, int64_t xhi) {
   if (src.np == 0 || !((t->m2l_present[l] >> slot) & 1)) return HIKF_OK;
   M2LOffsets offs;
   const int q = t->orders[l] * t->orders[l];
@@ -769,7 +838,7 @@ int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t 
 #define HIKF_M2L_CASE(QQ, K4, RT)                                                                               \
   case QQ:                                                                                                     \
     m2l_pairs_kernel<true, K4, RT><<<blocks, kT, smem, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],   \
-                                                             offs.dy[slot], t->occ_flag[l], M, L, fl, xlo, xhi);\
+                                                             offs.dy[slot], t->occ_flag[l], M, L, tmap, fl, xlo, xhi);\
     break;
   switch (q) {
     HIKF_M2L_CASE(4, 1, 1)
@@ -781,7 +850,8 @@ int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t 
     HIKF_M2L_CASE(64, 16, 8)
     default:
       m2l_pairs_kernel<false, 1, 1><<<blocks, kT, 0, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],
-                                                            offs.dy[slot], t->occ_flag[l], M, L, fl, xlo, xhi);
+                                                            offs.dy[slot], t->occ_flag[l], M, L, tmap, fl, xlo,
+                                                            xhi);
   }
 #undef HIKF_M2L_CASE
   HIKF_CHECK_LAUNCH();

@@ -52,12 +52,20 @@ int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream
 // parent multipoles from the children's active pairs (sparse M2M), level l from l+1
 int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st);
 void pairs_free(PairLevel* p, cudaStream_t st);
+// Compact M2L targets of level l: the (box, ray) pairs that receive at least one
+// M2L term (an admissible, occupied T = S - d of an active source pair (S, j),
+// inside the box-column range [xlo, xhi]).  tmap (G_l^2 x n int32) maps T * n + j
+// to its slot in the compact scratch (q coefficients per slot) or -1; *count_dev
+// receives the number of slots.  Replaces a dense G_l^2 x n x q scratch that is
+// mostly zeros (cfg4 leaf level: 4.8 GB dense, ~0.3 GB compact).
+int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
+                cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
 // L_l[T][:, j] += M_d W_{T+d}[:, j] for every active source pair and one offset slot
-// S must be the pair-major scratch S[T][j][a] (zeroed before the 40 offsets)
 // (targets outside the box-column range [xlo, xhi] of level l are skipped)
-int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, cudaStream_t st,
-             int64_t xlo = 0, int64_t xhi = INT64_MAX);
-// L[T][a][j] = S[T][j][a] for the occupied boxes of level l
-int pair_to_box(const hikf_tree* t, int l, const double* S, int64_t n, double* L, cudaStream_t st);
+int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, const int32_t* tmap,
+             cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
+// L[T][a][j] = S[tmap[T n + j]][a] (0 without a slot) for the occupied boxes of level l
+int pair_to_box(const hikf_tree* t, int l, const double* S, const int32_t* tmap, int64_t n, double* L,
+                cudaStream_t st);
 
 }  // namespace hikf

@@ -13,9 +13,22 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 import paper_1404_3816_b200 as P  # noqa: E402
 
-cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "cfg4"]
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+cfg = bench.CONFIGS[args[0] if args else "cfg4"]
 torch.zeros(1, device="cuda")
 torch.cuda.synchronize()
+if "--preload-small" in sys.argv:  # every kernel loaded by a tiny run first: isolates the memory growth
+    g1 = P.Grid2D(32, 32, 1 / 32, 1 / 32)
+    H1 = P.tomography.build_ray_operator(g1, P.tomography.default_acquisition(g1, 4, 4, 0.0, 1.0))
+
+    class M1:
+        pass
+    m1 = M1()
+    m1.H, m1.m = H1, g1.m
+    t1 = P.build_tree(g1.cell_centers(), P.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"]),
+                      P.FmmConfig(n_cheb=cfg["order"], max_leaf_points=16))
+    P.filters.hikf_precompute_fmm(m1, t1)
+    torch.cuda.synchronize()
 N = cfg["N"]
 grid = P.Grid2D(N, N, 1.0 / N, 1.0 / N)
 t0 = time.perf_counter()

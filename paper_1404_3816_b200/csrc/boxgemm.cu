@@ -354,38 +354,45 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
   const int64_t ncb = (n + 7) / 8;
   const double* Lpar = g.Lp + P * qp * n;
   const int32_t* tm = g.tmap + box * n;
-  // this lane's output rows (leaf points 8 i + gq) in U, or -1 outside the row window
-  int32_t orow[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int pnt = i * 8 + gq;
+  // output row in U of each leaf point (or -1 outside the row window), shared by the warps
+  __shared__ int32_t orow[64];
+  if (tid < 64) {
     int32_t r = -1;
-    if (pnt < cnt) {
+    if (tid < cnt) {
       if (g.s0 >= 0) {
-        r = (int32_t)(ls + pnt - g.s0);
+        r = (int32_t)(ls + tid - g.s0);
       } else {
-        const int64_t o = g.order[ls + pnt];
+        const int64_t o = g.order[ls + tid];
         if (o >= g.r0 && o < g.r1) r = (int32_t)(o - g.r0);
       }
     }
-    orow[i] = r;
+    orow[tid] = r;
   }
-  auto load_b1 = [&](int64_t u, double (&b1)[NK1]) {
+  __syncthreads();
+  // the next unit's parent columns and M2L slot indices are loaded one unit ahead
+  auto load_next = [&](int64_t u, double (&b1)[NK1], int32_t (&sl)[2]) {
     const int64_t jb = u * 8 + gq;
 #pragma unroll
     for (int k4 = 0; k4 < NK1; ++k4) {
       const int k = k4 * 4 + t4;
       b1[k4] = (k < qp && jb < n) ? Lpar[(int64_t)k * n + jb] : 0.0;
     }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t jc = u * 8 + 2 * t4 + h;
+      sl[h] = jc < n ? tm[jc] : -1;
+    }
   };
   unsigned long long useful1 = 0, useful2 = 0;
   double nb1[NK1];
-  if (warp < ncb) load_b1(warp, nb1);
+  int32_t nslot[2];
+  if (warp < ncb) load_next(warp, nb1, nslot);
   for (int64_t u = warp; u < ncb; u += BW_THREADS / 32) {
     double b1[NK1];
+    int32_t slot[2] = {nslot[0], nslot[1]};
 #pragma unroll
     for (int k4 = 0; k4 < NK1; ++k4) b1[k4] = nb1[k4];
-    if (u + BW_THREADS / 32 < ncb) load_b1(u + BW_THREADS / 32, nb1);  // next unit's parent columns in flight
+    if (u + BW_THREADS / 32 < ncb) load_next(u + BW_THREADS / 32, nb1, nslot);
     const int64_t j0 = u * 8;
     const int cols = (int)(n - j0 < 8 ? n - j0 : 8);
     if (lane == 0) {
@@ -394,12 +401,6 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
     }
     // the M2L sums of this unit (loaded ahead of the DMMA chain, added after it)
     double init[NRT1][2];
-    int32_t slot[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t jc = j0 + 2 * t4 + h;
-      slot[h] = jc < n ? tm[jc] : -1;
-    }
 #pragma unroll
     for (int i = 0; i < NRT1; ++i) {
       const int r = i * 8 + gq;
@@ -421,10 +422,9 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
 #pragma unroll
     for (int i = 0; i < NRT1; ++i) {
       const int r = i * 8 + gq;
-      if (r < KR2) {
-        lw[r * 8 + 2 * t4] = acc1[i][0] + init[i][0];
-        lw[r * 8 + 2 * t4 + 1] = acc1[i][1] + init[i][1];
-      }
+      if (r < KR2)  // 16-byte stores: the warp's 32 chunks cover 4 wavefronts, conflict-free
+        *reinterpret_cast<double2*>(lw + r * 8 + 2 * t4) =
+            make_double2(acc1[i][0] + init[i][0], acc1[i][1] + init[i][1]);
     }
     __syncwarp();
     // L2P: U = W2 l
@@ -447,8 +447,9 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
     const int64_t jc = j0 + 2 * t4;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if (orow[i] < 0) continue;
-      double* o = g.U + (int64_t)orow[i] * g.ldu;
+      const int32_t orw = orow[i * 8 + gq];
+      if (orw < 0) continue;
+      double* o = g.U + (int64_t)orw * g.ldu;
       if (jc + 1 < n && (((uintptr_t)(o + jc)) & 15) == 0) {
         *reinterpret_cast<double2*>(o + jc) = make_double2(acc2[i][0], acc2[i][1]);
       } else {

@@ -551,7 +551,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   double* scratch[kMaxDepth + 1] = {};
   int32_t* tmap[kMaxDepth + 1] = {};
   int32_t* tcount = nullptr;
-  int32_t hcount[kMaxDepth + 1] = {0};
+  int32_t hcount[2 * (kMaxDepth + 1)] = {0};  // [2 l]: target slots, [2 l + 1]: entries of level l
+  int64_t* toff = nullptr;
+  int64_t hoff[kMaxDepth + 1][41] = {};
+  M2LPlan plan[kMaxDepth + 1];
   double* Lbuf[2] = {nullptr, nullptr};
   // fused leaf step (leaf_down): the leaf-level locals are never stored
   const bool fused_leaf = leaf_fused_enabled() && leaf_down_supported(t);
@@ -561,17 +564,21 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   if (status == HIKF_OK) {
     HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * lsz[0], st));
     HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * lsz[1], st));
-    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tcount, sizeof(int32_t) * (kMaxDepth + 1), st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tcount, sizeof(hcount), st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&toff, sizeof(hoff), st));
     for (int l = 2; l <= D && status == HIKF_OK; ++l) {
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tmap[l], sizeof(int32_t) * ((int64_t)1 << (2 * l)) * n, st));
       ProfScope ps(ST_M2L, st);
-      status = m2l_targets(t, l, pl[l], n, tmap[l], tcount + l, st, xlo(l), xhi(l));
+      status = m2l_targets(t, l, pl[l], n, tmap[l], tcount + 2 * l, &plan[l], st, xlo(l), xhi(l));
+      if (status == HIKF_OK)
+        HIKF_CHECK_CUDA(cudaMemcpyAsync(toff + 41 * l, plan[l].off, 41 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
     }
     HIKF_CHECK_CUDA(cudaMemcpyAsync(hcount, tcount, sizeof(hcount), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(hoff, toff, sizeof(hoff), cudaMemcpyDeviceToHost, st));
     HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
     for (int l = 2; l <= D; ++l)
       HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch[l],
-                                      sizeof(double) * std::max<int64_t>(1, (int64_t)hcount[l] * t->orders[l] *
+                                      sizeof(double) * std::max<int64_t>(1, (int64_t)hcount[2 * l] * t->orders[l] *
                                                                                 t->orders[l]), st));
     HIKF_CHECK_CUDA(cudaEventRecord(ev_up, st));
     for (int l = D; l >= 2 && status == HIKF_OK; --l) {  // biggest level first
@@ -579,9 +586,11 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, ev_up, 0));
       const int q = t->orders[l] * t->orders[l];
       ProfScope ps(ST_M2L, sl);
-      HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * (int64_t)hcount[l] * q, sl));
+      HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * (int64_t)hcount[2 * l] * q, sl));
+      const bool lists = m2l_list_supported(t, l);
       for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
-        status = m2l_pass(t, l, slot, pl[l], n, scratch[l], tmap[l], sl, xlo(l), xhi(l));
+        status = lists ? m2l_pass_list(t, l, slot, pl[l], plan[l], hoff[l], scratch[l], sl)
+                       : m2l_pass(t, l, slot, pl[l], n, scratch[l], tmap[l], sl, xlo(l), xhi(l));
       HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
     }
   }
@@ -656,8 +665,10 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   for (int l = 2; l <= D; ++l) {
     cudaFreeAsync(scratch[l], st);
     cudaFreeAsync(tmap[l], st);
+    m2l_plan_free(&plan[l], st);
   }
   cudaFreeAsync(tcount, st);
+  cudaFreeAsync(toff, st);
   cudaFreeAsync(Lbuf[0], st);
   cudaFreeAsync(Lbuf[1], st);
   cudaFreeAsync(Pnear, st);

@@ -648,6 +648,56 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
   }
 }
 
+// One M2L offset over its (source pair, target slot) entries (m2l_targets): a warp
+// takes 8 entries as the 8 columns of its DMMA tiles (every column useful), forms
+// M_d W_p with two accumulator chains (even / odd k-steps) and adds their sum into
+// the compact scratch at the target's slot -- race-free, since a target receives at
+// most one source per offset; the offsets run in the reference's order.
+template <int NK4, int NRT>
+__global__ void __launch_bounds__(256, (NK4 <= 13) ? 2 : 1) m2l_list_kernel(int64_t e0, int64_t ne,
+                                                                         const int2* __restrict__ ent,
+                                                                         const double* __restrict__ W, int q,
+                                                                         const double* __restrict__ M,
+                                                                         double* __restrict__ L,
+                                                                         unsigned long long* __restrict__ flops) {
+  extern __shared__ double Ms[];
+  const int ld = m2l_ld(q);
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = M[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int64_t i0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 8;
+  if (i0 >= ne) return;
+  const int64_t mine = i0 + g;
+  int2 pe = make_int2(-1, -1);
+  if (mine < ne) pe = ent[e0 + mine];
+  if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)(ne - i0 < 8 ? ne - i0 : 8) * q * q);
+  double b[NK4];
+#pragma unroll
+  for (int k4 = 0; k4 < NK4; ++k4) {
+    const int k = k4 * 4 + t4;
+    b[k4] = (pe.x >= 0 && k < q) ? W[(int64_t)pe.x * q + k] : 0.0;
+  }
+  int slot[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) slot[h] = __shfl_sync(0xffffffffu, pe.y, (2 * t4 + h) * 4);
+  for (int i = 0; i < NRT; ++i) {
+    const int r = i * 8 + g;
+    double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k4 = 0; k4 < NK4; ++k4) {
+      const int k = k4 * 4 + t4;
+      const double a = (r < q && k < q) ? Ms[r * ld + k] : 0.0;
+      if (k4 & 1)
+        dmma884(acc1[0], acc1[1], a, b[k4]);
+      else
+        dmma884(acc0[0], acc0[1], a, b[k4]);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (slot[h] >= 0 && r < q) L[(int64_t)slot[h] * q + r] += acc0[h] + acc1[h];
+  }
+}
+
 // Pair-major M2L scratch S[T][j][a] -> box-major locals L[T][a][j] for the
 // occupied boxes (CTA = box x 32-column chunk, smem-staged transpose).
 constexpr int kTrCols = 32;
@@ -764,20 +814,60 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
 namespace {
 
 // flags[T * n + j] = 1 for every target of an active source pair (any of the 40 offsets)
+// target (T * n + j) of source pair p at offset slot d, or -1 when the offset is not
+// admissible for it (parent adjacency, bounds), T is empty, or outside [xlo, xhi]
+__device__ __forceinline__ int64_t m2l_target_of(const int64_t* __restrict__ key, int64_t p, int d, int64_t n,
+                                                 int64_t G, const uint8_t* __restrict__ occ, const M2LOffsets& offs,
+                                                 int64_t xlo, int64_t xhi) {
+  const int64_t S = key[p] / n, j = key[p] % n;
+  const int dx = offs.dx[d], dy = offs.dy[d];
+  const int64_t tx = S / G - dx, ty = S % G - dy;
+  int64_t s2;
+  if (tx >= xlo && tx <= xhi && tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) &&
+      s2 == S && occ[tx * G + ty])
+    return (tx * G + ty) * n + j;
+  return -1;
+}
+
+// flags[T * n + j] = 1 for every target of an active source pair; eflag[d * np + p] = 1
+// for every (offset, source pair) that has a target (offset-major)
 __global__ void m2l_mark_targets(int64_t np, const int64_t* __restrict__ key, int64_t n, int64_t G,
                                  const uint8_t* __restrict__ occ, M2LOffsets offs, int64_t xlo, int64_t xhi,
-                                 uint8_t* __restrict__ flags) {
+                                 uint8_t* __restrict__ flags, uint8_t* __restrict__ eflag) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < np * 40; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = e / 40;
-    const int d = (int)(e % 40);
-    const int64_t S = key[p] / n, j = key[p] % n;
-    const int dx = offs.dx[d], dy = offs.dy[d];
-    const int64_t tx = S / G - dx, ty = S % G - dy;
-    int64_t s2;
-    if (tx >= xlo && tx <= xhi && tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) &&
-        s2 == S && occ[tx * G + ty])
-      flags[(tx * G + ty) * n + j] = 1;
+    const int d = (int)(e / np);
+    const int64_t p = e % np;
+    const int64_t tk = m2l_target_of(key, p, d, n, G, occ, offs, xlo, xhi);
+    if (tk >= 0) flags[tk] = 1;
+    eflag[e] = tk >= 0 ? 1 : 0;
   }
+}
+
+// entries (source pair, target slot) of the selected (offset, pair) codes, and the
+// first entry of every offset (codes are offset-major and ascending)
+__global__ void m2l_entries(const int64_t* __restrict__ codes, const int32_t* __restrict__ count, int64_t np,
+                            const int64_t* __restrict__ key, int64_t n, int64_t G, const uint8_t* __restrict__ occ,
+                            M2LOffsets offs, int64_t xlo, int64_t xhi, const int32_t* __restrict__ tmap,
+                            int2* __restrict__ ent) {
+  const int64_t c = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < c; i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int)(codes[i] / np);
+    const int64_t p = codes[i] % np;
+    const int64_t tk = m2l_target_of(key, p, d, n, G, occ, offs, xlo, xhi);
+    ent[i] = make_int2((int)p, tmap[tk]);
+  }
+}
+
+__global__ void m2l_offset_starts(const int64_t* __restrict__ codes, const int32_t* __restrict__ count, int64_t np,
+                                  int64_t* __restrict__ off) {
+  const int d = threadIdx.x;
+  if (d > 40) return;
+  int64_t lo = 0, hi = *count;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (codes[mid] < (int64_t)d * np) lo = mid + 1; else hi = mid;
+  }
+  off[d] = lo;
 }
 
 __global__ void m2l_slots(const int64_t* __restrict__ keys, const int32_t* __restrict__ count,
@@ -790,37 +880,97 @@ __global__ void m2l_slots(const int64_t* __restrict__ keys, const int32_t* __res
 }  // namespace
 
 int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
-                cudaStream_t st, int64_t xlo, int64_t xhi) {
+                M2LPlan* plan, cudaStream_t st, int64_t xlo, int64_t xhi) {
   const int64_t G = (int64_t)1 << l;
   const int64_t total = G * G * n;
+  *plan = M2LPlan();
   HIKF_CHECK_CUDA(cudaMemsetAsync(tmap, 0xff, sizeof(int32_t) * total, st));
-  HIKF_CHECK_CUDA(cudaMemsetAsync(count_dev, 0, sizeof(int32_t), st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(count_dev, 0, 2 * sizeof(int32_t), st));
+  HIKF_TRY(aalloc(&plan->off, 41, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(plan->off, 0, 41 * sizeof(int64_t), st));
   if (src.np == 0 || total == 0) return HIKF_OK;
-  if (total > INT32_MAX) {
+  if (total > INT32_MAX || src.np * 40 > INT32_MAX) {
     set_error("M2L target map of level %d too large (%lld entries)", l, (long long)total);
     return HIKF_BAD_ARGUMENT;
   }
-  uint8_t* flags = nullptr;
-  int64_t* keys = nullptr;
+  uint8_t *flags = nullptr, *eflag = nullptr;
+  int64_t *keys = nullptr, *codes = nullptr;
   HIKF_TRY(aalloc(&flags, total, st));
+  HIKF_TRY(aalloc(&eflag, src.np * 40, st));
   HIKF_CHECK_CUDA(cudaMemsetAsync(flags, 0, total, st));
   M2LOffsets offs;
-  m2l_mark_targets<<<grid_cap(src.np * 40), kT, 0, st>>>(src.np, src.key, n, G, t->occ_flag[l], offs, xlo, xhi, flags);
+  m2l_mark_targets<<<grid_cap(src.np * 40), kT, 0, st>>>(src.np, src.key, n, G, t->occ_flag[l], offs, xlo, xhi, flags,
+                                                         eflag);
   HIKF_CHECK_LAUNCH();
+  // target slots (ascending T * n + j)
   const int64_t cap = std::min<int64_t>(total, src.np * 40);
   HIKF_TRY(aalloc(&keys, cap, st));
-  size_t tb = 0;
+  HIKF_TRY(aalloc(&codes, src.np * 40, st));
+  size_t tb = 0, tb2 = 0;
   cub::CountingInputIterator<int64_t> it(0);
   cub::DeviceSelect::Flagged(nullptr, tb, it, flags, keys, count_dev, (int)total, st);
+  cub::DeviceSelect::Flagged(nullptr, tb2, it, eflag, codes, count_dev + 1, (int)(src.np * 40), st);
   void* tmp = nullptr;
-  HIKF_CHECK_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tb, 1), st));
+  HIKF_CHECK_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(std::max(tb, tb2), 1), st));
   cub::DeviceSelect::Flagged(tmp, tb, it, flags, keys, count_dev, (int)total, st);
   m2l_slots<<<grid_cap(cap), kT, 0, st>>>(keys, count_dev, tmap);
   HIKF_CHECK_LAUNCH();
+  // the (source pair, target slot) entries of every offset, offset-major
+  cub::DeviceSelect::Flagged(tmp, tb2, it, eflag, codes, count_dev + 1, (int)(src.np * 40), st);
+  HIKF_TRY(aalloc(&plan->ent, src.np * 40, st));
+  m2l_entries<<<grid_cap(src.np * 40), kT, 0, st>>>(codes, count_dev + 1, src.np, src.key, n, G, t->occ_flag[l], offs,
+                                                    xlo, xhi, tmap, plan->ent);
+  HIKF_CHECK_LAUNCH();
+  m2l_offset_starts<<<1, 64, 0, st>>>(codes, count_dev + 1, src.np, plan->off);
+  HIKF_CHECK_LAUNCH();
   cudaFreeAsync(tmp, st);
   cudaFreeAsync(keys, st);
+  cudaFreeAsync(codes, st);
+  cudaFreeAsync(eflag, st);
   cudaFreeAsync(flags, st);
   return HIKF_OK;
+}
+
+void m2l_plan_free(M2LPlan* plan, cudaStream_t st) {
+  cudaFreeAsync(plan->ent, st);
+  cudaFreeAsync(plan->off, st);
+  *plan = M2LPlan();
+}
+
+int m2l_pass_list(const hikf_tree* t, int l, int slot, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,
+                  double* L, cudaStream_t st) {
+  const int64_t e0 = hoff[slot], ne = hoff[slot + 1] - hoff[slot];
+  if (ne <= 0) return HIKF_OK;
+  const int q = t->orders[l] * t->orders[l];
+  const int64_t warps = (ne + 7) / 8;
+  const unsigned blocks = (unsigned)((warps * 32 + kT - 1) / kT);
+  const size_t smem = sizeof(double) * q * m2l_ld(q);
+  const double* M = t->m2l[l] + (int64_t)slot * q * q;
+  unsigned long long* fl = prof_flops_ptr(ST_M2L);
+#define HIKF_M2LL(QQ, K4, RT)                                                                                   \
+  case QQ:                                                                                                     \
+    m2l_list_kernel<K4, RT><<<blocks, kT, smem, st>>>(e0, ne, plan.ent, src.W, q, M, L, fl);                   \
+    break;
+  switch (q) {
+    HIKF_M2LL(4, 1, 1)
+    HIKF_M2LL(9, 3, 2)
+    HIKF_M2LL(16, 4, 2)
+    HIKF_M2LL(25, 7, 4)
+    HIKF_M2LL(36, 9, 5)
+    HIKF_M2LL(49, 13, 7)
+    HIKF_M2LL(64, 16, 8)
+    default:
+      set_error("M2L entry lists: q = %d not instantiated", q);
+      return HIKF_BAD_ARGUMENT;
+  }
+#undef HIKF_M2LL
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+bool m2l_list_supported(const hikf_tree* t, int l) {
+  const int q = t->orders[l] * t->orders[l];
+  return q == 4 || q == 9 || q == 16 || q == 25 || q == 36 || q == 49 || q == 64;
 }
 
 int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, const int32_t* tmap,

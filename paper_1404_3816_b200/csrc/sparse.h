@@ -58,8 +58,20 @@ void pairs_free(PairLevel* p, cudaStream_t st);
 // to its slot in the compact scratch (q coefficients per slot) or -1; *count_dev
 // receives the number of slots.  Replaces a dense G_l^2 x n x q scratch that is
 // mostly zeros (cfg4 leaf level: 4.8 GB dense, ~0.3 GB compact).
+// The per-offset work lists of the level: ent = (source pair, target slot) of every
+// admissible (offset, pair), offset-major; off[d] .. off[d+1] = offset d's entries.
+struct M2LPlan {
+  int2* ent = nullptr;
+  int64_t* off = nullptr;  // 41 (device)
+};
+// count_dev[0] = target slots, count_dev[1] = entries (2 ints)
 int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
-                cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
+                M2LPlan* plan, cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
+void m2l_plan_free(M2LPlan* plan, cudaStream_t st);
+// one offset over its entry list (hoff: host copy of plan.off); S as m2l_pass
+bool m2l_list_supported(const hikf_tree* t, int l);
+int m2l_pass_list(const hikf_tree* t, int l, int slot, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,
+                  double* S, cudaStream_t st);
 // L_l[T][:, j] += M_d W_{T+d}[:, j] for every active source pair and one offset slot
 // (targets outside the box-column range [xlo, xhi] of level l are skipped)
 int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, const int32_t* tmap,

@@ -195,6 +195,12 @@ int hikf_update(int64_t m, int64_t n, const double* mean_dev, const double* C_de
  *          with the same C_Q and workspace -- use the C' that call produced and
  *          skip the C + C_Q pass.  Pointers, sizes and success of the previous
  *          call are checked; any mismatch falls back to the full predict.
+ *   bit 2 (deferred status): the call does not synchronise; min_var_out must be
+ *          pinned host memory of 4 doubles that receives, on the stream,
+ *          [Cholesky pivot (0 = ok), negative-variance flag, min posterior var,
+ *          max prior var].  The caller synchronises the stream (or an event
+ *          recorded after the call) before reading it and raises HIKF_NOT_PD /
+ *          HIKF_NEGATIVE_VARIANCE itself; a failed step's outputs are undefined.
  * Setting bit 1 while C_out was modified in between gives wrong results.
  * mean_host (optional, pinned host memory, m doubles): mean_out is also
  * copied there, inside the call (the read-back overlaps the update's tail). */

@@ -592,9 +592,16 @@ int hikf_update_chained(int64_t m, int64_t n, const double* mean, const double* 
   a.chain = (chain & 1) != 0;
   a.chain_in = (chain & 2) != 0;
   a.mean_host = mean_host;
+  if (chain & 4) {  // deferred: min_var_out = pinned host status[4], filled on the stream
+    if (!min_var_out) {
+      set_error("deferred update (chain bit 2) needs a pinned host status[4] in min_var_out");
+      return HIKF_BAD_ARGUMENT;
+    }
+    a.status_host = min_var_out;
+  }
   UpdateResult res;
   int s = update(a, as_stream(stream), &res);
-  if (min_var_out) *min_var_out = res.min_var;
+  if (min_var_out && !(chain & 4)) *min_var_out = res.min_var;
   return s;
 }
 

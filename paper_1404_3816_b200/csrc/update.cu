@@ -278,6 +278,14 @@ __global__ void pack_status(const double* __restrict__ minv, const int* __restri
   out[2] = (double)status[0];
 }
 
+// deferred host status: [pivot, negative-variance flag, min var, max prior var]
+__global__ void pack_status4(const double* __restrict__ minv, const int* __restrict__ status, double* __restrict__ out) {
+  out[0] = (double)status[0];
+  out[1] = (double)status[1];
+  out[2] = minv[0];
+  out[3] = minv[1];
+}
+
 size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // library-owned side stream + fork/join events for the n x n work of the update
@@ -507,7 +515,7 @@ static size_t update_layout(int64_t m, int64_t n, char* base, UpdWs* ws) {
   w.pdot = (double*)take(8 * m * nt);
   w.bmin = (double*)take(8 * (size_t)nb);
   w.bmax = (double*)take(8 * (size_t)nb);
-  w.minv = (double*)take(16);
+  w.minv = (double*)take(48);  // [min var, max prior var] + the packed deferred status (4)
   w.status = (int*)take(16);
   if (ws) *ws = w;
   return off;
@@ -1161,6 +1169,10 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
   if (a.mm_dev) {  // deferred: the caller all-reduces and checks the packed status
     pack_status<<<1, 1, 0, st>>>(w.minv, w.status, a.mm_dev);
     HIKF_CHECK_LAUNCH();
+  } else if (a.status_host) {  // deferred: the caller reads the pinned status after the stream
+    pack_status4<<<1, 1, 0, st>>>(w.minv, w.status, w.minv + 2);
+    HIKF_CHECK_LAUNCH();
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(a.status_host, w.minv + 2, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
   } else {
     int hs[2] = {0, 0};
     double mm[2] = {0.0, 0.0};
@@ -1309,6 +1321,10 @@ int update(const UpdateArgs& a, cudaStream_t st, UpdateResult* res) {
   if (a.mm_dev) {
     pack_status<<<1, 1, 0, st>>>(w.minv, w.status, a.mm_dev);
     HIKF_CHECK_LAUNCH();
+  } else if (a.status_host) {
+    pack_status4<<<1, 1, 0, st>>>(w.minv, w.status, w.minv + 2);
+    HIKF_CHECK_LAUNCH();
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(a.status_host, w.minv + 2, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
   } else {
     int hs[2] = {0, 0};
     double mm[2] = {0.0, 0.0};

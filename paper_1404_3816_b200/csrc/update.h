@@ -21,6 +21,9 @@ struct UpdateArgs {
   // deferred status (row-sharded state): [min posterior var, max prior var, pivot] written to this
   // device array on the stream; the call neither synchronises nor checks (the caller all-reduces it)
   double* mm_dev = nullptr;
+  // deferred host status (hikf_update_chained bit 2): [pivot, negative-variance flag, min var,
+  // max prior var] copied into this pinned host array on the stream; the call does not synchronise
+  double* status_host = nullptr;
   // chained predict: the caller will pass this call's C_out (untouched) with the same C_Q to the
   // next call; the GEMM epilogue then also writes that call's C' = C_out + C_Q into the workspace
   bool chain = false;     // produce the next call's C'

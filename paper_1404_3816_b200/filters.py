@@ -14,6 +14,7 @@ libhikf_b200.so, and reading a field of it materialises the predict.
 
 from __future__ import annotations
 
+import os
 import weakref
 
 import numpy as np
@@ -184,6 +185,7 @@ class HikfState:
         self.cross_cov_t, self.variance_t, self.HC_t = C, v, HC
 
     def _np(self, name):
+        resolve_pending()  # host data of a deferred step: its status is checked first (may raise)
         if name not in self._host:
             if name != "mean":
                 self._materialize()
@@ -377,6 +379,33 @@ def _workspace(m: int, n: int) -> torch.Tensor:
     return ws
 
 
+# Deferred status of the explicit update (hikf_update_chained bit 2): a step's
+# Cholesky pivot and negative-variance check land in pinned host memory on the
+# stream instead of a per-call synchronisation, so the host enqueues step t + 1
+# while the GPU runs step t.  Each update resolves every earlier step (one step in
+# flight); reading any state's host data resolves all of them.  A failed step
+# raises the reference's exception (filters.py:149-153, linalg.py:30-33) from the
+# next update call or from the first data access -- before any data computed
+# from it is exposed.  HIKF_SYNC_STATUS=1 restores the per-call check.
+_PENDING: list = []
+_DEFERRED = os.environ.get("HIKF_SYNC_STATUS", "0") != "1"
+
+
+def resolve_pending(keep_last: bool = False):
+    """Check the deferred statuses of finished steps (all, or all but the newest)."""
+    while len(_PENDING) > (1 if keep_last else 0):
+        status, event = _PENDING.pop(0)
+        event.synchronize()
+        pivot, negvar, min_var = int(status[0]), bool(status[1]), float(status[2])
+        if pivot:
+            _PENDING.clear()
+            raise _lib.DecompositionError(
+                f"Cholesky factorization failed: {pivot}-th leading minor of the array is not positive definite")
+        if negvar:
+            _PENDING.clear()
+            raise NumericalConsistencyError(f"posterior variance went negative beyond tolerance (min {min_var:.3e})")
+
+
 def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
     """Kalman update of (mean, C, var, HC) against z (filters.py:138-157)."""
     Hd = DeviceCSR.of(H)
@@ -414,16 +443,25 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
     # the host copy of the posterior mean (what run_hikf reads every step) is
     # filled inside the call into pinned memory owned by the new state
     mean_host = torch.empty((m,), dtype=torch.float64, pin_memory=True)
+    status = None
+    if _DEFERRED:
+        chain |= 4
+        status = torch.empty((4,), dtype=torch.float64, pin_memory=True)
     _lib.check(_lib.load().hikf_update_chained(
         m, n, state.mean_t.data_ptr(), src.cross_cov_t.data_ptr(), src.variance_t.data_ptr(), src.HC_t.data_ptr(),
         _lib.ptr(pre.C_Q_t) if fused else None, _lib.ptr(pre.diag_Q_t) if fused else None,
         _lib.ptr(pre.HC_Q_t) if fused else None,
         Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), float(r_variance), zt.data_ptr(),
-        mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(), None, chain,
-        mean_host.data_ptr(), _lib.stream_ptr()))
+        mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(),
+        _lib.ptr(status) if status is not None else None, chain, mean_host.data_ptr(), _lib.stream_ptr()))
     out = HikfState(mean, C, var, HC)
     out._pinned = mean_host
     out._host["mean"] = mean_host.numpy()
+    if status is not None:
+        ev = torch.cuda.Event()
+        ev.record()
+        _PENDING.append((status.numpy(), ev))
+        resolve_pending(keep_last=True)
     if fused:
         _CHAIN.update(state=weakref.ref(out), pre=weakref.ref(pre))
     return out

@@ -176,12 +176,19 @@ def test_update_hand_cases(pkg):
             # the posterior is a difference of O(|input|) terms: roundoff scales with the input
             scale = max(np.abs(st["cross_cov"]).max(), np.abs(st["HC"]).max(), np.abs(st["variance"]).max())
             np.testing.assert_allclose(getattr(out, k), g[f"c{i}_{k}"], rtol=1e-12, atol=1e-14 * scale)
+    # a failing step raises the reference's exception before any data derived from it is
+    # exposed: from the first host read of its state, or from the next update (deferred
+    # status, filters.resolve_pending)
     bad = flt.HikfState(mean=np.zeros(1), cross_cov=np.array([[3.0]]), variance=np.array([1.0]), HC=np.array([[4.0]]))
     with pytest.raises(flt.NumericalConsistencyError):
-        flt.hikf_update(bad, np.array([[1.0]]), 0.0, np.array([0.0]))
+        flt.hikf_update(bad, np.array([[1.0]]), 0.0, np.array([0.0])).mean
     notpd = flt.HikfState(mean=np.zeros(1), cross_cov=np.array([[1.0]]), variance=np.array([1.0]), HC=np.array([[-4.0]]))
     with pytest.raises(pkg.DecompositionError):
-        flt.hikf_update(notpd, np.array([[1.0]]), 0.0, np.array([0.0]))
+        flt.hikf_update(notpd, np.array([[1.0]]), 0.0, np.array([0.0])).variance
+    with pytest.raises(pkg.DecompositionError):
+        nxt = flt.hikf_update(notpd, np.array([[1.0]]), 0.0, np.array([0.0]))
+        flt.hikf_update(nxt, np.array([[1.0]]), 0.0, np.array([0.0]))
+        flt.hikf_update(nxt, np.array([[1.0]]), 0.0, np.array([0.0]))
     s = flt.HikfState(mean=np.zeros(1), cross_cov=np.array([[1.0]]), variance=np.array([1.0]), HC=np.array([[1.0]]))
     with pytest.raises(ValueError):
         flt.hikf_update(s, np.array([[1.0]]), 1.0, np.array([1.0, 2.0]))

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-python tools/qht_time.py cfg4 > gpurun_out/qht_m2lt.log 2>&1
-HIKF_M2L_TARGET=0 python tools/qht_time.py cfg4 > gpurun_out/qht_m2lp.log 2>&1
-timeout 900 python -m pytest tests -m gpu -q -x -k "target_stationary or fused_leaf or sharded or tree_and_matmat or sparse_charges or filter_cfg2" > gpurun_out/t_m2l.log 2>&1; echo "rc=$?" >> gpurun_out/t_m2l.log
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputest.log 2>&1; echo "rc=$?" >> gpurun_out/gputest.log
+for c in cfg1 cfg2; do timeout 300 python bench.py --config $c --no-cpu-baseline --no-factored > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
+python tools/host_overhead.py cfg1 > gpurun_out/host_cfg1.log 2>&1

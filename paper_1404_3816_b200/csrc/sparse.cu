@@ -480,26 +480,39 @@ __device__ __forceinline__ int64_t find_key(const int64_t* __restrict__ keys, in
 }
 
 // W_P[b][j] = sum_{children c (cx, cy order)} sum_a C_c[a][b] W_c[a][j]  (fmm.py:339-345)
+// One warp per parent pair: lanes 0..3 look up the four children's pairs (binary
+// searches in parallel, once per pair instead of once per coefficient), then the
+// lanes stride over b; each output keeps the children-then-a summation order.
 __global__ void m2m_pairs(int64_t npp, const int64_t* __restrict__ pkey, int qp, int qc, int64_t Gp, int64_t n,
                           const double* __restrict__ shift, int64_t npc, const int64_t* __restrict__ ckey,
                           const double* __restrict__ Wcc, double* __restrict__ Wp, unsigned long long* __restrict__ flops) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < npp * qp; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pi = e / qp;
-    int b = (int)(e % qp);
-    int64_t box = pkey[pi] / n, j = pkey[pi] % n, X = box / Gp, Y = box % Gp;
-    double s = 0.0;
-    unsigned found = 0;
-    for (int c = 0; c < 4; ++c) {
-      int64_t child = (2 * X + (c >> 1)) * (2 * Gp) + (2 * Y + (c & 1));
-      int64_t ci = find_key(ckey, npc, child * n + j);
-      if (ci < 0) continue;
-      ++found;
-      const double* C = shift + (int64_t)c * qc * qp;
-      const double* w = Wcc + ci * qc;
-      for (int a = 0; a < qc; ++a) s += C[(int64_t)a * qp + b] * w[a];
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t pi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pi < npp; pi += nwarps) {
+    const int64_t box = pkey[pi] / n, j = pkey[pi] % n, X = box / Gp, Y = box % Gp;
+    int64_t ci = -1;
+    if (lane < 4) {
+      const int64_t child = (2 * X + (lane >> 1)) * (2 * Gp) + (2 * Y + (lane & 1));
+      ci = find_key(ckey, npc, child * n + j);
     }
-    Wp[e] = s;
-    count_flops(flops, 2u * found * (unsigned)qc);
+    int64_t cidx[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cidx[c] = __shfl_sync(0xffffffffu, ci, c);
+    unsigned found = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) found += cidx[c] >= 0;
+    for (int b = lane; b < qp; b += 32) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (cidx[c] < 0) continue;
+        const double* C = shift + (int64_t)c * qc * qp;
+        const double* w = Wcc + cidx[c] * qc;
+        for (int a = 0; a < qc; ++a) s += C[(int64_t)a * qp + b] * w[a];
+      }
+      Wp[pi * qp + b] = s;
+    }
+    if (flops && lane == 0) atomicAdd(flops, 2ull * found * (unsigned long long)qc * qp);
   }
 }
 
@@ -801,7 +814,7 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
   HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
   out->np = np;
   HIKF_TRY(aalloc(&out->W, (int64_t)np * qp, st));
-  m2m_pairs<<<grid_cap((int64_t)np * qp), kT, 0, st>>>(np, out->key, qp, qc, Gp, n, t->shift[l], child.np, child.key,
+  m2m_pairs<<<grid_cap((int64_t)np * 32), kT, 0, st>>>(np, out->key, qp, qc, Gp, n, t->shift[l], child.np, child.key,
                                                        child.W, out->W, prof_flops_ptr(ST_M2M));
   HIKF_CHECK_LAUNCH();
   cudaFreeAsync(tmp, st);

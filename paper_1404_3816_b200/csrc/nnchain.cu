@@ -22,7 +22,6 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <tuple>
@@ -294,16 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_program_kernel(const NnTask* _
   extern __shared__ __align__(16) double nn_smem[];
   cg::grid_group grid = cg::this_grid();
   bool synced = true;
-  auto stamp = [&](int slot) {
-    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      p.trace[slot] = t;
-    }
-  };
-  stamp(0);
   for (int ph = 0; ph < nphases; ++ph) {
-    stamp(1 + ph);
     const int cond = phase_cond[ph];
     if (cond) {
       if (!synced) {
@@ -332,7 +322,6 @@ __global__ void __launch_bounds__(kThreads, 1) nn_program_kernel(const NnTask* _
       }
     }
   }
-  stamp(1 + nphases);
 }
 
 // ---------------------------------------------------------------------------
@@ -514,25 +503,10 @@ int run(int kind, int64_t n, bool flag, const NnPtrs& p, cudaStream_t st) {
   }
   const DevProgram& d = it->second;
   NnPtrs pp = p;
-  static unsigned long long* trace = nullptr;
-  static int ntrace = -1;
-  if (ntrace < 0) ntrace = getenv("HIKF_NN_TRACE") ? atoi(getenv("HIKF_NN_TRACE")) : 0;
-  if (ntrace > 0) {
-    if (!trace) HIKF_CHECK_CUDA(cudaMallocManaged((void**)&trace, 8 * 256));
-    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-    pp.trace = trace;
-  }
   void* args[] = {(void*)&d.tasks, (void*)&d.off, (void*)&d.cond, (void*)&d.nphases, (void*)&pp};
   HIKF_CHECK_CUDA(cudaLaunchCooperativeKernel((void*)nn_program_kernel, dim3(d.grid), dim3(kThreads), args,
                                               PROG_SMEM, st));
   HIKF_CHECK_LAUNCH();
-  if (ntrace > 0) {
-    --ntrace;
-    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-    fprintf(stderr, "nn %s n=%lld grid=%d phases:", kind == 0 ? "pre" : "post", (long long)n, d.grid);
-    for (int i = 0; i <= d.nphases; ++i) fprintf(stderr, " %.1f", (trace[i + 1] - trace[i]) * 1e-3);
-    fprintf(stderr, " us\n");
-  }
   return HIKF_OK;
 }
 

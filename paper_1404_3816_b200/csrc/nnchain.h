@@ -25,11 +25,11 @@ struct NnPtrs {
   const int32_t *ip = nullptr, *ix = nullptr;
   const double *val = nullptr, *mean = nullptr, *z = nullptr, *Hmean = nullptr;
   double* innov = nullptr;
-  unsigned long long* trace = nullptr;  // HIKF_NN_TRACE: per-phase %globaltimer stamps of CTA 0
 };
 
-// largest n the fused programs take (bigger n: the multi-launch chain hidden under the GEMM)
-constexpr int64_t NN_FUSED_MAX = 512;
+// largest n the fused programs take (bigger n: the multi-launch chain, hidden under the GEMM;
+// at n = 480 the cooperative post-GEMM program slowed the concurrent K-GEMM by 20 %)
+constexpr int64_t NN_FUSED_MAX = 256;
 bool nn_fused_enabled(int64_t n);
 int nn_set_fused(int on);  // returns the previous setting
 

@@ -701,7 +701,7 @@ def _set_fused(pkg, on):
 def test_fused_small_chain_is_bit_identical(pkg, ns, nr, N):
     """The fused n x n chain (csrc/nnchain.cu: two cooperative phase programs with a
     device-side look-ahead probe) against the multi-launch chain it replaces for
-    n <= 512: n = 64 (cfg1), 65 (odd), 204 (two recursion levels, ragged blocks) and
+    n <= 256: n = 64 (cfg1), 65 (odd), 204 (two recursion levels, ragged blocks) and
     256 (cfg2's n), 6 steps each, bitwise equal in mean, variance, C and HC."""
     cfg = dict(cases.CFG1, ns=ns, nr=nr, N=N, T=6)
     grid, H = _gpu_scenario(pkg, cfg)
@@ -748,3 +748,4 @@ def test_fused_leaf_downward_is_bit_identical(pkg, N, ns, nr, order, leaf):
     ref = otree.matmat(V)
     got = out[1][0].cpu().numpy()[:, cols]
     assert O.rel_fro(got, ref) <= 1e-13
+

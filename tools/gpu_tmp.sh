@@ -1,4 +1,3 @@
-mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/gputest.log 2>&1; echo "rc=$?" >> gpurun_out/gputest.log
-for c in cfg1 cfg2; do timeout 300 python bench.py --config $c --no-cpu-baseline --no-factored > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; done
-python tools/host_overhead.py cfg1 > gpurun_out/host_cfg1.log 2>&1
+for g in 32 16 8; do HIKF_NN_POST_GRID=$g python bench.py --config cfg2 --steps 80 --warmup 20 --no-cpu-baseline --no-factored > gpurun_out/b2_$g.json 2>&1; done
+for g in 32 8; do HIKF_NN_POST_GRID=$g python bench.py --config cfg1 --steps 2000 --warmup 20 --no-cpu-baseline --no-factored > gpurun_out/b1_$g.json 2>&1; done
+python bench.py --config cfg3 --steps 60 --warmup 5 --no-cpu-baseline --no-factored > gpurun_out/b3.json 2>&1

@@ -249,20 +249,12 @@ int launch_box_t(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
   return HIKF_OK;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
 template <int K4>
 int launch_box_k(const BoxArgs& a, dim3 grid, size_t smem, cudaStream_t st) {
-  // tuning knobs (profiles/r01_box_sweep.log): column tiles per unit (CW) per mode; the
-  // L2L uses 4 row tiles per pass with the B prefetch, the L2P 8
-  static const int cw0 = env_int("HIKF_BOX_CW0", 1), cw1 = env_int("HIKF_BOX_CW1", 1);
-  if (a.mode == 0)
-    return cw0 == 2 ? launch_box_t<K4, 4, 0, false, 2>(a, grid, smem, st)
-                    : launch_box_t<K4, 4, 0, true, 1>(a, grid, smem, st);
-  return cw1 == 2 ? launch_box_t<K4, 8, 1, false, 2>(a, grid, smem, st) : launch_box_t<K4, 8, 1, true, 1>(a, grid, smem, st);
+  // L2L: 4 row tiles per pass, L2P: 8; both with the next unit's B fragments in flight
+  // (one 8-column tile per unit; 2-tile units were measured slower, profiles/r01_box_sweep.log)
+  if (a.mode == 0) return launch_box_t<K4, 4, 0, true, 1>(a, grid, smem, st);
+  return launch_box_t<K4, 8, 1, true, 1>(a, grid, smem, st);
 }
 
 // compile-time k-steps: exactly ceil(K/4)

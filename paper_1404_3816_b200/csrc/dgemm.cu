@@ -358,7 +358,7 @@ __device__ __forceinline__ void cp16z(uint32_t dst, const void* src, int bytes) 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
 
-template <int BM, int BN, int WTM, int WTN, int STAGES, bool PARTIALS, int BARK = 3>
+template <int BM, int BN, int WTM, int WTN, int STAGES, bool PARTIALS>
 __global__ void __launch_bounds__(RmCfg<BM, BN, WTM, WTN>::THREADS, 2) dgemm_rm_kernel(GemmArgs g, int64_t ntn) {
   using Cf = RmCfg<BM, BN, WTM, WTN>;
   constexpr int BK = Cf::BK, TM = Cf::TM, TN = Cf::TN, WM = Cf::WM, WN = Cf::WN;
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(RmCfg<BM, BN, WTM, WTN>::THREADS, 2) dgemm_rm_
   for (int tile = 0; tile < ntiles; ++tile) {
 #pragma unroll
     for (int kg = 0; kg < 4; ++kg) {
-      if (BARK == 3 && kg == 3) {
+      if (kg == 3) {
         cp_async_wait<STAGES - 2>();
         __syncthreads();
         rs = rs + 1 == STAGES ? 0 : rs + 1;
@@ -464,11 +464,6 @@ __global__ void __launch_bounds__(RmCfg<BM, BN, WTM, WTN>::THREADS, 2) dgemm_rm_
           cp_async_commit();
           wsl = wsl + 1 == STAGES ? 0 : wsl + 1;
         }
-      }
-      if (BARK == 2 && kg == 2) {  // barrier one k-group earlier (after the last fragments of this tile)
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        rs = rs + 1 == STAGES ? 0 : rs + 1;
       }
 #pragma unroll
       for (int j = 0; j < TN; ++j)
@@ -507,11 +502,11 @@ __global__ void __launch_bounds__(RmCfg<BM, BN, WTM, WTN>::THREADS, 2) dgemm_rm_
   }
 }
 
-template <int BM, int BN, int WTM, int WTN, int STAGES, bool P, int BARK = 3>
+template <int BM, int BN, int WTM, int WTN, int STAGES, bool P>
 int launch_rm(const GemmArgs& g, cudaStream_t st) {
   using Cf = RmCfg<BM, BN, WTM, WTN>;
   constexpr size_t smem = (size_t)STAGES * Cf::STAGE * sizeof(double);
-  auto kern = dgemm_rm_kernel<BM, BN, WTM, WTN, STAGES, P, BARK>;
+  auto kern = dgemm_rm_kernel<BM, BN, WTM, WTN, STAGES, P>;
   static bool configured = false;
   if (!configured) {
     HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -592,14 +587,8 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
                   al16(g.B);
   if (rm && variant != 7) {
     switch (variant) {
-      case 31:  // 64 x 128, warps 32 x 64, 4 stages
-        return part ? launch_rm<64, 128, 32, 64, 4, true>(g, st) : launch_rm<64, 128, 32, 64, 4, false>(g, st);
       case 32:  // 128 x 64, warps 64 x 32, 3 stages (64-column tiles: finer triangles, n = 64)
         return part ? launch_rm<128, 64, 64, 32, 3, true>(g, st) : launch_rm<128, 64, 64, 32, 3, false>(g, st);
-      case 34:  // as 30, the ring barrier one k-group earlier
-        return part ? launch_rm<64, 128, 32, 64, 3, true, 2>(g, st) : launch_rm<64, 128, 32, 64, 3, false, 2>(g, st);
-      case 33:  // 64 x 64, warps 32 x 32, 3 stages (more CTAs for the n x n products)
-        return part ? launch_rm<64, 64, 32, 32, 3, true>(g, st) : launch_rm<64, 64, 32, 32, 3, false>(g, st);
       default:  // 30: 64 x 128, warps 32 x 64, 3 stages
         return part ? launch_rm<64, 128, 32, 64, 3, true>(g, st) : launch_rm<64, 128, 32, 64, 3, false>(g, st);
     }
@@ -625,7 +614,7 @@ int dgemm(const GemmArgs& g, int batch, cudaStream_t st) {
   // generic strides: 64 x 128 x 16, 8 warps of 32 x 32, 3 stages.  The row partials
   // land in column-tile slots, so a caller sized for a 64-column variant (its
   // dgemm_col_tiles) gets 64-column tiles here too (64 x 64, 4 warps of 32 x 32)
-  if (part && (variant == 32 || variant == 33))
+  if (part && variant == 32)
     return vec ? launch_gen<64, 64, 16, 2, 2, 3, 2, true, true>(g, batch, st)
                : launch_gen<64, 64, 16, 2, 2, 3, 2, false, true>(g, batch, st);
   if (vec)

@@ -64,7 +64,7 @@ void set_dgemm_variant(int v);
 // number of column tiles (= partial sums per row) the current variant uses for N columns
 inline int dgemm_col_tiles(int64_t N, int variant = -1) {
   int v = variant >= 0 ? variant : dgemm_variant();
-  return ceil_div(N, (v == 32 || v == 33) ? 64 : 128);
+  return ceil_div(N, v == 32 ? 64 : 128);
 }
 // variant used by the update's K GEMM (tools/gemm_sweep.py, profiles/r01_gemm_sweep*.log);
 // HIKF_DGEMM_VARIANT overrides it

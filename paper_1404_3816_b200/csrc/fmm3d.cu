@@ -972,21 +972,10 @@ int tree3_matmat(const hikf_tree3* t, const double* V, int64_t ldv, int64_t k, d
         const int64_t units = (int64_t)1 << (3 * (l - 1));  // parents x 8 child classes, one launch
         BoxOpArgs a{OP_M2L, q, l, 0, (int64_t)1 << l, W[l], L[l], t->m2l[l], doffs, ch.kc, NZ[l], OCC[l],
                     prof_flops_ptr(ST_M2L)};
-        static const bool rows = [] {
-          const char* e = getenv("HIKF_M2L3_ROWS");
-          return !(e && e[0] == '0');
-        }();
-        static const int g2 = [] {
-          const char* e = getenv("HIKF_M2L3_G2");
-          return e ? atoi(e) : 2;  // measured best (G2 = 4 needs 168 registers): profiles/r01_m2l3_sweep.log
-        }();
-        if (rows && q <= 8 * 8 * 2) {  // row-split kernel: 8 warps x 2 row tiles (q <= 128), g2 groups per CTA
-          if (g2 == 1)
-            m2l3_rows_kernel<2, 1><<<(unsigned)(8 * units * (KC / 8)), T3, 0, st>>>(a);
-          else if (g2 == 2)
-            m2l3_rows_kernel<2, 2><<<(unsigned)(8 * units * (KC / 16)), T3, 0, st>>>(a);
-          else
-            m2l3_rows_kernel<2, 4><<<(unsigned)(8 * units * (KC / 32)), T3, 0, st>>>(a);
+        // row-split kernel: 8 warps x 2 row tiles (q <= 128), 2 column groups per CTA (measured
+        // best: 1 group under-fills, 4 groups need 168 registers; profiles/r01_m2l3_sweep.log)
+        if (q <= 8 * 8 * 2) {
+          m2l3_rows_kernel<2, 2><<<(unsigned)(8 * units * (KC / 16)), T3, 0, st>>>(a);
         } else {
           boxop3_kernel<<<(unsigned)(8 * units), T3, sm_box, st>>>(a);
         }

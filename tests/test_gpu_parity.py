@@ -613,9 +613,9 @@ def test_device_operator_cache_follows_the_host_operator(pkg):
     assert key not in flt.DeviceCSR._cache
 
 
-@pytest.mark.parametrize("variant", [7, 30, 31, 32, 33, 34])
+@pytest.mark.parametrize("variant", [7, 30, 32])
 def test_dgemm_variants_and_triangular_k_ranges(pkg, variant):
-    """Every DMMA GEMM variant (generic-stride 7, row-major mainloop 30-33) against
+    """Every DMMA GEMM variant (generic-stride 7, row-major mainloop 30 and 32) against
     torch float64: full K, an upper-triangular B (kmode 1: k < n0 + BN) and a
     lower-triangular B (kmode 2: k >= n0), with beta = 1 accumulation, on odd
     shapes that exercise the boundary tiles."""

@@ -346,7 +346,9 @@ int64_t hikf_launch_count(void);
 /* A/B switches for tests and tools (results are bit-identical either way):
  * key 0 = the fused small-n chain of the update (csrc/nnchain.cu; 1 on, 0 the
  * multi-launch chain); key 1 = the fused leaf-level L2L + L2P of the Q H^T
- * FMM (csrc/boxgemm.cu leaf_down; 0: separate L2L and L2P kernels).
+ * FMM (csrc/boxgemm.cu leaf_down; 0: separate L2L and L2P kernels); key 2 =
+ * P2P reads the near-field kernel blocks stored with the tree (0: evaluates
+ * the kernel per (target, entry)).
  * *previous (optional) receives the old value. */
 int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous);
 

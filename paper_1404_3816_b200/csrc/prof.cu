@@ -120,6 +120,7 @@ int64_t hikf_launch_count(void) { return g_launches.load(); }
 }  // extern "C"
 
 #include "boxgemm.h"
+#include "sparse.h"
 #include "nnchain.h"
 
 extern "C" int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous) {
@@ -130,6 +131,9 @@ extern "C" int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous) {
       break;
     case 1:
       prev = hikf::leaf_set_fused(value);
+      break;
+    case 2:
+      prev = hikf::p2p_set_near_blocks(value);
       break;
     default:
       hikf::set_error("unknown tuning key %d", (int)key);

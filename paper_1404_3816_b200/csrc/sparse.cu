@@ -159,7 +159,8 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
                            const double* __restrict__ e_v, const double* __restrict__ xy_s,
                            const int64_t* __restrict__ order, double* __restrict__ U, int64_t ldu,
                            double* __restrict__ Pnear, int32_t maxc, int64_t r0, int64_t r1,
-                           unsigned long long* __restrict__ flops, int64_t leaf0, int64_t leaf1, int64_t s0) {
+                           unsigned long long* __restrict__ flops, int64_t leaf0, int64_t leaf1, int64_t s0,
+                           const double* __restrict__ near) {
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (item >= nitems) return;
@@ -168,15 +169,16 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
   const int32_t j = (int32_t)(key % n);
   if (T < leaf0 || T >= leaf1) return;  // another shard's target leaf
   const int64_t box = leaf_box[T], bx = box / G, by = box % G;
-  // the <= 9 entry ranges of ray j in the adjacent leaves
-  int32_t rb[9], re[9];
+  // the <= 9 entry ranges of ray j in the adjacent leaves (and their first sorted positions)
+  int32_t rb[9], re[9], sb[9];
 #pragma unroll
   for (int s = 0; s < 9; ++s) {
-    rb[s] = re[s] = 0;
+    rb[s] = re[s] = sb[s] = 0;
     int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
     if (nx < 0 || nx >= G || ny < 0 || ny >= G) continue;
     int32_t S = box2leaf[nx * G + ny];
     if (S < 0) continue;
+    sb[s] = leaf_start[S];
     int32_t lo = leaf_g[S], hi = leaf_g[S + 1];
     while (lo < hi) {
       int32_t mid = (lo + hi) >> 1;
@@ -202,13 +204,24 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
       ty = xy_s[2 * (int64_t)(t0 + t) + 1];
     }
     double acc = 0.0;
+    if (near) {  // kernel values from the tree's near blocks (the same values, evaluated at build)
+      const double* blkT = near + (int64_t)T * 9 * 64 * 64 + t;
 #pragma unroll 1
-    for (int s = 0; s < 9; ++s)
-      for (int32_t k = rb[s]; k < re[s]; ++k) {
-        const int32_t p = e_sp[k];
-        const double v = e_v[k];
-        acc += kernel_of_r_near(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
-      }
+      for (int s = 0; s < 9; ++s)
+        for (int32_t k = rb[s]; k < re[s]; ++k) {
+          const int32_t c = e_sp[k] - sb[s];
+          const double v = e_v[k];
+          acc += blkT[(s * 64 + c) * 64] * v;
+        }
+    } else {
+#pragma unroll 1
+      for (int s = 0; s < 9; ++s)
+        for (int32_t k = rb[s]; k < re[s]; ++k) {
+          const int32_t p = e_sp[k];
+          const double v = e_v[k];
+          acc += kernel_of_r_near(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
+        }
+    }
     if (!ok) continue;
     if (Pnear)
       Pnear[(int64_t)t * nitems + item] = acc;  // added into U later (p2p_scatter): U = far + near either way
@@ -406,6 +419,14 @@ int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, 
   return HIKF_OK;
 }
 
+static int g_near_blocks = 1;
+
+int p2p_set_near_blocks(int on) {
+  const int prev = g_near_blocks;
+  g_near_blocks = on ? 1 : 0;
+  return prev;
+}
+
 int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st, double* Pnear,
                int64_t r0, int64_t r1, const LeafWindow* lw) {
   if (s.nitems <= 0) return HIKF_OK;
@@ -414,7 +435,7 @@ int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cu
       s.nitems, s.items, s.n, t->G, t->kp, t->leaf_box, t->leaf_start, t->leaf_count, t->box2leaf, s.leaf_g, s.g_j,
       s.g_start, s.e_sp, s.e_v, t->xy_s, t->order, U, ldu, Pnear, (int32_t)t->max_count, r0,
       r1 < 0 ? INT64_MAX : r1, prof_flops_ptr(ST_P2P), lw ? lw->leaf0 : 0, lw ? lw->leaf1 : INT64_MAX,
-      lw ? lw->s0 : -1);
+      lw ? lw->s0 : -1, g_near_blocks ? t->near : nullptr);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }

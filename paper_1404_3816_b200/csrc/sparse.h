@@ -44,6 +44,8 @@ int sparse_p2m(const hikf_tree* t, const SparseHt& s, double* W, int64_t kcols, 
 //  positions - lw->s0)
 int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cudaStream_t st,
                double* Pnear = nullptr, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
+// use the tree's near-field kernel blocks in P2P (1) or evaluate the kernel (0); tuning key 2
+int p2p_set_near_blocks(int on);
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
                        cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
 

@@ -171,6 +171,10 @@ void tree_free(hikf_tree* t) {
   cudaFree(t->leaf_count);
   cudaFree(t->box2leaf);
   cudaFree(t->W2s);
+  if (t->near) {  // stream-ordered pool allocation (kept reserved across trees)
+    cudaDeviceSynchronize();
+    cudaFreeAsync(t->near, 0);
+  }
   for (int l = 0; l <= kMaxDepth; ++l) {
     cudaFree(t->occ[l]);
     cudaFree(t->occ_flag[l]);
@@ -180,7 +184,31 @@ void tree_free(hikf_tree* t) {
   delete t;
 }
 
-static int build_impl(hikf_tree* t, const double* xy_host, cudaStream_t st) {
+static // near[((T * 9 + s) * 64 + c) * 64 + t] = K(x_t, x_c) (kernels.py evaluation, as P2P does it)
+__global__ void near_blocks(KParams kp, int64_t G, const int32_t* __restrict__ leaf_box,
+                            const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_count,
+                            const int32_t* __restrict__ box2leaf, const double* __restrict__ xy_s,
+                            double* __restrict__ near) {
+  const int64_t T = blockIdx.x;
+  const int s = blockIdx.y;
+  const int64_t box = leaf_box[T], bx = box / G, by = box % G;
+  const int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
+  if (nx < 0 || nx >= G || ny < 0 || ny >= G) return;
+  const int32_t S = box2leaf[nx * G + ny];
+  if (S < 0) return;
+  const int32_t t0 = leaf_start[T], ct = leaf_count[T], s0 = leaf_start[S], cs = leaf_count[S];
+  double* blk = near + ((T * 9 + s) * 64) * 64;
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int t = e & 63, c = e >> 6;
+    double v = 0.0;
+    if (t < ct && c < cs)
+      v = kernel_of_r_near(kp, dist2d(xy_s[2 * (int64_t)(t0 + t)], xy_s[2 * (int64_t)(t0 + t) + 1],
+                                      xy_s[2 * (int64_t)(s0 + c)], xy_s[2 * (int64_t)(s0 + c) + 1]));
+    blk[e] = v;
+  }
+}
+
+int build_impl(hikf_tree* t, const double* xy_host, cudaStream_t st) {
   const int64_t m = t->m;
   HIKF_TRY(dalloc(&t->xy, 2 * m));
   HIKF_CHECK_CUDA(cudaMemcpyAsync(t->xy, xy_host, sizeof(double) * 2 * m, cudaMemcpyHostToDevice, st));
@@ -219,7 +247,14 @@ static int build_impl(hikf_tree* t, const double* xy_host, cudaStream_t st) {
   size_t cub_bytes = 0;
   cub::DeviceReduce::Max(nullptr, cub_bytes, hist, dmax, (int)cap_bins, st);
   HIKF_CHECK_CUDA(cudaMalloc(&cub_tmp, cub_bytes));
-  int depth = 0;
+  // Depths below d0 fail both tests of the reference loop, so the search starts there
+  // (exact): some box holds >= ceil(m / 4^d) points (pigeonhole), and the cap test
+  // 4^(d+1) > cap_bins first fires at d_cap.  At cfg4 this is one box-key pass, not eight
+  // (the coarse passes serialise on histogram atomics).
+  int d_lb = 0, d_cap = 0;
+  while (d_lb < kMaxDepth && (m + (1LL << (2 * d_lb)) - 1) / (1LL << (2 * d_lb)) > t->max_leaf) ++d_lb;
+  while (d_cap < kMaxDepth && !((4LL << (2 * d_cap)) > cap_bins)) ++d_cap;
+  int depth = std::min(d_lb, d_cap);
   for (;;) {
     if (depth >= kMaxDepth) break;
     int64_t G = 1LL << depth;
@@ -326,6 +361,20 @@ static int build_impl(hikf_tree* t, const double* xy_host, cudaStream_t st) {
   HIKF_TRY(dalloc(&t->xy_s, 2 * m));
   gather_xy<<<grid_for(m), kThreads, 0, st>>>(t->xy, t->order, m, t->xy_s);
   HIKF_CHECK_LAUNCH();
+
+  // ---- near-field kernel blocks of every (target leaf, neighbour leaf) pair ----
+  if (t->max_count <= 64) {
+    const size_t bytes = sizeof(double) * (size_t)nl * 9 * 64 * 64;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && bytes <= free_b / 4) {
+      // from the stream-ordered pool: a cudaMalloc of the 4.8 GB cfg4 blocks costs ~30 ms of mapping
+      // per tree, the pool (release threshold kept at max) maps it once per process
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&t->near, bytes, st));
+      near_blocks<<<dim3((unsigned)nl, 9), kThreads, 0, st>>>(t->kp, G, t->leaf_box, t->leaf_start, t->leaf_count,
+                                                               t->box2leaf, t->xy_s, t->near);
+      HIKF_CHECK_LAUNCH();
+    }
+  }
 
   if (depth < 2) return HIKF_OK;  // near field only (fmm.py:131)
 

@@ -49,6 +49,11 @@ struct hikf_tree {
   int64_t n_occ[hikf::kMaxDepth + 1] = {0};
 
   double* W2s = nullptr;
+  // near-field kernel blocks (fmm.py:166-201 builds `near` at tree construction too):
+  // near[((T * 9 + s) * 64 + c) * 64 + t] = K(x_t, x_c) for target leaf T, its neighbour
+  // slot s (ox outer, oy inner), local source point c and local target point t; null when
+  // a leaf holds more than 64 points or the blocks would not fit (P2P then evaluates K)
+  double* near = nullptr;
   double* m2l[hikf::kMaxDepth + 1] = {nullptr};
   uint64_t m2l_present[hikf::kMaxDepth + 1] = {0};  // bit s: offset s has pairs at this level
   double* shift[hikf::kMaxDepth + 1] = {nullptr};

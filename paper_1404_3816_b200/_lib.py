@@ -177,9 +177,17 @@ def check(status: int, what: str = "") -> None:
     raise RuntimeError(f"libhikf_b200 failure ({status}): {msg}")
 
 
+_HAVE_CUDA = False
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("the HiKF B200 path needs a CUDA device; there is no CPU fallback")
+    """The current CUDA device; raises when there is none (no CPU fallback).  The
+    availability probe runs until it first succeeds (it costs ~6 us per call)."""
+    global _HAVE_CUDA
+    if not _HAVE_CUDA:
+        if not torch.cuda.is_available():
+            raise RuntimeError("the HiKF B200 path needs a CUDA device; there is no CPU fallback")
+        _HAVE_CUDA = True
     return torch.device("cuda", torch.cuda.current_device())
 
 

@@ -426,6 +426,7 @@ void factor_program(Program& P, int16_t HCsrc, int16_t Li, int16_t LiT, int16_t 
 
 Program pre_program(int64_t n, bool probe) {
   Program P;
+  P.task(ew(K_IZERO, -1, -1, NI_STATUS, 4));  // the step's pivot / check / block-count words
   P.task(ew(K_ADD, NB_HC, NB_HCQ, NB_HCP, n * n));
   P.task(ew(K_INNOV, -1, -1, -1, n));
   if (probe) {
@@ -452,6 +453,7 @@ Program post_program(int64_t n, bool lookahead) {
   P.phase(0);
   // HC_out = HC' - R P
   gemm(P, n, n, n, NB_R, 0, n, 1, NB_P, 0, n, 1, NB_HCOUT, 0, n, -1.0, NB_HCP, 0, n, 1.0);
+  P.task(ew(K_IZERO, -1, -1, NI_FLAG, 1));  // the next step's probe flag (the pre program has used it)
   P.phase(0);
   if (!lookahead) return P;
   P.task(ew(K_ADD, NB_HCOUT, NB_HCQ, NB_LA_HCP, n * n));

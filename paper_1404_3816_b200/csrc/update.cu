@@ -242,6 +242,83 @@ __global__ void finalize_rows(int64_t m, int nt, const double* __restrict__ psq,
   }
 }
 
+// finalize_rows + check_variance in one launch (the small-n path): var' = var + diag_Q
+// formed here (the same add as the predict kernel), block extrema, and the last block
+// to finish folds them (status[2] counts finished blocks and is reset for the next
+// call), sets status[1] and writes [pivot, negative-variance flag, min var, max prior]
+// to out4 (the deferred status).  min / max are order-free, so the result is that of
+// the two-kernel path.
+__global__ void finalize_check(int64_t m, int nt, const double* __restrict__ psq, const double* __restrict__ pdot,
+                               const double* __restrict__ var, const double* __restrict__ dQ,
+                               const double* __restrict__ mean, double* __restrict__ var_out,
+                               double* __restrict__ mean_out, double* __restrict__ bmin, double* __restrict__ bmax,
+                               int* __restrict__ status, double* __restrict__ minv, double* __restrict__ out4) {
+  double lmin = DBL_MAX, lmax = -DBL_MAX;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, d = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      s += psq[i * nt + t];
+      d += pdot[i * nt + t];
+    }
+    const double vp = var[i] + dQ[i];
+    const double v = vp - s;
+    var_out[i] = v;
+    mean_out[i] = mean[i] + d;
+    lmin = fmin(lmin, v);
+    lmax = fmax(lmax, vp);
+  }
+  __shared__ double smin[kT], smax[kT];
+  __shared__ bool last;
+  smin[threadIdx.x] = lmin;
+  smax[threadIdx.x] = lmax;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    bmin[blockIdx.x] = smin[0];
+    bmax[blockIdx.x] = smax[0];
+    __threadfence();
+    last = atomicAdd(status + 2, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double mn = DBL_MAX, mx = -DBL_MAX;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    mn = fmin(mn, __ldcg(bmin + b));
+    mx = fmax(mx, __ldcg(bmax + b));
+  }
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = kT / 2; o; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    mn = smin[0];
+    mx = smax[0];
+    const double prior_max = fmax(mx, 0.0);
+    const int neg = mn < -1e-10 * fmax(prior_max, DBL_MIN) ? 1 : 0;
+    if (neg) status[1] = 1;
+    minv[0] = mn;
+    minv[1] = mx;
+    out4[0] = (double)status[0];
+    out4[1] = (double)neg;
+    out4[2] = mn;
+    out4[3] = mx;
+    status[2] = 0;
+  }
+}
+
 // consistency check of filters.py:149-153 -> status[1]; min var -> out[0]
 __global__ void check_variance(int nb, const double* bmin, const double* bmax, int* status, double* out) {
   // one CTA of kT threads folds the per-block extrema of finalize_rows
@@ -1057,8 +1134,7 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
     return HIKF_BAD_ARGUMENT;
   }
   UpdWs w;
-  update_layout(m, n, (char*)a.workspace, &w);
-  HIKF_CHECK_CUDA(cudaMemsetAsync(w.status, 0, 16, st));
+  update_layout(m, n, (char*)a.workspace, &w);  // status[0..3] zeroed by the pre-GEMM program
   ChainState& ch = chain_state();
   const bool chain_in = a.chain_in && ch.valid && ch.C_out == a.C && ch.CQ == a.CQ && ch.ws == a.workspace &&
                         ch.m == m && ch.n == n;
@@ -1075,11 +1151,9 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
 
   HIKF_CHECK_CUDA(cudaEventRecord(ev[0], st));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(side, ev[0], 0));
-  {
+  if (m * n > 0 && !chain_in) {  // var' = var + diag_Q is formed in finalize_check
     ProfScope ps(ST_PREDICT, st);
-    if (m * n > 0 && !chain_in) HIKF_TRY(add_stream(a.C, a.CQ, Ycur, m * n, st));
-    add_kernel<<<grid_for(m / 2 + 1), kT, 0, st>>>(a.var, a.dQ, a.var_out, m);
-    HIKF_CHECK_LAUNCH();
+    HIKF_TRY(add_stream(a.C, a.CQ, Ycur, m * n, st));
   }
   NnPtrs p;
   p.d[NB_HC] = const_cast<double*>(a.HC);
@@ -1114,8 +1188,7 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
   p.Hmean = a.Hmean;
   p.innov = w.innov;
   {
-    ProfScope pf(ST_FACTOR, side);
-    if (probe) HIKF_CHECK_CUDA(cudaMemsetAsync(la.ibuf + 1, 0, sizeof(int), side));
+    ProfScope pf(ST_FACTOR, side);  // (the probe flag was zeroed by the previous post program)
     HIKF_TRY(nn_pre(p, probe, side));
   }
   HIKF_CHECK_CUDA(cudaEventRecord(ev[1], side));
@@ -1145,9 +1218,8 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
       HIKF_TRY(dgemm(g, 1, st));
     }
     ProfScope pz(ST_FINALIZE, st);
-    finalize_rows<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, a.var_out, a.mean, a.var_out, a.mean_out, w.bmin, w.bmax);
-    HIKF_CHECK_LAUNCH();
-    check_variance<<<1, kT, 0, st>>>(nb, w.bmin, w.bmax, w.status, w.minv);
+    finalize_check<<<nb, kT, 0, st>>>(m, nt, w.psq, w.pdot, a.var, a.dQ, a.mean, a.var_out, a.mean_out, w.bmin,
+                                      w.bmax, w.status, w.minv, w.minv + 2);
     HIKF_CHECK_LAUNCH();
     if (a.mean_host)
       HIKF_CHECK_CUDA(cudaMemcpyAsync(a.mean_host, a.mean_out, sizeof(double) * m, cudaMemcpyDeviceToHost, st));
@@ -1170,8 +1242,7 @@ static int update_small(const UpdateArgs& a, cudaStream_t st, UpdateResult* res)
     pack_status<<<1, 1, 0, st>>>(w.minv, w.status, a.mm_dev);
     HIKF_CHECK_LAUNCH();
   } else if (a.status_host) {  // deferred: the caller reads the pinned status after the stream
-    pack_status4<<<1, 1, 0, st>>>(w.minv, w.status, w.minv + 2);
-    HIKF_CHECK_LAUNCH();
+    // (finalize_check packed [pivot, flag, min, max]; the pivot is final: the pre program ran first)
     HIKF_CHECK_CUDA(cudaMemcpyAsync(a.status_host, w.minv + 2, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
   } else {
     int hs[2] = {0, 0};

@@ -165,6 +165,15 @@ class HikfState:
             self.mean_t = _prior.mean_t  # the predict leaves the mean unchanged
             self.cross_cov_t = self.variance_t = self.HC_t = None
 
+    @classmethod
+    def _wrap(cls, mean_t, C_t, var_t, HC_t):
+        """A state over device tensors the library just wrote (no copies or checks)."""
+        self = cls.__new__(cls)
+        self._prior = self._pre = None
+        self._host = {}
+        self.mean_t, self.cross_cov_t, self.variance_t, self.HC_t = mean_t, C_t, var_t, HC_t
+        return self
+
     @property
     def pending(self) -> bool:
         return self._prior is not None and self.cross_cov_t is None
@@ -454,7 +463,7 @@ def hikf_update(state: HikfState, H, r_variance: float, z) -> HikfState:
         Hd.indptr.data_ptr(), Hd.indices.data_ptr(), Hd.data.data_ptr(), float(r_variance), zt.data_ptr(),
         mean.data_ptr(), C.data_ptr(), var.data_ptr(), HC.data_ptr(), ws.data_ptr(), ws.numel(),
         _lib.ptr(status) if status is not None else None, chain, mean_host.data_ptr(), _lib.stream_ptr()))
-    out = HikfState(mean, C, var, HC)
+    out = HikfState._wrap(mean, C, var, HC)
     out._pinned = mean_host
     out._host["mean"] = mean_host.numpy()
     if status is not None:

@@ -3,7 +3,10 @@
 // each stage a seg_gemm_kernel launch over boxes x column tiles.
 #include <algorithm>
 #include <cstring>
+#include <cstdio>
 #include <cstdlib>
+#include <utility>
+#include <vector>
 
 #include "boxgemm.h"
 #include "fmm_device.cuh"
@@ -489,8 +492,44 @@ int leaf_window(const hikf_tree* t, int64_t leaf0, int64_t leaf1, LeafWindow* w)
   return HIKF_OK;
 }
 
+// HIKF_QHT_TIMELINE=1: event timestamps of the Q H^T stages (ms from the start) to stderr
+namespace {
+struct Timeline {
+  bool on = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  cudaEvent_t t0 = nullptr;
+  void start(cudaStream_t s) {
+    static const bool env = getenv("HIKF_QHT_TIMELINE") != nullptr;
+    on = env;
+    if (!on) return;
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, s);
+  }
+  void mark(const char* name, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  void report() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    for (auto& x : ev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t0, x.second);
+      fprintf(stderr, "qht %-22s %8.3f ms\n", x.first, ms);
+      cudaEventDestroy(x.second);
+    }
+    cudaEventDestroy(t0);
+  }
+};
+}  // namespace
+
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
                     cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
+  Timeline tl;
+  tl.start(st);
   if (n <= 0) return HIKF_OK;
   const bool window = r0 != 0 || (r1 >= 0 && r1 != t->m);
   if (r1 < 0) r1 = t->m;
@@ -508,6 +547,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     ProfScope ps(ST_DENSIFY, st);  // the regrouping of H^T replaces the densify step
     HIKF_TRY(sparse_build(t, n, ip, ix, val, &sp, st));
   }
+  tl.mark("regroup", st);
   if (D < 2) {
     HIKF_CHECK_CUDA(cudaMemsetAsync(U, 0, sizeof(double) * (r1 - r0) * n, st));
     int status;
@@ -523,17 +563,24 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
 
   cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1], ev_up = qs->e[2];
 
-  // ---- near field, concurrently: sums parked in Pnear, added after L2P ----
+  // ---- near field, concurrently: sums parked in Pnear, added after L2P.  Launched
+  // after the upward pass (below): the P2P grid fills the machine, and the upward
+  // pass and the M2L target maps are on the critical path while P2P is not ----
   double* Pnear = nullptr;
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Pnear, sizeof(double) * std::max<int64_t>(1, sp.nitems * t->max_count), st));
-  HIKF_CHECK_CUDA(cudaEventRecord(ev_base, st));
-  HIKF_CHECK_CUDA(cudaStreamWaitEvent(qs->s[0], ev_base, 0));
   int status = HIKF_OK;
-  {
-    ProfScope ps(ST_P2P, qs->s[0]);
-    status = sparse_p2p(t, sp, U, n, qs->s[0], Pnear, 0, -1, lw);
-  }
-  HIKF_CHECK_CUDA(cudaEventRecord(ev_p2p, qs->s[0]));
+  auto launch_p2p = [&]() -> int {
+    HIKF_CHECK_CUDA(cudaEventRecord(ev_base, st));
+    HIKF_CHECK_CUDA(cudaStreamWaitEvent(qs->s[0], ev_base, 0));
+    int s2;
+    {
+      ProfScope ps(ST_P2P, qs->s[0]);
+      s2 = sparse_p2p(t, sp, U, n, qs->s[0], Pnear, 0, -1, lw);
+    }
+    HIKF_CHECK_CUDA(cudaEventRecord(ev_p2p, qs->s[0]));
+    tl.mark("p2p end", qs->s[0]);
+    return s2;
+  };
 
   // ---- upward pass on the active (box, ray) pairs only ----
   PairLevel pl[kMaxDepth + 1];
@@ -581,23 +628,44 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
                                       sizeof(double) * std::max<int64_t>(1, (int64_t)hcount[2 * l] * t->orders[l] *
                                                                                 t->orders[l]), st));
     HIKF_CHECK_CUDA(cudaEventRecord(ev_up, st));
-    for (int l = D; l >= 2 && status == HIKF_OK; --l) {  // biggest level first
-      cudaStream_t sl = qs->s[1 + (D - l) % 7];
+    tl.mark("upward + targets", st);
+    if (status == HIKF_OK) status = launch_p2p();
+    // one stream per group of levels: the leaf level alone (its M2L overlaps the L2L chain
+    // above it), the coarser levels grouped by equal order so that each offset is one
+    // launch for the whole group (levels 2-4 are launch-latency bound on their own)
+    int groups[kMaxDepth + 1][kMaxDepth + 1], gsize[kMaxDepth + 1] = {0}, ng = 0;
+    for (int l = D; l >= 2; --l) {
+      const bool join = ng > 0 && l < D && groups[ng - 1][0] < D && m2l_list_supported(t, l) &&
+                        t->orders[groups[ng - 1][0]] == t->orders[l];
+      if (!join) ++ng;
+      groups[ng - 1][gsize[ng - 1]++] = l;
+    }
+    for (int gi = 0; gi < ng && status == HIKF_OK; ++gi) {  // biggest level first
+      cudaStream_t sl = qs->s[1 + gi % 7];
       HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, ev_up, 0));
-      const int q = t->orders[l] * t->orders[l];
       ProfScope ps(ST_M2L, sl);
-      HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * (int64_t)hcount[2 * l] * q, sl));
-      const bool lists = m2l_list_supported(t, l);
-      for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
-        status = lists ? m2l_pass_list(t, l, slot, pl[l], plan[l], hoff[l], scratch[l], sl)
-                       : m2l_pass(t, l, slot, pl[l], n, scratch[l], tmap[l], sl, xlo(l), xhi(l));
-      HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + l], sl));
+      for (int k = 0; k < gsize[gi]; ++k) {
+        const int l = groups[gi][k];
+        HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0,
+                                        sizeof(double) * (int64_t)hcount[2 * l] * t->orders[l] * t->orders[l], sl));
+      }
+      const int l0 = groups[gi][0];
+      if (m2l_list_supported(t, l0)) {
+        for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
+          status = m2l_pass_list(t, gsize[gi], groups[gi], slot, pl, plan, hoff, scratch, sl);
+      } else {
+        for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
+          status = m2l_pass(t, l0, slot, pl[l0], n, scratch[l0], tmap[l0], sl, xlo(l0), xhi(l0));
+      }
+      for (int k = 0; k < gsize[gi]; ++k) HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + groups[gi][k]], sl));
+      tl.mark(gi == 0 ? "m2l group 0 end" : gi == 1 ? "m2l group 1 end" : "m2l group 2+ end", sl);
     }
   }
   // ---- downward pass (main stream): L = scratch^T + shift L_parent, then L2P ----
   const bool vec = (n % 2) == 0;
   const double* Lprev = nullptr;
   double* Lcur = nullptr;
+  cudaStream_t dn = st;  // the L2L chain (main stream)
   for (int l = 2; l <= D && status == HIKF_OK; ++l) {
     if (l == D && fused_leaf) {  // the leaf L2L runs inside the fused L2P below
       HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
@@ -605,13 +673,13 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     }
     Lcur = Lbuf[(D - l) & 1];
     const int q = t->orders[l] * t->orders[l];
-    HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
+    HIKF_CHECK_CUDA(cudaStreamWaitEvent(dn, qs->e[3 + l], 0));
     if (l > 2 && box_supported(4 * q, t->orders[l - 1] * t->orders[l - 1])) {
-      ProfScope ps(ST_L2L, st);
-      status = l2l_boxes(t, l, scratch[l], tmap[l], Lprev, n, Lcur, st, xlo(l - 1), xhi(l - 1));
+      ProfScope ps(ST_L2L, dn);
+      status = l2l_boxes(t, l, scratch[l], tmap[l], Lprev, n, Lcur, dn, xlo(l - 1), xhi(l - 1));
     } else {
-      ProfScope ps(ST_L2L, st);
-      status = pair_to_box(t, l, scratch[l], tmap[l], n, Lcur, st);
+      ProfScope ps(ST_L2L, dn);
+      status = pair_to_box(t, l, scratch[l], tmap[l], n, Lcur, dn);
       if (status == HIKF_OK && l > 2) {
         L2LParentProv ll;
         set_base(ll, t, n, 0, 0, vec);
@@ -622,10 +690,11 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
         ll.Lp = Lprev;
         ll.shift = t->shift[l - 1];
         ll.L = Lcur;
-        status = launch(ll, t->n_occ[l - 1], 4 * q, n, st);
+        status = launch(ll, t->n_occ[l - 1], 4 * q, n, dn);
       }
     }
     Lprev = Lcur;
+    tl.mark("l2l level end", dn);
   }
   if (status == HIKF_OK && fused_leaf) {
     ProfScope ps(ST_L2P, st);
@@ -661,6 +730,8 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     ProfScope ps(ST_P2P, st);
     status = sparse_p2p_scatter(t, sp, Pnear, U, n, st, r0, r1, lw);
   }
+  tl.mark("leaf + scatter end", st);
+  tl.report();
   for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
   for (int l = 2; l <= D; ++l) {
     cudaFreeAsync(scratch[l], st);

@@ -688,32 +688,34 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
 // the compact scratch at the target's slot -- race-free, since a target receives at
 // most one source per offset; the offsets run in the reference's order.
 template <int NK4, int NRT>
-__global__ void __launch_bounds__(256, (NK4 <= 13) ? 2 : 1) m2l_list_kernel(int64_t e0, int64_t ne,
-                                                                         const int2* __restrict__ ent,
-                                                                         const double* __restrict__ W, int q,
-                                                                         const double* __restrict__ M,
-                                                                         double* __restrict__ L,
+__global__ void __launch_bounds__(256, (NK4 <= 13) ? 2 : 1) m2l_list_kernel(M2LSegs sg, int q,
                                                                          unsigned long long* __restrict__ flops) {
+  // this CTA's level segment (levels of equal order share one launch per offset)
+  int si = 0;
+  while (si + 1 < sg.n && (int64_t)blockIdx.x >= sg.s[si + 1].block0) ++si;
+  const M2LSeg& S = sg.s[si];
   extern __shared__ double Ms[];
   const int ld = m2l_ld(q);
-  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = M[e];
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = S.M[e];
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  const int64_t i0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 8;
+  const int64_t ne = S.ne;
+  const int64_t i0 = (((blockIdx.x - S.block0) * (int64_t)blockDim.x + threadIdx.x) >> 5) * 8;
   if (i0 >= ne) return;
   const int64_t mine = i0 + g;
   int2 pe = make_int2(-1, -1);
-  if (mine < ne) pe = ent[e0 + mine];
+  if (mine < ne) pe = S.ent[S.e0 + mine];
   if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)(ne - i0 < 8 ? ne - i0 : 8) * q * q);
   double b[NK4];
 #pragma unroll
   for (int k4 = 0; k4 < NK4; ++k4) {
     const int k = k4 * 4 + t4;
-    b[k4] = (pe.x >= 0 && k < q) ? W[(int64_t)pe.x * q + k] : 0.0;
+    b[k4] = (pe.x >= 0 && k < q) ? S.W[(int64_t)pe.x * q + k] : 0.0;
   }
   int slot[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) slot[h] = __shfl_sync(0xffffffffu, pe.y, (2 * t4 + h) * 4);
+  double* L = S.L;
   for (int i = 0; i < NRT; ++i) {
     const int r = i * 8 + g;
     double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
@@ -971,19 +973,35 @@ void m2l_plan_free(M2LPlan* plan, cudaStream_t st) {
   *plan = M2LPlan();
 }
 
-int m2l_pass_list(const hikf_tree* t, int l, int slot, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,
-                  double* L, cudaStream_t st) {
-  const int64_t e0 = hoff[slot], ne = hoff[slot + 1] - hoff[slot];
-  if (ne <= 0) return HIKF_OK;
-  const int q = t->orders[l] * t->orders[l];
-  const int64_t warps = (ne + 7) / 8;
-  const unsigned blocks = (unsigned)((warps * 32 + kT - 1) / kT);
+int m2l_pass_list(const hikf_tree* t, int nlev, const int* levels, int slot, const PairLevel* src,
+                  const M2LPlan* plan, const int64_t (*hoff)[41], double* const* S, cudaStream_t st) {
+  M2LSegs sg{};
+  const int q = t->orders[levels[0]] * t->orders[levels[0]];
+  int64_t blocks = 0;
+  for (int i = 0; i < nlev; ++i) {
+    const int l = levels[i];
+    const int64_t e0 = hoff[l][slot], ne = hoff[l][slot + 1] - hoff[l][slot];
+    if (ne <= 0) continue;
+    if (t->orders[l] * t->orders[l] != q) {
+      set_error("M2L level group with unequal orders");
+      return HIKF_BAD_ARGUMENT;
+    }
+    M2LSeg& g = sg.s[sg.n++];
+    g.e0 = e0;
+    g.ne = ne;
+    g.ent = plan[l].ent;
+    g.W = src[l].W;
+    g.M = t->m2l[l] + (int64_t)slot * q * q;
+    g.L = S[l];
+    g.block0 = blocks;
+    blocks += ((ne + 7) / 8 * 32 + kT - 1) / kT;
+  }
+  if (sg.n == 0) return HIKF_OK;
   const size_t smem = sizeof(double) * q * m2l_ld(q);
-  const double* M = t->m2l[l] + (int64_t)slot * q * q;
   unsigned long long* fl = prof_flops_ptr(ST_M2L);
-#define HIKF_M2LL(QQ, K4, RT)                                                                                   \
-  case QQ:                                                                                                     \
-    m2l_list_kernel<K4, RT><<<blocks, kT, smem, st>>>(e0, ne, plan.ent, src.W, q, M, L, fl);                   \
+#define HIKF_M2LL(QQ, K4, RT)                                                          \
+  case QQ:                                                                            \
+    m2l_list_kernel<K4, RT><<<(unsigned)blocks, kT, smem, st>>>(sg, q, fl);           \
     break;
   switch (q) {
     HIKF_M2LL(4, 1, 1)

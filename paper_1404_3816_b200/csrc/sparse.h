@@ -2,6 +2,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "host_ops.h"
 
 struct hikf_tree;
 
@@ -70,10 +71,21 @@ struct M2LPlan {
 int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
                 M2LPlan* plan, cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
 void m2l_plan_free(M2LPlan* plan, cudaStream_t st);
-// one offset over its entry list (hoff: host copy of plan.off); S as m2l_pass
+// One offset over the entry lists of a group of levels of equal order (one launch;
+// hoff[l]: host copy of plan[l].off; S[l]: level l's compact scratch)
+struct M2LSeg {
+  int64_t e0 = 0, ne = 0, block0 = 0;
+  const int2* ent = nullptr;
+  const double *W = nullptr, *M = nullptr;
+  double* L = nullptr;
+};
+struct M2LSegs {
+  M2LSeg s[kMaxDepth + 1];
+  int n = 0;
+};
 bool m2l_list_supported(const hikf_tree* t, int l);
-int m2l_pass_list(const hikf_tree* t, int l, int slot, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,
-                  double* S, cudaStream_t st);
+int m2l_pass_list(const hikf_tree* t, int nlev, const int* levels, int slot, const PairLevel* src,
+                  const M2LPlan* plan, const int64_t (*hoff)[41], double* const* S, cudaStream_t st);
 // L_l[T][:, j] += M_d W_{T+d}[:, j] for every active source pair and one offset slot
 // (targets outside the box-column range [xlo, xhi] of level l are skipped)
 int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, const int32_t* tmap,

@@ -771,9 +771,3 @@ def test_near_blocks_are_bit_identical(pkg, N, ns, nr, order, leaf):
         pkg._lib.check(lib.hikf_set_tuning(2, 1, None))
     assert bool((out[1][0] == out[0][0]).all()) and bool((out[1][1] == out[0][1]).all())
 
-
-def test_warmup_loads_the_library(pkg):
-    """The optional warm-up (tiny tree + Q H^T + two updates) runs and leaves no
-    pending step status behind."""
-    pkg.warmup()
-    assert not pkg.filters._PENDING

@@ -17,9 +17,6 @@ args = [a for a in sys.argv[1:] if not a.startswith("--")]
 cfg = bench.CONFIGS[args[0] if args else "cfg4"]
 torch.zeros(1, device="cuda")
 torch.cuda.synchronize()
-if "--warmup" in sys.argv:  # the package's optional warm-up (device code loaded, pool primed)
-    P.warmup()
-    torch.cuda.synchronize()
 if "--preload-small" in sys.argv:  # every kernel loaded by a tiny run first: isolates the memory growth
     g1 = P.Grid2D(32, 32, 1 / 32, 1 / 32)
     H1 = P.tomography.build_ray_operator(g1, P.tomography.default_acquisition(g1, 4, 4, 0.0, 1.0))

@@ -90,15 +90,17 @@ class DeviceCSR:
 
     @staticmethod
     def _fingerprint(H):
-        """Cheap identity of the host operator's contents: shape, nnz, the
-        buffer addresses and checksums of the first and last 1024 values and
-        indices (a few microseconds at cfg4), so a reallocated operator or an
-        in-place edit such as H.data *= s is not served from a stale device copy."""
+        """Cheap identity of the host operator's contents: shape, nnz, the buffer
+        addresses and a strided sample of 16 values and indices (~2 us; the update
+        calls this every step), so a reallocated operator or an in-place edit such as
+        H.data *= s is not served from a stale device copy."""
         if scipy.sparse.issparse(H) and H.format == "csr":
             d, ix = H.data, H.indices
+            if d.size == 0:
+                return (H.shape, 0, H.indptr.ctypes.data)
+            step = max(1, d.size // 16)
             return (H.shape, H.nnz, d.ctypes.data, ix.ctypes.data, H.indptr.ctypes.data,
-                    float(np.add.reduce(d[:1024])), float(np.add.reduce(d[-1024:])),
-                    int(np.add.reduce(ix[:1024], dtype=np.int64)), int(np.add.reduce(ix[-1024:], dtype=np.int64)))
+                    d[::step].tobytes(), ix[::step].tobytes())
         return None
 
     @classmethod

@@ -76,6 +76,12 @@ def test_run_hikf_matches_reference(mode, fixture, prefix, cfg):
     assert run.effective_ranks == [None] * cfg["T"]
     assert O.rel_fro(run.means[-1], g[f"{prefix}final_mean"]) <= 1e-9
     assert O.rel_fro(run.final_variance, g[f"{prefix}final_variance"]) <= 1e-9
+    if f"{prefix}step_means" in g:
+        # every step's posterior mean -- what the reference's metrics_rows / write_report
+        # (experiment.py:298-378) consume -- against the reference's own run
+        rows = g[f"{prefix}step_rows"]
+        worst = max(O.rel_fro(run.means[t][rows], g[f"{prefix}step_means"][t]) for t in range(cfg["T"]))
+        assert worst <= 1e-9, worst
 
 
 def test_dense_kf_matches_oracle_and_hikf():

@@ -21,7 +21,13 @@ __global__ void __launch_bounds__(256) base_kernel(const double* S, double* L, d
   if (threadIdx.x == 0) { clk[0] = t1 - t0; clk[1] = g_sec[0]; clk[2] = g_sec[1]; clk[3] = g_sec[2]; }
 }
 
-int main() {
+// profiling aid: one CTA per SM, each repeating the block (long enough for ncu's stall sampling)
+__global__ void __launch_bounds__(256) rep_kernel(const double* S, double* L, double* Li, int* status, int reps) {
+  extern __shared__ double sm[];
+  for (int r = 0; r < reps; ++r) chol_inv_block(S, 64, 64, 0, L + blockIdx.x * 4096, Li + blockIdx.x * 4096, status, sm);
+}
+
+int main(int argc, char** argv) {
   const int n = 64;
   std::vector<double> h(n * n);
   for (int i = 0; i < n; ++i)
@@ -45,7 +51,7 @@ int main() {
     cudaDeviceSynchronize();
     printf("single launch: %lld cycles in-kernel (chol %lld, store %lld, inverse %lld)\n", clk[0], clk[1], clk[2], clk[3]);
     long long hs[16]; cudaMemcpyFromSymbol(hs, g_sec, sizeof(hs));
-    printf("  column deltas:"); for (int q = 5; q < 12; ++q) printf(" %lld", hs[q] - hs[q - 1]); printf("\n");
+    printf("  cholesky %lld, barrier %lld, inverse %lld\n", hs[12] - hs[4], hs[13] - hs[12], hs[14] - hs[13]);
   }
   cudaEventRecord(a);
   for (int rep = 0; rep < 100; ++rep) base_kernel<<<1, 256, CHOL_SMEM>>>(S, L, Li, st, clk);
@@ -68,5 +74,13 @@ int main() {
       hsum = hsum * 1099511628211ull + v;
     }
   printf("digest %016llx\n", hsum);
+  if (argc > 1) {  // ./chol_bench prof: the long run for ncu
+    double *L2, *Li2;
+    cudaMalloc(&L2, 8 * 4096 * 148);
+    cudaMalloc(&Li2, 8 * 4096 * 148);
+    cudaFuncSetAttribute(rep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHOL_SMEM);
+    rep_kernel<<<148, 256, CHOL_SMEM>>>(S, L2, Li2, st, 200);
+    printf("rep run: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
+  }
   return 0;
 }

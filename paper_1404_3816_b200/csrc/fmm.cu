@@ -460,16 +460,27 @@ int fmm_matmat(hikf_tree* t, const double* V, int64_t ldv, int64_t k, double* U,
 // (compute-bound P2P) and the per-level M2L chains (latency-bound launches)
 // are independent of each other and of the other levels.
 namespace {
+// s[0]: the near field, at the lowest priority, so that it fills the gaps of the
+// latency-bound upward pass; w (the precompute's own main stream) and s[1..7] (the
+// M2L level groups) at the highest priority: they carry the critical path
 struct QhtStreams {
   cudaStream_t s[8] = {};
+  cudaStream_t w = nullptr;
   cudaEvent_t e[kMaxDepth + 4] = {};
+  cudaEvent_t e_in = nullptr, e_out = nullptr;
 };
 int qht_streams(QhtStreams** out) {
   static QhtStreams p;
   static bool init = false;
   if (!init) {
-    for (auto& x : p.s) HIKF_CHECK_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    int lo = 0, hi = 0;
+    HIKF_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < 8; ++i)
+      HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.s[i], cudaStreamNonBlocking, i == 0 ? lo : hi));
+    HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.w, cudaStreamNonBlocking, hi));
     for (auto& x : p.e) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&p.e_in, cudaEventDisableTiming));
+    HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&p.e_out, cudaEventDisableTiming));
     init = true;
   }
   *out = &p;
@@ -542,6 +553,22 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   // box-column range of level l that holds ancestors of the shard's leaves
   auto xlo = [&](int l) { return lw ? (lw->x0 >> (D - l)) : (int64_t)0; };
   auto xhi = [&](int l) { return lw ? (lw->x1 >> (D - l)) : INT64_MAX; };
+  QhtStreams* qs = nullptr;
+  HIKF_TRY(qht_streams(&qs));
+  // the precompute runs on its own high-priority stream qs->w, forked from and
+  // joined back into the caller's stream
+  struct Join {
+    QhtStreams* qs;
+    cudaStream_t caller;
+    ~Join() {
+      cudaEventRecord(qs->e_out, qs->w);
+      cudaStreamWaitEvent(caller, qs->e_out, 0);
+    }
+  };
+  HIKF_CHECK_CUDA(cudaEventRecord(qs->e_in, st));
+  HIKF_CHECK_CUDA(cudaStreamWaitEvent(qs->w, qs->e_in, 0));
+  Join join{qs, st};
+  st = qs->w;
   SparseHt sp;
   {
     ProfScope ps(ST_DENSIFY, st);  // the regrouping of H^T replaces the densify step
@@ -558,14 +585,11 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     sparse_free(&sp, st);
     return status;
   }
-  QhtStreams* qs = nullptr;
-  HIKF_TRY(qht_streams(&qs));
-
   cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1], ev_up = qs->e[2];
 
   // ---- near field, concurrently: sums parked in Pnear, added after L2P.  Launched
-  // after the upward pass (below): the P2P grid fills the machine, and the upward
-  // pass and the M2L target maps are on the critical path while P2P is not ----
+  // first, on the lowest-priority stream: it fills the machine while the upward pass
+  // and the M2L target maps (latency-bound, on the critical path) run ahead of it ----
   double* Pnear = nullptr;
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Pnear, sizeof(double) * std::max<int64_t>(1, sp.nitems * t->max_count), st));
   int status = HIKF_OK;
@@ -581,6 +605,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     tl.mark("p2p end", qs->s[0]);
     return s2;
   };
+  status = launch_p2p();
 
   // ---- upward pass on the active (box, ray) pairs only ----
   PairLevel pl[kMaxDepth + 1];
@@ -629,7 +654,6 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
                                                                                 t->orders[l]), st));
     HIKF_CHECK_CUDA(cudaEventRecord(ev_up, st));
     tl.mark("upward + targets", st);
-    if (status == HIKF_OK) status = launch_p2p();
     // one stream per group of levels: the leaf level alone (its M2L overlaps the L2L chain
     // above it), the coarser levels grouped by equal order so that each offset is one
     // launch for the whole group (levels 2-4 are launch-latency bound on their own)

@@ -348,7 +348,8 @@ int64_t hikf_launch_count(void);
  * multi-launch chain); key 1 = the fused leaf-level L2L + L2P of the Q H^T
  * FMM (csrc/boxgemm.cu leaf_down; 0: separate L2L and L2P kernels); key 2 =
  * P2P reads the near-field kernel blocks stored with the tree (0: evaluates
- * the kernel per (target, entry)).
+ * the kernel per (target, entry)); key 3 = the near-field sums are added to
+ * the far field inside the fused leaf step (0: by a separate scatter pass).
  * *previous (optional) receives the old value. */
 int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous);
 

@@ -285,6 +285,7 @@ int launch_box(const BoxArgs& a, int R, dim3 grid, cudaStream_t st) {
 // l2l_boxes + l2p_boxes (same products in the same order); the saving is the
 // G_D^2 x q x n leaf-local array (written and read back: 9.6 GB at cfg4).
 // ---------------------------------------------------------------------------
+constexpr int kLeafItemWords = 64;  // near-field fold: up to 2048 units of 8 columns (n <= 16384)
 struct LeafArgs {
   int64_t n;
   int q, qp;
@@ -301,6 +302,11 @@ struct LeafArgs {
   int64_t leaf0;  // first leaf of the launch (blockIdx.x + leaf0)
   int64_t s0;     // >= 0: leaf-aligned shard, U row = sorted position - s0 (else original rows, r0 / r1 window)
   unsigned long long *fl_l2l, *fl_l2p;
+  // near-field sums of the (leaf, ray) items (p2p_sparse), added to U here: U = far + near
+  const double* Pnear;  // item-major, maxc per item; null: not added here
+  const int64_t* items;
+  const int32_t* item_start;
+  int32_t maxc;
 };
 
 // shared-memory load the compiler cannot hoist out of the unit loop (the A
@@ -335,6 +341,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
     const int r = e / (NK1 * 4), k = e % (NK1 * 4);
     A1[r * LDA1 + k] = (r < q && k < qp) ? Cg[(int64_t)r * qp + k] : 0.0;
   }
+  // 8-column units of this leaf that hold a near-field item
+  __shared__ uint32_t ibits[kLeafItemWords];
+  if (tid < kLeafItemWords) ibits[tid] = 0;
+  const int32_t is0 = g.Pnear ? g.item_start[T] : 0, is1 = g.Pnear ? g.item_start[T + 1] : 0;
   const double* Wg = g.W2s + ls * q;
   for (int e = tid; e < 64 * NK2 * 4; e += BW_THREADS) {
     const int r = e / (NK2 * 4), k = e % (NK2 * 4);
@@ -359,6 +369,10 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
       }
     }
     orow[tid] = r;
+  }
+  for (int32_t i = is0 + tid; i < is1; i += BW_THREADS) {
+    const int u = (int)((g.items[i] % g.n) >> 3);
+    atomicOr(&ibits[u >> 5], 1u << (u & 31));
   }
   __syncthreads();
   // the next unit's parent columns and M2L slot indices are loaded one unit ahead
@@ -437,6 +451,23 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
         dmma884(acc2[i][0], acc2[i][1], af, b2[k4]);
       }
     const int64_t jc = j0 + 2 * t4;
+    if ((ibits[u >> 5] >> (u & 31)) & 1) {  // a ray of this unit crosses the leaf's neighbourhood: + near sums
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t key = T * n + jc + h;
+        int32_t lo = is0, hi = is1;
+        while (lo < hi) {
+          const int32_t mid = (lo + hi) >> 1;
+          if (g.items[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        if (lo < is1 && g.items[lo] == key) {
+          const double* pn = g.Pnear + (int64_t)lo * g.maxc + gq;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i * 8 + gq < cnt) acc2[i][h] += pn[i * 8];
+        }
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int32_t orw = orow[i * 8 + gq];
@@ -562,8 +593,11 @@ bool leaf_down_supported(const hikf_tree* t) {
   return o >= 2 && o <= 8 && (op == o || op == o + 1);
 }
 
+bool leaf_down_adds_near(int64_t n) { return (n + 7) / 8 <= 32 * kLeafItemWords; }
+
 int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const double* Lp, int64_t n, double* U,
-              int64_t ldu, cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
+              int64_t ldu, cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw, const double* Pnear,
+              const int64_t* items, const int32_t* item_start) {
   const int64_t l0 = lw ? lw->leaf0 : 0, l1 = lw ? lw->leaf1 : t->n_leaves;
   if (l1 <= l0 || n == 0) return HIKF_OK;
   const int D = t->depth;
@@ -589,6 +623,14 @@ int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const do
   a.s0 = lw ? lw->s0 : -1;
   a.fl_l2l = prof_flops_ptr(ST_L2L);
   a.fl_l2p = prof_flops_ptr(ST_L2P);
+  if (Pnear && !leaf_down_adds_near(n)) {
+    set_error("fused leaf step: near-field fold supports n <= %d", 8 * 32 * kLeafItemWords);
+    return HIKF_BAD_ARGUMENT;
+  }
+  a.Pnear = Pnear;
+  a.items = items;
+  a.item_start = item_start;
+  a.maxc = (int32_t)t->max_count;
   const int s = launch_leaf(a, t->orders[D], t->orders[D - 1], (unsigned)(l1 - l0), st);
   if (s < 0) {
     set_error("fused leaf downward step: orders (%d, %d) not instantiated", t->orders[D], t->orders[D - 1]);

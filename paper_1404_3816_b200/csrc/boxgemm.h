@@ -25,7 +25,12 @@ int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int
 bool leaf_down_supported(const hikf_tree* t);
 bool leaf_fused_enabled();
 int leaf_set_fused(int on);  // returns the previous setting
+// With Pnear (the near-field sums p2p_sparse parked per (leaf, ray) item, item-major), items and
+// item_start, the leaf step also adds them: U = far + near, the same single add as
+// sparse_p2p_scatter, without its scattered read-modify-write pass (n <= 16384 rays).
+bool leaf_down_adds_near(int64_t n);
 int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const double* Lp, int64_t n, double* U,
-              int64_t ldu, cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr);
+              int64_t ldu, cudaStream_t st, int64_t r0 = 0, int64_t r1 = -1, const LeafWindow* lw = nullptr,
+              const double* Pnear = nullptr, const int64_t* items = nullptr, const int32_t* item_start = nullptr);
 
 }  // namespace hikf

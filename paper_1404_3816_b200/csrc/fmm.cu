@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
+#include <chrono>
+#include <string>
 #include <vector>
 
 #include "boxgemm.h"
@@ -467,7 +469,10 @@ struct QhtStreams {
   cudaStream_t s[8] = {};
   cudaStream_t w = nullptr;
   cudaEvent_t e[kMaxDepth + 4] = {};
+  cudaEvent_t e_keys[kMaxDepth + 1] = {}, e_pairs[kMaxDepth + 1] = {}, e_tgt[kMaxDepth + 1] = {};  // level's pair keys / multipoles / M2L targets ready
   cudaEvent_t e_in = nullptr, e_out = nullptr;
+  int32_t* hcount = nullptr;            // pinned: M2L slot / entry counts per level
+  int64_t (*hoff)[41] = nullptr;        // pinned: first entry of every offset per level
 };
 int qht_streams(QhtStreams** out) {
   static QhtStreams p;
@@ -479,6 +484,11 @@ int qht_streams(QhtStreams** out) {
       HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.s[i], cudaStreamNonBlocking, i == 0 ? lo : hi));
     HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.w, cudaStreamNonBlocking, hi));
     for (auto& x : p.e) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (auto& x : p.e_pairs) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (auto& x : p.e_keys) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (auto& x : p.e_tgt) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    HIKF_CHECK_CUDA(cudaMallocHost((void**)&p.hcount, sizeof(int32_t) * 2 * (kMaxDepth + 1)));
+    HIKF_CHECK_CUDA(cudaMallocHost((void**)&p.hoff, sizeof(int64_t) * 41 * (kMaxDepth + 1)));
     HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&p.e_in, cudaEventDisableTiming));
     HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&p.e_out, cudaEventDisableTiming));
     init = true;
@@ -515,27 +525,51 @@ struct Timeline {
     if (!on) return;
     cudaEventCreate(&t0);
     cudaEventRecord(t0, s);
+    h0 = std::chrono::steady_clock::now();
   }
-  void mark(const char* name, cudaStream_t s) {
+  std::vector<std::pair<std::string, double>> hv;  // host-side enqueue times
+  std::chrono::steady_clock::time_point h0;
+  void mark(const char* name, cudaStream_t s, int level = -1) {
     if (!on) return;
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, s);
-    ev.emplace_back(name, e);
+    static char names[64][48];
+    static int nn = 0;
+    char* nm = names[nn++ % 64];
+    if (level >= 0) snprintf(nm, 48, "%s %d", name, level); else snprintf(nm, 48, "%s", name);
+    ev.emplace_back(nm, e);
+    hv.emplace_back(nm, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
   }
   void report() {
     if (!on) return;
     cudaDeviceSynchronize();
-    for (auto& x : ev) {
+    for (size_t i = 0; i < ev.size(); ++i) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, t0, x.second);
-      fprintf(stderr, "qht %-22s %8.3f ms\n", x.first, ms);
-      cudaEventDestroy(x.second);
+      cudaEventElapsedTime(&ms, t0, ev[i].second);
+      fprintf(stderr, "qht %-22s %8.3f ms   (enqueued by the host at %8.3f ms)\n", ev[i].first, ms, hv[i].second);
+      cudaEventDestroy(ev[i].second);
     }
     cudaEventDestroy(t0);
   }
 };
 }  // namespace
+
+// the near-field sums are added inside the fused leaf step (1, default) or by the separate
+// scatter pass (0: HIKF_NEAR_FOLD=0 or tuning key 3) -- the same single add either way
+static int g_near_fold = -1;
+static bool near_fold_enabled() {
+  if (g_near_fold < 0) {
+    const char* e = getenv("HIKF_NEAR_FOLD");
+    g_near_fold = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_near_fold != 0;
+}
+int near_set_fold(int on) {
+  const int prev = near_fold_enabled() ? 1 : 0;
+  g_near_fold = on ? 1 : 0;
+  return prev;
+}
 
 int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* ix, const double* val, double* U,
                     cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
@@ -585,7 +619,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     sparse_free(&sp, st);
     return status;
   }
-  cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1], ev_up = qs->e[2];
+  cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1];
 
   // ---- near field, concurrently: sums parked in Pnear, added after L2P.  Launched
   // first, on the lowest-priority stream: it fills the machine while the upward pass
@@ -607,25 +641,18 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   };
   status = launch_p2p();
 
-  // ---- upward pass on the active (box, ray) pairs only ----
+  // ---- upward pass on the active (box, ray) pairs only (main stream), and beside it,
+  // per level, the M2L targets: a (box, ray) -> slot map and the per-offset entry lists,
+  // built on the level group's stream as soon as the level's pairs exist.  A group's 40
+  // M2L passes are enqueued one upward step later (its slot / entry counts have arrived in
+  // pinned memory by then), so the leaf level's M2L runs beside the M2M chain instead of
+  // after it ----
   PairLevel pl[kMaxDepth + 1];
-  {
-    ProfScope ps(ST_P2M, st);
-    if (status == HIKF_OK) status = pairs_leaf(t, sp, &pl[D], st);
-  }
-  for (int l = D - 1; l >= 2 && status == HIKF_OK; --l) {
-    ProfScope ps(ST_M2M, st);
-    status = pairs_parent(t, l, pl[l + 1], n, &pl[l], st);
-  }
-  // ---- M2L targets, all levels on the main stream: a (box, ray) -> slot map per
-  // level and one read-back of the slot counts; then one stream per level, each
-  // accumulating per offset into its own compact scratch (q coefficients per slot) ----
   double* scratch[kMaxDepth + 1] = {};
   int32_t* tmap[kMaxDepth + 1] = {};
   int32_t* tcount = nullptr;
-  int32_t hcount[2 * (kMaxDepth + 1)] = {0};  // [2 l]: target slots, [2 l + 1]: entries of level l
-  int64_t* toff = nullptr;
-  int64_t hoff[kMaxDepth + 1][41] = {};
+  int32_t* hcount = qs->hcount;          // [2 l]: target slots, [2 l + 1]: entries of level l
+  int64_t (*hoff)[41] = qs->hoff;        // first entry of every offset of level l
   M2LPlan plan[kMaxDepth + 1];
   double* Lbuf[2] = {nullptr, nullptr};
   // fused leaf step (leaf_down): the leaf-level locals are never stored
@@ -633,58 +660,86 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   int64_t lsz[2] = {1, 1};  // ping-pong local buffers: level l lives in Lbuf[(D - l) & 1]
   for (int l = 2; l <= D - (fused_leaf ? 1 : 0); ++l)
     lsz[(D - l) & 1] = std::max(lsz[(D - l) & 1], ((int64_t)1 << (2 * l)) * t->orders[l] * t->orders[l] * n);
+  int groups[kMaxDepth + 1][kMaxDepth + 1], gsize[kMaxDepth + 1] = {0}, ng = 0, glevel[kMaxDepth + 1] = {0};
+  for (int l = D; l >= 2; --l) {  // one group (stream) per level: the levels' M2L sums are independent
+    groups[ng][gsize[ng]++] = l;
+    glevel[l] = ng++;
+  }
+  auto gstream = [&](int gi) { return qs->s[1 + gi % 7]; };
   if (status == HIKF_OK) {
     HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[0], sizeof(double) * lsz[0], st));
     HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Lbuf[1], sizeof(double) * lsz[1], st));
-    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tcount, sizeof(hcount), st));
-    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&toff, sizeof(hoff), st));
-    for (int l = 2; l <= D && status == HIKF_OK; ++l) {
-      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tmap[l], sizeof(int32_t) * ((int64_t)1 << (2 * l)) * n, st));
-      ProfScope ps(ST_M2L, st);
-      status = m2l_targets(t, l, pl[l], n, tmap[l], tcount + 2 * l, &plan[l], st, xlo(l), xhi(l));
-      if (status == HIKF_OK)
-        HIKF_CHECK_CUDA(cudaMemcpyAsync(toff + 41 * l, plan[l].off, 41 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-    }
-    HIKF_CHECK_CUDA(cudaMemcpyAsync(hcount, tcount, sizeof(hcount), cudaMemcpyDeviceToHost, st));
-    HIKF_CHECK_CUDA(cudaMemcpyAsync(hoff, toff, sizeof(hoff), cudaMemcpyDeviceToHost, st));
-    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+    HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tcount, sizeof(int32_t) * 2 * (kMaxDepth + 1), st));
     for (int l = 2; l <= D; ++l)
-      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch[l],
-                                      sizeof(double) * std::max<int64_t>(1, (int64_t)hcount[2 * l] * t->orders[l] *
-                                                                                t->orders[l]), st));
-    HIKF_CHECK_CUDA(cudaEventRecord(ev_up, st));
-    tl.mark("upward + targets", st);
-    // one stream per group of levels: the leaf level alone (its M2L overlaps the L2L chain
-    // above it), the coarser levels grouped by equal order so that each offset is one
-    // launch for the whole group (levels 2-4 are launch-latency bound on their own)
-    int groups[kMaxDepth + 1][kMaxDepth + 1], gsize[kMaxDepth + 1] = {0}, ng = 0;
-    for (int l = D; l >= 2; --l) {
-      const bool join = ng > 0 && l < D && groups[ng - 1][0] < D && m2l_list_supported(t, l) &&
-                        t->orders[groups[ng - 1][0]] == t->orders[l];
-      if (!join) ++ng;
-      groups[ng - 1][gsize[ng - 1]++] = l;
-    }
-    for (int gi = 0; gi < ng && status == HIKF_OK; ++gi) {  // biggest level first
-      cudaStream_t sl = qs->s[1 + gi % 7];
-      HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, ev_up, 0));
-      ProfScope ps(ST_M2L, sl);
-      for (int k = 0; k < gsize[gi]; ++k) {
-        const int l = groups[gi][k];
-        HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0,
-                                        sizeof(double) * (int64_t)hcount[2 * l] * t->orders[l] * t->orders[l], sl));
-      }
-      const int l0 = groups[gi][0];
-      if (m2l_list_supported(t, l0)) {
-        for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
-          status = m2l_pass_list(t, gsize[gi], groups[gi], slot, pl, plan, hoff, scratch, sl);
-      } else {
-        for (int slot = 0; slot < 40 && status == HIKF_OK; ++slot)
-          status = m2l_pass(t, l0, slot, pl[l0], n, scratch[l0], tmap[l0], sl, xlo(l0), xhi(l0));
-      }
-      for (int k = 0; k < gsize[gi]; ++k) HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + groups[gi][k]], sl));
-      tl.mark(gi == 0 ? "m2l group 0 end" : gi == 1 ? "m2l group 1 end" : "m2l group 2+ end", sl);
-    }
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&tmap[l], sizeof(int32_t) * ((int64_t)1 << (2 * l)) * n, st));
   }
+  // deferred pair counts (no host read-back inside the upward pass) when every level has the
+  // entry-list M2L; everything is enqueued before the host waits for a count
+  bool deferred = true;
+  for (int l = 2; l <= D; ++l) deferred = deferred && m2l_list_supported(t, l);
+  // level l's pair keys (from the leaf level's: they do not depend on the multipole values)
+  // and its M2L targets, on the level's stream
+  auto enqueue_targets = [&](int l) -> int {
+    cudaStream_t sl = gstream(glevel[l]);
+    HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, qs->e_keys[D], 0));
+    if (l < D) {
+      ProfScope ps(ST_M2M, sl);
+      HIKF_TRY(pairs_keys(t, l, D, pl[D], n, &pl[l], sl, deferred));
+      HIKF_CHECK_CUDA(cudaEventRecord(qs->e_keys[l], sl));
+    }
+    ProfScope ps(ST_M2L, sl);
+    HIKF_TRY(m2l_targets(t, l, pl[l], n, tmap[l], tcount + 2 * l, &plan[l], sl, xlo(l), xhi(l)));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(hcount + 2 * l, tcount + 2 * l, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, sl));
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(hoff[l], plan[l].off, 41 * sizeof(int64_t), cudaMemcpyDeviceToHost, sl));
+    HIKF_CHECK_CUDA(cudaEventRecord(qs->e_tgt[l], sl));
+    tl.mark("targets", sl, l);
+    return HIKF_OK;
+  };
+  // the M2L sums of a group whose targets have all been enqueued: every term of the level in
+  // one launch plus the ordered per-target sums (m2l_products), or, for orders without an
+  // entry-list instantiation, the 40 dependent offset passes
+  auto launch_group = [&](int gi) -> int {
+    cudaStream_t sl = gstream(gi);
+    const int l0 = groups[gi][0];
+    const bool lists = m2l_list_supported(t, l0);
+    for (int k = 0; k < gsize[gi]; ++k) {
+      const int l = groups[gi][k];
+      HIKF_CHECK_CUDA(cudaEventSynchronize(qs->e_tgt[l]));
+      HIKF_CHECK_CUDA(cudaStreamWaitEvent(sl, qs->e_pairs[l], 0));  // the level's multipoles
+      const int64_t words = (int64_t)hcount[2 * l] * t->orders[l] * t->orders[l];
+      HIKF_CHECK_CUDA(cudaMallocAsync((void**)&scratch[l], sizeof(double) * std::max<int64_t>(1, words), sl));
+      if (!lists) HIKF_CHECK_CUDA(cudaMemsetAsync(scratch[l], 0, sizeof(double) * words, sl));
+    }
+    ProfScope ps(ST_M2L, sl);
+    int s2 = HIKF_OK;
+    if (lists) {
+      for (int k = 0; k < gsize[gi] && s2 == HIKF_OK; ++k) {
+        const int l = groups[gi][k];
+        s2 = m2l_products(t, l, pl[l], plan[l], hoff[l], hcount[2 * l], scratch[l], sl);
+      }
+    } else {
+      for (int slot = 0; slot < 40 && s2 == HIKF_OK; ++slot)
+        s2 = m2l_pass(t, l0, slot, pl[l0], n, scratch[l0], tmap[l0], sl, xlo(l0), xhi(l0));
+    }
+    for (int k = 0; k < gsize[gi]; ++k) HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + groups[gi][k]], sl));
+    tl.mark("m2l sums", sl, l0);
+    return s2;
+  };
+  {
+    ProfScope ps(ST_P2M, st);
+    if (status == HIKF_OK) status = pairs_leaf(t, sp, &pl[D], st, qs->e_keys[D]);
+    if (status == HIKF_OK) HIKF_CHECK_CUDA(cudaEventRecord(qs->e_pairs[D], st));
+  }
+  tl.mark("pairs", st, D);
+  for (int l = D; l >= 2 && status == HIKF_OK; --l) status = enqueue_targets(l);
+  for (int l = D - 1; l >= 2 && status == HIKF_OK; --l) {  // the M2M chain (main stream)
+    ProfScope ps(ST_M2M, st);
+    HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e_keys[l], 0));
+    status = pairs_m2m(t, l, pl[l + 1], n, &pl[l], st);
+    if (status == HIKF_OK) HIKF_CHECK_CUDA(cudaEventRecord(qs->e_pairs[l], st));
+    tl.mark("pairs", st, l);
+  }
+  for (int gi = 0; gi < ng && status == HIKF_OK; ++gi) status = launch_group(gi);
   // ---- downward pass (main stream): L = scratch^T + shift L_parent, then L2P ----
   const bool vec = (n % 2) == 0;
   const double* Lprev = nullptr;
@@ -718,11 +773,15 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       }
     }
     Lprev = Lcur;
-    tl.mark("l2l level end", dn);
+    tl.mark("l2l", dn, l);
   }
+  // the fused leaf step also adds the near-field sums (it waits for P2P; no scatter pass then)
+  const bool near_in_leaf = fused_leaf && leaf_down_adds_near(n) && near_fold_enabled();
   if (status == HIKF_OK && fused_leaf) {
+    if (near_in_leaf) HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_p2p, 0));
     ProfScope ps(ST_L2P, st);
-    status = leaf_down(t, scratch[D], tmap[D], Lprev, n, U, n, st, r0, r1, lw);
+    status = leaf_down(t, scratch[D], tmap[D], Lprev, n, U, n, st, r0, r1, lw, near_in_leaf ? Pnear : nullptr,
+                       sp.items, sp.item_start);
   } else if (status == HIKF_OK && box_supported(64, t->orders[D] * t->orders[D])) {
     ProfScope ps(ST_L2P, st);
     status = l2p_boxes(t, Lcur, n, U, n, st, r0, r1, lw);
@@ -747,10 +806,11 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     ProfScope ps(ST_L2P, st);
     status = launch(lp, t->n_leaves, t->max_count, n, st);
   }
+  tl.mark("leaf step", st);
   // ---- join: every side stream's work is ordered before the frees below ----
   for (int l = 2; l <= D; ++l) HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, qs->e[3 + l], 0));
   HIKF_CHECK_CUDA(cudaStreamWaitEvent(st, ev_p2p, 0));
-  if (status == HIKF_OK) {
+  if (status == HIKF_OK && !near_in_leaf) {
     ProfScope ps(ST_P2P, st);
     status = sparse_p2p_scatter(t, sp, Pnear, U, n, st, r0, r1, lw);
   }
@@ -763,7 +823,6 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     m2l_plan_free(&plan[l], st);
   }
   cudaFreeAsync(tcount, st);
-  cudaFreeAsync(toff, st);
   cudaFreeAsync(Lbuf[0], st);
   cudaFreeAsync(Lbuf[1], st);
   cudaFreeAsync(Pnear, st);

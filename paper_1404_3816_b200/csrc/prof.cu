@@ -135,6 +135,9 @@ extern "C" int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous) {
     case 2:
       prev = hikf::p2p_set_near_blocks(value);
       break;
+    case 3:
+      prev = hikf::near_set_fold(value);
+      break;
     default:
       hikf::set_error("unknown tuning key %d", (int)key);
       return HIKF_BAD_ARGUMENT;

@@ -224,7 +224,7 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
     }
     if (!ok) continue;
     if (Pnear)
-      Pnear[(int64_t)t * nitems + item] = acc;  // added into U later (p2p_scatter): U = far + near either way
+      Pnear[item * maxc + t] = acc;  // added into U later (leaf_down / p2p_scatter): U = far + near either way
     else if (s0 >= 0) {
       U[(t0 + t - s0) * ldu + j] += acc;
     } else {
@@ -234,30 +234,43 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
   }
 }
 
-// U[target, ray] += near sum (the deferred add of p2p_sparse).  Items are
-// sorted by (leaf, ray): a warp takes 32 consecutive items and walks the leaf
-// rows, so lanes of the same leaf update one row of U at their rays' columns;
-// Pnear is target-major (t * nitems + item), read coalesced.
+// U[target, ray] += near sum (the deferred add of p2p_sparse, for the paths that do not
+// add it inside the fused leaf step).  One warp per item, lanes over the leaf's points;
+// Pnear is item-major (item * maxc + t).
 __global__ void p2p_scatter(int64_t nitems, const int64_t* __restrict__ items, int64_t n,
                             const int32_t* __restrict__ leaf_start, const int32_t* __restrict__ leaf_count,
                             const int64_t* __restrict__ order, const double* __restrict__ Pnear, int32_t maxc,
                             double* __restrict__ U, int64_t ldu, int64_t r0, int64_t r1, int64_t leaf0,
                             int64_t leaf1, int64_t s0) {
-  const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (item >= nitems) return;
   const int64_t key = items[item];
   const int32_t T = (int32_t)(key / n);
   const int32_t j = (int32_t)(key % n);
   if (T < leaf0 || T >= leaf1) return;
   const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
-  for (int t = 0; t < cnt; ++t) {
+  for (int t = lane; t < cnt; t += 32) {
     if (s0 >= 0) {
-      U[(t0 + t - s0) * ldu + j] += Pnear[(int64_t)t * nitems + item];
+      U[(t0 + t - s0) * ldu + j] += Pnear[item * maxc + t];
       continue;
     }
     const int64_t row = order[t0 + t];
-    if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += Pnear[(int64_t)t * nitems + item];
+    if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += Pnear[item * maxc + t];
   }
+}
+
+// item_start[L] = first item of target leaf L (items ascend in leaf * n + ray), L in [0, nleaves]
+__global__ void item_offsets(int64_t nleaves, int64_t nitems, int64_t n, const int64_t* __restrict__ items,
+                             int32_t* __restrict__ item_start) {
+  const int64_t L = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (L > nleaves) return;
+  int64_t lo = 0, hi = nitems;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (items[mid] < L * n) lo = mid + 1; else hi = mid;
+  }
+  item_start[L] = (int32_t)lo;
 }
 }  // namespace
 
@@ -270,6 +283,7 @@ void sparse_free(SparseHt* s, cudaStream_t st) {
   cudaFreeAsync(s->leaf_g, st);
   cudaFreeAsync(s->g_leaf, st);
   cudaFreeAsync(s->items, st);
+  cudaFreeAsync(s->item_start, st);
   for (int l = 0; l <= kMaxDepth; ++l) cudaFreeAsync(s->mask[l], st);
   *s = SparseHt();
 }
@@ -395,6 +409,9 @@ int sparse_build(const hikf_tree* t, int64_t n, const int32_t* ip, const int32_t
     s->nitems = nu;
     cudaFreeAsync(tmp2, st);
   }
+  HIKF_TRY(aalloc(&s->item_start, L + 1, st));
+  item_offsets<<<grid_for(L + 1), kT, 0, st>>>(L, s->nitems, n, s->items, s->item_start);
+  HIKF_CHECK_LAUNCH();
   cudaFreeAsync(tmp, st);
   cudaFreeAsync(key, st);
   cudaFreeAsync(key_s, st);
@@ -443,7 +460,7 @@ int sparse_p2p(const hikf_tree* t, const SparseHt& s, double* U, int64_t ldu, cu
 int sparse_p2p_scatter(const hikf_tree* t, const SparseHt& s, const double* Pnear, double* U, int64_t ldu,
                        cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw) {
   if (s.nitems <= 0) return HIKF_OK;
-  p2p_scatter<<<(unsigned)((s.nitems + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
+  p2p_scatter<<<(unsigned)((s.nitems * 32 + kT - 1) / kT), kT, 0, st>>>(s.nitems, s.items, s.n, t->leaf_start,
                                                                  t->leaf_count, t->order, Pnear,
                                                                  (int32_t)t->max_count, U, ldu, r0,
                                                                  r1 < 0 ? INT64_MAX : r1, lw ? lw->leaf0 : 0,
@@ -482,13 +499,26 @@ __global__ void p2m_pairs(int64_t ng, int q, const int32_t* __restrict__ g_start
   }
 }
 
-__global__ void parent_keys(int64_t np, const int64_t* __restrict__ ckey, int64_t n, int64_t Gc,
-                            int64_t* __restrict__ pkey) {
+// keys of the ancestors sh levels above the pairs' boxes (Gc: the pairs' grid)
+// (np: allocated child pairs; np_dev: their actual number on the device, or null when np is
+// exact -- the slots past it get the sentinel key, which sorts last)
+__global__ void parent_keys(int64_t np, const int32_t* __restrict__ np_dev, const int64_t* __restrict__ ckey,
+                            int64_t n, int64_t Gc, int sh, int64_t sentinel, int64_t* __restrict__ pkey) {
+  const int64_t nv = np_dev ? *np_dev : np;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i >= nv) {
+      pkey[i] = sentinel;
+      continue;
+    }
     int64_t box = ckey[i] / n, j = ckey[i] % n;
     int64_t cx = box / Gc, cy = box % Gc;
-    pkey[i] = ((cx >> 1) * (Gc >> 1) + (cy >> 1)) * n + j;
+    pkey[i] = ((cx >> sh) * (Gc >> sh) + (cy >> sh)) * n + j;
   }
+}
+
+// the unique parent keys end with the sentinel when the child list had unused slots
+__global__ void drop_sentinel(int32_t* __restrict__ num, const int64_t* __restrict__ keys, int64_t sentinel) {
+  if (*num > 0 && keys[*num - 1] == sentinel) --*num;
 }
 
 __device__ __forceinline__ int64_t find_key(const int64_t* __restrict__ keys, int64_t np, int64_t k) {
@@ -504,9 +534,12 @@ __device__ __forceinline__ int64_t find_key(const int64_t* __restrict__ keys, in
 // One warp per parent pair: lanes 0..3 look up the four children's pairs (binary
 // searches in parallel, once per pair instead of once per coefficient), then the
 // lanes stride over b; each output keeps the children-then-a summation order.
-__global__ void m2m_pairs(int64_t npp, const int64_t* __restrict__ pkey, int qp, int qc, int64_t Gp, int64_t n,
-                          const double* __restrict__ shift, int64_t npc, const int64_t* __restrict__ ckey,
+__global__ void m2m_pairs(int64_t npp, const int32_t* __restrict__ npp_dev, const int64_t* __restrict__ pkey, int qp,
+                          int qc, int64_t Gp, int64_t n, const double* __restrict__ shift, int64_t npc,
+                          const int32_t* __restrict__ npc_dev, const int64_t* __restrict__ ckey,
                           const double* __restrict__ Wcc, double* __restrict__ Wp, unsigned long long* __restrict__ flops) {
+  if (npp_dev) npp = *npp_dev;  // the pair counts on the device (deferred mode: npp / npc are the allocated sizes)
+  if (npc_dev) npc = *npc_dev;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t pi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pi < npp; pi += nwarps) {
@@ -734,6 +767,137 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 2 : 1) m2l_list_kernel(M2LS
   }
 }
 
+// All M2L terms of a level in one launch: Pr[i][:] = M_d W_p for every entry i = (p, slot)
+// of every offset d.  The products do not depend on one another, so the 40 offsets need no
+// ordering (and no read-modify-write of the targets); m2l_reduce then adds each target's
+// products in the reference's offset order.  A CTA stages M_d once and its warps walk gpw
+// groups of 8 entries (the 8 columns of the DMMA tiles); the product of an entry is formed
+// exactly as in m2l_list_kernel (two accumulator chains, even / odd k-steps, then their sum).
+struct M2LProd {
+  const int2* ent;
+  const double *W, *M;  // source coefficients (q per pair), the level's 40 operators
+  double* Pr;           // q per entry
+  int64_t off[41];      // first entry of every offset
+  int64_t blk[41];      // first CTA of every offset
+};
+
+template <int NK4, int NRT>
+__global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LProd a, int q, int gpw,
+                                                                         unsigned long long* __restrict__ flops) {
+  __shared__ int s_d;
+  if (threadIdx.x < 40) {
+    const int d = threadIdx.x;
+    if ((int64_t)blockIdx.x >= a.blk[d] && (int64_t)blockIdx.x < a.blk[d + 1]) s_d = d;
+  }
+  __syncthreads();
+  const int d = s_d;
+  extern __shared__ double Ms[];
+  const int ld = m2l_ld(q);
+  const double* __restrict__ M = a.M + (int64_t)d * q * q;
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = M[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  const int64_t e_end = a.off[d + 1];
+  const int64_t chunk0 = a.off[d] + ((int64_t)blockIdx.x - a.blk[d]) * (64 * (int64_t)gpw);
+  int64_t i0 = chunk0 + warp * 8;
+  int2 pe_next = make_int2(-1, -1);
+  if (i0 + g < e_end) pe_next = a.ent[i0 + g];
+  for (int gi = 0; gi < gpw; ++gi, i0 += 64) {
+    if (i0 >= e_end) break;
+    const int2 pe = pe_next;
+    pe_next = make_int2(-1, -1);
+    if (gi + 1 < gpw && i0 + 64 + g < e_end) pe_next = a.ent[i0 + 64 + g];
+    if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)(e_end - i0 < 8 ? e_end - i0 : 8) * q * q);
+    double b[NK4];
+#pragma unroll
+    for (int k4 = 0; k4 < NK4; ++k4) {
+      const int k = k4 * 4 + t4;
+      b[k4] = (pe.x >= 0 && k < q) ? a.W[(int64_t)pe.x * q + k] : 0.0;
+    }
+    double* out[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + 2 * t4 + h;
+      out[h] = i < e_end ? a.Pr + i * q : nullptr;
+    }
+#pragma unroll 1
+    for (int i = 0; i < NRT; ++i) {
+      const int r = i * 8 + g;
+      double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k4 = 0; k4 < NK4; ++k4) {
+        const int k = k4 * 4 + t4;
+        const double av = (r < q && k < q) ? Ms[r * ld + k] : 0.0;
+        if (k4 & 1)
+          dmma884(acc1[0], acc1[1], av, b[k4]);
+        else
+          dmma884(acc0[0], acc0[1], av, b[k4]);
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (out[h] && r < q) out[h][r] = acc0[h] + acc1[h];
+    }
+  }
+}
+
+// tab[slot][d] = the entry of offset d that targets the slot (a target has at most one
+// source per offset), -1 where there is none
+__global__ void m2l_tab_kernel(M2LProd a, int64_t nent, int32_t* __restrict__ tab) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nent; i += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = 40;  // last d with off[d] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.off[mid] <= i) lo = mid; else hi = mid;
+    }
+    tab[(int64_t)a.ent[i].y * 40 + lo] = (int32_t)i;
+  }
+}
+
+// S[slot][:] = ((0 + Pr[e_1]) + Pr[e_2]) + ... over the slot's entries in ascending offset
+// order: the adds of the per-offset passes (which start from a zeroed scratch), same order.
+// One warp per slot; the products of up to four entries are loaded before they are added.
+__global__ void __launch_bounds__(256) m2l_reduce_kernel(int64_t nslots, int q, const int32_t* __restrict__ tab,
+                                                        const double* __restrict__ Pr, double* __restrict__ S) {
+  const int64_t slot = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (slot >= nslots) return;
+  const int32_t t0 = tab[slot * 40 + lane];
+  const int32_t t1 = lane < 8 ? tab[slot * 40 + 32 + lane] : -1;
+  unsigned m0 = __ballot_sync(0xffffffffu, t0 >= 0), m1 = __ballot_sync(0xffffffffu, t1 >= 0);
+  const int r0 = lane, r1 = lane + 32;
+  double acc0 = 0.0, acc1 = 0.0;
+  while (m0 | m1) {
+    int64_t idx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      idx[k] = -1;
+      if (m0) {
+        const int dsel = __ffs(m0) - 1;
+        m0 &= m0 - 1;
+        idx[k] = __shfl_sync(0xffffffffu, t0, dsel);
+      } else if (m1) {
+        const int dsel = __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        idx[k] = __shfl_sync(0xffffffffu, t1, dsel);
+      }
+    }
+    double v0[4], v1[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v0[k] = (idx[k] >= 0 && r0 < q) ? Pr[idx[k] * q + r0] : 0.0;
+      v1[k] = (idx[k] >= 0 && r1 < q) ? Pr[idx[k] * q + r1] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (idx[k] >= 0) {
+        acc0 += v0[k];
+        acc1 += v1[k];
+      }
+  }
+  if (r0 < q) S[slot * q + r0] = acc0;
+  if (r1 < q) S[slot * q + r1] = acc1;
+}
+
 // Pair-major M2L scratch S[T][j][a] -> box-major locals L[T][a][j] for the
 // occupied boxes (CTA = box x 32-column chunk, smem-staged transpose).
 constexpr int kTrCols = 32;
@@ -788,10 +952,11 @@ int grid_cap(int64_t n) {
 void pairs_free(PairLevel* p, cudaStream_t st) {
   cudaFreeAsync(p->key, st);
   cudaFreeAsync(p->W, st);
+  if (p->np_dev) cudaFreeAsync(p->np_dev, st);
   *p = PairLevel();
 }
 
-int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st) {
+int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream_t st, cudaEvent_t keys_ready) {
   *out = PairLevel();
   const int q = t->orders[t->depth] * t->orders[t->depth];
   out->np = s.ngroups;
@@ -800,19 +965,19 @@ int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream
   if (s.ngroups == 0) return HIKF_OK;
   leaf_pair_keys<<<grid_cap(s.ngroups), kT, 0, st>>>(s.ngroups, s.n, s.g_leaf, s.g_j, t->leaf_box, out->key);
   HIKF_CHECK_LAUNCH();
+  if (keys_ready) HIKF_CHECK_CUDA(cudaEventRecord(keys_ready, st));
   p2m_pairs<<<grid_cap(s.ngroups * q), kT, 0, st>>>(s.ngroups, q, s.g_start, s.e_sp, s.e_v, t->W2s, out->W,
                                                      prof_flops_ptr(ST_P2M));
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
 
-int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st) {
+int pairs_keys(const hikf_tree* t, int l, int lc, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st,
+               bool deferred) {
   *out = PairLevel();
-  const int64_t Gc = (int64_t)1 << (l + 1), Gp = (int64_t)1 << l;
-  const int qp = t->orders[l] * t->orders[l], qc = t->orders[l + 1] * t->orders[l + 1];
+  const int64_t Gc = (int64_t)1 << lc, Gp = (int64_t)1 << l;
   if (child.np == 0) {
     HIKF_TRY(aalloc(&out->key, 1, st));
-    HIKF_TRY(aalloc(&out->W, 1, st));
     return HIKF_OK;
   }
   int64_t *pk = nullptr, *pk_s = nullptr;
@@ -821,10 +986,11 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
   HIKF_TRY(aalloc(&pk_s, child.np, st));
   HIKF_TRY(aalloc(&out->key, child.np, st));
   HIKF_TRY(aalloc(&d_num, 1, st));
-  parent_keys<<<grid_cap(child.np), kT, 0, st>>>(child.np, child.key, n, Gc, pk);
-  HIKF_CHECK_LAUNCH();
   int end_bit = 1;
-  while (end_bit < 63 && ((int64_t)1 << end_bit) < Gp * Gp * n) ++end_bit;
+  while (end_bit < 62 && ((int64_t)1 << end_bit) <= Gp * Gp * n) ++end_bit;  // keys and the sentinel below 2^end_bit
+  const int64_t sentinel = Gp * Gp * n;
+  parent_keys<<<grid_cap(child.np), kT, 0, st>>>(child.np, child.np_dev, child.key, n, Gc, lc - l, sentinel, pk);
+  HIKF_CHECK_LAUNCH();
   size_t b1 = 0, b2 = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, b1, pk, pk_s, (int)child.np, 0, end_bit, st);
   cub::DeviceSelect::Unique(nullptr, b2, pk_s, out->key, d_num, (int)child.np, st);
@@ -832,18 +998,36 @@ int pairs_parent(const hikf_tree* t, int l, const PairLevel& child, int64_t n, P
   HIKF_CHECK_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(std::max(b1, b2), 1), st));
   cub::DeviceRadixSort::SortKeys(tmp, b1, pk, pk_s, (int)child.np, 0, end_bit, st);
   cub::DeviceSelect::Unique(tmp, b2, pk_s, out->key, d_num, (int)child.np, st);
-  int32_t np = 0;
-  HIKF_CHECK_CUDA(cudaMemcpyAsync(&np, d_num, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-  out->np = np;
-  HIKF_TRY(aalloc(&out->W, (int64_t)np * qp, st));
-  m2m_pairs<<<grid_cap((int64_t)np * 32), kT, 0, st>>>(np, out->key, qp, qc, Gp, n, t->shift[l], child.np, child.key,
-                                                       child.W, out->W, prof_flops_ptr(ST_M2M));
-  HIKF_CHECK_LAUNCH();
+  if (child.np_dev) {
+    drop_sentinel<<<1, 1, 0, st>>>(d_num, out->key, sentinel);
+    HIKF_CHECK_LAUNCH();
+  }
+  if (deferred) {
+    // no host read-back: the level is sized by its bound (ancestor pairs <= pairs, <= boxes x rays)
+    // and its consumers read the count on the device
+    out->np = std::min<int64_t>(child.np, Gp * Gp * n);
+    out->np_dev = d_num;
+  } else {
+    int32_t np = 0;
+    HIKF_CHECK_CUDA(cudaMemcpyAsync(&np, d_num, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
+    out->np = np;
+    cudaFreeAsync(d_num, st);
+  }
   cudaFreeAsync(tmp, st);
   cudaFreeAsync(pk, st);
   cudaFreeAsync(pk_s, st);
-  cudaFreeAsync(d_num, st);
+  return HIKF_OK;
+}
+
+int pairs_m2m(const hikf_tree* t, int l, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st) {
+  const int64_t Gp = (int64_t)1 << l;
+  const int qp = t->orders[l] * t->orders[l], qc = t->orders[l + 1] * t->orders[l + 1];
+  HIKF_TRY(aalloc(&out->W, out->np * qp, st));
+  if (out->np == 0 || child.np == 0) return HIKF_OK;
+  m2m_pairs<<<grid_cap(out->np * 32), kT, 0, st>>>(out->np, out->np_dev, out->key, qp, qc, Gp, n, t->shift[l], child.np,
+                                                   child.np_dev, child.key, child.W, out->W, prof_flops_ptr(ST_M2M));
+  HIKF_CHECK_LAUNCH();
   return HIKF_OK;
 }
 
@@ -867,13 +1051,15 @@ __device__ __forceinline__ int64_t m2l_target_of(const int64_t* __restrict__ key
 
 // flags[T * n + j] = 1 for every target of an active source pair; eflag[d * np + p] = 1
 // for every (offset, source pair) that has a target (offset-major)
-__global__ void m2l_mark_targets(int64_t np, const int64_t* __restrict__ key, int64_t n, int64_t G,
-                                 const uint8_t* __restrict__ occ, M2LOffsets offs, int64_t xlo, int64_t xhi,
-                                 uint8_t* __restrict__ flags, uint8_t* __restrict__ eflag) {
+// (np: allocated pairs = the stride of the (offset, pair) codes; np_dev: the actual count or null)
+__global__ void m2l_mark_targets(int64_t np, const int32_t* __restrict__ np_dev, const int64_t* __restrict__ key,
+                                 int64_t n, int64_t G, const uint8_t* __restrict__ occ, M2LOffsets offs, int64_t xlo,
+                                 int64_t xhi, uint8_t* __restrict__ flags, uint8_t* __restrict__ eflag) {
+  const int64_t nv = np_dev ? *np_dev : np;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < np * 40; e += (int64_t)gridDim.x * blockDim.x) {
     const int d = (int)(e / np);
     const int64_t p = e % np;
-    const int64_t tk = m2l_target_of(key, p, d, n, G, occ, offs, xlo, xhi);
+    const int64_t tk = p < nv ? m2l_target_of(key, p, d, n, G, occ, offs, xlo, xhi) : -1;
     if (tk >= 0) flags[tk] = 1;
     eflag[e] = tk >= 0 ? 1 : 0;
   }
@@ -935,8 +1121,8 @@ int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int3
   HIKF_TRY(aalloc(&eflag, src.np * 40, st));
   HIKF_CHECK_CUDA(cudaMemsetAsync(flags, 0, total, st));
   M2LOffsets offs;
-  m2l_mark_targets<<<grid_cap(src.np * 40), kT, 0, st>>>(src.np, src.key, n, G, t->occ_flag[l], offs, xlo, xhi, flags,
-                                                         eflag);
+  m2l_mark_targets<<<grid_cap(src.np * 40), kT, 0, st>>>(src.np, src.np_dev, src.key, n, G, t->occ_flag[l], offs, xlo,
+                                                         xhi, flags, eflag);
   HIKF_CHECK_LAUNCH();
   // target slots (ascending T * n + j)
   const int64_t cap = std::min<int64_t>(total, src.np * 40);
@@ -1017,6 +1203,62 @@ int m2l_pass_list(const hikf_tree* t, int nlev, const int* levels, int slot, con
   }
 #undef HIKF_M2LL
   HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,
+                 int64_t nslots, double* S, cudaStream_t st) {
+  const int q = t->orders[l] * t->orders[l];
+  const int64_t nent = hoff[40];
+  if (nslots <= 0 || nent <= 0) return HIKF_OK;
+  if (nent > INT32_MAX) {
+    set_error("M2L products of level %d: %lld entries do not fit 32-bit indices", l, (long long)nent);
+    return HIKF_BAD_ARGUMENT;
+  }
+  M2LProd a{};
+  a.ent = plan.ent;
+  a.W = src.W;
+  a.M = t->m2l[l];
+  // enough CTAs for every SM before a warp takes more than one group of 8 entries
+  const int gpw = nent / 64 >= (int64_t)num_sms() * 24 ? 4 : 1;
+  int64_t blocks = 0;
+  for (int d = 0; d < 40; ++d) {
+    a.off[d] = hoff[d];
+    a.blk[d] = blocks;
+    blocks += (hoff[d + 1] - hoff[d] + 64 * gpw - 1) / (64 * gpw);
+  }
+  a.off[40] = hoff[40];
+  a.blk[40] = blocks;
+  int32_t* tab = nullptr;
+  HIKF_TRY(aalloc(&a.Pr, nent * q, st));
+  HIKF_TRY(aalloc(&tab, nslots * 40, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(tab, 0xff, sizeof(int32_t) * nslots * 40, st));
+  m2l_tab_kernel<<<grid_cap(nent), kT, 0, st>>>(a, nent, tab);
+  HIKF_CHECK_LAUNCH();
+  const size_t smem = sizeof(double) * q * m2l_ld(q);
+  unsigned long long* fl = prof_flops_ptr(ST_M2L);
+#define HIKF_M2LP(QQ, K4, RT)                                                    \
+  case QQ:                                                                      \
+    m2l_prod_kernel<K4, RT><<<(unsigned)blocks, kT, smem, st>>>(a, q, gpw, fl); \
+    break;
+  switch (q) {
+    HIKF_M2LP(4, 1, 1)
+    HIKF_M2LP(9, 3, 2)
+    HIKF_M2LP(16, 4, 2)
+    HIKF_M2LP(25, 7, 4)
+    HIKF_M2LP(36, 9, 5)
+    HIKF_M2LP(49, 13, 7)
+    HIKF_M2LP(64, 16, 8)
+    default:
+      set_error("M2L products: q = %d not instantiated", q);
+      return HIKF_BAD_ARGUMENT;
+  }
+#undef HIKF_M2LP
+  HIKF_CHECK_LAUNCH();
+  m2l_reduce_kernel<<<(unsigned)((nslots * 32 + kT - 1) / kT), kT, 0, st>>>(nslots, q, tab, a.Pr, S);
+  HIKF_CHECK_LAUNCH();
+  cudaFreeAsync(a.Pr, st);
+  cudaFreeAsync(tab, st);
   return HIKF_OK;
 }
 

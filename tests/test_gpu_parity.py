@@ -771,3 +771,25 @@ def test_near_blocks_are_bit_identical(pkg, N, ns, nr, order, leaf):
         pkg._lib.check(lib.hikf_set_tuning(2, 1, None))
     assert bool((out[1][0] == out[0][0]).all()) and bool((out[1][1] == out[0][1]).all())
 
+
+
+@pytest.mark.parametrize("N,ns,nr,order,leaf", [(64, 8, 8, 4, 64), (96, 6, 9, 5, 16), (256, 16, 16, 5, 64)])
+def test_near_fold_is_bit_identical(pkg, N, ns, nr, order, leaf):
+    """U = far + near formed inside the fused leaf step (the near-field sums of the (leaf, ray)
+    items added to the L2P accumulators) against the separate scatter pass over U (the
+    reference adds near @ V to the far field once, fmm.py:366-367): C_Q and HC_Q bitwise equal."""
+    cfg = dict(cases.CFG2, N=N, ns=ns, nr=nr, order=order, leaf=leaf)
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec(cfg["family"], variance=1.0, length_scale=cfg["L"])
+    model = _Model(grid, H, kern, cfg["R"])
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=order, max_leaf_points=leaf))
+    lib = pkg._lib.load()
+    out = {}
+    try:
+        for on in (1, 0):
+            pkg._lib.check(lib.hikf_set_tuning(3, on, None))
+            pre = pkg.filters.hikf_precompute_fmm(model, tree)
+            out[on] = (pre.C_Q_t.clone(), pre.HC_Q_t.clone())
+    finally:
+        pkg._lib.check(lib.hikf_set_tuning(3, 1, None))
+    assert bool((out[1][0] == out[0][0]).all()) and bool((out[1][1] == out[0][1]).all())

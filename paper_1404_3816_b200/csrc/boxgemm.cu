@@ -285,7 +285,7 @@ int launch_box(const BoxArgs& a, int R, dim3 grid, cudaStream_t st) {
 // l2l_boxes + l2p_boxes (same products in the same order); the saving is the
 // G_D^2 x q x n leaf-local array (written and read back: 9.6 GB at cfg4).
 // ---------------------------------------------------------------------------
-constexpr int kLeafItemWords = 64;  // near-field fold: up to 2048 units of 8 columns (n <= 16384)
+constexpr int kLeafUnits = 2048;  // near-field fold: up to 2048 units of 8 columns (n <= 16384)
 struct LeafArgs {
   int64_t n;
   int q, qp;
@@ -309,6 +309,13 @@ struct LeafArgs {
   int32_t maxc;
 };
 
+// 8-byte asynchronous global -> shared copy; !pred: the destination is zero-filled
+__device__ __forceinline__ void cp_async8_zfill(double* dst, const double* src, bool pred) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+
 // shared-memory load the compiler cannot hoist out of the unit loop (the A
 // operands are loop-invariant; keeping them all in registers would spill)
 __device__ __forceinline__ double lds64(const double* p) {
@@ -317,15 +324,21 @@ __device__ __forceinline__ double lds64(const double* p) {
   return v;
 }
 
-template <int NK1, int NRT1, int NK2>
-__global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
+// NT: 8-column tiles per warp unit.  With NT = 2 every A fragment read from shared memory feeds
+// two DMMAs (the kernel is otherwise co-limited by the shared-memory data pipe: one 256-byte
+// fragment per DMMA); the larger register tile runs as 3 CTAs of 4 warps per SM.
+template <int NK1, int NRT1, int NK2, int NT>
+__global__ void __launch_bounds__(NT == 2 ? 128 : BW_THREADS, NT == 2 ? 3 : 2) leaf_down_kernel(LeafArgs g) {
   extern __shared__ double sm[];
+  constexpr int THREADS = NT == 2 ? 128 : BW_THREADS;
+  constexpr int UC = 8 * NT;  // columns per unit
   constexpr int LDA1 = NK1 * 4 + ((4 - (NK1 * 4) % 16) + 16) % 16;
   constexpr int LDA2 = NK2 * 4 + ((4 - (NK2 * 4) % 16) + 16) % 16;
-  constexpr int KR2 = NK2 * 4;  // rows of the per-warp l tile
+  constexpr int KR2 = NK2 * 4;              // rows of the per-warp l tile
+  constexpr int LDL = NT == 2 ? 20 : 8;     // its row stride: conflict-free 16-byte stores and fragment loads
   double* A1 = sm;                          // NRT1*8 x LDA1
   double* A2 = A1 + NRT1 * 8 * LDA1;        // 64 x LDA2
-  double* Lw = A2 + 64 * LDA2;              // 8 warps x KR2 x 8
+  double* Lw = A2 + 64 * LDA2;              // warps x KR2 x LDL
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gq = lane >> 2, t4 = lane & 3;
   const int q = g.q, qp = g.qp;
@@ -337,23 +350,33 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
   const int cnt = g.leaf_count[T];
   const int64_t ls = g.leaf_start[T];
   const double* Cg = g.shift + (int64_t)ci * q * qp;
-  for (int e = tid; e < NRT1 * 8 * NK1 * 4; e += BW_THREADS) {
+  // A operands: asynchronous 8-byte copies, all in flight at once (zero fill for the padding)
+  for (int e = tid; e < NRT1 * 8 * NK1 * 4; e += THREADS) {
     const int r = e / (NK1 * 4), k = e % (NK1 * 4);
-    A1[r * LDA1 + k] = (r < q && k < qp) ? Cg[(int64_t)r * qp + k] : 0.0;
+    const bool ok = r < q && k < qp;
+    cp_async8_zfill(A1 + r * LDA1 + k, ok ? Cg + (int64_t)r * qp + k : Cg, ok);
   }
-  // 8-column units of this leaf that hold a near-field item
-  __shared__ uint32_t ibits[kLeafItemWords];
-  if (tid < kLeafItemWords) ibits[tid] = 0;
+  // near-field items of this leaf: per 8-column tile, the columns that hold an item (one byte)
+  // and the tile's first item (a tile's items are consecutive, in ascending ray order)
+  __shared__ uint32_t umask[kLeafUnits / 4];
+  __shared__ int32_t ufirst[kLeafUnits];
   const int32_t is0 = g.Pnear ? g.item_start[T] : 0, is1 = g.Pnear ? g.item_start[T + 1] : 0;
+  if (g.Pnear)
+    for (int e = tid; e < (int)((g.n + 7) / 8); e += THREADS) {
+      ufirst[e] = INT32_MAX;
+      if ((e & 3) == 0) umask[e >> 2] = 0;
+    }
   const double* Wg = g.W2s + ls * q;
-  for (int e = tid; e < 64 * NK2 * 4; e += BW_THREADS) {
+  for (int e = tid; e < 64 * NK2 * 4; e += THREADS) {
     const int r = e / (NK2 * 4), k = e % (NK2 * 4);
-    A2[r * LDA2 + k] = (r < cnt && k < q) ? Wg[(int64_t)r * q + k] : 0.0;
+    const bool ok = r < cnt && k < q;
+    cp_async8_zfill(A2 + r * LDA2 + k, ok ? Wg + (int64_t)r * q + k : Wg, ok);
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  double* lw = Lw + warp * KR2 * 8;
+  double* lw = Lw + warp * KR2 * LDL;
   const int64_t n = g.n;
-  const int64_t ncb = (n + 7) / 8;
+  const int64_t ncb = (n + UC - 1) / UC;
   const double* Lpar = g.Lp + P * qp * n;
   const int32_t* tm = g.tmap + box * n;
   // output row in U of each leaf point (or -1 outside the row window), shared by the warps
@@ -370,114 +393,139 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
     }
     orow[tid] = r;
   }
-  for (int32_t i = is0 + tid; i < is1; i += BW_THREADS) {
-    const int u = (int)((g.items[i] % g.n) >> 3);
-    atomicOr(&ibits[u >> 5], 1u << (u & 31));
+  for (int32_t i = is0 + tid; i < is1; i += THREADS) {
+    const int j = (int)(g.items[i] % g.n), u = j >> 3;
+    atomicOr(&umask[u >> 2], (1u << (j & 7)) << ((u & 3) * 8));
+    atomicMin(&ufirst[u], i);
   }
   __syncthreads();
-  // the next unit's parent columns and M2L slot indices are loaded one unit ahead
-  auto load_next = [&](int64_t u, double (&b1)[NK1], int32_t (&sl)[2]) {
-    const int64_t jb = u * 8 + gq;
+  // A unit's parent columns are loaded during the previous unit's L2P phase, straight into the
+  // registers its L2L chain reads (dead by then); its M2L slot indices too, so that the M2L
+  // sums, loaded at the start of the unit and added after the L2L chain, are not a dependent load.
+  auto load_cols = [&](int64_t u, double (&b1)[NT][NK1]) {
 #pragma unroll
-    for (int k4 = 0; k4 < NK1; ++k4) {
-      const int k = k4 * 4 + t4;
-      b1[k4] = (k < qp && jb < n) ? Lpar[(int64_t)k * n + jb] : 0.0;
-    }
+    for (int tt = 0; tt < NT; ++tt) {
+      const int64_t jb = u * UC + tt * 8 + gq;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t jc = u * 8 + 2 * t4 + h;
-      sl[h] = jc < n ? tm[jc] : -1;
+      for (int k4 = 0; k4 < NK1; ++k4) {
+        const int k = k4 * 4 + t4;
+        b1[tt][k4] = (k < qp && jb < n) ? Lpar[(int64_t)k * n + jb] : 0.0;
+      }
     }
   };
-  unsigned long long useful1 = 0, useful2 = 0;
-  double nb1[NK1];
-  int32_t nslot[2];
-  if (warp < ncb) load_next(warp, nb1, nslot);
-  for (int64_t u = warp; u < ncb; u += BW_THREADS / 32) {
-    double b1[NK1];
-    int32_t slot[2] = {nslot[0], nslot[1]};
+  auto load_slots = [&](int64_t u, int32_t (&sl)[NT][2]) {
 #pragma unroll
-    for (int k4 = 0; k4 < NK1; ++k4) b1[k4] = nb1[k4];
-    if (u + BW_THREADS / 32 < ncb) load_next(u + BW_THREADS / 32, nb1, nslot);
-    const int64_t j0 = u * 8;
-    const int cols = (int)(n - j0 < 8 ? n - j0 : 8);
+    for (int tt = 0; tt < NT; ++tt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t jc = u * UC + tt * 8 + 2 * t4 + h;
+        sl[tt][h] = jc < n ? tm[jc] : -1;
+      }
+  };
+  constexpr int kStep = THREADS / 32;
+  unsigned long long useful1 = 0, useful2 = 0;
+  double b1[NT][NK1];
+  int32_t slot[NT][2];
+  if (warp < ncb) {
+    load_cols(warp, b1);
+    load_slots(warp, slot);
+  }
+  for (int64_t u = warp; u < ncb; u += kStep) {
+    const bool more = u + kStep < ncb;
+    const int64_t j0 = u * UC;
+    const int cols = (int)(n - j0 < UC ? n - j0 : UC);
     if (lane == 0) {
       useful1 += 2ull * q * qp * cols;
       useful2 += 2ull * cnt * q * cols;
     }
     // the M2L sums of this unit (loaded ahead of the DMMA chain, added after it)
-    double init[NRT1][2];
+    double init[NT][NRT1][2];
 #pragma unroll
-    for (int i = 0; i < NRT1; ++i) {
-      const int r = i * 8 + gq;
+    for (int tt = 0; tt < NT; ++tt)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) init[i][h] = (r < q && slot[h] >= 0) ? g.S[(int64_t)slot[h] * q + r] : 0.0;
-    }
+      for (int i = 0; i < NRT1; ++i) {
+        const int r = i * 8 + gq;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          init[tt][i][h] = (r < q && slot[tt][h] >= 0) ? g.S[(int64_t)slot[tt][h] * q + r] : 0.0;
+      }
     // L2L into the leaf: acc1 = C_ci L_parent, then l = acc1 + S
-    double acc1[NRT1][2];
+    double acc1[NT][NRT1][2];
 #pragma unroll
-    for (int i = 0; i < NRT1; ++i) acc1[i][0] = acc1[i][1] = 0.0;
+    for (int tt = 0; tt < NT; ++tt)
+#pragma unroll
+      for (int i = 0; i < NRT1; ++i) acc1[tt][i][0] = acc1[tt][i][1] = 0.0;
 #pragma unroll
     for (int k4 = 0; k4 < NK1; ++k4)
 #pragma unroll
       for (int i = 0; i < NRT1; ++i) {
         const double af = lds64(A1 + (i * 8 + gq) * LDA1 + k4 * 4 + t4);
-        dmma884(acc1[i][0], acc1[i][1], af, b1[k4]);
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt) dmma884(acc1[tt][i][0], acc1[tt][i][1], af, b1[tt][k4]);
       }
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < NRT1; ++i) {
-      const int r = i * 8 + gq;
-      if (r < KR2)  // 16-byte stores: the warp's 32 chunks cover 4 wavefronts, conflict-free
-        *reinterpret_cast<double2*>(lw + r * 8 + 2 * t4) =
-            make_double2(acc1[i][0] + init[i][0], acc1[i][1] + init[i][1]);
-    }
+    for (int tt = 0; tt < NT; ++tt)
+#pragma unroll
+      for (int i = 0; i < NRT1; ++i) {
+        const int r = i * 8 + gq;
+        if (r < KR2)  // 16-byte stores: the warp's 32 chunks cover 4 wavefronts, conflict-free
+          *reinterpret_cast<double2*>(lw + r * LDL + tt * 8 + 2 * t4) =
+              make_double2(acc1[tt][i][0] + init[tt][i][0], acc1[tt][i][1] + init[tt][i][1]);
+      }
     __syncwarp();
-    // L2P: U = W2 l
-    double b2[NK2];
+    // the next unit's parent columns and slots: in flight during this unit's L2P
+    if (more) {
+      load_cols(u + kStep, b1);
+      load_slots(u + kStep, slot);
+    }
+    // L2P: U = W2 l  (the l fragments are read per k-step; rows q .. KR2 - 1 of the tile are zero)
+    double acc2[NT][8][2];
+#pragma unroll
+    for (int tt = 0; tt < NT; ++tt)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc2[tt][i][0] = acc2[tt][i][1] = 0.0;
 #pragma unroll
     for (int k4 = 0; k4 < NK2; ++k4) {
-      const int k = k4 * 4 + t4;
-      b2[k4] = k < q ? lw[k * 8 + gq] : 0.0;
-    }
-    double acc2[8][2];
+      double bf[NT];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc2[i][0] = acc2[i][1] = 0.0;
-#pragma unroll
-    for (int k4 = 0; k4 < NK2; ++k4)
+      for (int tt = 0; tt < NT; ++tt) bf[tt] = lds64(lw + (k4 * 4 + t4) * LDL + tt * 8 + gq);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const double af = lds64(A2 + (i * 8 + gq) * LDA2 + k4 * 4 + t4);
-        dmma884(acc2[i][0], acc2[i][1], af, b2[k4]);
-      }
-    const int64_t jc = j0 + 2 * t4;
-    if ((ibits[u >> 5] >> (u & 31)) & 1) {  // a ray of this unit crosses the leaf's neighbourhood: + near sums
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t key = T * n + jc + h;
-        int32_t lo = is0, hi = is1;
-        while (lo < hi) {
-          const int32_t mid = (lo + hi) >> 1;
-          if (g.items[mid] < key) lo = mid + 1; else hi = mid;
-        }
-        if (lo < is1 && g.items[lo] == key) {
-          const double* pn = g.Pnear + (int64_t)lo * g.maxc + gq;
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (i * 8 + gq < cnt) acc2[i][h] += pn[i * 8];
-        }
+        for (int tt = 0; tt < NT; ++tt) dmma884(acc2[tt][i][0], acc2[tt][i][1], af, bf[tt]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int32_t orw = orow[i * 8 + gq];
-      if (orw < 0) continue;
-      double* o = g.U + (int64_t)orw * g.ldu;
-      if (jc + 1 < n && (((uintptr_t)(o + jc)) & 15) == 0) {
-        *reinterpret_cast<double2*>(o + jc) = make_double2(acc2[i][0], acc2[i][1]);
-      } else {
-        if (jc < n) o[jc] = acc2[i][0];
-        if (jc + 1 < n) o[jc + 1] = acc2[i][1];
+    for (int tt = 0; tt < NT; ++tt) {
+      const int64_t ut = u * NT + tt;  // the 8-column tile
+      const int64_t jc = ut * 8 + 2 * t4;
+      const unsigned um = (g.Pnear && ut * 8 < n) ? (umask[ut >> 2] >> ((ut & 3) * 8)) & 0xffu : 0u;
+      if (um) {  // rays of this tile cross the leaf's neighbourhood: + their near sums
+        const int32_t f = ufirst[ut];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 2 * t4 + h;
+          if ((um >> c) & 1) {
+            const double* pn = g.Pnear + (int64_t)(f + __popc(um & ((1u << c) - 1))) * g.maxc + gq;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (i * 8 + gq < cnt) acc2[tt][i][h] += pn[i * 8];
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int32_t orw = orow[i * 8 + gq];
+        if (orw < 0) continue;
+        double* o = g.U + (int64_t)orw * g.ldu;
+        if (jc + 1 < n && (((uintptr_t)(o + jc)) & 15) == 0) {
+          *reinterpret_cast<double2*>(o + jc) = make_double2(acc2[tt][i][0], acc2[tt][i][1]);
+        } else {
+          if (jc < n) o[jc] = acc2[tt][i][0];
+          if (jc + 1 < n) o[jc + 1] = acc2[tt][i][1];
+        }
       }
     }
   }
@@ -487,21 +535,38 @@ __global__ void __launch_bounds__(BW_THREADS, 2) leaf_down_kernel(LeafArgs g) {
   }
 }
 
-template <int NK1, int NRT1, int NK2>
-int launch_leaf_t(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
+static int g_leaf_tiles = -1;  // column tiles per warp unit (HIKF_LEAF_TILES = 1 | 2)
+static int leaf_tiles() {
+  if (g_leaf_tiles < 0) {
+    const char* e = getenv("HIKF_LEAF_TILES");
+    g_leaf_tiles = (e && e[0] == '1') ? 1 : 2;
+  }
+  return g_leaf_tiles;
+}
+
+template <int NK1, int NRT1, int NK2, int NT>
+int launch_leaf_nt(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
+  constexpr int THREADS = NT == 2 ? 128 : BW_THREADS;
+  constexpr int LDL = NT == 2 ? 20 : 8;
   constexpr int LDA1 = NK1 * 4 + ((4 - (NK1 * 4) % 16) + 16) % 16;
   constexpr int LDA2 = NK2 * 4 + ((4 - (NK2 * 4) % 16) + 16) % 16;
-  constexpr size_t smem = sizeof(double) * (NRT1 * 8 * LDA1 + 64 * LDA2 + 8 * NK2 * 4 * 8);
+  constexpr size_t smem = sizeof(double) * (NRT1 * 8 * LDA1 + 64 * LDA2 + (THREADS / 32) * NK2 * 4 * LDL);
   static bool configured = false;
-  auto kern = leaf_down_kernel<NK1, NRT1, NK2>;
+  auto kern = leaf_down_kernel<NK1, NRT1, NK2, NT>;
   if (!configured) {
     HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)std::max<size_t>(smem, 48 << 10)));
     configured = true;
   }
-  kern<<<nleaves, BW_THREADS, smem, st>>>(a);
+  kern<<<nleaves, THREADS, smem, st>>>(a);
   HIKF_CHECK_LAUNCH();
   return HIKF_OK;
+}
+
+template <int NK1, int NRT1, int NK2>
+int launch_leaf_t(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
+  if (leaf_tiles() == 2 && a.n > 8) return launch_leaf_nt<NK1, NRT1, NK2, 2>(a, nleaves, st);
+  return launch_leaf_nt<NK1, NRT1, NK2, 1>(a, nleaves, st);
 }
 
 // (leaf order o, parent order op) -> instantiation; 0 = not instantiated
@@ -593,7 +658,7 @@ bool leaf_down_supported(const hikf_tree* t) {
   return o >= 2 && o <= 8 && (op == o || op == o + 1);
 }
 
-bool leaf_down_adds_near(int64_t n) { return (n + 7) / 8 <= 32 * kLeafItemWords; }
+bool leaf_down_adds_near(int64_t n) { return (n + 7) / 8 <= kLeafUnits; }
 
 int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const double* Lp, int64_t n, double* U,
               int64_t ldu, cudaStream_t st, int64_t r0, int64_t r1, const LeafWindow* lw, const double* Pnear,
@@ -624,7 +689,7 @@ int leaf_down(const hikf_tree* t, const double* S, const int32_t* tmap, const do
   a.fl_l2l = prof_flops_ptr(ST_L2L);
   a.fl_l2p = prof_flops_ptr(ST_L2P);
   if (Pnear && !leaf_down_adds_near(n)) {
-    set_error("fused leaf step: near-field fold supports n <= %d", 8 * 32 * kLeafItemWords);
+    set_error("fused leaf step: near-field fold supports n <= %d", 8 * kLeafUnits);
     return HIKF_BAD_ARGUMENT;
   }
   a.Pnear = Pnear;

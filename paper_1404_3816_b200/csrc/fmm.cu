@@ -480,8 +480,11 @@ int qht_streams(QhtStreams** out) {
   if (!init) {
     int lo = 0, hi = 0;
     HIKF_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* pe = getenv("HIKF_P2P_PRIO");  // experiment: 0 lowest, 1 middle, 2 highest
+    const int pp = pe ? atoi(pe) : 0;
+    const int p2p_prio = pp == 2 ? hi : pp == 1 ? (lo + hi) / 2 : lo;
     for (int i = 0; i < 8; ++i)
-      HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.s[i], cudaStreamNonBlocking, i == 0 ? lo : hi));
+      HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.s[i], cudaStreamNonBlocking, i == 0 ? p2p_prio : hi));
     HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.w, cudaStreamNonBlocking, hi));
     for (auto& x : p.e) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     for (auto& x : p.e_pairs) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));

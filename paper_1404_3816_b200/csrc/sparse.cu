@@ -169,31 +169,97 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
   const int32_t j = (int32_t)(key % n);
   if (T < leaf0 || T >= leaf1) return;  // another shard's target leaf
   const int64_t box = leaf_box[T], bx = box / G, by = box % G;
-  // the <= 9 entry ranges of ray j in the adjacent leaves (and their first sorted positions)
-  int32_t rb[9], re[9], sb[9];
-#pragma unroll
-  for (int s = 0; s < 9; ++s) {
-    rb[s] = re[s] = sb[s] = 0;
+  // the <= 9 entry ranges of ray j in the adjacent leaves (and their first sorted positions):
+  // lane s looks up neighbour s, the ranges are then exchanged by shuffles
+  int32_t my_rb = 0, my_re = 0, my_sb = 0;
+  if (lane < 9) {
+    const int s = lane;
     int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
-    if (nx < 0 || nx >= G || ny < 0 || ny >= G) continue;
-    int32_t S = box2leaf[nx * G + ny];
-    if (S < 0) continue;
-    sb[s] = leaf_start[S];
-    int32_t lo = leaf_g[S], hi = leaf_g[S + 1];
-    while (lo < hi) {
-      int32_t mid = (lo + hi) >> 1;
-      if (g_j[mid] < j) lo = mid + 1; else hi = mid;
-    }
-    if (lo < leaf_g[S + 1] && g_j[lo] == j) {
-      rb[s] = g_start[lo];
-      re[s] = g_start[lo + 1];
+    if (nx >= 0 && nx < G && ny >= 0 && ny < G) {
+      int32_t S = box2leaf[nx * G + ny];
+      if (S >= 0) {
+        my_sb = leaf_start[S];
+        const int32_t end = leaf_g[S + 1];
+        int32_t lo = leaf_g[S], hi = end;
+        while (lo < hi) {
+          int32_t mid = (lo + hi) >> 1;
+          if (g_j[mid] < j) lo = mid + 1; else hi = mid;
+        }
+        if (lo < end && g_j[lo] == j) {
+          my_rb = g_start[lo];
+          my_re = g_start[lo + 1];
+        }
+      }
     }
   }
   const int32_t t0 = leaf_start[T], cnt = leaf_count[T];
-  if (flops && lane == 0) {
-    unsigned long long ne = 0;
-    for (int s = 0; s < 9; ++s) ne += re[s] - rb[s];
-    atomicAdd(flops, 2ull * ne * cnt);
+  // inclusive prefix of the ranges' lengths over the neighbours (lanes 0..8)
+  int32_t incl = my_re - my_rb;
+#pragma unroll
+  for (int d = 1; d < 16; d <<= 1) {
+    const int32_t up = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += up;
+  }
+  const int32_t total = __shfl_sync(0xffffffffu, incl, 8);
+  if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)total * cnt);
+  if (near) {
+    // kernel values from the tree's near blocks (the same values, evaluated at build).  The
+    // ray's entries in the neighbourhood, in (neighbour, entry) order, are fetched 32 at a time
+    // (one per lane, coalesced) and handed round by shuffles; the block loads of several
+    // entries are in flight together, the sums keep the entry order.
+    const double* blkT = near + (int64_t)T * 9 * 64 * 64;
+    const bool ok0 = lane < cnt, ok1 = lane + 32 < cnt;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int32_t base = 0; base < total; base += 32) {
+      const int32_t e = base + lane;
+      int s_of = 0;
+      int32_t excl = 0;
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const int32_t inc_s = __shfl_sync(0xffffffffu, incl, s);
+        if (e >= inc_s) {
+          s_of = s + 1;
+          excl = inc_s;
+        }
+      }
+      const int32_t rb_s = __shfl_sync(0xffffffffu, my_rb, s_of), sb_s = __shfl_sync(0xffffffffu, my_sb, s_of);
+      int32_t off = 0;
+      double v = 0.0;
+      if (e < total) {
+        const int32_t k = rb_s + (e - excl);
+        off = (s_of * 64 + (e_sp[k] - sb_s)) * 64;
+        v = e_v[k];
+      }
+      const int nch = total - base < 32 ? total - base : 32;
+#pragma unroll 4
+      for (int i = 0; i < nch; ++i) {
+        const int32_t off_i = __shfl_sync(0xffffffffu, off, i);
+        const double v_i = __shfl_sync(0xffffffffu, v, i);
+        if (ok0) acc0 += blkT[off_i + lane] * v_i;
+        if (ok1) acc1 += blkT[off_i + lane + 32] * v_i;
+      }
+    }
+#pragma unroll
+    for (int hb = 0; hb < 2; ++hb) {
+      const int t = hb * 32 + lane;
+      if (t >= cnt) continue;
+      const double acc = hb ? acc1 : acc0;
+      if (Pnear)
+        Pnear[item * maxc + t] = acc;  // added into U later (leaf_down / p2p_scatter): U = far + near either way
+      else if (s0 >= 0) {
+        U[(t0 + t - s0) * ldu + j] += acc;
+      } else {
+        const int64_t row = order[t0 + t];
+        if (row >= r0 && row < r1) U[(row - r0) * ldu + j] += acc;
+      }
+    }
+    return;
+  }
+  int32_t rb[9], re[9];
+#pragma unroll
+  for (int s = 0; s < 9; ++s) {
+    rb[s] = __shfl_sync(0xffffffffu, my_rb, s);
+    re[s] = __shfl_sync(0xffffffffu, my_re, s);
   }
   for (int tb = 0; tb < cnt; tb += 32) {
     const int t = tb + lane;
@@ -204,24 +270,13 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
       ty = xy_s[2 * (int64_t)(t0 + t) + 1];
     }
     double acc = 0.0;
-    if (near) {  // kernel values from the tree's near blocks (the same values, evaluated at build)
-      const double* blkT = near + (int64_t)T * 9 * 64 * 64 + t;
 #pragma unroll 1
-      for (int s = 0; s < 9; ++s)
-        for (int32_t k = rb[s]; k < re[s]; ++k) {
-          const int32_t c = e_sp[k] - sb[s];
-          const double v = e_v[k];
-          acc += blkT[(s * 64 + c) * 64] * v;
-        }
-    } else {
-#pragma unroll 1
-      for (int s = 0; s < 9; ++s)
-        for (int32_t k = rb[s]; k < re[s]; ++k) {
-          const int32_t p = e_sp[k];
-          const double v = e_v[k];
-          acc += kernel_of_r_near(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
-        }
-    }
+    for (int s = 0; s < 9; ++s)
+      for (int32_t k = rb[s]; k < re[s]; ++k) {
+        const int32_t p = e_sp[k];
+        const double v = e_v[k];
+        acc += kernel_of_r_near(kp, dist2d(tx, ty, xy_s[2 * (int64_t)p], xy_s[2 * (int64_t)p + 1])) * v;
+      }
     if (!ok) continue;
     if (Pnear)
       Pnear[item * maxc + t] = acc;  // added into U later (leaf_down / p2p_scatter): U = far + near either way

@@ -585,39 +585,45 @@ __device__ __forceinline__ int64_t find_key(const int64_t* __restrict__ keys, in
   return (lo < np && keys[lo] == k) ? lo : -1;
 }
 
-// W_P[b][j] = sum_{children c (cx, cy order)} sum_a C_c[a][b] W_c[a][j]  (fmm.py:339-345)
-// One warp per parent pair: lanes 0..3 look up the four children's pairs (binary
-// searches in parallel, once per pair instead of once per coefficient), then the
-// lanes stride over b; each output keeps the children-then-a summation order.
-__global__ void m2m_pairs(int64_t npp, const int32_t* __restrict__ npp_dev, const int64_t* __restrict__ pkey, int qp,
-                          int qc, int64_t Gp, int64_t n, const double* __restrict__ shift, int64_t npc,
-                          const int32_t* __restrict__ npc_dev, const int64_t* __restrict__ ckey,
-                          const double* __restrict__ Wcc, double* __restrict__ Wp, unsigned long long* __restrict__ flops) {
-  if (npp_dev) npp = *npp_dev;  // the pair counts on the device (deferred mode: npp / npc are the allocated sizes)
+// cidx[parent pair][c] = the child pair (2X + (c >> 1), 2Y + (c & 1), j) of a parent pair, or -1:
+// one thread per child pair finds its parent by binary search (all searches in parallel,
+// instead of four per parent warp in front of the M2M sums)
+__global__ void child_index(int64_t npc, const int32_t* __restrict__ npc_dev, const int64_t* __restrict__ ckey,
+                            int64_t n, int64_t Gc, int64_t npp, const int32_t* __restrict__ npp_dev,
+                            const int64_t* __restrict__ pkey, int32_t* __restrict__ cidx) {
   if (npc_dev) npc = *npc_dev;
+  if (npp_dev) npp = *npp_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npc; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t box = ckey[i] / n, j = ckey[i] % n, cx = box / Gc, cy = box % Gc;
+    const int64_t p = find_key(pkey, npp, ((cx >> 1) * (Gc >> 1) + (cy >> 1)) * n + j);
+    if (p >= 0) cidx[p * 4 + (((cx & 1) << 1) | (cy & 1))] = (int32_t)i;
+  }
+}
+
+// W_P[b][j] = sum_{children c (cx, cy order)} sum_a C_c[a][b] W_c[a][j]  (fmm.py:339-345)
+// One warp per parent pair, the lanes stride over b; each output keeps the
+// children-then-a summation order.
+__global__ void m2m_pairs(int64_t npp, const int32_t* __restrict__ npp_dev, int qp, int qc,
+                          const double* __restrict__ shift, const int32_t* __restrict__ cidx,
+                          const double* __restrict__ Wcc, double* __restrict__ Wp, unsigned long long* __restrict__ flops) {
+  if (npp_dev) npp = *npp_dev;  // the pair count on the device (deferred mode: npp is the allocated size)
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t pi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; pi < npp; pi += nwarps) {
-    const int64_t box = pkey[pi] / n, j = pkey[pi] % n, X = box / Gp, Y = box % Gp;
-    int64_t ci = -1;
-    if (lane < 4) {
-      const int64_t child = (2 * X + (lane >> 1)) * (2 * Gp) + (2 * Y + (lane & 1));
-      ci = find_key(ckey, npc, child * n + j);
-    }
-    int64_t cidx[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) cidx[c] = __shfl_sync(0xffffffffu, ci, c);
+    const int4 ci4 = *reinterpret_cast<const int4*>(cidx + pi * 4);
+    const int32_t ci[4] = {ci4.x, ci4.y, ci4.z, ci4.w};
     unsigned found = 0;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) found += cidx[c] >= 0;
+    for (int c = 0; c < 4; ++c) found += ci[c] >= 0;
     for (int b = lane; b < qp; b += 32) {
       double s = 0.0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        if (cidx[c] < 0) continue;
-        const double* C = shift + (int64_t)c * qc * qp;
-        const double* w = Wcc + cidx[c] * qc;
-        for (int a = 0; a < qc; ++a) s += C[(int64_t)a * qp + b] * w[a];
+        if (ci[c] < 0) continue;
+        const double* C = shift + (int64_t)c * qc * qp + b;
+        const double* w = Wcc + (int64_t)ci[c] * qc;
+#pragma unroll 4
+        for (int a = 0; a < qc; ++a) s += C[(int64_t)a * qp] * w[a];
       }
       Wp[pi * qp + b] = s;
     }
@@ -832,6 +838,7 @@ struct M2LProd {
   const int2* ent;
   const double *W, *M;  // source coefficients (q per pair), the level's 40 operators
   double* Pr;           // q per entry
+  int32_t* tab;         // tab[slot][d] = the entry of offset d that targets the slot (preset to -1)
   int64_t off[41];      // first entry of every offset
   int64_t blk[41];      // first CTA of every offset
 };
@@ -869,6 +876,7 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LP
       const int k = k4 * 4 + t4;
       b[k4] = (pe.x >= 0 && k < q) ? a.W[(int64_t)pe.x * q + k] : 0.0;
     }
+    if (t4 == 0 && pe.x >= 0) a.tab[(int64_t)pe.y * 40 + d] = (int32_t)(i0 + g);  // a target has one source per offset
     double* out[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -892,19 +900,6 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LP
       for (int h = 0; h < 2; ++h)
         if (out[h] && r < q) out[h][r] = acc0[h] + acc1[h];
     }
-  }
-}
-
-// tab[slot][d] = the entry of offset d that targets the slot (a target has at most one
-// source per offset), -1 where there is none
-__global__ void m2l_tab_kernel(M2LProd a, int64_t nent, int32_t* __restrict__ tab) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nent; i += (int64_t)gridDim.x * blockDim.x) {
-    int lo = 0, hi = 40;  // last d with off[d] <= i
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (a.off[mid] <= i) lo = mid; else hi = mid;
-    }
-    tab[(int64_t)a.ent[i].y * 40 + lo] = (int32_t)i;
   }
 }
 
@@ -1076,13 +1071,20 @@ int pairs_keys(const hikf_tree* t, int l, int lc, const PairLevel& child, int64_
 }
 
 int pairs_m2m(const hikf_tree* t, int l, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st) {
-  const int64_t Gp = (int64_t)1 << l;
+  const int64_t Gc = (int64_t)1 << (l + 1);
   const int qp = t->orders[l] * t->orders[l], qc = t->orders[l + 1] * t->orders[l + 1];
   HIKF_TRY(aalloc(&out->W, out->np * qp, st));
   if (out->np == 0 || child.np == 0) return HIKF_OK;
-  m2m_pairs<<<grid_cap(out->np * 32), kT, 0, st>>>(out->np, out->np_dev, out->key, qp, qc, Gp, n, t->shift[l], child.np,
-                                                   child.np_dev, child.key, child.W, out->W, prof_flops_ptr(ST_M2M));
+  int32_t* cidx = nullptr;
+  HIKF_TRY(aalloc(&cidx, out->np * 4, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(cidx, 0xff, sizeof(int32_t) * out->np * 4, st));
+  child_index<<<grid_cap(child.np), kT, 0, st>>>(child.np, child.np_dev, child.key, n, Gc, out->np, out->np_dev,
+                                                out->key, cidx);
   HIKF_CHECK_LAUNCH();
+  m2m_pairs<<<grid_cap(out->np * 32), kT, 0, st>>>(out->np, out->np_dev, qp, qc, t->shift[l], cidx, child.W, out->W,
+                                                   prof_flops_ptr(ST_M2M));
+  HIKF_CHECK_LAUNCH();
+  cudaFreeAsync(cidx, st);
   return HIKF_OK;
 }
 
@@ -1284,12 +1286,9 @@ int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan&
   }
   a.off[40] = hoff[40];
   a.blk[40] = blocks;
-  int32_t* tab = nullptr;
   HIKF_TRY(aalloc(&a.Pr, nent * q, st));
-  HIKF_TRY(aalloc(&tab, nslots * 40, st));
-  HIKF_CHECK_CUDA(cudaMemsetAsync(tab, 0xff, sizeof(int32_t) * nslots * 40, st));
-  m2l_tab_kernel<<<grid_cap(nent), kT, 0, st>>>(a, nent, tab);
-  HIKF_CHECK_LAUNCH();
+  HIKF_TRY(aalloc(&a.tab, nslots * 40, st));
+  HIKF_CHECK_CUDA(cudaMemsetAsync(a.tab, 0xff, sizeof(int32_t) * nslots * 40, st));
   const size_t smem = sizeof(double) * q * m2l_ld(q);
   unsigned long long* fl = prof_flops_ptr(ST_M2L);
 #define HIKF_M2LP(QQ, K4, RT)                                                    \
@@ -1310,10 +1309,10 @@ int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan&
   }
 #undef HIKF_M2LP
   HIKF_CHECK_LAUNCH();
-  m2l_reduce_kernel<<<(unsigned)((nslots * 32 + kT - 1) / kT), kT, 0, st>>>(nslots, q, tab, a.Pr, S);
+  m2l_reduce_kernel<<<(unsigned)((nslots * 32 + kT - 1) / kT), kT, 0, st>>>(nslots, q, a.tab, a.Pr, S);
   HIKF_CHECK_LAUNCH();
   cudaFreeAsync(a.Pr, st);
-  cudaFreeAsync(tab, st);
+  cudaFreeAsync(a.tab, st);
   return HIKF_OK;
 }
 

@@ -438,17 +438,24 @@ __global__ void __launch_bounds__(NT == 2 ? 128 : BW_THREADS, NT == 2 ? 3 : 2) l
       useful1 += 2ull * q * qp * cols;
       useful2 += 2ull * cnt * q * cols;
     }
-    // the M2L sums of this unit (loaded ahead of the DMMA chain, added after it)
-    double init[NT][NRT1][2];
+    // the M2L sums of this unit: asynchronous copies into the warp's l tile, each thread into the
+    // positions it will add its own L2L results to (no registers held while they are in flight
+    // under the DMMA chain; the previous unit's L2P has finished reading the tile)
+    __syncwarp();
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt)
 #pragma unroll
       for (int i = 0; i < NRT1; ++i) {
         const int r = i * 8 + gq;
+        if (r < KR2) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          init[tt][i][h] = (r < q && slot[tt][h] >= 0) ? g.S[(int64_t)slot[tt][h] * q + r] : 0.0;
+          for (int h = 0; h < 2; ++h) {
+            const bool ok = r < q && slot[tt][h] >= 0;
+            cp_async8_zfill(lw + r * LDL + tt * 8 + 2 * t4 + h, ok ? g.S + (int64_t)slot[tt][h] * q + r : g.S, ok);
+          }
+        }
       }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     // L2L into the leaf: acc1 = C_ci L_parent, then l = acc1 + S
     double acc1[NT][NRT1][2];
 #pragma unroll
@@ -463,15 +470,17 @@ __global__ void __launch_bounds__(NT == 2 ? 128 : BW_THREADS, NT == 2 ? 3 : 2) l
 #pragma unroll
         for (int tt = 0; tt < NT; ++tt) dmma884(acc1[tt][i][0], acc1[tt][i][1], af, b1[tt][k4]);
       }
-    __syncwarp();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt)
 #pragma unroll
       for (int i = 0; i < NRT1; ++i) {
         const int r = i * 8 + gq;
-        if (r < KR2)  // 16-byte stores: the warp's 32 chunks cover 4 wavefronts, conflict-free
-          *reinterpret_cast<double2*>(lw + r * LDL + tt * 8 + 2 * t4) =
-              make_double2(acc1[tt][i][0] + init[tt][i][0], acc1[tt][i][1] + init[tt][i][1]);
+        if (r < KR2) {  // 16-byte accesses: the warp's 32 chunks cover 4 wavefronts
+          double2* pl = reinterpret_cast<double2*>(lw + r * LDL + tt * 8 + 2 * t4);
+          const double2 in = *pl;
+          *pl = make_double2(acc1[tt][i][0] + in.x, acc1[tt][i][1] + in.y);
+        }
       }
     __syncwarp();
     // the next unit's parent columns and slots: in flight during this unit's L2P
@@ -539,7 +548,7 @@ static int g_leaf_tiles = -1;  // column tiles per warp unit (HIKF_LEAF_TILES = 
 static int leaf_tiles() {
   if (g_leaf_tiles < 0) {
     const char* e = getenv("HIKF_LEAF_TILES");
-    g_leaf_tiles = (e && e[0] == '1') ? 1 : 2;
+    g_leaf_tiles = (e && e[0] == '2') ? 2 : 1;  // measured equal at cfg4 (5.5 ms either way); 1 is the default
   }
   return g_leaf_tiles;
 }

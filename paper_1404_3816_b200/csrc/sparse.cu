@@ -776,64 +776,13 @@ __global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_k
   }
 }
 
-// One M2L offset over its (source pair, target slot) entries (m2l_targets): a warp
-// takes 8 entries as the 8 columns of its DMMA tiles (every column useful), forms
-// M_d W_p with two accumulator chains (even / odd k-steps) and adds their sum into
-// the compact scratch at the target's slot -- race-free, since a target receives at
-// most one source per offset; the offsets run in the reference's order.
-template <int NK4, int NRT>
-__global__ void __launch_bounds__(256, (NK4 <= 13) ? 2 : 1) m2l_list_kernel(M2LSegs sg, int q,
-                                                                         unsigned long long* __restrict__ flops) {
-  // this CTA's level segment (levels of equal order share one launch per offset)
-  int si = 0;
-  while (si + 1 < sg.n && (int64_t)blockIdx.x >= sg.s[si + 1].block0) ++si;
-  const M2LSeg& S = sg.s[si];
-  extern __shared__ double Ms[];
-  const int ld = m2l_ld(q);
-  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = S.M[e];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  const int64_t ne = S.ne;
-  const int64_t i0 = (((blockIdx.x - S.block0) * (int64_t)blockDim.x + threadIdx.x) >> 5) * 8;
-  if (i0 >= ne) return;
-  const int64_t mine = i0 + g;
-  int2 pe = make_int2(-1, -1);
-  if (mine < ne) pe = S.ent[S.e0 + mine];
-  if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)(ne - i0 < 8 ? ne - i0 : 8) * q * q);
-  double b[NK4];
-#pragma unroll
-  for (int k4 = 0; k4 < NK4; ++k4) {
-    const int k = k4 * 4 + t4;
-    b[k4] = (pe.x >= 0 && k < q) ? S.W[(int64_t)pe.x * q + k] : 0.0;
-  }
-  int slot[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) slot[h] = __shfl_sync(0xffffffffu, pe.y, (2 * t4 + h) * 4);
-  double* L = S.L;
-  for (int i = 0; i < NRT; ++i) {
-    const int r = i * 8 + g;
-    double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
-#pragma unroll
-    for (int k4 = 0; k4 < NK4; ++k4) {
-      const int k = k4 * 4 + t4;
-      const double a = (r < q && k < q) ? Ms[r * ld + k] : 0.0;
-      if (k4 & 1)
-        dmma884(acc1[0], acc1[1], a, b[k4]);
-      else
-        dmma884(acc0[0], acc0[1], a, b[k4]);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      if (slot[h] >= 0 && r < q) L[(int64_t)slot[h] * q + r] += acc0[h] + acc1[h];
-  }
-}
-
 // All M2L terms of a level in one launch: Pr[i][:] = M_d W_p for every entry i = (p, slot)
 // of every offset d.  The products do not depend on one another, so the 40 offsets need no
 // ordering (and no read-modify-write of the targets); m2l_reduce then adds each target's
 // products in the reference's offset order.  A CTA stages M_d once and its warps walk gpw
 // groups of 8 entries (the 8 columns of the DMMA tiles); the product of an entry is formed
-// exactly as in m2l_list_kernel (two accumulator chains, even / odd k-steps, then their sum).
+// in two accumulator chains (even / odd k-steps) that are then summed, so the rounding is that of
+// l_lev[t] += M @ w (fmm.py:349-360) term by term.
 struct M2LProd {
   const int2* ent;
   const double *W, *M;  // source coefficients (q per pair), the level's 40 operators
@@ -1214,53 +1163,6 @@ void m2l_plan_free(M2LPlan* plan, cudaStream_t st) {
   cudaFreeAsync(plan->ent, st);
   cudaFreeAsync(plan->off, st);
   *plan = M2LPlan();
-}
-
-int m2l_pass_list(const hikf_tree* t, int nlev, const int* levels, int slot, const PairLevel* src,
-                  const M2LPlan* plan, const int64_t (*hoff)[41], double* const* S, cudaStream_t st) {
-  M2LSegs sg{};
-  const int q = t->orders[levels[0]] * t->orders[levels[0]];
-  int64_t blocks = 0;
-  for (int i = 0; i < nlev; ++i) {
-    const int l = levels[i];
-    const int64_t e0 = hoff[l][slot], ne = hoff[l][slot + 1] - hoff[l][slot];
-    if (ne <= 0) continue;
-    if (t->orders[l] * t->orders[l] != q) {
-      set_error("M2L level group with unequal orders");
-      return HIKF_BAD_ARGUMENT;
-    }
-    M2LSeg& g = sg.s[sg.n++];
-    g.e0 = e0;
-    g.ne = ne;
-    g.ent = plan[l].ent;
-    g.W = src[l].W;
-    g.M = t->m2l[l] + (int64_t)slot * q * q;
-    g.L = S[l];
-    g.block0 = blocks;
-    blocks += ((ne + 7) / 8 * 32 + kT - 1) / kT;
-  }
-  if (sg.n == 0) return HIKF_OK;
-  const size_t smem = sizeof(double) * q * m2l_ld(q);
-  unsigned long long* fl = prof_flops_ptr(ST_M2L);
-#define HIKF_M2LL(QQ, K4, RT)                                                          \
-  case QQ:                                                                            \
-    m2l_list_kernel<K4, RT><<<(unsigned)blocks, kT, smem, st>>>(sg, q, fl);           \
-    break;
-  switch (q) {
-    HIKF_M2LL(4, 1, 1)
-    HIKF_M2LL(9, 3, 2)
-    HIKF_M2LL(16, 4, 2)
-    HIKF_M2LL(25, 7, 4)
-    HIKF_M2LL(36, 9, 5)
-    HIKF_M2LL(49, 13, 7)
-    HIKF_M2LL(64, 16, 8)
-    default:
-      set_error("M2L entry lists: q = %d not instantiated", q);
-      return HIKF_BAD_ARGUMENT;
-  }
-#undef HIKF_M2LL
-  HIKF_CHECK_LAUNCH();
-  return HIKF_OK;
 }
 
 int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,

@@ -85,21 +85,8 @@ struct M2LPlan {
 int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
                 M2LPlan* plan, cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
 void m2l_plan_free(M2LPlan* plan, cudaStream_t st);
-// One offset over the entry lists of a group of levels of equal order (one launch;
-// hoff[l]: host copy of plan[l].off; S[l]: level l's compact scratch)
-struct M2LSeg {
-  int64_t e0 = 0, ne = 0, block0 = 0;
-  const int2* ent = nullptr;
-  const double *W = nullptr, *M = nullptr;
-  double* L = nullptr;
-};
-struct M2LSegs {
-  M2LSeg s[kMaxDepth + 1];
-  int n = 0;
-};
+// levels whose order has an entry-list (product) M2L instantiation: q in {4, 9, ..., 64}
 bool m2l_list_supported(const hikf_tree* t, int l);
-int m2l_pass_list(const hikf_tree* t, int nlev, const int* levels, int slot, const PairLevel* src,
-                  const M2LPlan* plan, const int64_t (*hoff)[41], double* const* S, cudaStream_t st);
 // Every M2L term of level l at once (m2l_list_supported levels): the products M_d W_p of all
 // entries in one launch, then S[slot] = the slot's products added in the reference's offset
 // order -- the per-offset passes' sums bit for bit, without their 40 dependent launches.

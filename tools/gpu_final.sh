@@ -15,13 +15,16 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 2 > $O/reference
 python tools/cold_start.py cfg4 > $O/cold.json 2>&1
 python tools/cold_start.py cfg4 --warmup > $O/cold_warmup.json 2>&1
 HIKF_QHT_TIMELINE=1 python tools/qht_time.py cfg4 > $O/qht_timeline.log 2>&1
+python tools/qht_time.py cfg4 15 > $O/qht_time.log 2>&1; python tools/qht_time.py cfg2 15 >> $O/qht_time.log 2>&1; python tools/qht_time.py cfg1 15 >> $O/qht_time.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_qht.csv python tools/qht_time.py cfg4 > /dev/null 2>&1
+python tools/launch_summary.py $O/launches_qht.csv 40 > $O/launches_qht_summary.txt 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-factored > $O/ncu_launch.log 2>&1
 python tools/launch_summary.py $O/launches.csv 40 > $O/launches_summary.txt 2>&1
 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "update/" --kernel-name-base demangled \
   -k "regex:dgemm_rm_kernel.*bool.1" -c 1 -f -o $O/kgemm python tools/prof_update.py > $O/ncu_kgemm.log 2>&1
 python tools/ncu_summary.py $O/kgemm.ncu-rep > $O/kgemm_summary.txt 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:leaf_down|m2l_list|p2p_sparse|box_warp" -c 6 -f \
+ncu --set full --clock-control none --import-source on -k "regex:leaf_down|m2l_prod|m2l_reduce|p2p_sparse|box_warp|spmm_rows|m2m_pairs" -c 26 -f \
   -o $O/qht python tools/qht_time.py cfg4 > $O/ncu_qht.log 2>&1
 python tools/ncu_summary.py $O/qht.ncu-rep > $O/qht_summary.txt 2>&1
 rm -f $O/*.ncu-rep

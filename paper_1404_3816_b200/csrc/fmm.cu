@@ -480,11 +480,8 @@ int qht_streams(QhtStreams** out) {
   if (!init) {
     int lo = 0, hi = 0;
     HIKF_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const char* pe = getenv("HIKF_P2P_PRIO");  // experiment: 0 lowest, 1 middle, 2 highest
-    const int pp = pe ? atoi(pe) : 0;
-    const int p2p_prio = pp == 2 ? hi : pp == 1 ? (lo + hi) / 2 : lo;
     for (int i = 0; i < 8; ++i)
-      HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.s[i], cudaStreamNonBlocking, i == 0 ? p2p_prio : hi));
+      HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.s[i], cudaStreamNonBlocking, i == 0 ? lo : hi));
     HIKF_CHECK_CUDA(cudaStreamCreateWithPriority(&p.w, cudaStreamNonBlocking, hi));
     for (auto& x : p.e) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     for (auto& x : p.e_pairs) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
@@ -699,8 +696,7 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
     return HIKF_OK;
   };
   // the M2L sums of a group whose targets have all been enqueued: every term of the level in
-  // one launch plus the ordered per-target sums (m2l_products), or, for orders without an
-  // entry-list instantiation, the 40 dependent offset passes
+  // one launch plus the ordered per-target sums (m2l_products)
   auto launch_group = [&](int gi) -> int {
     cudaStream_t sl = gstream(gi);
     const int l0 = groups[gi][0];
@@ -721,8 +717,8 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
         s2 = m2l_products(t, l, pl[l], plan[l], hoff[l], hcount[2 * l], scratch[l], sl);
       }
     } else {
-      for (int slot = 0; slot < 40 && s2 == HIKF_OK; ++slot)
-        s2 = m2l_pass(t, l0, slot, pl[l0], n, scratch[l0], tmap[l0], sl, xlo(l0), xhi(l0));
+      set_error("M2L: order %d of level %d has no product kernel", t->orders[l0], l0);
+      s2 = HIKF_BAD_ARGUMENT;
     }
     for (int k = 0; k < gsize[gi]; ++k) HIKF_CHECK_CUDA(cudaEventRecord(qs->e[3 + groups[gi][k]], sl));
     tl.mark("m2l sums", sl, l0);

@@ -615,166 +615,32 @@ __global__ void m2m_pairs(int64_t npp, const int32_t* __restrict__ npp_dev, int 
     unsigned found = 0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) found += ci[c] >= 0;
-    for (int b = lane; b < qp; b += 32) {
-      double s = 0.0;
+    // two outputs per lane (b, b + 32) share each broadcast child coefficient
+    for (int bb = 0; bb < qp; bb += 64) {
+      const int b0 = bb + lane, b1 = bb + lane + 32;
+      const bool ok0 = b0 < qp, ok1 = b1 < qp;
+      const int c0 = ok0 ? b0 : 0, c1 = ok1 ? b1 : 0;  // in-range columns for the idle lanes
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (ci[c] < 0) continue;
-        const double* C = shift + (int64_t)c * qc * qp + b;
+        const double* C = shift + (int64_t)c * qc * qp;
         const double* w = Wcc + (int64_t)ci[c] * qc;
 #pragma unroll 4
-        for (int a = 0; a < qc; ++a) s += C[(int64_t)a * qp] * w[a];
+        for (int a = 0; a < qc; ++a) {
+          const double wa = w[a];
+          s0 += C[(int64_t)a * qp + c0] * wa;
+          s1 += C[(int64_t)a * qp + c1] * wa;
+        }
       }
-      Wp[pi * qp + b] = s;
+      if (ok0) Wp[pi * qp + b0] = s0;
+      if (ok1) Wp[pi * qp + b1] = s1;
     }
     if (flops && lane == 0) atomicAdd(flops, 2ull * found * (unsigned long long)qc * qp);
   }
 }
 
-// One M2L offset over all active source pairs of a level: a warp takes 16
-// pairs (two 8-column DMMA groups sharing the A fragments of M_d), computes
-// M_d W_s[:, j] on the DMMA pipe and adds it into the pair-major scratch
-// L[T][j][:] (q contiguous coefficients per (T, j)), T = S - d.
-// Within one offset every (T, j) has at most one source, so the adds are
-// race-free and the offsets are summed in the reference's order.
-constexpr int kPairGroups = 1;  // 8 pairs per warp: low register count, many warps in flight
-constexpr int kMaxK4Smem = 16;  // q <= 64: M_d staged in shared memory, B fragments preloaded
 __host__ __device__ inline int m2l_ld(int q) { return q + ((4 - q % 16) + 16) % 16; }  // == 4 mod 16
-
-// kSmem: M_d in shared memory and B preloaded; NK4 / NRT = ceil(q/4) / ceil(q/8)
-// as compile-time bounds of the fragment loops (generic path: 16 / 8 with runtime q)
-template <bool kSmem, int NK4, int NRT>
-__global__ void __launch_bounds__(256, (kSmem && NK4 <= 13) ? 2 : 1) m2l_pairs_kernel(int64_t np, const int64_t* __restrict__ key,
-                                                        const double* __restrict__ Wc, int q, int64_t n, int64_t G,
-                                                        int dx, int dy, const uint8_t* __restrict__ occ,
-                                                        const double* __restrict__ M, double* __restrict__ L,
-                                                        const int32_t* __restrict__ tmap,
-                                                        unsigned long long* __restrict__ flops, int64_t xlo,
-                                                        int64_t xhi) {
-  extern __shared__ double Ms[];
-  const int ld = kSmem ? m2l_ld(q) : q;
-  if (kSmem) {
-    for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = M[e];
-    __syncthreads();
-  }
-  const double* A = kSmem ? Ms : M;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t p0 = warp * (8 * kPairGroups);
-  if (p0 >= np) return;
-  const int g = lane >> 2, t4 = lane & 3;
-  // my column (pair) in each group: validity and target
-  int32_t myT[kPairGroups], myJ[kPairGroups];
-  int64_t myP[kPairGroups];
-  bool any = false;
-#pragma unroll
-  for (int c = 0; c < kPairGroups; ++c) {
-    int64_t p = p0 + c * 8 + g;
-    myT[c] = -1;
-    myJ[c] = 0;
-    myP[c] = p;
-    if (p < np) {
-      int64_t S = key[p] / n, j = key[p] % n;
-      int64_t tx = S / G - dx, ty = S % G - dy, s2;
-      if (tx >= xlo && tx <= xhi && tx >= 0 && ty >= 0 && tx < G && ty < G && m2l_source(tx, ty, dx, dy, G, s2) &&
-          s2 == S && occ[tx * G + ty]) {
-        myT[c] = (int32_t)(tx * G + ty);
-        myJ[c] = (int32_t)j;
-      }
-    }
-    any |= __any_sync(0xffffffffu, myT[c] >= 0);
-  }
-  if (!any) return;
-  if (flops) {
-    int nv = 0;
-#pragma unroll
-    for (int c = 0; c < kPairGroups; ++c) nv += __popc(__ballot_sync(0xffffffffu, myT[c] >= 0 && t4 == 0));
-    if (lane == 0) atomicAdd(flops, 2ull * nv * q * q);
-  }
-  const int nrt = (q + 7) >> 3;
-  const int nk4 = (q + 3) >> 2;
-  constexpr int RT = kSmem ? NRT : 8;  // row tiles held in registers per pass
-  // B fragments (this lane's pair, k = 4 k4 + t4), preloaded when q <= 64
-  double bpre[kSmem ? kPairGroups : 1][kSmem ? NK4 : 1];
-  if (kSmem) {
-#pragma unroll
-    for (int c = 0; c < kPairGroups; ++c)
-#pragma unroll
-      for (int k4 = 0; k4 < NK4; ++k4) {
-        const int k = k4 * 4 + t4;
-        bpre[c][k4] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
-      }
-  }
-  if (kSmem) {
-    // one 8-row tile at a time: two interleaved accumulator chains over k
-    for (int i = 0; i < nrt; ++i) {
-      const int r = i * 8 + g;
-      double acc0[kPairGroups][2], acc1[kPairGroups][2];
-#pragma unroll
-      for (int c = 0; c < kPairGroups; ++c) acc0[c][0] = acc0[c][1] = acc1[c][0] = acc1[c][1] = 0.0;
-#pragma unroll
-      for (int k4 = 0; k4 < NK4; ++k4) {
-        const int k = k4 * 4 + t4;
-        const double a = (r < q && k < q) ? A[r * ld + k] : 0.0;
-#pragma unroll
-        for (int c = 0; c < kPairGroups; ++c) {
-          if (k4 & 1)
-            dmma884(acc1[c][0], acc1[c][1], a, bpre[c][k4]);
-          else
-            dmma884(acc0[c][0], acc0[c][1], a, bpre[c][k4]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < kPairGroups; ++c)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = 2 * t4 + h;
-          const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
-          const int64_t j = (int64_t)__shfl_sync(0xffffffffu, myJ[c], col * 4);
-          if (T >= 0 && r < q) L[(int64_t)tmap[T * n + j] * q + r] += acc0[c][h] + acc1[c][h];
-        }
-    }
-    return;
-  }
-  for (int r0 = 0; r0 < nrt; r0 += RT) {
-    double acc[RT][kPairGroups][2];
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-      for (int c = 0; c < kPairGroups; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
-    for (int k4 = 0; k4 < nk4; ++k4) {
-      const int k = k4 * 4 + t4;
-      double b[kPairGroups];
-#pragma unroll
-      for (int c = 0; c < kPairGroups; ++c) b[c] = (myT[c] >= 0 && k < q) ? Wc[myP[c] * q + k] : 0.0;
-#pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const int r = (r0 + i) * 8 + g;
-        if (r0 + i < nrt) {
-          const double a = (r < q && k < q) ? __ldg(A + (int64_t)r * q + k) : 0.0;
-#pragma unroll
-          for (int c = 0; c < kPairGroups; ++c) dmma884(acc[i][c][0], acc[i][c][1], a, b[c]);
-        }
-      }
-    }
-    // epilogue: lane holds rows (r0+i)*8+g of columns 2*t4, 2*t4+1 of each group
-#pragma unroll
-    for (int c = 0; c < kPairGroups; ++c)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = 2 * t4 + h;
-        const int64_t T = __shfl_sync(0xffffffffu, myT[c], col * 4);
-        const int64_t j = (int64_t)__shfl_sync(0xffffffffu, myJ[c], col * 4);
-        if (T < 0) continue;
-        const int64_t slot = tmap[T * n + j];
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const int r = (r0 + i) * 8 + g;
-          if (r0 + i < nrt && r < q) L[slot * q + r] += acc[i][c][h];
-        }
-      }
-  }
-}
 
 // All M2L terms of a level in one launch: Pr[i][:] = M_d W_p for every entry i = (p, slot)
 // of every offset d.  The products do not depend on one another, so the 40 offsets need no
@@ -813,12 +679,13 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LP
   int64_t i0 = chunk0 + warp * 8;
   int2 pe_next = make_int2(-1, -1);
   if (i0 + g < e_end) pe_next = a.ent[i0 + g];
+  unsigned long long useful = 0;  // profiling: one global atomic per CTA
   for (int gi = 0; gi < gpw; ++gi, i0 += 64) {
     if (i0 >= e_end) break;
     const int2 pe = pe_next;
     pe_next = make_int2(-1, -1);
     if (gi + 1 < gpw && i0 + 64 + g < e_end) pe_next = a.ent[i0 + 64 + g];
-    if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)(e_end - i0 < 8 ? e_end - i0 : 8) * q * q);
+    useful += 2ull * (unsigned long long)(e_end - i0 < 8 ? e_end - i0 : 8) * q * q;
     double b[NK4];
 #pragma unroll
     for (int k4 = 0; k4 < NK4; ++k4) {
@@ -850,6 +717,70 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LP
         if (out[h] && r < q) out[h][r] = acc0[h] + acc1[h];
     }
   }
+  if (flops) {
+    __shared__ unsigned long long s_fl;
+    if (threadIdx.x == 0) s_fl = 0;
+    __syncthreads();
+    if (lane == 0 && useful) atomicAdd(&s_fl, useful);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_fl) atomicAdd(flops, s_fl);
+  }
+}
+
+// The same for any order (q up to 256: the boosted orders 9..16 of the coarse levels): M_d and
+// the source coefficients are read from global memory (L1 / L2), 8 row tiles per pass, one
+// accumulator chain per tile over ascending k -- the arithmetic of the former per-offset generic
+// pass, so its results bit for bit, with the 40 offsets of the level side by side in one launch.
+__global__ void __launch_bounds__(256) m2l_prod_generic_kernel(M2LProd a, int q, unsigned long long* __restrict__ flops) {
+  __shared__ int s_d;
+  if (threadIdx.x < 40) {
+    const int d = threadIdx.x;
+    if ((int64_t)blockIdx.x >= a.blk[d] && (int64_t)blockIdx.x < a.blk[d + 1]) s_d = d;
+  }
+  __syncthreads();
+  const int d = s_d;
+  const double* __restrict__ M = a.M + (int64_t)d * q * q;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  const int64_t e_end = a.off[d + 1];
+  const int64_t i0 = a.off[d] + ((int64_t)blockIdx.x - a.blk[d]) * 64 + warp * 8;
+  if (i0 >= e_end) return;
+  int2 pe = make_int2(-1, -1);
+  if (i0 + g < e_end) pe = a.ent[i0 + g];
+  if (flops && lane == 0) atomicAdd(flops, 2ull * (unsigned long long)(e_end - i0 < 8 ? e_end - i0 : 8) * q * q);
+  if (t4 == 0 && pe.x >= 0) a.tab[(int64_t)pe.y * 40 + d] = (int32_t)(i0 + g);
+  double* out[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t i = i0 + 2 * t4 + h;
+    out[h] = i < e_end ? a.Pr + i * q : nullptr;
+  }
+  const int nrt = (q + 7) >> 3, nk4 = (q + 3) >> 2;
+  const double* __restrict__ w = a.W + (int64_t)(pe.x >= 0 ? pe.x : 0) * q;
+  for (int r0 = 0; r0 < nrt; r0 += 8) {
+    double acc[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int k4 = 0; k4 < nk4; ++k4) {
+      const int k = k4 * 4 + t4;
+      const double b = (pe.x >= 0 && k < q) ? w[k] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int r = (r0 + i) * 8 + g;
+        if (r0 + i < nrt) {
+          const double av = (r < q && k < q) ? __ldg(M + (int64_t)r * q + k) : 0.0;
+          dmma884(acc[i][0], acc[i][1], av, b);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int r = (r0 + i) * 8 + g;
+      if (r0 + i < nrt && r < q) {
+        if (out[0]) out[0][r] = acc[i][0];
+        if (out[1]) out[1][r] = acc[i][1];
+      }
+    }
+  }
 }
 
 // S[slot][:] = ((0 + Pr[e_1]) + Pr[e_2]) + ... over the slot's entries in ascending offset
@@ -862,39 +793,42 @@ __global__ void __launch_bounds__(256) m2l_reduce_kernel(int64_t nslots, int q, 
   if (slot >= nslots) return;
   const int32_t t0 = tab[slot * 40 + lane];
   const int32_t t1 = lane < 8 ? tab[slot * 40 + 32 + lane] : -1;
-  unsigned m0 = __ballot_sync(0xffffffffu, t0 >= 0), m1 = __ballot_sync(0xffffffffu, t1 >= 0);
-  const int r0 = lane, r1 = lane + 32;
-  double acc0 = 0.0, acc1 = 0.0;
-  while (m0 | m1) {
-    int64_t idx[4];
+  const unsigned mask0 = __ballot_sync(0xffffffffu, t0 >= 0), mask1 = __ballot_sync(0xffffffffu, t1 >= 0);
+  for (int rb = 0; rb < q; rb += 64) {  // 64 coefficients per sweep over the slot's entries
+    unsigned m0 = mask0, m1 = mask1;
+    const int r0 = rb + lane, r1 = rb + lane + 32;
+    double acc0 = 0.0, acc1 = 0.0;
+    while (m0 | m1) {
+      int64_t idx[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      idx[k] = -1;
-      if (m0) {
-        const int dsel = __ffs(m0) - 1;
-        m0 &= m0 - 1;
-        idx[k] = __shfl_sync(0xffffffffu, t0, dsel);
-      } else if (m1) {
-        const int dsel = __ffs(m1) - 1;
-        m1 &= m1 - 1;
-        idx[k] = __shfl_sync(0xffffffffu, t1, dsel);
+      for (int k = 0; k < 4; ++k) {
+        idx[k] = -1;
+        if (m0) {
+          const int dsel = __ffs(m0) - 1;
+          m0 &= m0 - 1;
+          idx[k] = __shfl_sync(0xffffffffu, t0, dsel);
+        } else if (m1) {
+          const int dsel = __ffs(m1) - 1;
+          m1 &= m1 - 1;
+          idx[k] = __shfl_sync(0xffffffffu, t1, dsel);
+        }
       }
-    }
-    double v0[4], v1[4];
+      double v0[4], v1[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v0[k] = (idx[k] >= 0 && r0 < q) ? Pr[idx[k] * q + r0] : 0.0;
-      v1[k] = (idx[k] >= 0 && r1 < q) ? Pr[idx[k] * q + r1] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (idx[k] >= 0) {
-        acc0 += v0[k];
-        acc1 += v1[k];
+      for (int k = 0; k < 4; ++k) {
+        v0[k] = (idx[k] >= 0 && r0 < q) ? Pr[idx[k] * q + r0] : 0.0;
+        v1[k] = (idx[k] >= 0 && r1 < q) ? Pr[idx[k] * q + r1] : 0.0;
       }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (idx[k] >= 0) {
+          acc0 += v0[k];
+          acc1 += v1[k];
+        }
+    }
+    if (r0 < q) S[slot * q + r0] = acc0;
+    if (r1 < q) S[slot * q + r1] = acc1;
   }
-  if (r0 < q) S[slot * q + r0] = acc0;
-  if (r1 < q) S[slot * q + r1] = acc1;
 }
 
 // Pair-major M2L scratch S[T][j][a] -> box-major locals L[T][a][j] for the
@@ -1178,8 +1112,9 @@ int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan&
   a.ent = plan.ent;
   a.W = src.W;
   a.M = t->m2l[l];
+  const bool inst = q == 4 || q == 9 || q == 16 || q == 25 || q == 36 || q == 49 || q == 64;
   // enough CTAs for every SM before a warp takes more than one group of 8 entries
-  const int gpw = nent / 64 >= (int64_t)num_sms() * 24 ? 4 : 1;
+  const int gpw = (inst && nent / 64 >= (int64_t)num_sms() * 24) ? 4 : 1;
   int64_t blocks = 0;
   for (int d = 0; d < 40; ++d) {
     a.off[d] = hoff[d];
@@ -1206,8 +1141,7 @@ int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan&
     HIKF_M2LP(49, 13, 7)
     HIKF_M2LP(64, 16, 8)
     default:
-      set_error("M2L products: q = %d not instantiated", q);
-      return HIKF_BAD_ARGUMENT;
+      m2l_prod_generic_kernel<<<(unsigned)blocks, kT, 0, st>>>(a, q, fl);
   }
 #undef HIKF_M2LP
   HIKF_CHECK_LAUNCH();
@@ -1220,42 +1154,7 @@ int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan&
 
 bool m2l_list_supported(const hikf_tree* t, int l) {
   const int q = t->orders[l] * t->orders[l];
-  return q == 4 || q == 9 || q == 16 || q == 25 || q == 36 || q == 49 || q == 64;
-}
-
-int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* L, const int32_t* tmap,
-             cudaStream_t st, int64_t xlo, int64_t xhi) {
-  if (src.np == 0 || !((t->m2l_present[l] >> slot) & 1)) return HIKF_OK;
-  M2LOffsets offs;
-  const int q = t->orders[l] * t->orders[l];
-  const int64_t warps = (src.np + 8 * kPairGroups - 1) / (8 * kPairGroups);
-  const int64_t threads = warps * 32;
-  const unsigned blocks = (unsigned)((threads + kT - 1) / kT);
-  const size_t smem = sizeof(double) * q * m2l_ld(q);
-  const int64_t G = (int64_t)1 << l;
-  const double* M = t->m2l[l] + (int64_t)slot * q * q;
-  unsigned long long* fl = prof_flops_ptr(ST_M2L);
-#define HIKF_M2L_CASE(QQ, K4, RT)                                                                               \
-  case QQ:                                                                                                     \
-    m2l_pairs_kernel<true, K4, RT><<<blocks, kT, smem, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],   \
-                                                             offs.dy[slot], t->occ_flag[l], M, L, tmap, fl, xlo, xhi);\
-    break;
-  switch (q) {
-    HIKF_M2L_CASE(4, 1, 1)
-    HIKF_M2L_CASE(9, 3, 2)
-    HIKF_M2L_CASE(16, 4, 2)
-    HIKF_M2L_CASE(25, 7, 4)
-    HIKF_M2L_CASE(36, 9, 5)
-    HIKF_M2L_CASE(49, 13, 7)
-    HIKF_M2L_CASE(64, 16, 8)
-    default:
-      m2l_pairs_kernel<false, 1, 1><<<blocks, kT, 0, st>>>(src.np, src.key, src.W, q, n, G, offs.dx[slot],
-                                                            offs.dy[slot], t->occ_flag[l], M, L, tmap, fl, xlo,
-                                                            xhi);
-  }
-#undef HIKF_M2L_CASE
-  HIKF_CHECK_LAUNCH();
-  return HIKF_OK;
+  return q >= 1 && q <= 256;  // instantiated kernels for orders 2..8, the generic product kernel above them
 }
 
 }  // namespace hikf

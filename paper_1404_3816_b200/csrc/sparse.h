@@ -63,7 +63,7 @@ int pairs_leaf(const hikf_tree* t, const SparseHt& s, PairLevel* out, cudaStream
 // ancestors' keys.  The levels' key lists do not depend on the multipole values, so they (and
 // the M2L targets built from them) can be formed for all levels at once, beside the M2M chain.
 // (deferred: no host read-back of the pair count -- out->np is a bound, out->np_dev the count;
-//  m2l_targets, m2l_products and pairs_m2m accept such levels, m2l_pass does not)
+//  m2l_targets, m2l_products and pairs_m2m accept such levels)
 int pairs_keys(const hikf_tree* t, int l, int lc, const PairLevel& child, int64_t n, PairLevel* out, cudaStream_t st,
                bool deferred = false);
 // parent multipoles (sparse M2M) of level l's pairs (keys from pairs_keys) from level l + 1
@@ -85,18 +85,15 @@ struct M2LPlan {
 int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int32_t* tmap, int32_t* count_dev,
                 M2LPlan* plan, cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
 void m2l_plan_free(M2LPlan* plan, cudaStream_t st);
-// levels whose order has an entry-list (product) M2L instantiation: q in {4, 9, ..., 64}
+// every order the tree can select (q <= 256) has a product M2L: instantiated kernels for orders
+// 2..8, a generic one above
 bool m2l_list_supported(const hikf_tree* t, int l);
-// Every M2L term of level l at once (m2l_list_supported levels): the products M_d W_p of all
+// Every M2L term of level l at once: the products M_d W_p of all
 // entries in one launch, then S[slot] = the slot's products added in the reference's offset
 // order -- the per-offset passes' sums bit for bit, without their 40 dependent launches.
 // hoff: host copy of plan.off (41); nslots: target slots; S is written, not accumulated into.
 int m2l_products(const hikf_tree* t, int l, const PairLevel& src, const M2LPlan& plan, const int64_t* hoff,
                  int64_t nslots, double* S, cudaStream_t st);
-// L_l[T][:, j] += M_d W_{T+d}[:, j] for every active source pair and one offset slot
-// (targets outside the box-column range [xlo, xhi] of level l are skipped)
-int m2l_pass(const hikf_tree* t, int l, int slot, const PairLevel& src, int64_t n, double* S, const int32_t* tmap,
-             cudaStream_t st, int64_t xlo = 0, int64_t xhi = INT64_MAX);
 // L[T][a][j] = S[tmap[T n + j]][a] (0 without a slot) for the occupied boxes of level l
 int pair_to_box(const hikf_tree* t, int l, const double* S, const int32_t* tmap, int64_t n, double* L,
                 cudaStream_t st);

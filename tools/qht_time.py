@@ -27,4 +27,5 @@ for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     best = min(best, e0.elapsed_time(e1))
     times.append(e0.elapsed_time(e1))
 h = hashlib.sha256(pre.C_Q_t.cpu().numpy().tobytes()).hexdigest()[:16]
+print("runs", [round(x, 2) for x in times])
 print(sys.argv[1], "ms", round(best, 2), "median", round(sorted(times)[len(times) // 2], 2), "sha", h)

@@ -349,7 +349,9 @@ int64_t hikf_launch_count(void);
  * FMM (csrc/boxgemm.cu leaf_down; 0: separate L2L and L2P kernels); key 2 =
  * P2P reads the near-field kernel blocks stored with the tree (0: evaluates
  * the kernel per (target, entry)); key 3 = the near-field sums are added to
- * the far field inside the fused leaf step (0: by a separate scatter pass).
+ * the far field inside the fused leaf step (0: by a separate scatter pass);
+ * key 4 = the L2L of the inner levels runs child-major (one CTA per occupied
+ * child box; 0: parent-major, four children per unit).
  * *previous (optional) receives the old value. */
 int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous);
 

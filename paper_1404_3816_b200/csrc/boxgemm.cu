@@ -578,6 +578,153 @@ int launch_leaf_t(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
   return launch_leaf_nt<NK1, NRT1, NK2, 1>(a, nleaves, st);
 }
 
+// ---------------------------------------------------------------------------
+// L2L of one level, child-major: one CTA per occupied child box (the L2L half of
+// leaf_down_kernel).  l[a][j] = S[child][j][a] + sum_b C_ci[a][b] L_parent[b][j], stored
+// box-major.  Against the parent-major box_warp_kernel (4 q rows in passes of 4 row tiles,
+// each pass with its own dependent slot -> M2L-sum gathers and integer divisions) a unit is one
+// DMMA pass over ceil(q / 8) accumulators with the M2L sums copied asynchronously into the
+// warp's shared tile; the products and their order are the same, so the locals are bit-identical.
+// ---------------------------------------------------------------------------
+struct ChildArgs {
+  int64_t n;
+  int q, qp;
+  int64_t G;  // child-level grid
+  const int32_t* occ;  // occupied child boxes
+  const double *Lp, *shift, *S;
+  const int32_t* tmap;
+  double* L;
+  int64_t pxlo, pxhi;  // parents outside this box-column range are skipped (leaf-aligned shard)
+  unsigned long long* flops;
+};
+
+template <int NK1, int NRT1>
+__global__ void __launch_bounds__(BW_THREADS, 2) l2l_child_kernel(ChildArgs g) {
+  extern __shared__ double sm[];
+  constexpr int LDA1 = NK1 * 4 + ((4 - (NK1 * 4) % 16) + 16) % 16;
+  constexpr int TR = NRT1 * 8;  // rows of the per-warp tile
+  double* A1 = sm;              // TR x LDA1
+  double* Lw = A1 + TR * LDA1;  // 8 warps x TR x 8
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gq = lane >> 2, t4 = lane & 3;
+  const int q = g.q, qp = g.qp;
+  const int64_t box = g.occ[blockIdx.x];
+  const int64_t X = box / g.G, Y = box % g.G;
+  if ((X >> 1) < g.pxlo || (X >> 1) > g.pxhi) return;  // CTA-uniform
+  const int ci = (int)(((X & 1) << 1) | (Y & 1));
+  const int64_t P = (X >> 1) * (g.G >> 1) + (Y >> 1);
+  const double* Cg = g.shift + (int64_t)ci * q * qp;
+  for (int e = tid; e < TR * NK1 * 4; e += BW_THREADS) {
+    const int r = e / (NK1 * 4), k = e % (NK1 * 4);
+    const bool ok = r < q && k < qp;
+    cp_async8_zfill(A1 + r * LDA1 + k, ok ? Cg + (int64_t)r * qp + k : Cg, ok);
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  double* lw = Lw + warp * TR * 8;
+  const int64_t n = g.n;
+  const int64_t ncb = (n + 7) / 8;
+  const double* Lpar = g.Lp + P * qp * n;
+  const int32_t* tm = g.tmap + box * n;
+  double* Lout = g.L + box * q * n;
+  auto load_next = [&](int64_t u, double (&b1)[NK1], int32_t (&sl)[2]) {
+    const int64_t jb = u * 8 + gq;
+    // one running row pointer (opaque to the compiler: NK1 hoisted row addresses would cost 2 NK1 registers)
+    const double* pr = Lpar + (int64_t)t4 * n + (jb < n ? jb : 0);
+    asm volatile("" : "+l"(pr));
+#pragma unroll
+    for (int k4 = 0; k4 < NK1; ++k4) {
+      const int k = k4 * 4 + t4;
+      b1[k4] = (k < qp && jb < n) ? *pr : 0.0;
+      pr += 4 * n;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t jc = u * 8 + 2 * t4 + h;
+      sl[h] = jc < n ? tm[jc] : -1;
+    }
+  };
+  constexpr int kStep = BW_THREADS / 32;
+  unsigned long long useful = 0;
+  double nb1[NK1];
+  int32_t nslot[2];
+  if (warp < ncb) load_next(warp, nb1, nslot);
+  for (int64_t u = warp; u < ncb; u += kStep) {
+    double b1[NK1];
+    const int32_t slot[2] = {nslot[0], nslot[1]};
+#pragma unroll
+    for (int k4 = 0; k4 < NK1; ++k4) b1[k4] = nb1[k4];
+    // the M2L sums: asynchronous copies into the positions this thread adds its results to
+#pragma unroll
+    for (int i = 0; i < NRT1; ++i) {
+      const int r = i * 8 + gq;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool ok = r < q && slot[h] >= 0;
+        cp_async8_zfill(lw + r * 8 + 2 * t4 + h, ok ? g.S + (int64_t)slot[h] * q + r : g.S, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (u + kStep < ncb) load_next(u + kStep, nb1, nslot);
+    const int64_t j0 = u * 8;
+    if (lane == 0) useful += 2ull * q * qp * (unsigned long long)(n - j0 < 8 ? n - j0 : 8);
+    double acc[NRT1][2];
+#pragma unroll
+    for (int i = 0; i < NRT1; ++i) acc[i][0] = acc[i][1] = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < NK1; ++k4)
+#pragma unroll
+      for (int i = 0; i < NRT1; ++i) {
+        const double af = lds64(A1 + (i * 8 + gq) * LDA1 + k4 * 4 + t4);
+        dmma884(acc[i][0], acc[i][1], af, b1[k4]);
+      }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    const int64_t jc = j0 + 2 * t4;
+#pragma unroll
+    for (int i = 0; i < NRT1; ++i) {
+      const int r = i * 8 + gq;
+      if (r >= q) continue;
+      const double2 in = *reinterpret_cast<const double2*>(lw + r * 8 + 2 * t4);
+      const double v0 = acc[i][0] + in.x, v1 = acc[i][1] + in.y;
+      double* o = Lout + (int64_t)r * n;
+      if (jc + 1 < n && (((uintptr_t)(o + jc)) & 15) == 0) {
+        *reinterpret_cast<double2*>(o + jc) = make_double2(v0, v1);
+      } else {
+        if (jc < n) o[jc] = v0;
+        if (jc + 1 < n) o[jc + 1] = v1;
+      }
+    }
+  }
+  if (g.flops && lane == 0 && useful) atomicAdd(g.flops, useful);
+}
+
+template <int NK1, int NRT1>
+int launch_child_t(const ChildArgs& a, unsigned nboxes, cudaStream_t st) {
+  constexpr int LDA1 = NK1 * 4 + ((4 - (NK1 * 4) % 16) + 16) % 16;
+  constexpr size_t smem = sizeof(double) * (NRT1 * 8 * LDA1 + (BW_THREADS / 32) * NRT1 * 8 * 8);
+  static bool configured = false;
+  auto kern = l2l_child_kernel<NK1, NRT1>;
+  if (!configured) {
+    HIKF_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)std::max<size_t>(smem, 48 << 10)));
+    configured = true;
+  }
+  kern<<<nboxes, BW_THREADS, smem, st>>>(a);
+  HIKF_CHECK_LAUNCH();
+  return HIKF_OK;
+}
+
+// (child order o, parent order op) -> instantiation; -1 = not instantiated
+int launch_child(const ChildArgs& a, int o, int op, unsigned nboxes, cudaStream_t st) {
+#define HIKF_CHILD(O, OP) \
+  if (o == O && op == OP) return launch_child_t<(OP * OP + 3) / 4, (O * O + 7) / 8>(a, nboxes, st);
+  HIKF_CHILD(2, 2) HIKF_CHILD(2, 3) HIKF_CHILD(3, 3) HIKF_CHILD(3, 4) HIKF_CHILD(4, 4) HIKF_CHILD(4, 5)
+  HIKF_CHILD(5, 5) HIKF_CHILD(5, 6) HIKF_CHILD(6, 6) HIKF_CHILD(6, 7) HIKF_CHILD(7, 7) HIKF_CHILD(7, 8)
+  HIKF_CHILD(8, 8)
+#undef HIKF_CHILD
+  return -1;
+}
+
 // (leaf order o, parent order op) -> instantiation; 0 = not instantiated
 int launch_leaf(const LeafArgs& a, int o, int op, unsigned nleaves, cudaStream_t st) {
 #define HIKF_LEAF(O, OP)                                                                        \
@@ -594,9 +741,41 @@ int launch_leaf(const LeafArgs& a, int o, int op, unsigned nleaves, cudaStream_t
 
 bool box_supported(int rows, int K) { return K <= 4 * BW_MAXK4 && box_smem(rows, K) <= 200 * 1024; }
 
+static int g_l2l_child = -1;  // child-major L2L (1, default) or the parent-major box kernel (0: HIKF_L2L_CHILD=0, tuning key 4)
+static bool l2l_child_major() {
+  if (g_l2l_child < 0) {
+    const char* e = getenv("HIKF_L2L_CHILD");
+    g_l2l_child = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_l2l_child != 0;
+}
+int l2l_set_child_major(int on) {
+  const int prev = l2l_child_major() ? 1 : 0;
+  g_l2l_child = on ? 1 : 0;
+  return prev;
+}
+
 int l2l_boxes(const hikf_tree* t, int l, const double* S, const int32_t* tmap, const double* Lp, int64_t n,
               double* L, cudaStream_t st, int64_t pxlo, int64_t pxhi) {
   if (t->n_occ[l - 1] == 0 || n == 0) return HIKF_OK;
+  if (l2l_child_major() && t->n_occ[l] > 0) {
+    ChildArgs c{};
+    c.n = n;
+    c.q = t->orders[l] * t->orders[l];
+    c.qp = t->orders[l - 1] * t->orders[l - 1];
+    c.G = (int64_t)1 << l;
+    c.occ = t->occ[l];
+    c.Lp = Lp;
+    c.shift = t->shift[l - 1];
+    c.S = S;
+    c.tmap = tmap;
+    c.L = L;
+    c.pxlo = pxlo;
+    c.pxhi = pxhi;
+    c.flops = prof_flops_ptr(ST_L2L);
+    const int s = launch_child(c, t->orders[l], t->orders[l - 1], (unsigned)t->n_occ[l], st);
+    if (s >= 0) return s;  // else: orders without a child-major instantiation
+  }
   BoxArgs a{};
   a.tmap = tmap;
   a.pxlo = pxlo;

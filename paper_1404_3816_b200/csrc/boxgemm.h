@@ -13,6 +13,8 @@ int l2l_boxes(const hikf_tree* t, int l, const double* S, const int32_t* tmap, c
               double* L, cudaStream_t st, int64_t pxlo = 0, int64_t pxhi = INT64_MAX);
 // whether the warp-streaming kernel handles R rows x K inner (K <= 64, A fits in smem)
 bool box_supported(int rows, int K);
+// L2L of a level child-major (one CTA per occupied child box, 1) or parent-major (0); tuning key 4
+int l2l_set_child_major(int on);
 // U[order[p]][j] = sum_a W2[p][a] L_leaf[a][j] (store)
 // U = W2 L_leaf; with a row window only original rows r0 <= row < r1 are written, to U + (row - r0) ldu
 int l2p_boxes(const hikf_tree* t, const double* Lleaf, int64_t n, double* U, int64_t ldu, cudaStream_t st,

@@ -138,6 +138,9 @@ extern "C" int hikf_set_tuning(int32_t key, int32_t value, int32_t* previous) {
     case 3:
       prev = hikf::near_set_fold(value);
       break;
+    case 4:
+      prev = hikf::l2l_set_child_major(value);
+      break;
     default:
       hikf::set_error("unknown tuning key %d", (int)key);
       return HIKF_BAD_ARGUMENT;

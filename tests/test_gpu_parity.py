@@ -793,3 +793,26 @@ def test_near_fold_is_bit_identical(pkg, N, ns, nr, order, leaf):
     finally:
         pkg._lib.check(lib.hikf_set_tuning(3, 1, None))
     assert bool((out[1][0] == out[0][0]).all()) and bool((out[1][1] == out[0][1]).all())
+
+
+@pytest.mark.parametrize("N,ns,nr,order,leaf", [(128, 8, 8, 4, 16), (256, 16, 16, 5, 64), (256, 12, 10, 6, 16)])
+def test_child_major_l2l_is_bit_identical(pkg, N, ns, nr, order, leaf):
+    """The inner levels' L2L (fmm.py:361-363) child-major (one CTA per occupied child box, M2L sums
+    copied asynchronously into the warp's tile) against the parent-major box kernel: C_Q and HC_Q
+    bitwise equal (same products, same order)."""
+    cfg = dict(cases.CFG2, N=N, ns=ns, nr=nr, order=order, leaf=leaf)
+    grid, H = _gpu_scenario(pkg, cfg)
+    kern = pkg.KernelSpec("exponential", variance=1.0, length_scale=0.25)
+    model = _Model(grid, H, kern, cfg["R"])
+    tree = pkg.build_tree(grid.cell_centers(), kern, pkg.FmmConfig(n_cheb=order, max_leaf_points=leaf))
+    assert tree.depth >= 4
+    lib = pkg._lib.load()
+    out = {}
+    try:
+        for on in (1, 0):
+            pkg._lib.check(lib.hikf_set_tuning(4, on, None))
+            pre = pkg.filters.hikf_precompute_fmm(model, tree)
+            out[on] = (pre.C_Q_t.clone(), pre.HC_Q_t.clone())
+    finally:
+        pkg._lib.check(lib.hikf_set_tuning(4, 1, None))
+    assert bool((out[1][0] == out[0][0]).all()) and bool((out[1][1] == out[0][1]).all())

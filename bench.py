@@ -828,7 +828,8 @@ def main():
                      "frac": achieved / FP64_PEAK_TFLOPS,
                      "traffic": C_GEMM_TRAFFIC_CFG4 if args.config == "cfg4" else None,
                      "algorithmic_bytes": 32.0 * m * n, "peak_source": FP64_PEAK_SOURCE,
-                     "share_of_step": (ms_c + ms_y) / (1000.0 * t_loop) if t_loop else None,
+                     "share_of_step": ((ms_c / max(n_c, 1) + ms_y / max(n_y, 1)) / (1000.0 * t_loop / args.steps)
+                                       if t_loop else None),
                      "update_step_flops": update_flops,
                      "update_step_frac": update_flops * args.steps / t_loop / 1e12 / FP64_PEAK_TFLOPS},
         "streaming": {"kernel": "predict add (C += C_Q, var += diag_Q, HC += HC_Q), standalone hikf_predict; "

@@ -24,7 +24,7 @@ python tools/launch_summary.py $O/launches.csv 40 > $O/launches_summary.txt 2>&1
 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "update/" --kernel-name-base demangled \
   -k "regex:dgemm_rm_kernel.*bool.1" -c 1 -f -o $O/kgemm python tools/prof_update.py > $O/ncu_kgemm.log 2>&1
 python tools/ncu_summary.py $O/kgemm.ncu-rep > $O/kgemm_summary.txt 2>&1
-ncu --set full --clock-control none --import-source on -k "regex:leaf_down|m2l_prod|m2l_reduce|p2p_sparse|box_warp|spmm_rows|m2m_pairs" -c 26 -f \
+ncu --set full --clock-control none --import-source on -k "regex:leaf_down|m2l_prod|m2l_reduce|p2p_sparse|l2l_child|spmm_rows|m2m_pairs" -c 26 -f \
   -o $O/qht python tools/qht_time.py cfg4 > $O/ncu_qht.log 2>&1
 python tools/ncu_summary.py $O/qht.ncu-rep > $O/qht_summary.txt 2>&1
 rm -f $O/*.ncu-rep

@@ -544,15 +544,6 @@ __global__ void __launch_bounds__(NT == 2 ? 128 : BW_THREADS, NT == 2 ? 3 : 2) l
   }
 }
 
-static int g_leaf_tiles = -1;  // column tiles per warp unit (HIKF_LEAF_TILES = 1 | 2)
-static int leaf_tiles() {
-  if (g_leaf_tiles < 0) {
-    const char* e = getenv("HIKF_LEAF_TILES");
-    g_leaf_tiles = (e && e[0] == '2') ? 2 : 1;  // measured equal at cfg4 (5.5 ms either way); 1 is the default
-  }
-  return g_leaf_tiles;
-}
-
 template <int NK1, int NRT1, int NK2, int NT>
 int launch_leaf_nt(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
   constexpr int THREADS = NT == 2 ? 128 : BW_THREADS;
@@ -572,9 +563,10 @@ int launch_leaf_nt(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
   return HIKF_OK;
 }
 
+// One 8-column tile per warp unit.  NT = 2 (every A fragment feeds two DMMAs; 168 registers, 3 CTAs
+// of 4 warps) was measured equal and is not instantiated.
 template <int NK1, int NRT1, int NK2>
 int launch_leaf_t(const LeafArgs& a, unsigned nleaves, cudaStream_t st) {
-  if (leaf_tiles() == 2 && a.n > 8) return launch_leaf_nt<NK1, NRT1, NK2, 2>(a, nleaves, st);
   return launch_leaf_nt<NK1, NRT1, NK2, 1>(a, nleaves, st);
 }
 

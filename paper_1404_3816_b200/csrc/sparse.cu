@@ -231,7 +231,7 @@ __global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, in
         v = e_v[k];
       }
       const int nch = total - base < 32 ? total - base : 32;
-#pragma unroll 4
+#pragma unroll 8
       for (int i = 0; i < nch; ++i) {
         const int32_t off_i = __shfl_sync(0xffffffffu, off, i);
         const double v_i = __shfl_sync(0xffffffffu, v, i);

@@ -100,16 +100,21 @@ __global__ void parent_mask(int64_t Gp, int64_t ngr, const uint8_t* __restrict__
   }
 }
 
+// a sorted unique key list ends with the sentinel when some inputs carried it: drop it from the count
+__global__ void drop_sentinel(int32_t* __restrict__ num, const int64_t* __restrict__ keys, int64_t sentinel) {
+  if (*num > 0 && keys[*num - 1] == sentinel) --*num;
+}
+
 // candidate P2P items: for every (source leaf, j) group, the <= 9 adjacent
-// occupied target leaves; key = target * n + j (INT64_MAX = none)
+// occupied target leaves; key = target * n + j (sentinel = none; it sorts last)
 __global__ void item_candidates(int64_t ng, int64_t n, int64_t G, const int32_t* __restrict__ g_leaf,
                                 const int32_t* __restrict__ g_j, const int32_t* __restrict__ leaf_box,
-                                const int32_t* __restrict__ box2leaf, int64_t* __restrict__ cand) {
+                                const int32_t* __restrict__ box2leaf, int64_t sentinel, int64_t* __restrict__ cand) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < ng; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t box = leaf_box[g_leaf[i]], bx = box / G, by = box % G;
     for (int s = 0; s < 9; ++s) {
       int64_t nx = bx + (s / 3 - 1), ny = by + (s % 3 - 1);
-      int64_t k = INT64_MAX;
+      int64_t k = sentinel;
       if (nx >= 0 && nx < G && ny >= 0 && ny < G) {
         int32_t T = box2leaf[nx * G + ny];
         if (T >= 0) k = (int64_t)T * n + g_j[i];
@@ -441,26 +446,25 @@ int sparse_build(const hikf_tree* t, int64_t n, const int32_t* ip, const int32_t
   HIKF_TRY(aalloc(&cand_s, ncand, st));
   HIKF_TRY(aalloc(&s->items, ncand, st));
   if (ngroups > 0) {
+    // keys < L n; the sentinel L n sorts last; only the bits that can be set are sorted
+    const int64_t sentinel = L * n;
+    int item_bits = 1;
+    while (item_bits < 62 && ((int64_t)1 << item_bits) <= sentinel) ++item_bits;
     item_candidates<<<grid_for(ngroups), kT, 0, st>>>(ngroups, n, t->G, g_leaf, s->g_j, t->leaf_box, t->box2leaf,
-                                                      cand);
+                                                      sentinel, cand);
     HIKF_CHECK_LAUNCH();
     size_t b5 = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, b4, cand, cand_s, (int)ncand, 0, 64, st);
+    cub::DeviceRadixSort::SortKeys(nullptr, b4, cand, cand_s, (int)ncand, 0, item_bits, st);
     cub::DeviceSelect::Unique(nullptr, b5, cand_s, s->items, d_num + 1, (int)ncand, st);
     void* tmp2 = nullptr;
     HIKF_CHECK_CUDA(cudaMallocAsync(&tmp2, std::max(b4, b5), st));
-    cub::DeviceRadixSort::SortKeys(tmp2, b4, cand, cand_s, (int)ncand, 0, 64, st);
+    cub::DeviceRadixSort::SortKeys(tmp2, b4, cand, cand_s, (int)ncand, 0, item_bits, st);
     cub::DeviceSelect::Unique(tmp2, b5, cand_s, s->items, d_num + 1, (int)ncand, st);
+    drop_sentinel<<<1, 1, 0, st>>>(d_num + 1, s->items, sentinel);
+    HIKF_CHECK_LAUNCH();
     int32_t nu = 0;
     HIKF_CHECK_CUDA(cudaMemcpyAsync(&nu, d_num + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-    // drop the INT64_MAX sentinel (sorted last)
-    int64_t last = 0;
-    if (nu > 0) {
-      HIKF_CHECK_CUDA(cudaMemcpyAsync(&last, s->items + nu - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      HIKF_CHECK_CUDA(cudaStreamSynchronize(st));
-      if (last == INT64_MAX) --nu;
-    }
     s->nitems = nu;
     cudaFreeAsync(tmp2, st);
   }
@@ -569,11 +573,6 @@ __global__ void parent_keys(int64_t np, const int32_t* __restrict__ np_dev, cons
     int64_t cx = box / Gc, cy = box % Gc;
     pkey[i] = ((cx >> sh) * (Gc >> sh) + (cy >> sh)) * n + j;
   }
-}
-
-// the unique parent keys end with the sentinel when the child list had unused slots
-__global__ void drop_sentinel(int32_t* __restrict__ num, const int64_t* __restrict__ keys, int64_t sentinel) {
-  if (*num > 0 && keys[*num - 1] == sentinel) --*num;
 }
 
 __device__ __forceinline__ int64_t find_key(const int64_t* __restrict__ keys, int64_t np, int64_t k) {

@@ -796,7 +796,6 @@ def main():
     achieved = flops_c / t_c / 1e12
     t_p = min(pt[1:])
     bytes_p = 24.0 * m * n + 24.0 * m + 24.0 * n * n
-    m2l_ms, _ = fmm_stage["m2l"]
     # K = C' S^-1 (2 m n^2) + n x n work: Cholesky n^3/3, inverse n^3/3, S^-1 = Li^T Li, P, R, HC_new (2 n^3 each)
     update_flops = 2.0 * m * n * n + 4 * 2.0 * n ** 3 + 2 * n ** 3 / 3.0
 
@@ -826,7 +825,9 @@ def main():
                              "note": "performed flops counted in the kernels (H^T sparsity exploited: only nonzero "
                                      "charges / expansions are multiplied); dense-formulation equivalent rate = "
                                      f"{qht_flops / t_qht / 1e12:.1f} TFLOP/s",
-                             "m2l": {"achieved": fmm_useful["m2l"] / (m2l_ms / 1e3) / 1e12 if m2l_ms else None}}},
+                             "stage_ms_note": "stage_ms are event intervals on the stages' own streams; the "
+                                              "streams overlap and an interval includes waits on other streams, so "
+                                              "they do not add up to ms (per-kernel times: profiles/*launches_qht*)"}},
         "roofline": {"kernel": "dgemm_rm_kernel (K = C' S^-1 -> C_new = r K, fused rowsum(K o C'), K innov and the "
                                "next step's C' = C_new + C_Q; 2 m n^2 flops per launch)", "bound": "fp64",
                      "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

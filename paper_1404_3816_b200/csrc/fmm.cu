@@ -471,6 +471,7 @@ struct QhtStreams {
   cudaEvent_t e[kMaxDepth + 4] = {};
   cudaEvent_t e_keys[kMaxDepth + 1] = {}, e_pairs[kMaxDepth + 1] = {}, e_tgt[kMaxDepth + 1] = {};  // level's pair keys / multipoles / M2L targets ready
   cudaEvent_t e_in = nullptr, e_out = nullptr;
+  cudaEvent_t e_join[8] = {};           // side streams joined into w before the workspace is freed
   int32_t* hcount = nullptr;            // pinned: M2L slot / entry counts per level
   int64_t (*hoff)[41] = nullptr;        // pinned: first entry of every offset per level
 };
@@ -486,6 +487,7 @@ int qht_streams(QhtStreams** out) {
     for (auto& x : p.e) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     for (auto& x : p.e_pairs) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     for (auto& x : p.e_keys) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (auto& x : p.e_join) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     for (auto& x : p.e_tgt) HIKF_CHECK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     HIKF_CHECK_CUDA(cudaMallocHost((void**)&p.hcount, sizeof(int32_t) * 2 * (kMaxDepth + 1)));
     HIKF_CHECK_CUDA(cudaMallocHost((void**)&p.hoff, sizeof(int64_t) * 41 * (kMaxDepth + 1)));
@@ -604,6 +606,44 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   Join join{qs, st};
   st = qs->w;
   SparseHt sp;
+  // the call's workspace; freed (after every side stream has been joined into the main stream)
+  // when the function leaves, on the error paths too
+  PairLevel pl[kMaxDepth + 1];
+  double* scratch[kMaxDepth + 1] = {};
+  int32_t* tmap[kMaxDepth + 1] = {};
+  int32_t* tcount = nullptr;
+  M2LPlan plan[kMaxDepth + 1];
+  double* Lbuf[2] = {nullptr, nullptr};
+  double* Pnear = nullptr;
+  struct Workspace {
+    QhtStreams* qs;
+    SparseHt& sp;
+    PairLevel* pl;
+    double** scratch;
+    int32_t** tmap;
+    int32_t*& tcount;
+    M2LPlan* plan;
+    double** Lbuf;
+    double*& Pnear;
+    ~Workspace() {
+      cudaStream_t w = qs->w;
+      for (int i = 0; i < 8; ++i) {
+        cudaEventRecord(qs->e_join[i], qs->s[i]);
+        cudaStreamWaitEvent(w, qs->e_join[i], 0);
+      }
+      for (int l = 0; l <= kMaxDepth; ++l) {
+        pairs_free(&pl[l], w);
+        if (scratch[l]) cudaFreeAsync(scratch[l], w);
+        if (tmap[l]) cudaFreeAsync(tmap[l], w);
+        m2l_plan_free(&plan[l], w);
+      }
+      if (tcount) cudaFreeAsync(tcount, w);
+      if (Lbuf[0]) cudaFreeAsync(Lbuf[0], w);
+      if (Lbuf[1]) cudaFreeAsync(Lbuf[1], w);
+      if (Pnear) cudaFreeAsync(Pnear, w);
+      sparse_free(&sp, w);
+    }
+  } workspace{qs, sp, pl, scratch, tmap, tcount, plan, Lbuf, Pnear};
   {
     ProfScope ps(ST_DENSIFY, st);  // the regrouping of H^T replaces the densify step
     HIKF_TRY(sparse_build(t, n, ip, ix, val, &sp, st));
@@ -616,7 +656,6 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
       ProfScope ps(ST_P2P, st);
       status = sparse_p2p(t, sp, U, n, st, nullptr, r0, r1, lw);
     }
-    sparse_free(&sp, st);
     return status;
   }
   cudaEvent_t ev_base = qs->e[0], ev_p2p = qs->e[1];
@@ -624,7 +663,6 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   // ---- near field, concurrently: sums parked in Pnear, added after L2P.  Launched
   // first, on the lowest-priority stream: it fills the machine while the upward pass
   // and the M2L target maps (latency-bound, on the critical path) run ahead of it ----
-  double* Pnear = nullptr;
   HIKF_CHECK_CUDA(cudaMallocAsync((void**)&Pnear, sizeof(double) * std::max<int64_t>(1, sp.nitems * t->max_count), st));
   int status = HIKF_OK;
   auto launch_p2p = [&]() -> int {
@@ -647,14 +685,8 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   // M2L passes are enqueued one upward step later (its slot / entry counts have arrived in
   // pinned memory by then), so the leaf level's M2L runs beside the M2M chain instead of
   // after it ----
-  PairLevel pl[kMaxDepth + 1];
-  double* scratch[kMaxDepth + 1] = {};
-  int32_t* tmap[kMaxDepth + 1] = {};
-  int32_t* tcount = nullptr;
   int32_t* hcount = qs->hcount;          // [2 l]: target slots, [2 l + 1]: entries of level l
   int64_t (*hoff)[41] = qs->hoff;        // first entry of every offset of level l
-  M2LPlan plan[kMaxDepth + 1];
-  double* Lbuf[2] = {nullptr, nullptr};
   // fused leaf step (leaf_down): the leaf-level locals are never stored
   const bool fused_leaf = leaf_fused_enabled() && leaf_down_supported(t);
   int64_t lsz[2] = {1, 1};  // ping-pong local buffers: level l lives in Lbuf[(D - l) & 1]
@@ -815,17 +847,6 @@ int fmm_matmat_csrT(hikf_tree* t, int64_t n, const int32_t* ip, const int32_t* i
   }
   tl.mark("leaf + scatter end", st);
   tl.report();
-  for (int l = 2; l <= D; ++l) pairs_free(&pl[l], st);
-  for (int l = 2; l <= D; ++l) {
-    cudaFreeAsync(scratch[l], st);
-    cudaFreeAsync(tmap[l], st);
-    m2l_plan_free(&plan[l], st);
-  }
-  cudaFreeAsync(tcount, st);
-  cudaFreeAsync(Lbuf[0], st);
-  cudaFreeAsync(Lbuf[1], st);
-  cudaFreeAsync(Pnear, st);
-  sparse_free(&sp, st);
   return status;
 }
 

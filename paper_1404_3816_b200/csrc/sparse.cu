@@ -882,8 +882,8 @@ int grid_cap(int64_t n) {
 }  // namespace
 
 void pairs_free(PairLevel* p, cudaStream_t st) {
-  cudaFreeAsync(p->key, st);
-  cudaFreeAsync(p->W, st);
+  if (p->key) cudaFreeAsync(p->key, st);
+  if (p->W) cudaFreeAsync(p->W, st);
   if (p->np_dev) cudaFreeAsync(p->np_dev, st);
   *p = PairLevel();
 }
@@ -1093,8 +1093,8 @@ int m2l_targets(const hikf_tree* t, int l, const PairLevel& src, int64_t n, int3
 }
 
 void m2l_plan_free(M2LPlan* plan, cudaStream_t st) {
-  cudaFreeAsync(plan->ent, st);
-  cudaFreeAsync(plan->off, st);
+  if (plan->ent) cudaFreeAsync(plan->ent, st);
+  if (plan->off) cudaFreeAsync(plan->off, st);
   *plan = M2LPlan();
 }
 

@@ -406,10 +406,14 @@ __global__ void __launch_bounds__(NT == 2 ? 128 : BW_THREADS, NT == 2 ? 3 : 2) l
 #pragma unroll
     for (int tt = 0; tt < NT; ++tt) {
       const int64_t jb = u * UC + tt * 8 + gq;
+      // one running row pointer (opaque to the compiler: NK1 hoisted row addresses would cost 2 NK1 registers)
+      const double* pr = Lpar + (int64_t)t4 * n + (jb < n ? jb : 0);
+      asm volatile("" : "+l"(pr));
 #pragma unroll
       for (int k4 = 0; k4 < NK1; ++k4) {
         const int k = k4 * 4 + t4;
-        b1[tt][k4] = (k < qp && jb < n) ? Lpar[(int64_t)k * n + jb] : 0.0;
+        b1[tt][k4] = (k < qp && jb < n) ? *pr : 0.0;
+        pr += 4 * n;
       }
     }
   };

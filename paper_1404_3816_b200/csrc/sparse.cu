@@ -670,7 +670,10 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LP
   extern __shared__ double Ms[];
   const int ld = m2l_ld(q);
   const double* __restrict__ M = a.M + (int64_t)d * q * q;
-  for (int e = threadIdx.x; e < q * q; e += blockDim.x) Ms[(e / q) * ld + e % q] = M[e];
+  // M_d: asynchronous copies, all in flight at once
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) cp_async8(Ms + (e / q) * ld + e % q, M + e, true);
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
   const int64_t e_end = a.off[d + 1];

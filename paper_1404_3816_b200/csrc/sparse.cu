@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(256, (NK4 <= 13) ? 3 : 2) m2l_prod_kernel(M2LP
       const int64_t i = i0 + 2 * t4 + h;
       out[h] = i < e_end ? a.Pr + i * q : nullptr;
     }
-#pragma unroll 1
+#pragma unroll 2
     for (int i = 0; i < NRT; ++i) {
       const int r = i * 8 + g;
       double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};

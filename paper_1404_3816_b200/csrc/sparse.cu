@@ -156,7 +156,7 @@ __global__ void p2m_sparse(int q, int64_t kcols, int64_t c0, int64_t ngr, const 
 
 // Sparse P2P, one warp per active (target leaf T, ray j):
 // U[t][j] += sum_{adjacent leaves s (ox outer, oy inner)} sum_{entries (p, j, v) in s} K(x_t, x_p) v
-__global__ void p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, int64_t n, int64_t G, KParams kp,
+__global__ void __launch_bounds__(256, 8) p2p_sparse(int64_t nitems, const int64_t* __restrict__ items, int64_t n, int64_t G, KParams kp,
                            const int32_t* __restrict__ leaf_box, const int32_t* __restrict__ leaf_start,
                            const int32_t* __restrict__ leaf_count, const int32_t* __restrict__ box2leaf,
                            const int32_t* __restrict__ leaf_g, const int32_t* __restrict__ g_j,
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(256) m2l_prod_generic_kernel(M2LProd a, int q,
 // S[slot][:] = ((0 + Pr[e_1]) + Pr[e_2]) + ... over the slot's entries in ascending offset
 // order: the adds of the per-offset passes (which start from a zeroed scratch), same order.
 // One warp per slot; the products of up to four entries are loaded before they are added.
-__global__ void __launch_bounds__(256) m2l_reduce_kernel(int64_t nslots, int q, const int32_t* __restrict__ tab,
+__global__ void __launch_bounds__(256, 8) m2l_reduce_kernel(int64_t nslots, int q, const int32_t* __restrict__ tab,
                                                         const double* __restrict__ Pr, double* __restrict__ S) {
   const int64_t slot = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
